@@ -1,0 +1,204 @@
+"""O2/O3: the TLP / MTL-TLP network, forward and manual backward, float64.
+TEST INFRASTRUCTURE.
+
+Paper (P:295 [§4.4], P:431 [§6.1.3], P:355 [§5.2]):
+  "The model first upsamples the dimension to 256 or more through multiple
+   linear layers" -> upsample (R11: 22->128->256, ReLU after each).
+  "we use the self-attention ... module ... to capture contextual features"
+   with "8 heads", "one layer of the self-attention module is enough"
+   -> n_attn layers of 8-head self-attention; R8 no mask, R9 no positional
+   encoding, R10 identity residual and no LayerNorm, R14 scale 1/sqrt(d_h).
+  "Then two residual blocks follow" -> R12: h + relu(h Wa + a) Wb + b.
+  "Finally, multiple linear layers and a sum operation are used to obtain a
+   prediction score" -> R13: per position relu(h W1 + c1) w2 + c2, summed over
+   the L rows (pads included).
+  MTL-TLP: one such head per task on a shared backbone.
+
+Parameter order R24: upsample (W, b)...; per attention layer Wq, bq, Wk, bk,
+Wv, bv, Wo, bo; per residual block Wa, a, Wb, b; per task head W1, c1, w2, c2.
+W is [in, out].
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Dict, List, Tuple
+
+import numpy as np
+
+
+@dataclass
+class Config:
+    L: int = 25
+    E: int = 22
+    T: int = 11
+    hidden: int = 256
+    up_dims: Tuple[int, ...] = (128, 256)
+    attn_heads: int = 8
+    n_attn: int = 1
+    n_res: int = 2
+    head_dim: int = 128
+    n_tasks: int = 1
+
+    def __post_init__(self):
+        self.up_dims = tuple(self.up_dims)
+        assert self.up_dims[-1] == self.hidden
+        assert self.hidden % self.attn_heads == 0
+
+    @property
+    def d_h(self) -> int:
+        return self.hidden // self.attn_heads
+
+
+def param_shapes(cfg: Config) -> List[Tuple[str, Tuple[int, ...]]]:
+    """R24 flat order."""
+    out: List[Tuple[str, Tuple[int, ...]]] = []
+    d_in = cfg.E
+    for i, d in enumerate(cfg.up_dims):
+        out += [("up%d.W" % i, (d_in, d)), ("up%d.b" % i, (d,))]
+        d_in = d
+    H = cfg.hidden
+    for l in range(cfg.n_attn):
+        for nm in ("q", "k", "v", "o"):
+            out += [("attn%d.W%s" % (l, nm), (H, H)), ("attn%d.b%s" % (l, nm), (H,))]
+    for r in range(cfg.n_res):
+        out += [("res%d.Wa" % r, (H, H)), ("res%d.a" % r, (H,)),
+                ("res%d.Wb" % r, (H, H)), ("res%d.b" % r, (H,))]
+    for t in range(cfg.n_tasks):
+        out += [("head%d.W1" % t, (H, cfg.head_dim)), ("head%d.c1" % t, (cfg.head_dim,)),
+                ("head%d.w2" % t, (cfg.head_dim, 1)), ("head%d.c2" % t, (1,))]
+    return out
+
+
+def n_params(cfg: Config) -> int:
+    return int(sum(np.prod(s) for _, s in param_shapes(cfg)))
+
+
+def unflatten(cfg: Config, flat: np.ndarray) -> Dict[str, np.ndarray]:
+    flat = np.asarray(flat, np.float64)
+    p, o = {}, 0
+    for name, shp in param_shapes(cfg):
+        k = int(np.prod(shp))
+        p[name] = flat[o:o + k].reshape(shp).copy()
+        o += k
+    assert o == flat.size, "flat parameter vector has the wrong length"
+    return p
+
+
+def flatten(cfg: Config, p: Dict[str, np.ndarray]) -> np.ndarray:
+    return np.concatenate([np.asarray(p[n], np.float64).ravel() for n, _ in param_shapes(cfg)])
+
+
+def relu(x):
+    return np.maximum(x, 0.0)
+
+
+def softmax_rows(S):
+    """Row softmax, max-subtracted (O2)."""
+    m = S.max(axis=-1, keepdims=True)
+    e = np.exp(S - m)
+    return e / e.sum(axis=-1, keepdims=True)
+
+
+def forward(cfg: Config, p: Dict[str, np.ndarray], X: np.ndarray, save: bool = False):
+    """O2.  X [N, L, E] -> scores [N, n_tasks] (float64).  With ``save`` also
+    returns the activations backward() needs."""
+    h = np.asarray(X, np.float64)
+    N, L = h.shape[0], h.shape[1]
+    nh, dh, H = cfg.attn_heads, cfg.d_h, cfg.hidden
+    acts = {"up_in": [], "up_pre": [], "attn": [], "res": []}
+    for i in range(len(cfg.up_dims)):
+        acts["up_in"].append(h)
+        pre = h @ p["up%d.W" % i] + p["up%d.b" % i]
+        acts["up_pre"].append(pre)
+        h = relu(pre)
+    for l in range(cfg.n_attn):
+        pre = "attn%d." % l
+        Q = h @ p[pre + "Wq"] + p[pre + "bq"]
+        K = h @ p[pre + "Wk"] + p[pre + "bk"]
+        V = h @ p[pre + "Wv"] + p[pre + "bv"]
+        Qh = Q.reshape(N, L, nh, dh).transpose(0, 2, 1, 3)
+        Kh = K.reshape(N, L, nh, dh).transpose(0, 2, 1, 3)
+        Vh = V.reshape(N, L, nh, dh).transpose(0, 2, 1, 3)
+        S = Qh @ Kh.transpose(0, 1, 3, 2) / np.sqrt(dh)      # R14
+        A = softmax_rows(S)                                    # R8: no mask
+        Oh = A @ Vh
+        O = Oh.transpose(0, 2, 1, 3).reshape(N, L, H)
+        acts["attn"].append(dict(h=h, Qh=Qh, Kh=Kh, Vh=Vh, A=A, O=O))
+        h = h + O @ p[pre + "Wo"] + p[pre + "bo"]             # R10
+    for r in range(cfg.n_res):
+        pre = "res%d." % r
+        v = h @ p[pre + "Wa"] + p[pre + "a"]
+        rr = relu(v)
+        acts["res"].append(dict(h=h, v=v, r=rr))
+        h = h + rr @ p[pre + "Wb"] + p[pre + "b"]              # R12
+    acts["h"] = h
+    scores = np.zeros((N, cfg.n_tasks))
+    heads = []
+    for t in range(cfg.n_tasks):
+        pre = "head%d." % t
+        u = h @ p[pre + "W1"] + p[pre + "c1"]
+        z = relu(u)
+        per_pos = z @ p[pre + "w2"] + p[pre + "c2"]           # [N, L, 1]
+        scores[:, t] = per_pos[..., 0].sum(axis=1)             # R13: sum over L rows
+        heads.append(dict(u=u, z=z))
+    acts["heads"] = heads
+    return (scores, acts) if save else scores
+
+
+def backward(cfg: Config, p: Dict[str, np.ndarray], acts, g: np.ndarray) -> Dict[str, np.ndarray]:
+    """O3.  g = dLoss/dscores [N, n_tasks] -> gradient for every parameter.
+    relu'(0) := 0.  Sums over l run over all L rows, pads included."""
+    g = np.asarray(g, np.float64)
+    nh, dh, H = cfg.attn_heads, cfg.d_h, cfg.hidden
+    N, L = acts["h"].shape[0], acts["h"].shape[1]
+    grads: Dict[str, np.ndarray] = {}
+    h = acts["h"]
+    dh_ = np.zeros_like(h)
+    for t in range(cfg.n_tasks):
+        pre = "head%d." % t
+        u, z = acts["heads"][t]["u"], acts["heads"][t]["z"]
+        gt = g[:, t][:, None, None]                            # d s_t / d per_pos = 1
+        grads[pre + "w2"] = np.einsum("nlk,n->k", z, g[:, t])[:, None]
+        grads[pre + "c2"] = np.array([L * g[:, t].sum()])
+        du = gt * p[pre + "w2"][:, 0][None, None, :] * (u > 0)
+        grads[pre + "W1"] = np.einsum("nli,nlo->io", h, du)
+        grads[pre + "c1"] = du.sum(axis=(0, 1))
+        dh_ += du @ p[pre + "W1"].T
+    for r in reversed(range(cfg.n_res)):
+        pre = "res%d." % r
+        a = acts["res"][r]
+        grads[pre + "Wb"] = np.einsum("nli,nlo->io", a["r"], dh_)
+        grads[pre + "b"] = dh_.sum(axis=(0, 1))
+        dv = (dh_ @ p[pre + "Wb"].T) * (a["v"] > 0)
+        grads[pre + "Wa"] = np.einsum("nli,nlo->io", a["h"], dv)
+        grads[pre + "a"] = dv.sum(axis=(0, 1))
+        dh_ = dh_ + dv @ p[pre + "Wa"].T
+    for l in reversed(range(cfg.n_attn)):
+        pre = "attn%d." % l
+        a = acts["attn"][l]
+        grads[pre + "Wo"] = np.einsum("nli,nlo->io", a["O"], dh_)
+        grads[pre + "bo"] = dh_.sum(axis=(0, 1))
+        dO = dh_ @ p[pre + "Wo"].T
+        dOh = dO.reshape(N, L, nh, dh).transpose(0, 2, 1, 3)
+        A, Qh, Kh, Vh = a["A"], a["Qh"], a["Kh"], a["Vh"]
+        dA = dOh @ Vh.transpose(0, 1, 3, 2)
+        dVh = A.transpose(0, 1, 3, 2) @ dOh
+        dS = A * (dA - (dA * A).sum(axis=-1, keepdims=True))
+        dQh = dS @ Kh / np.sqrt(dh)
+        dKh = dS.transpose(0, 1, 3, 2) @ Qh / np.sqrt(dh)
+        dQ = dQh.transpose(0, 2, 1, 3).reshape(N, L, H)
+        dK = dKh.transpose(0, 2, 1, 3).reshape(N, L, H)
+        dV = dVh.transpose(0, 2, 1, 3).reshape(N, L, H)
+        hin = a["h"]
+        for nm, d in (("q", dQ), ("k", dK), ("v", dV)):
+            grads[pre + "W" + nm] = np.einsum("nli,nlo->io", hin, d)
+            grads[pre + "b" + nm] = d.sum(axis=(0, 1))
+        dh_ = dh_ + dQ @ p[pre + "Wq"].T + dK @ p[pre + "Wk"].T + dV @ p[pre + "Wv"].T
+    for i in reversed(range(len(cfg.up_dims))):
+        pre_ = "up%d." % i
+        dpre = dh_ * (acts["up_pre"][i] > 0)
+        grads[pre_ + "W"] = np.einsum("nli,nlo->io", acts["up_in"][i], dpre)
+        grads[pre_ + "b"] = dpre.sum(axis=(0, 1))
+        if i > 0:
+            dh_ = dpre @ p[pre_ + "W"].T
+    return grads
