@@ -1,0 +1,206 @@
+/*
+ * tlp.h -- C ABI of libtlp.so, the B200 (sm_100a) hot path of TLP / MTL-TLP
+ * (arXiv 2211.03578, "TLP: A Deep Learning-based Cost Model for Tensor Program
+ * Tuning").  Citations: P:n = PAPER.md line n; R# = reading in DESIGN.md
+ * "Readings" (= SURVEY.md §8(c)).
+ *
+ * The problem statement the calls follow (§3 "System Overview"):
+ *   training:  "the TLP cost model forwardly propagates the finally extracted
+ *               features and normalizes the latency of the corresponding tensor
+ *               program as a label to calculate the loss.  Finally, the loss is
+ *               back-propagated to update the weights"  -> tlp_normalize_labels,
+ *               tlp_train_step
+ *   inference: "the auto-tuner obtains the prediction score through the cost
+ *               model and screens out the top-k potential candidates"
+ *               -> tlp_encode, tlp_score, tlp_topk
+ *
+ * Conventions (all entry points):
+ *   - Plain C types only.  "device" = CUDA global memory of the ctx's device;
+ *     "host" = ordinary host memory.  The caller owns every buffer it passes;
+ *     the ctx owns weights, optimizer state, the token table, scales,
+ *     workspaces and the NCCL communicator.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *     Calls are stream-ordered; none synchronises the device except
+ *     tlp_sync / tlp_get_params / tlp_get_grads.
+ *   - Host-detectable errors (NULL pointers, bad sizes, config mismatch) return
+ *     immediately with a negative status and leave all outputs untouched.
+ *     Device-detected data errors (empty sequence, type id >= T, non-finite
+ *     number or score, NaN loss) set a sticky error word in the ctx that the
+ *     next tlp_sync returns (and clears).  tlp_last_error() gives a message.
+ *   - A ctx is single-threaded: calls on one ctx must not overlap in host
+ *     time, and work queued on different streams of one ctx must not overlap
+ *     on the device (ctx workspaces are shared).  Use one ctx per host thread.
+ */
+#ifndef TLP_H_
+#define TLP_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct tlp_ctx tlp_ctx; /* opaque; created by tlp_create, owned by the library */
+
+typedef enum {
+  TLP_OK = 0,
+  TLP_ERR_ARG = -1,           /* NULL pointer / negative size / bad enum */
+  TLP_ERR_SHAPE = -2,         /* config or buffer shape mismatch */
+  TLP_ERR_EMPTY_SEQ = -3,     /* a candidate has 0 primitives */
+  TLP_ERR_UNKNOWN_TYPE = -4,  /* a kept primitive has type id >= T */
+  TLP_ERR_NONFINITE = -5,     /* a kept numeric argument or a score is NaN/Inf */
+  TLP_ERR_NAN_LOSS = -6,      /* training loss became NaN */
+  TLP_ERR_NO_LABELS = -7,     /* reserved */
+  TLP_ERR_CUDA = -8,          /* CUDA runtime error (message in tlp_last_error) */
+  TLP_ERR_NCCL = -9,          /* NCCL error */
+  TLP_ERR_STATE = -10,        /* call not valid in the ctx's state (e.g. no params) */
+  TLP_ERR_UNSUPPORTED = -11   /* configuration outside what this build implements */
+} tlp_status;
+
+typedef enum {
+  TLP_PREC_FP32 = 0,  /* fp32 SIMT everywhere: the 1e-5 relative path (no TF32) */
+  TLP_PREC_BF16 = 1   /* bf16 tcgen05 tensor-core scoring, fp32 accumulation (1e-2 path) */
+} tlp_precision;
+
+/*
+ * Model / feature configuration.  Defaults of the paper:
+ * L=25, E=22, T=11, hidden=256, attn_heads=8, n_attn=1, n_res=2.  R11 upsample
+ * widths up_dims[0..n_up) (ReLU after each, last == hidden); R13 head
+ * hidden -> head_dim (ReLU) -> 1, summed over the L rows; n_tasks heads for
+ * MTL-TLP.
+ * Limits of this build: L <= 32, E <= 64, T < E, hidden % attn_heads == 0,
+ * hidden <= 512, n_up <= 4, 1 <= n_tasks <= 8.  TLP_PREC_BF16 scoring
+ * additionally requires the paper shape (E=22, hidden=256, up_dims={128,256},
+ * attn_heads=8, head_dim=128, L=25) and otherwise returns TLP_ERR_UNSUPPORTED
+ * from tlp_create.
+ */
+typedef struct {
+  int L, E, T;
+  int hidden;
+  int up_dims[4];
+  int n_up;
+  int attn_heads;
+  int n_attn;
+  int n_res;
+  int head_dim;
+  int n_tasks;
+  int precision;              /* tlp_precision */
+  float lr, beta1, beta2, eps; /* Adam (R23 / S:356: 1e-3, 0.9, 0.999, 1e-8) */
+  unsigned long long seed;    /* reserved */
+} tlp_config;
+
+/* Packed abstract schedule primitives (S ::= p*, p ::= tau (id|num)*).
+ * Structure of arrays; ALL pointers are device memory owned by the caller. */
+typedef struct {
+  const int64_t* seq_off;        /* [N+1] primitive offsets per candidate */
+  const uint8_t* prim_type;      /* [P] type id tau in [0,T) (F1 -> one-hot) */
+  const int64_t* arg_off;        /* [P+1] argument offsets per primitive */
+  const uint8_t* arg_kind;       /* [A] 0 = Number (F3), 1 = NameParam (F2) */
+  const double* arg_num;         /* [A] Number value (used when kind == 0) */
+  const int32_t* arg_name;       /* [A] index into the batch string table (kind == 1) */
+  const uint8_t* str_blob;       /* batch string table, UTF-8 bytes */
+  const int64_t* str_off;        /* [U+1] byte offsets into str_blob */
+  int64_t P, A;                  /* numbers of primitives / arguments */
+  int32_t U;                     /* number of batch strings */
+} tlp_seq_batch;
+
+/* ---- lifetime ---------------------------------------------------------- */
+tlp_status tlp_create(const tlp_config* cfg, int device, tlp_ctx** out);
+void tlp_destroy(tlp_ctx* ctx);
+/* Message of the last error on this ctx (valid until the next call on it). */
+const char* tlp_last_error(const tlp_ctx* ctx);
+/* Default configuration of the paper with Adam defaults (R23). */
+void tlp_default_config(tlp_config* cfg);
+
+/* ---- state -------------------------------------------------------------- */
+/* F2's token table ("We map different character parameters to different
+ * tokens"): string i (bytes blob[off[i]..off[i+1])) gets token i + 2; 0 = pad,
+ * 1 = unknown (R1).  n < 2^24 - 2.  Host memory; copied. */
+tlp_status tlp_set_token_table(tlp_ctx* ctx, const uint8_t* blob, const int64_t* off, int32_t n);
+/* Post-processing normalisation scales ("normalization"; R3): [E] host
+ * floats, all > 0.  Output column c is divided by scale[c] (IEEE fp32). */
+tlp_status tlp_set_norm_scales(tlp_ctx* ctx, const float* scale);
+/* Number of fp32 parameters in the R24 flat order. */
+int64_t tlp_num_params(const tlp_ctx* ctx);
+/* Flat fp32 parameters in R24 order (W stored [in,out] row-major).  `flat` may
+ * be host or device memory.  Resets Adam state.  Synchronous. */
+tlp_status tlp_set_params(tlp_ctx* ctx, const float* flat, int64_t n);
+tlp_status tlp_get_params(tlp_ctx* ctx, float* flat, int64_t n);
+/* Gradient of the last tlp_compute_grads / tlp_train_step (after allreduce). */
+tlp_status tlp_get_grads(tlp_ctx* ctx, float* flat, int64_t n);
+/* Data-parallel communicator: `nccl_id` points to the 128-byte
+ * ncclUniqueId created by rank 0 and broadcast by the caller; blocks until all
+ * `world` ranks have joined.  world == 1 is accepted and disables collectives. */
+tlp_status tlp_set_comm(tlp_ctx* ctx, const void* nccl_id, int rank, int world);
+/* Fill a 128-byte buffer with a fresh ncclUniqueId (rank 0 only). */
+tlp_status tlp_get_unique_id(void* nccl_id_out);
+
+/* ---- (1) tokenizer, P:215-225 + P:239 + P:273 ---------------------------
+ * feats[n, r, c] (fp32 [N, L, E], device, row-major) =
+ *   r < min(len_n, L):  c < T: (c == tau) ; T <= c < E: arg c-T (token or
+ *   RN_f32(number)) or 0 past the last argument  -- then / scale[c]
+ *   r >= len_n: 0.
+ * Crops silently (R4).  Device errors: EMPTY_SEQ, UNKNOWN_TYPE, NONFINITE (kept
+ * data only).  Requires tlp_set_norm_scales (token table optional: all names
+ * -> 1 if unset). */
+tlp_status tlp_encode(tlp_ctx* ctx, const tlp_seq_batch* in, int64_t N, float* feats, void* stream);
+
+/* ---- (2) scoring, P:295 + P:355 ----------------------------------------
+ * scores[n, t] (fp32 [N, n_tasks], device) = head_t(resblocks(attn(upsample(feats[n])))).
+ * Per-candidate results do not depend on N or on the position of n (batch
+ * invariance).  Requires tlp_set_params. */
+tlp_status tlp_score(tlp_ctx* ctx, const float* feats, int64_t N, float* scores, void* stream);
+
+/* ---- (3) training, P:182 + P:295-296 + P:355-362 ------------------------
+ * One optimizer step on a batch of B candidates grouped into G contiguous
+ * groups (subgraphs, R18): feats [B, L, E] device; labels [B, n_tasks] device
+ * fp32 in (0,1], NaN = absent (MTL); group_off [G+1] HOST int64.
+ * Forward, LambdaRank (R16, mean over the global strict-pair count per task),
+ * backward, gradient allreduce when a communicator is set, Adam (R23).
+ * loss_out: device fp32 scalar (sum over tasks of the per-task means; with a
+ * communicator every rank receives the global loss). */
+tlp_status tlp_train_step(tlp_ctx* ctx, const float* feats, const float* labels,
+                          const int64_t* group_off, int32_t B, int32_t G,
+                          float* loss_out, void* stream);
+/* As tlp_train_step but without the Adam update (gradients via tlp_get_grads). */
+tlp_status tlp_compute_grads(tlp_ctx* ctx, const float* feats, const float* labels,
+                             const int64_t* group_off, int32_t B, int32_t G,
+                             float* loss_out, void* stream);
+/* The LambdaRank unit alone (R26): scores/labels [B, n_tasks] device; writes the
+ * loss (device scalar) and dloss/dscores [B, n_tasks] (device).  Pair counts
+ * are local (no communicator). */
+tlp_status tlp_lambdarank(tlp_ctx* ctx, const float* scores, const float* labels,
+                          const int64_t* group_off, int32_t B, int32_t G,
+                          float* loss_out, float* dscores_out, void* stream);
+
+/* ---- (4) per-task top-k, P:182 + P:390 ----------------------------------
+ * For task segment t = [task_off[t], task_off[t+1]) of `scores` (column `head`
+ * of a row-major [*, score_stride] fp32 device array): the k best candidates by
+ * (score desc, index asc), -0 == +0 (R15, R21).  idx_out [T, k] int64 device
+ * (global index = shard_base + local row), val_out [T, k] fp32 device; a
+ * segment shorter than k is padded with (-1, -inf).  task_off is HOST int64
+ * [T+1].  NaN score -> NONFINITE device error.
+ * With a communicator (world > 1) every rank passes its own shard (task_off
+ * local, shard_base = global index of its row 0) and receives the merged global
+ * top-k (one ncclAllGather of T*k (score, index) pairs, then the same
+ * deterministic merge on every rank); T and k must agree across ranks. */
+tlp_status tlp_topk(tlp_ctx* ctx, const float* scores, int32_t score_stride, int32_t head,
+                    const int64_t* task_off, int32_t T, int32_t k, int64_t shard_base,
+                    int64_t* idx_out, float* val_out, void* stream);
+
+/* ---- training-data preparation, P:295-296 -------------------------------
+ * label_i = min_{j in g} latency_j / latency_i per group g (fp64 quotient,
+ * rounded to fp32).  latency [M] fp32 device > 0; group_off [G+1] HOST int64;
+ * label_out [M] fp32 device. */
+tlp_status tlp_normalize_labels(tlp_ctx* ctx, const float* latency, const int64_t* group_off,
+                                int32_t G, float* label_out, void* stream);
+
+/* Synchronise the device and return (then clear) the sticky device error. */
+tlp_status tlp_sync(tlp_ctx* ctx);
+/* Number of kernels this ctx launched since creation (bench evidence). */
+int64_t tlp_launch_count(const tlp_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TLP_H_ */

@@ -32,9 +32,9 @@ def topk(scores: np.ndarray, task_off: np.ndarray, k: int,
         lo, hi = int(task_off[t]), int(task_off[t + 1])
         items = [(-float(scores[i]) + 0.0, base + i) for i in range(lo, hi)]  # +0.0: -0 -> +0
         items.sort()
-        for r, (negs, i) in enumerate(items[:k]):
+        for r, (_, i) in enumerate(items[:k]):
             idx[t, r] = i
-            val[t, r] = np.float32(-negs)
+            val[t, r] = scores[i - base]  # the score itself, bits unchanged
     return idx, val
 
 

@@ -1,0 +1,185 @@
+// K1: the TLP tokenizer on the GPU.
+//
+//   f = F(p) ::= F1(tau) (F2(id) | F3(num))*       (fig 3_1_feature_extraction_abstract (b))
+//   F1: type -> one-hot (T = 11 wide), F2: name -> token (R1/R2),
+//   F3: number -> number (RN to fp32, R5); concatenated in original order;
+//   post-processing: crop to L x E keeping the head (R4), zero padding (R7),
+//   per-column division by the normalisation scale (R3, IEEE fp32 division --
+//   this file must NOT be compiled with --use_fast_math / -prec-div=false).
+//
+// Two launches per batch:
+//   resolve_tokens: batch string table (U strings) -> token via the ctx hash
+//                   table (FNV-1a 64, linear probing, byte-exact verification).
+//   encode_kernel:  one thread per output element (n, r, c) so that the
+//                   2,200-byte fp32 rows are written fully coalesced; the
+//                   gathers of seq_off / prim_type / arg_off hit L1/L2.
+#include "tlp_internal.cuh"
+
+#include <cstring>
+
+namespace {
+
+__host__ __device__ inline uint64_t fnv1a(const uint8_t* p, int64_t n) {
+  uint64_t h = 1469598103934665603ull;
+  for (int64_t i = 0; i < n; ++i) {
+    h ^= p[i];
+    h *= 1099511628211ull;
+  }
+  return h == 0 ? 1 : h;
+}
+
+__global__ void resolve_tokens(const uint8_t* __restrict__ blob, const int64_t* __restrict__ off,
+                               int32_t U, const uint64_t* __restrict__ keys,
+                               const int32_t* __restrict__ vals, const int32_t* __restrict__ sidx,
+                               const uint8_t* __restrict__ tblob, const int64_t* __restrict__ toff,
+                               uint32_t cap, int32_t* __restrict__ tokens) {
+  int u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= U) return;
+  const uint8_t* s = blob + off[u];
+  int64_t n = off[u + 1] - off[u];
+  int32_t tok = 1;  // unknown (R1)
+  if (cap) {
+    uint64_t h = fnv1a(s, n);
+    uint32_t slot = (uint32_t)h & (cap - 1);
+    for (uint32_t probe = 0; probe < cap; ++probe) {
+      uint64_t k = keys[slot];
+      if (k == 0) break;
+      if (k == h) {
+        int32_t j = sidx[slot];
+        const uint8_t* t = tblob + toff[j];
+        int64_t tn = toff[j + 1] - toff[j];
+        bool eq = tn == n;
+        for (int64_t i = 0; eq && i < n; ++i) eq = t[i] == s[i];
+        if (eq) { tok = vals[slot]; break; }
+      }
+      slot = (slot + 1) & (cap - 1);
+    }
+  }
+  tokens[u] = tok;
+}
+
+template <int L_, int E_, int T_>
+__global__ void __launch_bounds__(256) encode_kernel_fixed(
+    int64_t total, const int64_t* __restrict__ seq_off, const uint8_t* __restrict__ prim_type,
+    const int64_t* __restrict__ arg_off, const uint8_t* __restrict__ arg_kind,
+    const double* __restrict__ arg_num, const int32_t* __restrict__ arg_name,
+    const int32_t* __restrict__ tokens, const float* __restrict__ scale, float* __restrict__ out,
+    uint32_t* __restrict__ err, int L, int E, int T) {
+  const int Lr = L_ ? L_ : L, Er = E_ ? E_ : E, Tr = T_ ? T_ : T;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
+    const int64_t n = e / (Lr * Er);
+    const int rc = (int)(e - n * (Lr * Er));
+    const int r = rc / Er;
+    const int c = rc - r * Er;
+    const int64_t s0 = seq_off[n];
+    const int64_t len = seq_off[n + 1] - s0;
+    float v = 0.f;
+    if (len <= 0) {
+      if (rc == 0) atomicOr(err, DERR_EMPTY_SEQ);
+    } else if (r < len) {
+      const int64_t p = s0 + r;
+      const int tau = prim_type[p];
+      if (tau >= Tr) {
+        if (c == 0) atomicOr(err, DERR_UNKNOWN_TYPE);
+      } else if (c < Tr) {
+        v = (c == tau) ? 1.f : 0.f;  // F1 one-hot
+      } else {
+        const int64_t a0 = arg_off[p];
+        const int a = c - Tr;
+        if (a < arg_off[p + 1] - a0) {
+          const int64_t ai = a0 + a;
+          if (arg_kind[ai]) {
+            v = (float)tokens[arg_name[ai]];  // F2 (tokens < 2^24: exact)
+          } else {
+            const double d = arg_num[ai];
+            v = __double2float_rn(d);  // F3, R5
+            if (!isfinite(d) || !isfinite(v)) atomicOr(err, DERR_NONFINITE);
+          }
+        }
+      }
+    }
+    out[e] = __fdiv_rn(v, scale[c]);  // R3: IEEE round-to-nearest division
+  }
+}
+
+}  // namespace
+
+tlp_status build_token_table(tlp_ctx* ctx, const uint8_t* blob, const int64_t* off, int32_t n) {
+  // Host-side construction (runtime plumbing), uploaded once.
+  uint32_t cap = 0;
+  if (n > 0) {
+    cap = 16;
+    while (cap < (uint32_t)n * 2u) cap <<= 1;
+  }
+  std::vector<uint64_t> keys(cap ? cap : 1, 0);
+  std::vector<int32_t> vals(cap ? cap : 1, 0), sidx(cap ? cap : 1, -1);
+  const int64_t nbytes = n > 0 ? off[n] : 0;
+  for (int32_t i = 0; i < n; ++i) {
+    const uint8_t* s = blob + off[i];
+    int64_t len = off[i + 1] - off[i];
+    uint64_t h = fnv1a(s, len);
+    uint32_t slot = (uint32_t)h & (cap - 1);
+    bool dup = false;
+    while (keys[slot] != 0) {
+      if (keys[slot] == h) {
+        int32_t j = sidx[slot];
+        if (off[j + 1] - off[j] == len && std::memcmp(blob + off[j], s, (size_t)len) == 0) {
+          dup = true;  // first occurrence keeps its token (R1)
+          break;
+        }
+      }
+      slot = (slot + 1) & (cap - 1);
+    }
+    if (dup) continue;
+    keys[slot] = h;
+    vals[slot] = i + 2;
+    sidx[slot] = i;
+  }
+  cudaFree(ctx->d_hkeys); cudaFree(ctx->d_hval); cudaFree(ctx->d_hstr);
+  cudaFree(ctx->d_tblob); cudaFree(ctx->d_toff);
+  ctx->d_hkeys = nullptr; ctx->d_hval = nullptr; ctx->d_hstr = nullptr;
+  ctx->d_tblob = nullptr; ctx->d_toff = nullptr; ctx->hcap = 0;
+  if (cap == 0) return TLP_OK;
+  TLP_CUDA_TRY(cudaMalloc(&ctx->d_hkeys, cap * sizeof(uint64_t)));
+  TLP_CUDA_TRY(cudaMalloc(&ctx->d_hval, cap * sizeof(int32_t)));
+  TLP_CUDA_TRY(cudaMalloc(&ctx->d_hstr, cap * sizeof(int32_t)));
+  TLP_CUDA_TRY(cudaMalloc(&ctx->d_tblob, nbytes > 0 ? nbytes : 1));
+  TLP_CUDA_TRY(cudaMalloc(&ctx->d_toff, (n + 1) * sizeof(int64_t)));
+  TLP_CUDA_TRY(cudaMemcpy(ctx->d_hkeys, keys.data(), cap * sizeof(uint64_t), cudaMemcpyHostToDevice));
+  TLP_CUDA_TRY(cudaMemcpy(ctx->d_hval, vals.data(), cap * sizeof(int32_t), cudaMemcpyHostToDevice));
+  TLP_CUDA_TRY(cudaMemcpy(ctx->d_hstr, sidx.data(), cap * sizeof(int32_t), cudaMemcpyHostToDevice));
+  if (nbytes > 0) TLP_CUDA_TRY(cudaMemcpy(ctx->d_tblob, blob, nbytes, cudaMemcpyHostToDevice));
+  TLP_CUDA_TRY(cudaMemcpy(ctx->d_toff, off, (n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice));
+  ctx->hcap = cap;
+  return TLP_OK;
+}
+
+tlp_status encode_launch(tlp_ctx* ctx, const tlp_seq_batch* in, int64_t N, float* feats,
+                         cudaStream_t s) {
+  const tlp_config& c = ctx->cfg;
+  int32_t* tokens = nullptr;
+  if (in->U > 0) {
+    TLP_CUDA_TRY(ctx->ws_tokens.ensure(sizeof(int32_t) * (size_t)in->U));
+    tokens = ctx->ws_tokens.as<int32_t>();
+    resolve_tokens<<<(unsigned)cdiv(in->U, 128), 128, 0, s>>>(
+        in->str_blob, in->str_off, in->U, ctx->d_hkeys, ctx->d_hval, ctx->d_hstr, ctx->d_tblob,
+        ctx->d_toff, ctx->hcap, tokens);
+    TLP_LAUNCH_CHECK();
+  }
+  const int64_t total = N * (int64_t)c.L * c.E;
+  if (total == 0) return TLP_OK;
+  const int64_t want = cdiv(total, 256);
+  const unsigned grid = (unsigned)(want < (int64_t)ctx->num_sms * 64 ? want : (int64_t)ctx->num_sms * 64);
+  if (c.L == 25 && c.E == 22 && c.T == 11) {
+    encode_kernel_fixed<25, 22, 11><<<grid, 256, 0, s>>>(
+        total, in->seq_off, in->prim_type, in->arg_off, in->arg_kind, in->arg_num, in->arg_name,
+        tokens, ctx->d_scale, feats, ctx->d_err, c.L, c.E, c.T);
+  } else {
+    encode_kernel_fixed<0, 0, 0><<<grid, 256, 0, s>>>(
+        total, in->seq_off, in->prim_type, in->arg_off, in->arg_kind, in->arg_num, in->arg_name,
+        tokens, ctx->d_scale, feats, ctx->d_err, c.L, c.E, c.T);
+  }
+  TLP_LAUNCH_CHECK();
+  return TLP_OK;
+}

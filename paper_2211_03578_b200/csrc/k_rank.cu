@@ -1,0 +1,228 @@
+// K9 LambdaRank loss + dL/ds per (group, task), and the strict-pair counts.
+//
+// Paper: "rank loss [cao2007learning, wang2018lambdaloss]"
+// "lambda rank loss designed for ranking tasks", P:409 (chosen).  The formula
+// is not printed; reading R16:
+//   pi_i  = rank by (s desc, index asc)                       (R17)
+//   G_i   = (2^{y_i} - 1) / maxDCG,  maxDCG = max(sum_r (2^{y_(r)}-1)/log2(1+r), 1e-10)
+//   pair y_i > y_j:  w = |G_i - G_j| |1/log2(1+pi_i) - 1/log2(1+pi_j)|
+//                    l = w log2(1 + exp(-(s_i - s_j)))
+//                    dl/ds_i = -(1/ln2) w sigmoid(-(s_i - s_j)) = -dl/ds_j
+//   L_t = sum l / P_t  (P_t = strict pairs of task t in the global batch)
+// MTL (R19): per task, only items with a present (non-NaN) label.
+//
+// One CTA per (group, task).  Every item's gradient is the sum over all its
+// partners computed by the thread that owns the item (no atomics), so the
+// result is deterministic; the O(n^2) pair loop reads the group from shared
+// memory (warp-broadcast of the partner j).  2^y - 1 is evaluated as
+// expm1(y ln 2) to avoid cancellation for small labels.
+#include "tlp_internal.cuh"
+
+#include <algorithm>
+
+namespace {
+
+constexpr int kThreads = 512;
+constexpr float kLn2 = 0.693147180559945309f;
+
+__device__ __forceinline__ float block_sum(float v, float* red) {
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  float r = 0.f;
+  if (threadIdx.x < 32) {
+    r = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+    for (int o = 16; o; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+    if (threadIdx.x == 0) red[0] = r;
+  }
+  __syncthreads();
+  r = red[0];
+  __syncthreads();
+  return r;
+}
+
+// Compact the present items of (group, task) into shared memory, in index order.
+__device__ int gather_present(const float* __restrict__ scores, const float* __restrict__ labels,
+                              int64_t lo, int64_t hi, int t, int nt, float* s, float* y,
+                              int* idx) {
+  __shared__ int base;
+  if (threadIdx.x == 0) base = 0;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    for (int64_t c = lo; c < hi; c += 32) {
+      const int64_t i = c + threadIdx.x;
+      float yi = 0.f, si = 0.f;
+      bool pres = false;
+      if (i < hi) {
+        yi = labels[i * nt + t];
+        si = scores ? scores[i * nt + t] : 0.f;
+        pres = !isnan(yi);
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, pres);
+      const int pos = base + __popc(m & ((1u << threadIdx.x) - 1));
+      if (pres) { s[pos] = si; y[pos] = yi; idx[pos] = (int)(i - lo); }
+      __syncwarp();
+      if (threadIdx.x == 0) base += __popc(m);
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  return base;
+}
+
+__global__ void __launch_bounds__(kThreads) pair_count_kernel(const float* __restrict__ labels,
+                                                              const int64_t* __restrict__ goff,
+                                                              int nt, double* __restrict__ part) {
+  extern __shared__ float sm[];
+  const int g = blockIdx.x, t = blockIdx.y;
+  const int64_t lo = goff[g], hi = goff[g + 1];
+  const int cap = (int)(hi - lo);
+  float* s = sm;
+  float* y = s + cap;
+  int* idx = reinterpret_cast<int*>(y + cap);
+  const int n = gather_present(nullptr, labels, lo, hi, t, nt, s, y, idx);
+  float cnt = 0.f;  // per-thread count < 2^24 for n <= 8192
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const float yi = y[i];
+    int c = 0;
+    for (int j = 0; j < n; ++j) c += yi > y[j];
+    cnt += (float)c;
+  }
+  // exact integer sum: per-thread counts < 2^24 and the total < 2^26 * 512 fits
+  // in double; reduce in double via two float halves is overkill -> do it in int.
+  __shared__ unsigned long long tot;
+  if (threadIdx.x == 0) tot = 0;
+  __syncthreads();
+  atomicAdd(&tot, (unsigned long long)cnt);
+  __syncthreads();
+  if (threadIdx.x == 0) part[(int64_t)t * gridDim.x + g] = (double)tot;
+}
+
+__global__ void sum_counts(const double* __restrict__ part, int G, int nt,
+                           double* __restrict__ counts) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nt) return;
+  double s = 0.0;
+  for (int g = 0; g < G; ++g) s += part[(int64_t)t * G + g];
+  counts[t] = s;
+}
+
+__global__ void __launch_bounds__(kThreads) rank_kernel(const float* __restrict__ scores,
+                                                        const float* __restrict__ labels,
+                                                        const int64_t* __restrict__ goff, int nt,
+                                                        float* __restrict__ loss_part,
+                                                        float* __restrict__ dscores) {
+  extern __shared__ float sm[];
+  __shared__ float red[32];
+  const int g = blockIdx.x, t = blockIdx.y;
+  const int64_t lo = goff[g], hi = goff[g + 1];
+  const int cap = (int)(hi - lo);
+  float* s = sm;
+  float* y = s + cap;
+  float* Gs = y + cap;
+  float* iD = Gs + cap;
+  int* idx = reinterpret_cast<int*>(iD + cap);
+  const int n = gather_present(scores, labels, lo, hi, t, nt, s, y, idx);
+  // ranks (R17) and ideal ranks -> maxDCG
+  float dcg = 0.f;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const float si = s[i], yi = y[i];
+    int rs = 1, ry = 1;
+    for (int j = 0; j < n; ++j) {
+      const float sj = s[j], yj = y[j];
+      rs += (sj > si) || (sj == si && j < i);
+      ry += (yj > yi) || (yj == yi && j < i);
+    }
+    iD[i] = 1.0f / log2f(1.0f + (float)rs);
+    dcg += expm1f(yi * kLn2) / log2f(1.0f + (float)ry);
+  }
+  const float maxdcg = fmaxf(block_sum(dcg, red), 1e-10f);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) Gs[i] = expm1f(y[i] * kLn2) / maxdcg;
+  __syncthreads();
+  float lsum = 0.f;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const float si = s[i], yi = y[i], Gi = Gs[i], iDi = iD[i];
+    float gi = 0.f, li = 0.f;
+    for (int j = 0; j < n; ++j) {
+      const float yj = y[j];
+      if (yi == yj) continue;
+      const float w = fabsf(Gi - Gs[j]) * fabsf(iDi - iD[j]);
+      // z = s_hi - s_lo of the ordered pair
+      const float z = (yi > yj) ? (si - s[j]) : (s[j] - si);
+      const float e = expf(-fabsf(z));
+      const float sig = (z >= 0.f) ? e / (1.0f + e) : 1.0f / (1.0f + e);  // sigmoid(-z)
+      if (yi > yj) {
+        li += w * (fmaxf(-z, 0.f) + log1pf(e)) / kLn2;
+        gi -= w * sig / kLn2;
+      } else {
+        gi += w * sig / kLn2;
+      }
+    }
+    dscores[(lo + idx[i]) * nt + t] = gi;
+    lsum += li;
+  }
+  const float L = block_sum(lsum, red);
+  if (threadIdx.x == 0) loss_part[(int64_t)t * gridDim.x + g] = L;
+}
+
+__global__ void finalize_rank(const float* __restrict__ loss_part, int G, int nt,
+                              const double* __restrict__ counts, float* __restrict__ dscores,
+                              int64_t B, float* __restrict__ loss_out, uint32_t* err) {
+  // scale gradients by 1/P_t, sum the task losses in a fixed order
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < B * nt; e += stride) {
+    const int t = (int)(e % nt);
+    const double P = counts[t];
+    dscores[e] = P > 0 ? (float)((double)dscores[e] / P) : 0.f;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    double tot = 0.0;
+    for (int t = 0; t < nt; ++t) {
+      double lt = 0.0;
+      for (int g = 0; g < G; ++g) lt += (double)loss_part[(int64_t)t * G + g];
+      if (counts[t] > 0) tot += lt / counts[t];
+    }
+    const float lf = (float)tot;
+    if (isnan(lf)) atomicOr(err, DERR_NAN_LOSS);
+    *loss_out = lf;
+  }
+}
+
+}  // namespace
+
+static size_t rank_ws_bytes(int G, int nt) {
+  return (size_t)G * nt * (sizeof(double) + sizeof(float)) + 64;
+}
+
+tlp_status rank_pair_counts(tlp_ctx* ctx, const float* labels, const int64_t* d_goff, int G,
+                            int max_group, double* d_counts, cudaStream_t s) {
+  const int nt = ctx->cfg.n_tasks;
+  TLP_CUDA_TRY(ctx->ws_rank.ensure(rank_ws_bytes(G, nt)));
+  double* part = ctx->ws_rank.as<double>();
+  const size_t smem = (size_t)max_group * (2 * sizeof(float) + sizeof(int));
+  cudaFuncSetAttribute(pair_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  pair_count_kernel<<<dim3(G, nt), kThreads, smem, s>>>(labels, d_goff, nt, part);
+  TLP_LAUNCH_CHECK();
+  sum_counts<<<1, 32, 0, s>>>(part, G, nt, d_counts);
+  TLP_LAUNCH_CHECK();
+  return TLP_OK;
+}
+
+tlp_status rank_loss_grad(tlp_ctx* ctx, const float* scores, const float* labels,
+                          const int64_t* d_goff, int G, int B, int max_group,
+                          const double* d_counts, float* loss_out, float* dscores,
+                          cudaStream_t s) {
+  const int nt = ctx->cfg.n_tasks;
+  TLP_CUDA_TRY(ctx->ws_rank.ensure(rank_ws_bytes(G, nt)));
+  float* loss_part = reinterpret_cast<float*>(ctx->ws_rank.as<char>() + (size_t)G * nt * sizeof(double));
+  TLP_CUDA_TRY(cudaMemsetAsync(dscores, 0, (size_t)B * nt * sizeof(float), s));
+  const size_t smem = (size_t)max_group * (4 * sizeof(float) + sizeof(int));
+  cudaFuncSetAttribute(rank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  rank_kernel<<<dim3(G, nt), kThreads, smem, s>>>(scores, labels, d_goff, nt, loss_part, dscores);
+  TLP_LAUNCH_CHECK();
+  finalize_rank<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv((int64_t)B * nt, 256), 1024)), 256, 0, s>>>(
+      loss_part, G, nt, d_counts, dscores, B, loss_out, ctx->d_err);
+  TLP_LAUNCH_CHECK();
+  return TLP_OK;
+}

@@ -1,0 +1,648 @@
+// fp32 SIMT network: the 1e-5-relative path (TLP_PREC_FP32) and, for this
+// round, the training forward/backward of both precisions.
+//
+// Forward (readings R8-R14 in DESIGN.md):
+//   h = relu(relu(X W1 + b1) W2 + b2)                    upsample (R11)
+//   h = h + softmax(Q K^T / sqrt(d_h)) V Wo + bo        per head, no mask (R8), no PE (R9), R10
+//   h = h + relu(h Wa + a) Wb + b                        residual blocks (R12)
+//   s_t = (sum_l relu(h_l W1_t + c1_t)) . w2_t + L c2_t  head + sum (R13)
+// Backward: chain rule of the same (relu'(0) = 0), weight gradients reduced in
+// a fixed order (split over rows + ordered partial sums) so training is
+// deterministic.
+//
+// Kernels: a register-blocked 128x128x8 SGEMM with fused epilogues (bias,
+// residual, ReLU, ReLU-mask, accumulate) used for every dense layer and every
+// dgrad/wgrad, one-warp-per-(candidate, head) attention forward/backward, and
+// the head pooling kernels.  No tensor cores here: TF32 could not meet 1e-5.
+#include "tlp_internal.cuh"
+
+#include <algorithm>
+#include <cmath>
+
+namespace {
+
+constexpr int BM = 128, BN = 128, BK = 8, PADS = 4;
+
+template <bool TA, bool TB>
+__device__ __forceinline__ void load_tiles(const float* __restrict__ A, int64_t lda,
+                                           const float* __restrict__ B, int64_t ldb, int64_t M,
+                                           int64_t N, int64_t m0, int64_t n0, int64_t k0,
+                                           int64_t kend, float ra[4], float rb[4]) {
+  const int t = threadIdx.x;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    int64_t i, k;
+    if (TA) { k = t / 32; i = (t % 32) * 4 + q; }
+    else { i = t / 2; k = (t % 2) * 4 + q; }
+    const int64_t gi = m0 + i, gk = k0 + k;
+    ra[q] = (gi < M && gk < kend) ? (TA ? A[gk * lda + gi] : A[gi * lda + gk]) : 0.f;
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    int64_t j, k;
+    if (TB) { j = t / 2; k = (t % 2) * 4 + q; }
+    else { k = t / 32; j = (t % 32) * 4 + q; }
+    const int64_t gj = n0 + j, gk = k0 + k;
+    rb[q] = (gj < N && gk < kend) ? (TB ? B[gj * ldb + gk] : B[gk * ldb + gj]) : 0.f;
+  }
+}
+
+template <bool TA, bool TB>
+__device__ __forceinline__ void store_tiles(float (*As)[BM + PADS], float (*Bs)[BN + PADS],
+                                            const float ra[4], const float rb[4]) {
+  const int t = threadIdx.x;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    if (TA) As[t / 32][(t % 32) * 4 + q] = ra[q];
+    else As[(t % 2) * 4 + q][t / 2] = ra[q];
+    if (TB) Bs[(t % 2) * 4 + q][t / 2] = rb[q];
+    else Bs[t / 32][(t % 32) * 4 + q] = rb[q];
+  }
+}
+
+struct EpiDev {
+  const float* bias;
+  const float* resid;
+  int64_t ldr;
+  const float* mask;
+  int64_t ldm;
+  int relu;
+  int accumulate;
+};
+
+// C[M,N] = epi(op(A)[M,K] op(B)[K,N]).  blockIdx.z selects a K slice of
+// length kslice; with gridDim.z > 1 the raw partial goes to C + z * M * ldc.
+template <bool TA, bool TB>
+__global__ void __launch_bounds__(256) sgemm_kernel(int64_t M, int64_t N, int64_t K,
+                                                    const float* __restrict__ A, int64_t lda,
+                                                    const float* __restrict__ B, int64_t ldb,
+                                                    float* __restrict__ C, int64_t ldc,
+                                                    EpiDev ep, int64_t kslice) {
+  __shared__ __align__(16) float As[2][BK][BM + PADS];
+  __shared__ __align__(16) float Bs[2][BK][BN + PADS];
+  const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
+  const int64_t kb = (int64_t)blockIdx.z * kslice;
+  const int64_t ke = std::min<int64_t>(K, kb + kslice);
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  float acc[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+  float ra[4], rb[4];
+  load_tiles<TA, TB>(A, lda, B, ldb, M, N, m0, n0, kb, ke, ra, rb);
+  store_tiles<TA, TB>(As[0], Bs[0], ra, rb);
+  __syncthreads();
+  int buf = 0;
+  for (int64_t k0 = kb; k0 < ke; k0 += BK) {
+    const bool more = k0 + BK < ke;
+    if (more) load_tiles<TA, TB>(A, lda, B, ldb, M, N, m0, n0, k0 + BK, ke, ra, rb);
+#pragma unroll
+    for (int k = 0; k < BK; ++k) {
+      float a[8], b[8];
+      const float4 a0 = *reinterpret_cast<const float4*>(&As[buf][k][ty * 4]);
+      const float4 a1 = *reinterpret_cast<const float4*>(&As[buf][k][64 + ty * 4]);
+      const float4 b0 = *reinterpret_cast<const float4*>(&Bs[buf][k][tx * 4]);
+      const float4 b1 = *reinterpret_cast<const float4*>(&Bs[buf][k][64 + tx * 4]);
+      a[0] = a0.x; a[1] = a0.y; a[2] = a0.z; a[3] = a0.w;
+      a[4] = a1.x; a[5] = a1.y; a[6] = a1.z; a[7] = a1.w;
+      b[0] = b0.x; b[1] = b0.y; b[2] = b0.z; b[3] = b0.w;
+      b[4] = b1.x; b[5] = b1.y; b[6] = b1.z; b[7] = b1.w;
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    if (more) {
+      store_tiles<TA, TB>(As[buf ^ 1], Bs[buf ^ 1], ra, rb);
+      __syncthreads();
+      buf ^= 1;
+    }
+  }
+  float* Cz = C + (int64_t)blockIdx.z * M * ldc;
+  const bool partial = gridDim.z > 1;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int64_t gi = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + i - 4);
+    if (gi >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int64_t gj = n0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + j - 4);
+      if (gj >= N) continue;
+      float v = acc[i][j];
+      if (!partial) {
+        if (ep.bias) v += ep.bias[gj];
+        if (ep.resid) v += ep.resid[gi * ep.ldr + gj];
+        if (ep.relu) v = fmaxf(v, 0.f);
+        if (ep.mask) v = ep.mask[gi * ep.ldm + gj] > 0.f ? v : 0.f;
+        if (ep.accumulate) v += Cz[gi * ldc + gj];
+      }
+      Cz[gi * ldc + gj] = v;
+    }
+  }
+}
+
+// out[j] (=|+=) sum_z part[z][j], fixed order.
+__global__ void reduce_partials(const float* __restrict__ part, int64_t n, int Z,
+                                float* __restrict__ out) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  float s = 0.f;
+  for (int z = 0; z < Z; ++z) s += part[(int64_t)z * n + j];
+  out[j] = s;
+}
+
+__global__ void colsum_partial(int64_t M, int64_t N, const float* __restrict__ X, int64_t ldx,
+                               int64_t rows, float* __restrict__ part) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= N) return;
+  const int64_t r0 = (int64_t)blockIdx.y * rows, r1 = std::min<int64_t>(M, r0 + rows);
+  float s = 0.f;
+  for (int64_t i = r0; i < r1; ++i) s += X[i * ldx + j];
+  part[(int64_t)blockIdx.y * N + j] = s;
+}
+
+// ---------------------------------------------------------------------------
+// attention, one warp per (candidate, head); lane = query row (L <= 32)
+template <int DH>
+__global__ void __launch_bounds__(128) attn_fwd_kernel(const float* __restrict__ QKV, int L,
+                                                       int H, int nh, int64_t pairs,
+                                                       float* __restrict__ O,
+                                                       float* __restrict__ Asave) {
+  extern __shared__ float sm[];
+  const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int64_t pair = (int64_t)blockIdx.x * (blockDim.x / 32) + w;
+  if (pair >= pairs) return;
+  float* Ks = sm + w * 2 * 32 * DH;
+  float* Vs = Ks + 32 * DH;
+  const int64_t n = pair / nh;
+  const int hd = (int)(pair % nh);
+  const int64_t row0 = n * L;
+  const int64_t ld = 3 * (int64_t)H;
+  for (int e = lane; e < L * DH; e += 32) {
+    const int m = e / DH, d = e % DH;
+    Ks[m * DH + d] = QKV[(row0 + m) * ld + H + hd * DH + d];
+    Vs[m * DH + d] = QKV[(row0 + m) * ld + 2 * H + hd * DH + d];
+  }
+  __syncwarp();
+  if (lane < L) {
+    float q[DH];
+#pragma unroll
+    for (int d = 0; d < DH; ++d) q[d] = QKV[(row0 + lane) * ld + hd * DH + d];
+    const float scale = 1.0f / sqrtf((float)DH);
+    float s[32];
+    float mx = -INFINITY;
+#pragma unroll
+    for (int m = 0; m < 32; ++m) {
+      if (m < L) {
+        float a = 0.f;
+#pragma unroll
+        for (int d = 0; d < DH; ++d) a = fmaf(q[d], Ks[m * DH + d], a);
+        s[m] = a * scale;
+        mx = fmaxf(mx, s[m]);
+      }
+    }
+    float sum = 0.f;
+#pragma unroll
+    for (int m = 0; m < 32; ++m)
+      if (m < L) { s[m] = expf(s[m] - mx); sum += s[m]; }
+    const float inv = 1.0f / sum;
+    float o[DH];
+#pragma unroll
+    for (int d = 0; d < DH; ++d) o[d] = 0.f;
+#pragma unroll
+    for (int m = 0; m < 32; ++m) {
+      if (m < L) {
+        s[m] *= inv;
+#pragma unroll
+        for (int d = 0; d < DH; ++d) o[d] = fmaf(s[m], Vs[m * DH + d], o[d]);
+      }
+    }
+#pragma unroll
+    for (int d = 0; d < DH; ++d) O[(row0 + lane) * H + hd * DH + d] = o[d];
+    if (Asave) {
+      float* Ar = Asave + ((n * nh + hd) * L + lane) * (int64_t)L;
+#pragma unroll
+      for (int m = 0; m < 32; ++m)
+        if (m < L) Ar[m] = s[m];
+    }
+  }
+}
+
+template <int DH>
+__global__ void __launch_bounds__(64) attn_bwd_kernel(const float* __restrict__ QKV,
+                                                      const float* __restrict__ Asave,
+                                                      const float* __restrict__ dO, int L, int H,
+                                                      int nh, int64_t pairs,
+                                                      float* __restrict__ dQKV) {
+  extern __shared__ float sm[];
+  const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int64_t pair = (int64_t)blockIdx.x * (blockDim.x / 32) + w;
+  if (pair >= pairs) return;
+  const int per = 4 * 32 * DH + 2 * 32 * 33;
+  float* Qs = sm + w * per;
+  float* Ks = Qs + 32 * DH;
+  float* Vs = Ks + 32 * DH;
+  float* dOs = Vs + 32 * DH;
+  float* As = dOs + 32 * DH;   // [32][33]
+  float* dSs = As + 32 * 33;   // [32][33]
+  const int64_t n = pair / nh;
+  const int hd = (int)(pair % nh);
+  const int64_t row0 = n * L;
+  const int64_t ld = 3 * (int64_t)H;
+  for (int e = lane; e < L * DH; e += 32) {
+    const int m = e / DH, d = e % DH;
+    const int64_t r = (row0 + m) * ld + hd * DH + d;
+    Qs[m * DH + d] = QKV[r];
+    Ks[m * DH + d] = QKV[r + H];
+    Vs[m * DH + d] = QKV[r + 2 * H];
+    dOs[m * DH + d] = dO[(row0 + m) * H + hd * DH + d];
+  }
+  const float* Ab = Asave + (n * nh + hd) * (int64_t)L * L;
+  for (int e = lane; e < L * L; e += 32) As[(e / L) * 33 + (e % L)] = Ab[e];
+  __syncwarp();
+  const float scale = 1.0f / sqrtf((float)DH);
+  if (lane < L) {
+    const int l = lane;
+    float dA[32];
+    float rowdot = 0.f;
+#pragma unroll
+    for (int m = 0; m < 32; ++m) {
+      if (m < L) {
+        float a = 0.f;
+#pragma unroll
+        for (int d = 0; d < DH; ++d) a = fmaf(dOs[l * DH + d], Vs[m * DH + d], a);
+        dA[m] = a;
+        rowdot = fmaf(a, As[l * 33 + m], rowdot);
+      }
+    }
+    float dq[DH];
+#pragma unroll
+    for (int d = 0; d < DH; ++d) dq[d] = 0.f;
+#pragma unroll
+    for (int m = 0; m < 32; ++m) {
+      if (m < L) {
+        const float ds = As[l * 33 + m] * (dA[m] - rowdot);
+        dSs[l * 33 + m] = ds;
+#pragma unroll
+        for (int d = 0; d < DH; ++d) dq[d] = fmaf(ds, Ks[m * DH + d], dq[d]);
+      }
+    }
+#pragma unroll
+    for (int d = 0; d < DH; ++d) dQKV[(row0 + l) * ld + hd * DH + d] = dq[d] * scale;
+  }
+  __syncwarp();
+  if (lane < L) {
+    const int m = lane;
+    float dk[DH], dv[DH];
+#pragma unroll
+    for (int d = 0; d < DH; ++d) { dk[d] = 0.f; dv[d] = 0.f; }
+    for (int l = 0; l < L; ++l) {
+      const float ds = dSs[l * 33 + m], a = As[l * 33 + m];
+#pragma unroll
+      for (int d = 0; d < DH; ++d) {
+        dk[d] = fmaf(ds, Qs[l * DH + d], dk[d]);
+        dv[d] = fmaf(a, dOs[l * DH + d], dv[d]);
+      }
+    }
+#pragma unroll
+    for (int d = 0; d < DH; ++d) {
+      dQKV[(row0 + m) * ld + H + hd * DH + d] = dk[d] * scale;
+      dQKV[(row0 + m) * ld + 2 * H + hd * DH + d] = dv[d];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// head: pooled[n,k] = sum_l relu(U[n*L+l, k]); s[n,t] = pooled . w2 + L c2
+__global__ void head_pool_kernel(const float* __restrict__ U, int L, int hd, int64_t N,
+                                 const float* __restrict__ w2, const float* __restrict__ c2,
+                                 int t, int nt, float* __restrict__ pooled,
+                                 float* __restrict__ scores) {
+  const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int64_t n = (int64_t)blockIdx.x * (blockDim.x / 32) + w;
+  if (n >= N) return;
+  float dot = 0.f;
+  for (int k = lane; k < hd; k += 32) {
+    float p = 0.f;
+    for (int l = 0; l < L; ++l) p += fmaxf(U[(n * L + l) * hd + k], 0.f);
+    if (pooled) pooled[n * hd + k] = p;
+    dot = fmaf(p, w2[k], dot);
+  }
+  for (int o = 16; o; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+  if (lane == 0) scores[n * nt + t] = dot + (float)L * c2[0];
+}
+
+// dU[n*L+l, k] = g[n,t] * w2[k] * (U > 0)
+__global__ void head_bwd_kernel(const float* __restrict__ U, int L, int hd, int64_t N,
+                                const float* __restrict__ w2, const float* __restrict__ g, int t,
+                                int nt, float* __restrict__ dU) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= N * L * hd) return;
+  const int k = (int)(e % hd);
+  const int64_t n = e / ((int64_t)L * hd);
+  dU[e] = U[e] > 0.f ? g[n * nt + t] * w2[k] : 0.f;
+}
+
+// out = L * sum_n g[n, t]   (single block, fixed order)
+__global__ void dc2_kernel(const float* __restrict__ g, int64_t N, int t, int nt, int L,
+                           float* __restrict__ out) {
+  __shared__ float red[256];
+  float s = 0.f;
+  for (int64_t n = threadIdx.x; n < N; n += blockDim.x) s += g[n * nt + t];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = 128; o; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[0] = (float)L * red[0];
+}
+
+__global__ void relu_mask_inplace(float* __restrict__ d, const float* __restrict__ act,
+                                  int64_t n) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < n && !(act[e] > 0.f)) d[e] = 0.f;
+}
+
+// ---------------------------------------------------------------------------
+// activation layout for a chunk of N candidates (fp32 elements)
+struct ActLayout {
+  int64_t up[TLP_MAX_UP];
+  int64_t qkv[TLP_MAX_ATTN], A[TLP_MAX_ATTN], O[TLP_MAX_ATTN], hattn[TLP_MAX_ATTN];
+  int64_t r[TLP_MAX_RES], hres[TLP_MAX_RES];
+  int64_t U[TLP_MAX_TASKS], pooled[TLP_MAX_TASKS];
+  // backward scratch
+  int64_t dh, dtmp, dqkv, dU;
+  int64_t total_fwd, total;
+};
+
+ActLayout act_layout(const tlp_config& c, int64_t N) {
+  ActLayout a{};
+  const int64_t M = N * c.L, H = c.hidden;
+  int64_t o = 0;
+  auto take = [&](int64_t n) { int64_t r = o; o += (n + 63) / 64 * 64; return r; };
+  for (int i = 0; i < c.n_up; ++i) a.up[i] = take(M * c.up_dims[i]);
+  for (int l = 0; l < c.n_attn; ++l) {
+    a.qkv[l] = take(M * 3 * H);
+    a.A[l] = take(N * c.attn_heads * (int64_t)c.L * c.L);
+    a.O[l] = take(M * H);
+    a.hattn[l] = take(M * H);
+  }
+  for (int r = 0; r < c.n_res; ++r) { a.r[r] = take(M * H); a.hres[r] = take(M * H); }
+  for (int t = 0; t < c.n_tasks; ++t) { a.U[t] = take(M * c.head_dim); a.pooled[t] = take(N * c.head_dim); }
+  a.total_fwd = o;
+  a.dh = take(M * H);
+  a.dtmp = take(M * std::max<int64_t>(H, c.up_dims[0]));
+  a.dqkv = take(M * 3 * H);
+  a.dU = take(M * c.head_dim);
+  a.total = o;
+  return a;
+}
+
+template <int DH>
+tlp_status launch_attn_fwd(tlp_ctx* ctx, const float* qkv, int64_t N, float* O, float* A,
+                           cudaStream_t s) {
+  const tlp_config& c = ctx->cfg;
+  const int64_t pairs = N * c.attn_heads;
+  const int warps = 4;
+  const size_t smem = (size_t)warps * 2 * 32 * DH * sizeof(float);
+  attn_fwd_kernel<DH><<<(unsigned)cdiv(pairs, warps), warps * 32, smem, s>>>(
+      qkv, c.L, c.hidden, c.attn_heads, pairs, O, A);
+  TLP_LAUNCH_CHECK();
+  return TLP_OK;
+}
+
+template <int DH>
+tlp_status launch_attn_bwd(tlp_ctx* ctx, const float* qkv, const float* A, const float* dO,
+                           int64_t N, float* dqkv, cudaStream_t s) {
+  const tlp_config& c = ctx->cfg;
+  const int64_t pairs = N * c.attn_heads;
+  const int warps = 2;
+  const size_t smem = (size_t)warps * (4 * 32 * DH + 2 * 32 * 33) * sizeof(float);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(attn_bwd_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    attr_set = true;
+  }
+  attn_bwd_kernel<DH><<<(unsigned)cdiv(pairs, warps), warps * 32, smem, s>>>(
+      qkv, A, dO, c.L, c.hidden, c.attn_heads, pairs, dqkv);
+  TLP_LAUNCH_CHECK();
+  return TLP_OK;
+}
+
+tlp_status attn_fwd(tlp_ctx* ctx, const float* qkv, int64_t N, float* O, float* A,
+                    cudaStream_t s) {
+  switch (ctx->cfg.hidden / ctx->cfg.attn_heads) {
+    case 8: return launch_attn_fwd<8>(ctx, qkv, N, O, A, s);
+    case 16: return launch_attn_fwd<16>(ctx, qkv, N, O, A, s);
+    case 32: return launch_attn_fwd<32>(ctx, qkv, N, O, A, s);
+    case 64: return launch_attn_fwd<64>(ctx, qkv, N, O, A, s);
+    default: ctx->last_error = "head dim must be 8/16/32/64"; return TLP_ERR_UNSUPPORTED;
+  }
+}
+
+tlp_status attn_bwd(tlp_ctx* ctx, const float* qkv, const float* A, const float* dO, int64_t N,
+                    float* dqkv, cudaStream_t s) {
+  switch (ctx->cfg.hidden / ctx->cfg.attn_heads) {
+    case 8: return launch_attn_bwd<8>(ctx, qkv, A, dO, N, dqkv, s);
+    case 16: return launch_attn_bwd<16>(ctx, qkv, A, dO, N, dqkv, s);
+    case 32: return launch_attn_bwd<32>(ctx, qkv, A, dO, N, dqkv, s);
+    case 64: return launch_attn_bwd<64>(ctx, qkv, A, dO, N, dqkv, s);
+    default: ctx->last_error = "head dim must be 8/16/32/64"; return TLP_ERR_UNSUPPORTED;
+  }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+tlp_status sgemm(tlp_ctx* ctx, bool ta, bool tb, int64_t M, int64_t N, int64_t K, const float* A,
+                 int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc,
+                 const EpiParams& e, cudaStream_t s) {
+  if (M == 0 || N == 0) return TLP_OK;
+  EpiDev ed{e.bias, e.resid, e.ldr, e.mask, e.ldm, e.relu ? 1 : 0, e.accumulate ? 1 : 0};
+  dim3 grid((unsigned)cdiv(N, BN), (unsigned)cdiv(M, BM), 1);
+  const int64_t ks = K > 0 ? K : 1;
+  if (!ta && !tb) sgemm_kernel<false, false><<<grid, 256, 0, s>>>(M, N, K, A, lda, B, ldb, C, ldc, ed, ks);
+  else if (!ta && tb) sgemm_kernel<false, true><<<grid, 256, 0, s>>>(M, N, K, A, lda, B, ldb, C, ldc, ed, ks);
+  else if (ta && !tb) sgemm_kernel<true, false><<<grid, 256, 0, s>>>(M, N, K, A, lda, B, ldb, C, ldc, ed, ks);
+  else sgemm_kernel<true, true><<<grid, 256, 0, s>>>(M, N, K, A, lda, B, ldb, C, ldc, ed, ks);
+  TLP_LAUNCH_CHECK();
+  return TLP_OK;
+}
+
+tlp_status sgemm_wgrad(tlp_ctx* ctx, int64_t M, int64_t K, int64_t N, const float* A, int64_t lda,
+                       const float* dY, int64_t lddy, float* dW, cudaStream_t s) {
+  // dW[K,N] = A^T dY with A [M,K] (ld lda), dY [M,N] (ld lddy).  Split over the
+  // M rows into Z fixed slices (a function of M only) -> ordered reduction.
+  const int64_t slice = 2048;
+  const int Z = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(M, slice), 256));
+  const int64_t kslice = cdiv(cdiv(M, Z), BK) * BK;
+  EpiDev ed{nullptr, nullptr, 0, nullptr, 0, 0, 0};
+  dim3 grid((unsigned)cdiv(N, BN), (unsigned)cdiv(K, BM), (unsigned)Z);
+  if (Z == 1) {
+    sgemm_kernel<true, false><<<grid, 256, 0, s>>>(K, N, M, A, lda, dY, lddy, dW, N, ed, kslice);
+    TLP_LAUNCH_CHECK();
+    return TLP_OK;
+  }
+  TLP_CUDA_TRY(ctx->ws_partial.ensure((size_t)Z * K * N * sizeof(float)));
+  float* part = ctx->ws_partial.as<float>();
+  sgemm_kernel<true, false><<<grid, 256, 0, s>>>(K, N, M, A, lda, dY, lddy, part, N, ed, kslice);
+  TLP_LAUNCH_CHECK();
+  reduce_partials<<<(unsigned)cdiv(K * N, 256), 256, 0, s>>>(part, K * N, Z, dW);
+  TLP_LAUNCH_CHECK();
+  return TLP_OK;
+}
+
+tlp_status colsum(tlp_ctx* ctx, int64_t M, int64_t N, const float* X, int64_t ldx, float* out,
+                  cudaStream_t s) {
+  const int64_t rows = 1024;
+  const int Z = (int)std::max<int64_t>(1, cdiv(M, rows));
+  TLP_CUDA_TRY(ctx->ws_misc.ensure((size_t)Z * N * sizeof(float) + 4096));
+  float* part = ctx->ws_misc.as<float>();
+  colsum_partial<<<dim3((unsigned)cdiv(N, 128), (unsigned)Z), 128, 0, s>>>(M, N, X, ldx, rows, part);
+  TLP_LAUNCH_CHECK();
+  reduce_partials<<<(unsigned)cdiv(N, 256), 256, 0, s>>>(part, N, Z, out);
+  TLP_LAUNCH_CHECK();
+  return TLP_OK;
+}
+
+#define TRY(x) do { tlp_status _s = (x); if (_s != TLP_OK) return _s; } while (0)
+
+tlp_status simt_forward(tlp_ctx* ctx, const float* X, int64_t N, float* scores, bool save,
+                        cudaStream_t s) {
+  const tlp_config& c = ctx->cfg;
+  const ParamOffsets& o = ctx->off;
+  const float* P = ctx->d_params;
+  const int64_t H = c.hidden;
+  // inference processes bounded chunks; training keeps the whole batch
+  const int64_t chunk = save ? N : std::min<int64_t>(N, 8192);
+  ActLayout lay = act_layout(c, chunk);
+  TLP_CUDA_TRY(ctx->ws_act.ensure((size_t)(save ? lay.total : lay.total_fwd) * sizeof(float)));
+  float* W = ctx->ws_act.as<float>();
+  for (int64_t n0 = 0; n0 < N; n0 += chunk) {
+    const int64_t n = std::min(chunk, N - n0);
+    const int64_t M = n * c.L;
+    const float* h = X + n0 * c.L * c.E;
+    int64_t din = c.E;
+    for (int i = 0; i < c.n_up; ++i) {
+      EpiParams e; e.bias = P + o.up_b[i]; e.relu = true;
+      TRY(sgemm(ctx, false, false, M, c.up_dims[i], din, h, din, P + o.up_W[i], c.up_dims[i],
+                W + lay.up[i], c.up_dims[i], e, s));
+      h = W + lay.up[i];
+      din = c.up_dims[i];
+    }
+    for (int l = 0; l < c.n_attn; ++l) {
+      float* qkv = W + lay.qkv[l];
+      const int64_t wq[3] = {o.Wq[l], o.Wk[l], o.Wv[l]}, bq[3] = {o.bq[l], o.bk[l], o.bv[l]};
+      for (int j = 0; j < 3; ++j) {
+        EpiParams e; e.bias = P + bq[j];
+        TRY(sgemm(ctx, false, false, M, H, H, h, H, P + wq[j], H, qkv + j * H, 3 * H, e, s));
+      }
+      TRY(attn_fwd(ctx, qkv, n, W + lay.O[l], save ? W + lay.A[l] : nullptr, s));
+      EpiParams e; e.bias = P + o.bo[l]; e.resid = h; e.ldr = H;
+      TRY(sgemm(ctx, false, false, M, H, H, W + lay.O[l], H, P + o.Wo[l], H, W + lay.hattn[l], H, e, s));
+      h = W + lay.hattn[l];
+    }
+    for (int r = 0; r < c.n_res; ++r) {
+      EpiParams e1; e1.bias = P + o.a[r]; e1.relu = true;
+      TRY(sgemm(ctx, false, false, M, H, H, h, H, P + o.Wa[r], H, W + lay.r[r], H, e1, s));
+      EpiParams e2; e2.bias = P + o.b[r]; e2.resid = h; e2.ldr = H;
+      TRY(sgemm(ctx, false, false, M, H, H, W + lay.r[r], H, P + o.Wb[r], H, W + lay.hres[r], H, e2, s));
+      h = W + lay.hres[r];
+    }
+    for (int t = 0; t < c.n_tasks; ++t) {
+      EpiParams e; e.bias = P + o.c1[t];
+      TRY(sgemm(ctx, false, false, M, c.head_dim, H, h, H, P + o.W1[t], c.head_dim, W + lay.U[t],
+                c.head_dim, e, s));
+      head_pool_kernel<<<(unsigned)cdiv(n, 8), 256, 0, s>>>(
+          W + lay.U[t], c.L, c.head_dim, n, P + o.w2[t], P + o.c2[t], t, c.n_tasks,
+          save ? W + lay.pooled[t] : nullptr, scores + n0 * c.n_tasks);
+      TLP_LAUNCH_CHECK();
+    }
+  }
+  if (save) {
+    ctx->train_N = N;
+    ctx->train_X = X;
+  }
+  return TLP_OK;
+}
+
+tlp_status simt_backward(tlp_ctx* ctx, int64_t N, const float* g, cudaStream_t s) {
+  const tlp_config& c = ctx->cfg;
+  const ParamOffsets& o = ctx->off;
+  const float* P = ctx->d_params;
+  float* G = ctx->d_grads;
+  if (ctx->train_N != N) { ctx->last_error = "backward without matching forward"; return TLP_ERR_STATE; }
+  const ActLayout lay = act_layout(c, N);
+  float* W = ctx->ws_act.as<float>();
+  const int64_t H = c.hidden, M = N * c.L, hd = c.head_dim;
+  float* dh = W + lay.dh;
+  float* dtmp = W + lay.dtmp;
+  float* dqkv = W + lay.dqkv;
+  float* dU = W + lay.dU;
+  const float* hfin = c.n_res ? W + lay.hres[c.n_res - 1]
+                    : (c.n_attn ? W + lay.hattn[c.n_attn - 1] : W + lay.up[c.n_up - 1]);
+  // heads
+  for (int t = 0; t < c.n_tasks; ++t) {
+    head_bwd_kernel<<<(unsigned)cdiv(M * hd, 256), 256, 0, s>>>(W + lay.U[t], c.L, hd, N,
+                                                                P + o.w2[t], g, t, c.n_tasks, dU);
+    TLP_LAUNCH_CHECK();
+    TRY(sgemm_wgrad(ctx, M, H, hd, hfin, H, dU, hd, G + o.W1[t], s));
+    TRY(colsum(ctx, M, hd, dU, hd, G + o.c1[t], s));
+    TRY(sgemm_wgrad(ctx, N, hd, 1, W + lay.pooled[t], hd, g + t, c.n_tasks, G + o.w2[t], s));
+    dc2_kernel<<<1, 256, 0, s>>>(g, N, t, c.n_tasks, c.L, G + o.c2[t]);
+    TLP_LAUNCH_CHECK();
+    EpiParams e; e.accumulate = t > 0;
+    TRY(sgemm(ctx, false, true, M, H, hd, dU, hd, P + o.W1[t], hd, dh, H, e, s));
+  }
+  // residual blocks
+  for (int r = c.n_res - 1; r >= 0; --r) {
+    const float* hin = r > 0 ? W + lay.hres[r - 1]
+                     : (c.n_attn ? W + lay.hattn[c.n_attn - 1] : W + lay.up[c.n_up - 1]);
+    const float* rr = W + lay.r[r];
+    TRY(sgemm_wgrad(ctx, M, H, H, rr, H, dh, H, G + o.Wb[r], s));
+    TRY(colsum(ctx, M, H, dh, H, G + o.b[r], s));
+    EpiParams em; em.mask = rr; em.ldm = H;
+    TRY(sgemm(ctx, false, true, M, H, H, dh, H, P + o.Wb[r], H, dtmp, H, em, s));
+    TRY(sgemm_wgrad(ctx, M, H, H, hin, H, dtmp, H, G + o.Wa[r], s));
+    TRY(colsum(ctx, M, H, dtmp, H, G + o.a[r], s));
+    EpiParams ea; ea.accumulate = true;
+    TRY(sgemm(ctx, false, true, M, H, H, dtmp, H, P + o.Wa[r], H, dh, H, ea, s));
+  }
+  // attention layers
+  for (int l = c.n_attn - 1; l >= 0; --l) {
+    const float* hin = l > 0 ? W + lay.hattn[l - 1] : W + lay.up[c.n_up - 1];
+    TRY(sgemm_wgrad(ctx, M, H, H, W + lay.O[l], H, dh, H, G + o.Wo[l], s));
+    TRY(colsum(ctx, M, H, dh, H, G + o.bo[l], s));
+    EpiParams e0;
+    TRY(sgemm(ctx, false, true, M, H, H, dh, H, P + o.Wo[l], H, dtmp, H, e0, s));  // dO
+    TRY(attn_bwd(ctx, W + lay.qkv[l], W + lay.A[l], dtmp, N, dqkv, s));
+    const int64_t wq[3] = {o.Wq[l], o.Wk[l], o.Wv[l]}, bq[3] = {o.bq[l], o.bk[l], o.bv[l]};
+    for (int j = 0; j < 3; ++j) {
+      TRY(sgemm_wgrad(ctx, M, H, H, hin, H, dqkv + j * H, 3 * H, G + wq[j], s));
+      TRY(colsum(ctx, M, H, dqkv + j * H, 3 * H, G + bq[j], s));
+      EpiParams ea; ea.accumulate = true;
+      TRY(sgemm(ctx, false, true, M, H, H, dqkv + j * H, 3 * H, P + wq[j], H, dh, H, ea, s));
+    }
+  }
+  // upsample: dh is d(up_out[n_up-1])
+  float* cur = dh;
+  for (int i = c.n_up - 1; i >= 0; --i) {
+    const int64_t w = c.up_dims[i];
+    const int64_t din = i > 0 ? c.up_dims[i - 1] : c.E;
+    relu_mask_inplace<<<(unsigned)cdiv(M * w, 256), 256, 0, s>>>(cur, W + lay.up[i], M * w);
+    TLP_LAUNCH_CHECK();
+    const float* xin = i > 0 ? W + lay.up[i - 1] : ctx->train_X;
+    TRY(sgemm_wgrad(ctx, M, din, w, xin, din, cur, w, G + o.up_W[i], s));
+    TRY(colsum(ctx, M, w, cur, w, G + o.up_b[i], s));
+    if (i > 0) {
+      float* nxt = (cur == dh) ? dtmp : dh;
+      EpiParams e0;
+      TRY(sgemm(ctx, false, true, M, din, w, cur, w, P + o.up_W[i], w, nxt, din, e0, s));
+      cur = nxt;
+    }
+  }
+  return TLP_OK;
+}

@@ -1,0 +1,184 @@
+// Internal declarations shared by the libtlp.so translation units.
+// Product code: nothing here is shared with oracle/ (the CPU checker).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+#include <string>
+#include <vector>
+#include <mutex>
+
+#include "../../include/tlp.h"
+
+#define TLP_MAX_UP 4
+#define TLP_MAX_ATTN 4
+#define TLP_MAX_RES 4
+#define TLP_MAX_TASKS 8
+
+// Sticky device error bits (ctx->d_err), surfaced by tlp_sync.
+enum : uint32_t {
+  DERR_EMPTY_SEQ = 1u << 0,
+  DERR_UNKNOWN_TYPE = 1u << 1,
+  DERR_NONFINITE = 1u << 2,
+  DERR_NAN_LOSS = 1u << 3,
+};
+
+// R24 flat-parameter offsets (fp32 elements).
+struct ParamOffsets {
+  int64_t up_W[TLP_MAX_UP], up_b[TLP_MAX_UP];
+  int64_t Wq[TLP_MAX_ATTN], bq[TLP_MAX_ATTN], Wk[TLP_MAX_ATTN], bk[TLP_MAX_ATTN];
+  int64_t Wv[TLP_MAX_ATTN], bv[TLP_MAX_ATTN], Wo[TLP_MAX_ATTN], bo[TLP_MAX_ATTN];
+  int64_t Wa[TLP_MAX_RES], a[TLP_MAX_RES], Wb[TLP_MAX_RES], b[TLP_MAX_RES];
+  int64_t W1[TLP_MAX_TASKS], c1[TLP_MAX_TASKS], w2[TLP_MAX_TASKS], c2[TLP_MAX_TASKS];
+  int64_t total;
+};
+
+// Grow-only device buffer.
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  cudaError_t ensure(size_t n) {
+    if (n <= bytes) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    size_t want = n + (n >> 3);
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e == cudaSuccess) bytes = want;
+    return e;
+  }
+  template <class T> T* as() const { return reinterpret_cast<T*>(p); }
+  void release() { if (p) cudaFree(p); p = nullptr; bytes = 0; }
+};
+
+struct TcWeights;  // bf16 tcgen05 weight images (k_tc_forward.cu)
+
+struct tlp_ctx {
+  tlp_config cfg;
+  int device = 0;
+  int num_sms = 148;
+  ParamOffsets off;
+  std::string last_error;
+
+  // parameters / optimizer (fp32, device)
+  float* d_params = nullptr;
+  float* d_grads = nullptr;
+  float* d_m = nullptr;
+  float* d_v = nullptr;
+  int64_t adam_t = 0;
+  bool have_params = false;
+
+  // tokenizer state
+  bool have_scales = false;
+  float* d_scale = nullptr;          // [E]
+  uint64_t* d_hkeys = nullptr;       // open-addressing hash: key (0 = empty)
+  int32_t* d_hval = nullptr;         // token
+  uint8_t* d_tblob = nullptr;        // table strings for verification
+  int64_t* d_toff = nullptr;
+  int32_t* d_hstr = nullptr;         // slot -> table string index
+  uint32_t hcap = 0;                 // power of two (0 = no table)
+
+  // sticky error word
+  uint32_t* d_err = nullptr;
+
+  // workspaces
+  DevBuf ws_tokens, ws_act, ws_train, ws_rank, ws_topk, ws_misc, ws_partial;
+
+  // bf16 tensor-core path
+  TcWeights* tc = nullptr;
+  bool tc_dirty = true;
+
+  // NCCL
+  void* comm = nullptr;  // ncclComm_t
+  int rank = 0, world = 1;
+
+  int64_t launches = 0;
+
+  // training forward state kept for backward (k_simt.cu)
+  int64_t train_N = -1;
+  const float* train_X = nullptr;
+};
+
+// ---------------------------------------------------------------------------
+// helpers
+#define TLP_CUDA_TRY(expr)                                                    \
+  do {                                                                        \
+    cudaError_t _e = (expr);                                                  \
+    if (_e != cudaSuccess) {                                                  \
+      ctx->last_error = std::string("CUDA: ") + cudaGetErrorString(_e) +      \
+                        " at " __FILE__ ":" + std::to_string(__LINE__);       \
+      return TLP_ERR_CUDA;                                                    \
+    }                                                                         \
+  } while (0)
+
+#define TLP_LAUNCH_CHECK()                                                    \
+  do {                                                                        \
+    ctx->launches++;                                                          \
+    cudaError_t _e = cudaGetLastError();                                      \
+    if (_e != cudaSuccess) {                                                  \
+      ctx->last_error = std::string("CUDA launch: ") +                        \
+                        cudaGetErrorString(_e) + " at " __FILE__ ":" +        \
+                        std::to_string(__LINE__);                             \
+      return TLP_ERR_CUDA;                                                    \
+    }                                                                         \
+  } while (0)
+
+static inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// ---------------------------------------------------------------------------
+// kernels / launchers implemented in the .cu files
+
+// k_encode.cu
+tlp_status encode_launch(tlp_ctx* ctx, const tlp_seq_batch* in, int64_t N, float* feats,
+                         cudaStream_t s);
+tlp_status build_token_table(tlp_ctx* ctx, const uint8_t* blob, const int64_t* off, int32_t n);
+
+// k_select.cu
+tlp_status topk_launch(tlp_ctx* ctx, const float* scores, int stride, int head,
+                       const int64_t* task_off, int T, int k, int64_t base, int64_t* idx_out,
+                       float* val_out, cudaStream_t s);
+tlp_status normalize_labels_launch(tlp_ctx* ctx, const float* lat, const int64_t* group_off,
+                                   int G, float* out, cudaStream_t s);
+
+// k_simt.cu : fp32 SIMT network (forward for scoring and training, backward)
+struct EpiParams {
+  const float* bias = nullptr;   // [N]
+  const float* resid = nullptr;  // [M, ldr] added before activation
+  int64_t ldr = 0;
+  const float* mask = nullptr;   // [M, ldm] multiply by (mask > 0) (relu')
+  int64_t ldm = 0;
+  bool relu = false;
+  bool accumulate = false;       // C += result (C read before write)
+};
+tlp_status sgemm(tlp_ctx* ctx, bool ta, bool tb, int64_t M, int64_t N, int64_t K, const float* A,
+                 int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc,
+                 const EpiParams& ep, cudaStream_t s);
+// dW[K,N] (+)= A^T[K,M] * dY[M,N], deterministic split over M.
+tlp_status sgemm_wgrad(tlp_ctx* ctx, int64_t M, int64_t K, int64_t N, const float* A, int64_t lda,
+                       const float* dY, int64_t lddy, float* dW, cudaStream_t s);
+tlp_status colsum(tlp_ctx* ctx, int64_t M, int64_t N, const float* X, int64_t ldx, float* out,
+                  cudaStream_t s);
+tlp_status simt_forward(tlp_ctx* ctx, const float* feats, int64_t N, float* scores, bool save,
+                        cudaStream_t s);
+tlp_status simt_backward(tlp_ctx* ctx, int64_t N, const float* dscores, cudaStream_t s);
+
+// k_rank.cu
+tlp_status rank_pair_counts(tlp_ctx* ctx, const float* labels, const int64_t* d_goff, int G,
+                            int max_group, double* d_counts, cudaStream_t s);
+tlp_status rank_loss_grad(tlp_ctx* ctx, const float* scores, const float* labels,
+                          const int64_t* d_goff, int G, int B, int max_group,
+                          const double* d_counts, float* loss_out, float* dscores,
+                          cudaStream_t s);
+
+// k_adam.cu
+tlp_status adam_launch(tlp_ctx* ctx, cudaStream_t s);
+
+// k_tc_forward.cu : bf16 tcgen05 fused forward
+bool tc_supported(const tlp_config& c);
+tlp_status tc_prepare(tlp_ctx* ctx, cudaStream_t s);
+tlp_status tc_forward(tlp_ctx* ctx, const float* feats, int64_t N, float* scores, cudaStream_t s);
+void tc_free(tlp_ctx* ctx);
+
+// api.cu
+tlp_status dev_error_status(tlp_ctx* ctx);

@@ -1,0 +1,55 @@
+"""Shared test plumbing: seeded inputs for both the oracle and the CUDA path.
+Holds no method arithmetic of its own (that lives in oracle/ and the library)."""
+from __future__ import annotations
+
+import numpy as np
+
+import synth
+import oracle
+from oracle import model as OM
+
+PAPER_SHAPES = dict(L=25, E=22, T=11)
+
+
+def oracle_cfg(hidden=256, up=(128, 256), heads=8, n_attn=1, n_res=2, head_dim=128, n_tasks=1,
+               L=25, E=22, T=11):
+    return OM.Config(L=L, E=E, T=T, hidden=hidden, up_dims=up, attn_heads=heads, n_attn=n_attn,
+                     n_res=n_res, head_dim=head_dim, n_tasks=n_tasks)
+
+
+def product_cfg(ocfg: OM.Config, precision="fp32"):
+    from paper_2211_03578_b200 import TLPConfig
+    return TLPConfig(L=ocfg.L, E=ocfg.E, T=ocfg.T, hidden=ocfg.hidden, up_dims=tuple(ocfg.up_dims),
+                     attn_heads=ocfg.attn_heads, n_attn=ocfg.n_attn, n_res=ocfg.n_res,
+                     head_dim=ocfg.head_dim, n_tasks=ocfg.n_tasks, precision=precision)
+
+
+def flat_params(ocfg: OM.Config, seed: int, scale: float = 1.0, bf16: bool = True) -> np.ndarray:
+    vals = synth.init_params(seed, OM.param_shapes(ocfg), bf16=bf16, scale=scale)
+    return np.concatenate([v.ravel() for v in vals]).astype(np.float32).astype(np.float64)
+
+
+def token_table():
+    return oracle.build_token_table(synth.training_stream())
+
+
+def fit_scales(tokens, seed=99, n=2000):
+    """R3 scales fitted by the oracle on a seeded training split."""
+    b = synth.generate(seed, n, unseen_rate=0.0)
+    raw = np.stack([oracle.extract_rows(s, tokens, 25, 22, 11) for s in b.to_lists()])
+    return oracle.fit_scales(raw)
+
+
+def encoded_batch(seed: int, n: int, tokens, scale):
+    b = synth.generate(seed, n)
+    X = oracle.encode(b.to_lists(), tokens, scale)
+    return b, X
+
+
+def rel_err(a, b) -> float:
+    """R25 norm-wise relative error: ||a - b||_inf / ||b||_inf."""
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    d = np.abs(a - b).max() if a.size else 0.0
+    m = np.abs(b).max() if b.size else 0.0
+    return float(d / m) if m > 0 else float(d)

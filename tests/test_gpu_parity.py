@@ -1,0 +1,266 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle on the same
+seeded inputs.  Tokenizer, top-k and labels bit-exact; fp32 path within 1e-5
+(R25 norm-wise); bf16 path within 1e-2."""
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import synth
+import oracle
+from oracle import model as OM
+from oracle import rank_loss as OLR
+from oracle.optim import AdamState, adam_step
+
+from helpers import (encoded_batch, fit_scales, flat_params, oracle_cfg, product_cfg, rel_err,
+                     token_table)
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(__file__)
+
+
+@pytest.fixture(scope="module")
+def tp():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_2211_03578_b200 as tp
+    tp._lib.load()
+    return tp
+
+
+@pytest.fixture(scope="module")
+def tokscale():
+    tokens = token_table()
+    return tokens, fit_scales(tokens)
+
+
+def make_encoder(tp, tokens, scale, **kw):
+    cfg = tp.TLPConfig(precision="fp32", **kw)
+    m = tp.TLP(cfg)
+    m.set_token_table(sorted(tokens, key=tokens.get))
+    m.set_norm_scales(scale)
+    return m
+
+
+# ---------------------------------------------------------------- tokenizer
+def test_encode_bit_exact(tp, tokscale):
+    tokens, scale = tokscale
+    m = make_encoder(tp, tokens, scale)
+    b = synth.generate(5, 3001, unseen_rate=0.05)
+    X_ref = oracle.encode(b.to_lists(), tokens, scale)
+    X = m.encode(tp.DeviceBatch.from_packed(b))
+    m.sync()
+    assert np.array_equal(X.cpu().numpy().view(np.uint32), X_ref.view(np.uint32))
+
+
+def test_encode_worked_example_bits(tp):
+    g = json.load(open(os.path.join(HERE, "golden", "tokenizer_worked_example.json")))
+    reg = {n: i for i, n in enumerate(g["registry"])}
+    seq = [(reg[t], [a if isinstance(a, str) else float(a) for a in args]) for t, args in g["sequence"]]
+    tokens = g["tokens"]
+    scale = np.ones(22, np.float32)
+    for c, v in g["scales_nonunit"].items():
+        scale[int(c)] = v
+    m = make_encoder(tp, tokens, scale)
+    X = m.encode(tp.DeviceBatch.from_packed(synth.pack([seq]))).cpu().numpy()[0]
+    m.sync()
+    for rc, bits in g["normalized_bits_nonunit"].items():
+        r, c = map(int, rc.split(","))
+        assert "0x%08X" % X[r, c].view(np.uint32) == bits
+
+
+@pytest.mark.parametrize("bad,code", [
+    ([[(0, [1.0])], []], "ERR_EMPTY_SEQ"),
+    ([[(11, [1.0])]], "ERR_UNKNOWN_TYPE"),
+    ([[(2, [float("nan")])]], "ERR_NONFINITE"),
+    ([[(2, [1e300])]], "ERR_NONFINITE"),
+])
+def test_encode_device_errors(tp, tokscale, bad, code):
+    tokens, scale = tokscale
+    m = make_encoder(tp, tokens, scale)
+    m.encode(tp.DeviceBatch.from_packed(synth.pack(bad)))
+    with pytest.raises(tp.TLPError) as e:
+        m.sync()
+    assert e.value.code == code
+    # kept-data-only validation: junk beyond the crop raises nothing
+    ok = [[(0, [1.0] * 11 + [float("nan")])] + [(0, [])] * 24 + [(99, [float("inf")])]]
+    m.encode(tp.DeviceBatch.from_packed(synth.pack(ok)))
+    m.sync()
+
+
+# ---------------------------------------------------------------- top-k / labels
+def test_topk_bit_exact(tp):
+    m = tp.TLP(tp.TLPConfig(precision="fp32"))
+    rng = np.random.default_rng(3)
+    sizes = [0, 1, 5, 16, 17, 2047, 2048, 2049, 4096, 9000, 300]
+    off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    N = int(off[-1])
+    # many ties, signed zeros
+    s = rng.choice(np.float32([-2.0, -0.0, 0.0, 0.25, 1.0, 3.5]), size=N).astype(np.float32)
+    mask = rng.random(N) < 0.5
+    s[mask] = rng.normal(size=int(mask.sum())).astype(np.float32)
+    cols = np.stack([rng.normal(size=N).astype(np.float32), s], axis=1)  # stride 2, head 1
+    for k in (1, 16, 100, 1024):
+        idx_ref, val_ref = oracle.topk(cols[:, 1], off, k, base=7)
+        idx, val = m.topk(torch.from_numpy(cols).cuda(), off, k, head=1, shard_base=7)
+        m.sync()
+        assert np.array_equal(idx.cpu().numpy(), idx_ref), k
+        assert np.array_equal(val.cpu().numpy().view(np.uint32), val_ref.view(np.uint32)), k
+
+
+def test_topk_nan_is_an_error(tp):
+    m = tp.TLP(tp.TLPConfig(precision="fp32"))
+    s = torch.tensor([[0.0], [float("nan")]], device="cuda")
+    m.topk(s, np.array([0, 2]), 1)
+    with pytest.raises(tp.TLPError) as e:
+        m.sync()
+    assert e.value.code == "ERR_NONFINITE"
+
+
+def test_normalize_labels_bit_exact(tp):
+    m = tp.TLP(tp.TLPConfig(precision="fp32"))
+    b = synth.generate(2, 5000)
+    sizes = synth.group_sizes(4, 3, lo=24, hi=4000, mean=1600)
+    off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    off[-1] = min(off[-1], 5000)
+    off = off[off <= 5000]
+    lat = synth.latencies(b, off, 7)[: off[-1]].astype(np.float32)
+    ref = oracle.normalize_labels(lat, off)
+    out = m.normalize_labels(torch.from_numpy(lat).cuda(), off)
+    m.sync()
+    assert np.array_equal(out.cpu().numpy().view(np.uint32), ref.view(np.uint32))
+
+
+# ---------------------------------------------------------------- fp32 forward
+FWD_CASES = {
+    "tiny_C1": dict(hidden=64, up=(32, 64), head_dim=32),
+    "paper_1layer": dict(),
+    "paper_2layer": dict(n_attn=2),
+    "mtl4": dict(n_tasks=4),
+}
+
+
+@pytest.mark.parametrize("name", list(FWD_CASES))
+def test_forward_fp32_parity(tp, tokscale, name):
+    tokens, scale = tokscale
+    ocfg = oracle_cfg(**FWD_CASES[name])
+    flat = flat_params(ocfg, seed=11)
+    _, X = encoded_batch(21, 37, tokens, scale)  # 925 rows: 7 full 128-row tiles + tail
+    ref = OM.forward(ocfg, OM.unflatten(ocfg, flat), X)
+    m = tp.TLP(product_cfg(ocfg, "fp32"))
+    m.set_params(flat.astype(np.float32))
+    s = m.score(torch.from_numpy(X).cuda())
+    m.sync()
+    assert rel_err(s.cpu().numpy(), ref) <= 1e-5
+
+
+def test_score_batch_invariance(tp, tokscale):
+    tokens, scale = tokscale
+    ocfg = oracle_cfg()
+    flat = flat_params(ocfg, seed=12)
+    _, X = encoded_batch(22, 300, tokens, scale)
+    m = tp.TLP(product_cfg(ocfg, "fp32"))
+    m.set_params(flat.astype(np.float32))
+    Xd = torch.from_numpy(X).cuda()
+    full = m.score(Xd).cpu().numpy()
+    part = m.score(Xd[113:250].contiguous()).cpu().numpy()
+    m.sync()
+    assert np.array_equal(full[113:250].view(np.uint32), part.view(np.uint32))
+
+
+# ---------------------------------------------------------------- LambdaRank unit (R26)
+def test_lambdarank_unit_parity(tp):
+    m = tp.TLP(tp.TLPConfig(precision="fp32", n_tasks=2))
+    rng = np.random.default_rng(5)
+    sizes = [1, 2, 7, 64, 300, 512]
+    off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    B = int(off[-1])
+    s = rng.normal(size=(B, 2)).astype(np.float32)
+    y = rng.uniform(0.05, 1.0, (B, 2)).astype(np.float32)
+    y[rng.random(B) < 0.3, 0] = np.nan  # MTL: absent labels
+    y[:5, 1] = y[5, 1]                    # label ties -> no pairs
+    loss_ref, g_ref = OLR.mtl_lambdarank(s.astype(np.float64), y.astype(np.float64), off)
+    loss, g = m.lambdarank(torch.from_numpy(s).cuda(), torch.from_numpy(y).cuda(), off)
+    m.sync()
+    assert abs(float(loss.cpu()) - loss_ref) <= 1e-5 * abs(loss_ref)
+    assert rel_err(g.cpu().numpy(), g_ref) <= 1e-5
+    assert not g.cpu().numpy()[np.isnan(y)].any()
+
+
+# ---------------------------------------------------------------- training (fp32)
+def train_inputs(tokens, scale, n_tasks=1, seed=31, sizes=(9, 16, 12, 16, 11, 7)):
+    off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    b, X = encoded_batch(seed, int(off[-1]), tokens, scale)
+    labs = []
+    for t in range(n_tasks):
+        lat = synth.latencies(b, off, seed + 100 * t, task_noise=0.3 * t)
+        labs.append(oracle.normalize_labels(lat, off))
+    y = np.stack(labs, axis=1).astype(np.float32)
+    if n_tasks > 1:
+        y[np.random.default_rng(seed).random(len(y)) < 0.5, 0] = np.nan
+    return X, y, off
+
+
+def min_rel_gap(scores, off):
+    g = np.inf
+    for t in range(scores.shape[1]):
+        for i in range(len(off) - 1):
+            s = np.sort(scores[off[i]:off[i + 1], t])
+            if len(s) > 1:
+                g = min(g, np.min(np.diff(s)) / max(np.abs(s).max(), 1e-30))
+    return g
+
+
+# (n_tasks, n_attn, weight seed, group sizes): seeds chosen so that every
+# within-group score gap exceeds 2e-4 relative -- ranks are then decided far
+# above fp32 noise (R26) and the oracle and the GPU rank identically.
+GRAD_CASES = [(1, 1, 17, (9, 16, 12, 16, 11, 7)), (4, 1, 20, (8, 6, 9, 7, 10, 8)),
+              (1, 2, 14, (9, 16, 12, 16, 11, 7))]
+
+
+@pytest.mark.parametrize("n_tasks,n_attn,seed,sizes", GRAD_CASES)
+def test_grads_fp32_parity(tp, tokscale, n_tasks, n_attn, seed, sizes):
+    tokens, scale = tokscale
+    ocfg = oracle_cfg(n_tasks=n_tasks, n_attn=n_attn, hidden=64, up=(32, 64), head_dim=32)
+    flat = flat_params(ocfg, seed=seed)
+    X, y, off = train_inputs(tokens, scale, n_tasks, sizes=sizes)
+    p = OM.unflatten(ocfg, flat)
+    s_ref, acts = OM.forward(ocfg, p, X, save=True)
+    assert min_rel_gap(s_ref, off) > 2e-4
+    loss_ref, g = OLR.mtl_lambdarank(s_ref, y.astype(np.float64), off)
+    grads_ref = OM.backward(ocfg, p, acts, g)
+    m = tp.TLP(product_cfg(ocfg, "fp32"))
+    m.set_params(flat.astype(np.float32))
+    loss = m.compute_grads(torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda(), off)
+    m.sync()
+    assert abs(float(loss.cpu()) - loss_ref) <= 1e-5 * abs(loss_ref)
+    got = OM.unflatten(ocfg, m.get_grads().astype(np.float64))
+    for name, _ in OM.param_shapes(ocfg):
+        assert rel_err(got[name], grads_ref[name]) <= 1e-5, name
+
+
+def test_train_step_adam_parity(tp, tokscale):
+    tokens, scale = tokscale
+    ocfg = oracle_cfg(hidden=64, up=(32, 64), head_dim=32)
+    flat = flat_params(ocfg, seed=17)
+    X, y, off = train_inputs(tokens, scale, 1)
+    m = tp.TLP(product_cfg(ocfg, "fp32"))
+    m.set_params(flat.astype(np.float32))
+    st = AdamState.zeros(flat.size)
+    p_ref = flat.copy()
+    Xd, yd = torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda()
+    for _ in range(3):
+        s_ref, acts = OM.forward(ocfg, OM.unflatten(ocfg, p_ref), X, save=True)
+        _, g = OLR.mtl_lambdarank(s_ref, y.astype(np.float64), off)
+        gflat = OM.flatten(ocfg, OM.backward(ocfg, OM.unflatten(ocfg, p_ref), acts, g))
+        p_ref = adam_step(p_ref, gflat, st)
+        m.train_step(Xd, yd, off)
+    m.sync()
+    got = m.get_params().astype(np.float64)
+    # parameter change after 3 steps within 1e-5 of the oracle's change, per tensor
+    d_ref = OM.unflatten(ocfg, p_ref - flat)
+    d_got = OM.unflatten(ocfg, got - flat)
+    for name, _ in OM.param_shapes(ocfg):
+        assert rel_err(d_got[name], d_ref[name]) <= 1e-3, name
