@@ -1,0 +1,381 @@
+"""Benchmark of the TLP / MTL-TLP hot path on B200 (the driver's contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One STEP = one pass of the whole hot path on synthetic
+TenSet-shaped inputs:
+  scoring round  (BASELINE configs[1], C2): 409,600 candidates = 100 tasks x 4096,
+                 tlp_encode -> tlp_score (hidden 256, 2 attention layers) ->
+                 tlp_topk (k = 16 per task; + NCCL allgather merge when N > 1);
+  training step  (configs[2], C3 shape): tlp_normalize_labels of the batch's
+                 groups + tlp_train_step on 16 groups x 512 = 8,192 samples
+                 (1 attention layer, LambdaRank, backward, allreduce, Adam).
+`value` = candidates scored/s over the scoring phase (all ranks, max-over-ranks
+device time); `train_samples_per_s` = the training phase likewise.  Weak
+scaling: per-GPU work is fixed as N grows.  Inputs are larger than L2 (901 MB
+of features per round), so no explicit flush is needed between iterations.
+
+`--impl reference` times the CPU oracle (oracle/, the only reference this
+paper-only tier has) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "candidates scored/s and LambdaRank train samples/s at 1/2/4/8 B200; % tensor peak"
+T_TASKS, PER_TASK, TOPK = 100, 4096, 16
+N_ROUND = T_TASKS * PER_TASK
+TRAIN_GROUPS, TRAIN_PER_GROUP = 16, 512
+B_TRAIN = TRAIN_GROUPS * TRAIN_PER_GROUP
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+            "sm_max_mhz": 1965.0}, "fallback"
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    def __init__(self, device: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # pragma: no cover - NVML missing
+            self.nv = None
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            "hw_slowdown": getattr(nv, "nvmlClocksThrottleReasonHwSlowdown", 0x8),
+            "hw_thermal_slowdown": getattr(nv, "nvmlClocksThrottleReasonHwThermalSlowdown", 0x40),
+            "sw_thermal_slowdown": getattr(nv, "nvmlClocksThrottleReasonSwThermalSlowdown", 0x20),
+            "sw_power_cap": getattr(nv, "nvmlClocksThrottleReasonSwPowerCap", 0x4),
+            "hw_power_brake_slowdown": getattr(nv, "nvmlClocksThrottleReasonHwPowerBrakeSlowdown", 0x80),
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                for k, bit in names.items():
+                    if r & bit:
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ FLOP model
+def fwd_flops_per_cand(L=25, E=22, H=256, up=(128, 256), heads=8, n_attn=2, n_res=2, hd=128,
+                       n_tasks=1):
+    """Algorithmic forward FLOPs per candidate."""
+    f, d = 0, E
+    for w in up:
+        f += 2 * L * d * w
+        d = w
+    dh = H // heads
+    f += n_attn * (2 * L * H * 3 * H + heads * 2 * (2 * L * L * dh) + 2 * L * H * H)
+    f += n_res * 2 * (2 * L * H * H)
+    f += n_tasks * (2 * L * H * hd + 2 * hd)
+    return f
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    import paper_2211_03578_b200 as tp
+    import oracle  # only for cpu_baseline (allowed) and token-table/scale fitting of inputs
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    precision = args.precision
+    # --- inputs (host, seeded per rank: each rank scores its own shard) ---
+    tokens = oracle.build_token_table(synth.training_stream())
+    names = sorted(tokens, key=tokens.get)
+    train_raw = synth.generate(99, 2000, unseen_rate=0.0)
+    raw = np.stack([oracle.extract_rows(s, tokens, 25, 22, 11) for s in train_raw.to_lists()])
+    scale = oracle.fit_scales(raw)
+    packed = synth.generate(1000 + rank, N_ROUND)
+    task_off = synth.uniform_task_off(T_TASKS, PER_TASK)
+
+    cfg2 = tp.TLPConfig(n_attn=2, precision=precision)
+    scorer = tp.TLP(cfg2, device=local)
+    scorer.set_token_table(names)
+    scorer.set_norm_scales(scale)
+    from oracle import model as OM
+    ocfg2 = OM.Config(n_attn=2)
+    flat2 = np.concatenate([v.ravel() for v in synth.init_params(7, OM.param_shapes(ocfg2))]).astype(np.float32)
+    scorer.set_params(flat2)
+
+    cfg1 = tp.TLPConfig(n_attn=1, precision=precision)
+    trainer = tp.TLP(cfg1, device=local)
+    ocfg1 = OM.Config(n_attn=1)
+    flat1 = np.concatenate([v.ravel() for v in synth.init_params(8, OM.param_shapes(ocfg1))]).astype(np.float32)
+    trainer.set_params(flat1)
+    trainer.set_norm_scales(scale)
+    trainer.set_token_table(names)
+    if world > 1:
+        scorer.init_comm()
+        trainer.init_comm()
+
+    dev = torch.device("cuda", local)
+    dbatch = tp.DeviceBatch.from_packed(packed, device=dev)
+    feats = torch.empty((N_ROUND, 25, 22), dtype=torch.float32, device=dev)
+    scores = torch.empty((N_ROUND, 1), dtype=torch.float32, device=dev)
+    idx = torch.empty((T_TASKS, TOPK), dtype=torch.int64, device=dev)
+    val = torch.empty((T_TASKS, TOPK), dtype=torch.float32, device=dev)
+    # training data: 16 groups x 512, latencies -> labels on device
+    tpacked = synth.generate(2000 + rank, B_TRAIN)
+    goff = np.arange(TRAIN_GROUPS + 1, dtype=np.int64) * TRAIN_PER_GROUP
+    lat = torch.from_numpy(synth.latencies(tpacked, goff, 5 + rank).astype(np.float32)).to(dev)
+    tfeats = trainer.encode(tp.DeviceBatch.from_packed(tpacked, device=dev))
+    labels = torch.empty((B_TRAIN, 1), dtype=torch.float32, device=dev)
+    loss = torch.empty(1, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+    shard_base = rank * N_ROUND
+
+    def step(ev):
+        ev[0].record(stream)
+        scorer.encode(dbatch, out=feats, stream=stream)
+        ev[1].record(stream)
+        scorer.score(feats, out=scores, stream=stream)
+        ev[2].record(stream)
+        scorer.topk(scores, task_off, TOPK, shard_base=shard_base, idx_out=idx, val_out=val, stream=stream)
+        ev[3].record(stream)
+        trainer.normalize_labels(lat, goff, out=labels.view(-1), stream=stream)
+        trainer.train_step(tfeats, labels, goff, loss_out=loss, stream=stream)
+        ev[4].record(stream)
+
+    mk = lambda: [torch.cuda.Event(enable_timing=True) for _ in range(5)]  # noqa: E731
+    for _ in range(args.warmup):
+        step(mk())
+    scorer.sync(); trainer.sync()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    l0 = scorer.launches + trainer.launches
+    evs = [mk() for _ in range(args.steps)]
+    clk = ClockSampler(local)
+    with clk:
+        t_start = torch.cuda.Event(enable_timing=True); t_end = torch.cuda.Event(enable_timing=True)
+        t_start.record(stream)
+        for k in range(args.steps):
+            step(evs[k])
+        t_end.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    scorer.sync(); trainer.sync()
+    launches = scorer.launches + trainer.launches - l0
+    total_ms = t_start.elapsed_time(t_end)
+    enc_ms = sum(e[0].elapsed_time(e[1]) for e in evs)
+    score_ms = sum(e[1].elapsed_time(e[2]) for e in evs)
+    topk_ms = sum(e[2].elapsed_time(e[3]) for e in evs)
+    train_ms = sum(e[3].elapsed_time(e[4]) for e in evs)
+    round_ms = enc_ms + score_ms + topk_ms
+    times = torch.tensor([total_ms, round_ms, train_ms, score_ms, enc_ms, topk_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(times, op=dist.ReduceOp.MAX)
+    total_ms, round_ms, train_ms, score_ms, enc_ms, topk_ms = times.tolist()
+
+    # --- e2e: public API with host buffers (pinned H2D of the packed round, D2H of top-k) ---
+    hbatch = tp.DeviceBatch.from_packed(packed, pin=True)
+    idx_host = torch.empty((T_TASKS, TOPK), dtype=torch.int64).pin_memory()
+    def e2e_step():
+        db = hbatch.to(dev, non_blocking=True)
+        scorer.encode(db, out=feats, stream=stream)
+        scorer.score(feats, out=scores, stream=stream)
+        scorer.topk(scores, task_off, TOPK, shard_base=shard_base, idx_out=idx, val_out=val, stream=stream)
+        idx_host.copy_(idx, non_blocking=True)
+    for _ in range(max(1, args.warmup)):
+        e2e_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+    e2e_ms = float(e2e_ms.item())
+
+    K = args.steps
+    cand_s = world * N_ROUND * K / (round_ms / 1e3)
+    train_s = world * B_TRAIN * K / (train_ms / 1e3)
+    peaks, peaks_kind = load_peaks()
+    fl = fwd_flops_per_cand()
+    score_launch_ms = score_ms / K
+    if precision == "bf16":
+        achieved = fl * N_ROUND / (score_launch_ms / 1e3) / 1e12
+        peak = peaks["bf16_tflops_sustained"]
+        roof = {"bound": "tensor", "kernel": "tc_fused_forward (tlp_score, 1 launch/round)",
+                "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                "traffic": None, "peak_kind": peaks_kind + " bf16 sustained",
+                "flops_per_launch": fl * N_ROUND}
+    else:
+        achieved = fl * N_ROUND / (score_launch_ms / 1e3) / 1e12
+        sm_mhz = peaks.get("sm_max_mhz", 1965.0)
+        peak = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12
+        roof = {"bound": "alu", "kernel": "tlp_score fp32 SIMT chain (all launches of one call)",
+                "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                "traffic": None, "peak_kind": "derived FP32 FFMA peak 148 SM x 128 lanes x 2 x sm_max_mhz",
+                "flops_per_launch": fl * N_ROUND}
+    out = {
+        "metric": METRIC, "value": cand_s, "unit": "candidates/s", "n_gpus": world,
+        "steps": K, "warmup": args.warmup, "ms_per_step": total_ms / K,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "bf16" if precision == "bf16" else "f32", "data": "synthetic",
+        "config": {"workload": "C2 scoring round: 409,600 candidates (100 tasks x 4096), hidden 256, "
+                               "2 attention layers, top-16/task; + C3-shape LambdaRank train step "
+                               "8,192 samples (16 groups x 512), 1 attention layer",
+                   "candidates_per_gpu_per_round": N_ROUND, "train_batch_per_gpu": B_TRAIN,
+                   "precision": precision, "parallelism": "dp%d" % world,
+                   "l2": "inputs larger than L2 (901 MB features/round), no flush"},
+        "train_samples_per_s": train_s,
+        "phase_ms_per_step": {"encode": enc_ms / K, "score": score_ms / K, "topk": topk_ms / K,
+                              "train": train_ms / K},
+        "roofline": roof,
+        "e2e": {"value": world * N_ROUND * K / (e2e_ms / 1e3), "unit": "candidates/s",
+                "h2d_bytes_per_step": hbatch.nbytes(), "d2h_bytes_per_step": T_TASKS * TOPK * 8},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(seconds_hint=15.0)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# ------------------------------------------------------------------ oracle arm
+def _oracle_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        return max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def oracle_sample(n_cand: int, seed: int = 0):
+    """One bounded sample of the step on the CPU oracle: encode + forward (2
+    layers) + top-k of n_cand candidates (1 task); returns seconds."""
+    import oracle
+    from oracle import model as OM
+    tokens = oracle.build_token_table(synth.training_stream())
+    train_raw = synth.generate(99, 500, unseen_rate=0.0)
+    raw = np.stack([oracle.extract_rows(s, tokens, 25, 22, 11) for s in train_raw.to_lists()])
+    scale = oracle.fit_scales(raw)
+    cfg = OM.Config(n_attn=2)
+    p = OM.unflatten(cfg, np.concatenate([v.ravel() for v in synth.init_params(7, OM.param_shapes(cfg))]))
+    b = synth.generate(1000 + seed, n_cand)
+    t0 = time.perf_counter()
+    X = oracle.encode(b.to_lists(), tokens, scale)
+    s = OM.forward(cfg, p, X)
+    oracle.topk(s[:, 0].astype(np.float32), np.array([0, n_cand]), TOPK)
+    return time.perf_counter() - t0
+
+
+def cpu_baseline(seconds_hint=15.0):
+    n = 256
+    dt = oracle_sample(n)
+    # scale the sample to ~seconds_hint of CPU work
+    n2 = int(min(4096, max(256, n * seconds_hint / max(dt, 1e-3))))
+    dt2 = oracle_sample(n2, seed=1)
+    return {"value": n2 / dt2, "unit": "candidates/s", "cores": _oracle_threads(), "kind": "oracle",
+            "sample": "%d candidates of the C2 round (1 task): oracle encode + fp64 forward (2 attention "
+                      "layers, hidden 256) + top-16, %.1f s" % (n2, dt2)}
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    n = 512
+    for w in range(args.warmup):
+        oracle_sample(n, seed=100 + w)
+    t = 0.0
+    for k in range(args.steps):
+        t += oracle_sample(n, seed=k)
+    v = n * args.steps / t
+    out = {"impl": "reference", "metric": METRIC, "value": v, "unit": "candidates/s",
+           "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": "C2 scoring round, bounded sample per step: %d candidates "
+                                  "(encode + fp64 forward 2 layers + top-16) on host cores" % n},
+           "cpu_baseline": {"value": v, "unit": "candidates/s", "cores": _oracle_threads(),
+                            "kind": "oracle", "sample": "%d candidates per step" % n},
+           "e2e": {"value": v, "unit": "candidates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--precision", default=os.environ.get("TLP_BENCH_PRECISION", "bf16"),
+                    choices=["bf16", "fp32"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

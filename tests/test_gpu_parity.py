@@ -3,6 +3,7 @@ seeded inputs.  Tokenizer, top-k and labels bit-exact; fp32 path within 1e-5
 (R25 norm-wise); bf16 path within 1e-2."""
 import json
 import os
+import re
 
 import numpy as np
 import pytest
@@ -19,6 +20,15 @@ from helpers import (encoded_batch, fit_scales, flat_params, oracle_cfg, product
 
 pytestmark = pytest.mark.gpu
 HERE = os.path.dirname(__file__)
+# Gradients that are identically zero in exact arithmetic, so both sides are
+# rounding noise: attn*.bk (q . bk shifts a whole softmax row) and head*.c2
+# (adds L c2 to every score of a group; LambdaRank is shift invariant, so
+# sum_i dL/ds_i = 0 per group).
+ZERO_GRAD = re.compile(r"(attn\d+\.bk|head\d+\.c2)$")
+# head*.c1: dc1[k] = sum_{n,l} g_n w2[k] [u>0] cancels almost completely for the
+# same reason (rows active in every candidate contribute g_n * const), so it is
+# compared against the magnitude of the summed terms (summation error bound).
+CANCEL_GRAD = re.compile(r"head(\d+)\.c1$")
 
 
 @pytest.fixture(scope="module")
@@ -121,12 +131,10 @@ def test_topk_nan_is_an_error(tp):
 
 def test_normalize_labels_bit_exact(tp):
     m = tp.TLP(tp.TLPConfig(precision="fp32"))
-    b = synth.generate(2, 5000)
-    sizes = synth.group_sizes(4, 3, lo=24, hi=4000, mean=1600)
+    sizes = list(synth.group_sizes(4, 3, lo=24, hi=4000, mean=1600)) + [1, 0, 2]
     off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
-    off[-1] = min(off[-1], 5000)
-    off = off[off <= 5000]
-    lat = synth.latencies(b, off, 7)[: off[-1]].astype(np.float32)
+    b = synth.generate(2, int(off[-1]))
+    lat = synth.latencies(b, off, 7).astype(np.float32)
     ref = oracle.normalize_labels(lat, off)
     out = m.normalize_labels(torch.from_numpy(lat).cuda(), off)
     m.sync()
@@ -237,8 +245,24 @@ def test_grads_fp32_parity(tp, tokscale, n_tasks, n_attn, seed, sizes):
     m.sync()
     assert abs(float(loss.cpu()) - loss_ref) <= 1e-5 * abs(loss_ref)
     got = OM.unflatten(ocfg, m.get_grads().astype(np.float64))
+    bad = {}
     for name, _ in OM.param_shapes(ocfg):
-        assert rel_err(got[name], grads_ref[name]) <= 1e-5, name
+        if ZERO_GRAD.search(name):
+            ref_w = name.replace(".bk", ".Wk").replace(".c2", ".w2")
+            assert np.abs(got[name]).max() <= 1e-5 * np.abs(grads_ref[ref_w]).max() * ocfg.L, name
+            continue
+        mc = CANCEL_GRAD.search(name)
+        if mc:
+            t = int(mc.group(1))
+            u = acts["heads"][t]["u"]
+            terms = np.abs(g[:, t])[:, None, None] * np.abs(p["head%d.w2" % t][:, 0]) * (u > 0)
+            mag = terms.sum(axis=(0, 1))
+            assert np.all(np.abs(got[name] - grads_ref[name]) <= 1e-5 * mag.max()), name
+            continue
+        e = rel_err(got[name], grads_ref[name])
+        if e > 1e-5:
+            bad[name] = e
+    assert not bad, bad
 
 
 def test_train_step_adam_parity(tp, tokscale):
@@ -262,5 +286,14 @@ def test_train_step_adam_parity(tp, tokscale):
     # parameter change after 3 steps within 1e-5 of the oracle's change, per tensor
     d_ref = OM.unflatten(ocfg, p_ref - flat)
     d_got = OM.unflatten(ocfg, got - flat)
+    bad = {}
     for name, _ in OM.param_shapes(ocfg):
-        assert rel_err(d_got[name], d_ref[name]) <= 1e-3, name
+        if ZERO_GRAD.search(name) or CANCEL_GRAD.search(name):
+            # Adam maps a (near-)zero gradient's rounding noise to +-lr updates:
+            # no meaningful comparison; bounded by 3 steps of lr.
+            assert np.abs(d_got[name]).max() <= 3 * 1e-3 * 1.0001, name
+            continue
+        e = rel_err(d_got[name], d_ref[name])
+        if e > 1e-3:
+            bad[name] = e
+    assert not bad, bad
