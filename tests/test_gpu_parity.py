@@ -291,9 +291,97 @@ def test_train_step_adam_parity(tp, tokscale):
         if ZERO_GRAD.search(name) or CANCEL_GRAD.search(name):
             # Adam maps a (near-)zero gradient's rounding noise to +-lr updates:
             # no meaningful comparison; bounded by 3 steps of lr.
-            assert np.abs(d_got[name]).max() <= 3 * 1e-3 * 1.0001, name
+            # |Adam step| <= lr (1-b1)/sqrt(1-b2) ~ 3.17 lr per step
+            assert np.abs(d_got[name]).max() <= 3 * 3.17e-3, name
             continue
         e = rel_err(d_got[name], d_ref[name])
         if e > 1e-3:
             bad[name] = e
     assert not bad, bad
+
+
+# ---------------------------------------------------------------- bf16 tcgen05 path
+@pytest.mark.parametrize("N,K", [(16, 16), (96, 64), (160, 32), (32, 160), (256, 256)])
+def test_umma_building_block(tp, N, K):
+    """One tcgen05.mma chain (descriptors, TMEM, tcgen05.ld) vs an fp64 matmul of
+    the same bf16-rounded operands: products are exact, accumulation fp32."""
+    rng = np.random.default_rng(N * 1000 + K)
+    A = synth.bf16_round(rng.normal(size=(128, K))).astype(np.float32)
+    B = synth.bf16_round(rng.normal(size=(N, K))).astype(np.float32)
+    D = torch.zeros((128, N), dtype=torch.float32, device="cuda")
+    lib = tp._lib.load()
+    Ad, Bd = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()  # keep alive until sync
+    st = lib.tlp_debug_umma(Ad.data_ptr(), Bd.data_ptr(), D.data_ptr(), N, K,
+                            torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert st == 0
+    ref = A.astype(np.float64) @ B.astype(np.float64).T
+    assert rel_err(D.cpu().numpy(), ref) <= 1e-5
+
+
+BF16_CASES = {"paper_1layer": dict(), "paper_2layer": dict(n_attn=2), "mtl4": dict(n_tasks=4),
+              "no_res": dict(n_res=0), "no_attn": dict(n_attn=0)}
+
+
+@pytest.mark.parametrize("name", list(BF16_CASES))
+def test_forward_bf16_parity(tp, tokscale, name):
+    tokens, scale = tokscale
+    ocfg = oracle_cfg(**BF16_CASES[name])
+    flat = flat_params(ocfg, seed=11)
+    _, X = encoded_batch(23, 301, tokens, scale)  # 61 tiles of 5 candidates, last one ragged
+    ref = OM.forward(ocfg, OM.unflatten(ocfg, flat), X)
+    m = tp.TLP(product_cfg(ocfg, "bf16"))
+    m.set_params(flat.astype(np.float32))
+    s = m.score(torch.from_numpy(X).cuda())
+    m.sync()
+    assert rel_err(s.cpu().numpy(), ref) <= 1e-2
+
+
+def test_bf16_batch_invariance_and_retrain_refresh(tp, tokscale):
+    tokens, scale = tokscale
+    ocfg = oracle_cfg(n_attn=2)
+    flat = flat_params(ocfg, seed=12)
+    _, X = encoded_batch(24, 300, tokens, scale)
+    m = tp.TLP(product_cfg(ocfg, "bf16"))
+    m.set_params(flat.astype(np.float32))
+    Xd = torch.from_numpy(X).cuda()
+    full = m.score(Xd).cpu().numpy()
+    for lo, hi in ((113, 250), (1, 2), (7, 300)):  # slots shift by lo mod 5
+        part = m.score(Xd[lo:hi].contiguous()).cpu().numpy()
+        assert np.array_equal(full[lo:hi].view(np.uint32), part.view(np.uint32)), (lo, hi)
+    # new parameters must re-pack the bf16 weight stream
+    flat2 = flat_params(ocfg, seed=13)
+    m.set_params(flat2.astype(np.float32))
+    s2 = m.score(Xd).cpu().numpy()
+    m.sync()
+    assert rel_err(s2, OM.forward(ocfg, OM.unflatten(ocfg, flat2), X)) <= 1e-2
+
+
+def test_bf16_full_size_sampled(tp, tokscale):
+    """C2 at full size in bench.py's launch configuration: 409,600 candidates
+    (100 tasks x 4096), 2 layers, one tlp_score call; a seeded sample of 64
+    candidates is checked against the oracle one by one; top-16 of every task
+    equals the oracle top-k of the GPU's own scores (bit-exact selection)."""
+    tokens, scale = tokscale
+    ocfg = oracle_cfg(n_attn=2)
+    flat = flat_params(ocfg, seed=7)
+    N = 100 * 4096
+    b = synth.generate(1000, N)
+    m = tp.TLP(product_cfg(ocfg, "bf16"))
+    m.set_token_table(sorted(tokens, key=tokens.get))
+    m.set_norm_scales(scale)
+    m.set_params(flat.astype(np.float32))
+    X = m.encode(tp.DeviceBatch.from_packed(b))
+    s = m.score(X)
+    off = synth.uniform_task_off(100, 4096)
+    idx, val = m.topk(s, off, 16)
+    m.sync()
+    s_h = s.cpu().numpy()
+    rng = np.random.default_rng(0)
+    pick = np.sort(rng.choice(N, 64, replace=False))
+    Xs = oracle.encode([b.slice(int(i), int(i) + 1).to_lists()[0] for i in pick], tokens, scale)
+    assert np.array_equal(X[torch.from_numpy(pick).cuda()].cpu().numpy().view(np.uint32), Xs.view(np.uint32))
+    ref = OM.forward(ocfg, OM.unflatten(ocfg, flat), Xs)
+    assert rel_err(s_h[pick], ref) <= 1e-2
+    idx_ref, val_ref = oracle.topk(s_h[:, 0], off, 16)
+    assert np.array_equal(idx.cpu().numpy(), idx_ref)
