@@ -203,8 +203,10 @@ int64_t tlp_launch_count(const tlp_ctx* ctx);
 /* Test hook for the tensor-core building block (not part of the hot path):
  * D[128, N] = bf16(A)[128, K] * bf16(B)[N, K]^T with fp32 accumulation through
  * one tcgen05.mma chain (UMMA descriptors, TMEM, tcgen05.ld).  A, B, D fp32
- * device row-major; 16 <= N <= 256, N % 16 == 0; 16 <= K <= 256, K % 16 == 0. */
-tlp_status tlp_debug_umma(const float* A, const float* B, float* D, int32_t N, int32_t K, void* stream);
+ * device row-major; 16 <= N <= 256, N % 16 == 0; 32 <= K <= 256, K % 32 == 0.
+ * a_in_tmem != 0: A is staged in TMEM with tcgen05.st and read from there. */
+tlp_status tlp_debug_umma(const float* A, const float* B, float* D, int32_t N, int32_t K,
+                          int32_t a_in_tmem, void* stream);
 
 #ifdef __cplusplus
 }

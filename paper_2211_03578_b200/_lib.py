@@ -71,7 +71,7 @@ def load() -> C.CDLL:
         "tlp_normalize_labels": (C.c_int, [vp, vp, vp, i32, vp, vp]),
         "tlp_sync": (C.c_int, [vp]),
         "tlp_launch_count": (i64, [vp]),
-        "tlp_debug_umma": (C.c_int, [vp, vp, vp, i32, i32, vp]),
+        "tlp_debug_umma": (C.c_int, [vp, vp, vp, i32, i32, i32, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)

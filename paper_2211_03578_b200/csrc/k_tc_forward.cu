@@ -2,32 +2,36 @@
 //
 // One persistent CTA per SM walks tiles of 5 candidates = 125 rows (+3 pad
 // rows) = one M=128 UMMA tile, and runs the WHOLE network on chip for the tile
-// (readings R8-R14, R28 in DESIGN.md):
+// (readings R8-R14, R28, R33, R34 in DESIGN.md):
 //   X (fp32 [5,25,22] from HBM) -> bf16 smem
-//   h = relu(relu(X W1 + b1) W2 + b2)                          2 GEMMs
+//   U1 = relu(X W1 + b1)            -> bf16 in TMEM (A operand of the next GEMM)
+//   h  = relu(U1 W2 + b2)           -> bf16 smem (A operand + residual stream)
 //   per attention layer, per head j (8 heads, d_h = 32):
-//     [Q_j|K_j|V_j] = h W_qkv_j + b                             GEMM N=96
-//     S_j = Q_j K_j^T  (block-diagonal: 5 candidates x 32 padded keys) GEMM N=160
-//     P_j = softmax(S_j / sqrt(32)) over the candidate's 25 keys (fp32, epilogue)
-//     O_j = P_j V_j                                             GEMM N=32, K=160
-//     acc += O_j Wo[32j:32j+32, :]                              GEMM (accumulated in TMEM)
+//     [Q_j|K_j|V_j] = h W_qkv_j + b                          GEMM N=96 (issued one head ahead)
+//     S_j = Q_j K_j^T   keys at padded positions 32*slot+kk  GEMM N=160
+//     P_j = softmax(S_j / sqrt(32)) over the candidate's 25 keys, written
+//           in place over S_j in TMEM as bf16                 (epilogue, fp32 math)
+//     O_j = P_j V_j     (A = P_j from TMEM, K = 160)         GEMM N=32
+//     acc += O_j Wo[32j:32j+32, :]                            GEMM (accumulated in TMEM)
 //   h = h + acc + bo
-//   per residual block: h = h + relu(h Wa + a) Wb + b           4 GEMMs (N-split halves)
-//   per task t: s_t = sum_l relu(h_l W1_t + c1_t) . w2_t + 25 c2_t   GEMM + row dot + ordered sum
-// Only X (2,200 B/candidate) is read and n_tasks floats written per candidate;
-// all activations stay in SMEM/TMEM.  Weights (bf16, pre-packed in UMMA
-// canonical layout in consumption order) stream from L2 through a 3-stage
-// ring of 16 KB stages filled by 1-D bulk TMA (cp.async.bulk).
+//   per residual block: r = relu(h Wa + a) in two N-halves (bf16 in TMEM as the
+//     A operand), h = h + r Wb + b
+//   per task t: s_t = sum_l relu(h_l W1_t + c1_t) . w2_t + 25 c2_t (fixed-order row sum)
+// Only X (2,200 B/candidate) is read from HBM and n_tasks floats are written.
+// Weights (bf16, UMMA canonical layout, consumption order) stream from L2
+// through a 6-stage x 16 KB ring filled by 1-D bulk TMA (cp.async.bulk);
+// biases / w2 / c2 are staged once per CTA in shared memory.
 //
 // Warp roles: warp 0 = TMA producer (one lane), warp 1 = tcgen05.mma issuer
 // (one lane) and TMEM owner, warps 2..5 = epilogue (thread = tile row = TMEM
-// lane).  MMA -> epilogue: tcgen05.commit on `acc_bar`; epilogue -> MMA:
-// 128 arrivals on `opnd_bar` after fence.proxy.async.
+// lane).  MMA -> epilogue: tcgen05.commit on one of four mbarriers (acc, qkv,
+// s, pv) so that the QKV GEMM of head j+1 overlaps the softmax of head j;
+// epilogue -> MMA: 128 arrivals on `opnd` after fence.proxy.async / wait::st.
 //
-// Batch invariance: a candidate's keys sit at K positions 32*slot..32*slot+24
-// (zero padded to 32), so the PV accumulation grouping is identical for every
-// slot; every other step is row-local and the final 25-row sum runs in a fixed
-// order.  Scores therefore do not depend on the batch size or tile placement.
+// Batch invariance (R34): a candidate's keys sit at K positions
+// 32*slot..32*slot+24 (zero padded to 32), so the PV accumulation grouping is
+// identical for every slot; everything else is row-local and the 25-row head
+// sum runs in a fixed order.
 #include "tlp_internal.cuh"
 #include "tc_ptx.cuh"
 
@@ -42,29 +46,31 @@ constexpr int kL = 25, kE = 22, kH = 256, kHeads = 8, kDH = 32, kHD = 128;
 constexpr int kCand = 5;            // candidates per tile
 constexpr int kKX = 32;             // padded K of the first GEMM (22 -> 32)
 constexpr int kKP = 160;            // padded key positions (5 x 32)
-constexpr int kStages = 3;
+constexpr int kStages = 6;
 constexpr uint32_t kStageBytes = 16384;
 constexpr int kThreads = 192;
 
 // shared memory map (bytes)
-constexpr uint32_t OFF_H = 0;                              // h        [128 x 256] bf16, Kt=256
-constexpr uint32_t OFF_R = OFF_H + 65536;                  // X / U1 / r-half [128 x <=128]
-constexpr uint32_t OFF_Q = OFF_R + 32768;                  // Q_j      [128 x 32]
-constexpr uint32_t OFF_K = OFF_Q + 8192;                   // K_j      [160 x 32]  (B operand)
-constexpr uint32_t OFF_V = OFF_K + 10240;                  // V_j^T    [32 x 160]  (B operand)
-constexpr uint32_t OFF_P = OFF_V + 10240;                  // P_j      [128 x 160]
-constexpr uint32_t OFF_O = OFF_P + 40960;                  // O_j      [128 x 32]
-constexpr uint32_t OFF_RING = OFF_O + 8192;                // 3 x 16 KB weight stages
-constexpr uint32_t OFF_DOT = OFF_RING + kStages * kStageBytes;  // 128 fp32 row dots
-constexpr uint32_t OFF_BAR = OFF_DOT + 512;                // 2*kStages + 2 mbarriers
-constexpr uint32_t OFF_TPTR = OFF_BAR + 8 * (2 * kStages + 2);
-constexpr uint32_t SMEM_BYTES = OFF_TPTR + 16;
-static_assert(SMEM_BYTES <= 232448, "smem budget");
+constexpr uint32_t OFF_H = 0;                       // h      [128 x 256] bf16, Kt=256
+constexpr uint32_t OFF_X = OFF_H + 65536;           // X      [128 x 32]
+constexpr uint32_t OFF_Q = OFF_X + 8192;            // Q_j    [128 x 32]
+constexpr uint32_t OFF_O = OFF_Q + 8192;            // O_j    [128 x 32]
+constexpr uint32_t OFF_K = OFF_O + 8192;            // K_j    [160 x 32]  (B operand, padded keys)
+constexpr uint32_t OFF_V = OFF_K + 10240;           // V_j^T  [32 x 160]  (B operand)
+constexpr uint32_t OFF_DOT = OFF_V + 10240;         // 128 fp32 row dots
+constexpr uint32_t OFF_BAR = OFF_DOT + 512;         // mbarriers (<= 32)
+constexpr uint32_t OFF_TPTR = OFF_BAR + 256;
+constexpr uint32_t OFF_RING = OFF_TPTR + 128;       // kStages x 16 KB
+constexpr uint32_t OFF_VEC = OFF_RING + kStages * kStageBytes;  // epilogue vectors (fp32)
+constexpr uint32_t kMaxSmem = 232448;
+static_assert(OFF_RING % 128 == 0, "ring alignment");
 
 // TMEM column map (512 allocated)
-constexpr uint32_t T_A = 0;    // 256: up / oproj / residual-block / output accumulators
-constexpr uint32_t T_B = 256;  // 160: QKV_j, then S_j; resblock halves; head
-constexpr uint32_t T_O = 416;  // 32:  O_j
+constexpr uint32_t T_A = 0;    // 256: up1 / sum_j O_j Wo_j / residual-block output accumulators
+constexpr uint32_t T_B = 256;  // 160: up0, S_j -> P_j (bf16, cols 0..79) + O_j (cols 96..127),
+                               //      residual-block first GEMM halves, head
+constexpr uint32_t T_Q = 416;  // 96:  QKV_j accumulator; bf16 A operands U1 / r-half (64 cols)
+constexpr uint32_t T_PO = 96;  // O_j offset inside T_B
 
 struct ChunkRef {
   uint32_t off16;  // byte offset / 16 into the weight stream
@@ -79,7 +85,8 @@ struct TcArgs {
   const uint8_t* wstream;
   const ChunkRef* chunks;
   int nchunks;
-  const float* P;  // fp32 parameters (biases / w2 / c2 read by the epilogue)
+  const float* vec;  // epilogue vectors (aligned slots), staged into smem
+  int vec_floats;
   int64_t up_b0, up_b1;
   int64_t bq[TLP_MAX_ATTN], bk[TLP_MAX_ATTN], bv[TLP_MAX_ATTN], bo[TLP_MAX_ATTN];
   int64_t ra[TLP_MAX_RES], rb[TLP_MAX_RES];
@@ -97,22 +104,40 @@ __device__ __forceinline__ void store_row32(uint8_t* smem, uint32_t base, uint32
   }
 }
 
-__device__ __forceinline__ void load_bias32(const float* __restrict__ b, float (&o)[32]) {
+// 32 consecutive fp32 from shared memory (same address across the warp: broadcast)
+__device__ __forceinline__ void vec32(const float* v, float (&o)[32]) {
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
-    const float4 v = __ldg(reinterpret_cast<const float4*>(b) + i);
-    o[4 * i] = v.x; o[4 * i + 1] = v.y; o[4 * i + 2] = v.z; o[4 * i + 3] = v.w;
+    const float4 x = reinterpret_cast<const float4*>(v)[i];
+    o[4 * i] = x.x; o[4 * i + 1] = x.y; o[4 * i + 2] = x.z; o[4 * i + 3] = x.w;
   }
 }
 
-// relu(acc[c0..c0+ncol) + bias) -> bf16 operand (row r, k = c0..)
-__device__ __forceinline__ void epi_bias_relu(uint8_t* smem, uint32_t tl, uint32_t tcol,
-                                              int ncol, const float* bias, uint32_t dst,
-                                              uint32_t Kt, uint32_t r) {
+// relu(acc + bias) -> bf16 A operand in TMEM (two bf16 per column)
+__device__ __forceinline__ void epi_relu_to_tmem(uint32_t tl, uint32_t src, int ncol,
+                                                 const float* bias, uint32_t dst) {
   for (int c = 0; c < ncol; c += 32) {
     float v[32], b[32];
-    tc::tmem_ld32(tl + tcol + c, v);
-    load_bias32(bias + c, b);
+    tc::tmem_ld32(tl + src + c, v);
+    vec32(bias + c, b);
+    tc::tmem_wait_ld();
+    uint32_t pk[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      pk[i] = tc::pack_bf16(fmaxf(v[2 * i] + b[2 * i], 0.f), fmaxf(v[2 * i + 1] + b[2 * i + 1], 0.f));
+    tc::tmem_st16(tl + dst + c / 2, pk);
+  }
+  tc::tmem_wait_st();
+}
+
+// relu(acc + bias) -> bf16 smem operand (row r)
+__device__ __forceinline__ void epi_relu_to_smem(uint8_t* smem, uint32_t tl, uint32_t src,
+                                                 int ncol, const float* bias, uint32_t dst,
+                                                 uint32_t Kt, uint32_t r) {
+  for (int c = 0; c < ncol; c += 32) {
+    float v[32], b[32];
+    tc::tmem_ld32(tl + src + c, v);
+    vec32(bias + c, b);
     tc::tmem_wait_ld();
     uint32_t pk[16];
 #pragma unroll
@@ -122,13 +147,13 @@ __device__ __forceinline__ void epi_bias_relu(uint8_t* smem, uint32_t tl, uint32
   }
 }
 
-// h[r, :] = bf16(h[r, :] + acc[r, :] + bias)   (R10 / R12 residual)
+// h[r, :] = bf16(h[r, :] + acc[r, :] + bias)   (R10 / R12 residual, R33)
 __device__ __forceinline__ void epi_residual(uint8_t* smem, uint32_t tl, const float* bias,
                                              uint32_t r) {
   for (int c = 0; c < kH; c += 32) {
     float v[32], b[32];
     tc::tmem_ld32(tl + T_A + c, v);
-    load_bias32(bias + c, b);
+    vec32(bias + c, b);
     uint4 old[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
@@ -150,21 +175,30 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
   extern __shared__ __align__(128) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t sbase = tc::smem_u32(smem);
-  const uint32_t bar_full = sbase + OFF_BAR;               // kStages
-  const uint32_t bar_empty = bar_full + 8 * kStages;       // kStages
-  const uint32_t bar_acc = bar_empty + 8 * kStages;
-  const uint32_t bar_opnd = bar_acc + 8;
+  const uint32_t bar_full = sbase + OFF_BAR;             // kStages
+  const uint32_t bar_empty = bar_full + 8 * kStages;     // kStages
+  const uint32_t bar_acc = bar_empty + 8 * kStages;      // generic GEMM done
+  const uint32_t bar_qkv = bar_acc + 8;                  // QKV_j done
+  const uint32_t bar_s = bar_qkv + 8;                    // S_j done
+  const uint32_t bar_pv = bar_s + 8;                     // O_j done
+  const uint32_t bar_opnd = bar_pv + 8;                  // epilogue -> MMA (128 arrivals)
   uint32_t* tptr = reinterpret_cast<uint32_t*>(smem + OFF_TPTR);
+  float* vs = reinterpret_cast<float*>(smem + OFF_VEC);
 
-  // zero the attention operand buffers once: their pad entries must stay 0
-  for (uint32_t o = OFF_K + threadIdx.x * 16; o < OFF_O; o += kThreads * 16)
+  // V_j^T and K_j pad entries must stay exactly 0 / finite: zero them once.
+  for (uint32_t o = OFF_K + threadIdx.x * 16; o < OFF_DOT; o += kThreads * 16)
     *reinterpret_cast<uint4*>(smem + o) = make_uint4(0, 0, 0, 0);
+  for (int i = threadIdx.x; i < a.vec_floats / 4; i += kThreads)
+    reinterpret_cast<float4*>(vs)[i] = __ldg(reinterpret_cast<const float4*>(a.vec) + i);
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       tc::mbar_init(bar_full + 8 * s, 1);
       tc::mbar_init(bar_empty + 8 * s, 1);
     }
     tc::mbar_init(bar_acc, 1);
+    tc::mbar_init(bar_qkv, 1);
+    tc::mbar_init(bar_s, 1);
+    tc::mbar_init(bar_pv, 1);
     tc::mbar_init(bar_opnd, 128);
     tc::fence_barrier_init();
   }
@@ -202,9 +236,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
         op_phase ^= 1;
         tc::tc_fence_after();
       };
-      // D (+)= A[smem, Kt=a_kt] x (ring chunks of N x Kc)^T over K
-      auto gemm_w = [&](uint32_t a_off, uint32_t a_kt, uint32_t d_col, uint32_t N, int K, int Kc,
-                        bool acc) {
+      // D (+)= A x (ring chunks of N x Kc)^T over K.  A in smem (a_tmem == 0:
+      // canonical layout with Kt = a_kt at a_off) or in TMEM (column a_off).
+      auto gemm_w = [&](bool a_tmem, uint32_t a_off, uint32_t a_kt, uint32_t d_col, uint32_t N,
+                        int K, int Kc, bool acc) {
         const uint32_t idesc = tc::idesc_bf16(128, N);
         for (int kc = 0; kc < K; kc += Kc) {
           tc::mbar_wait(bar_full + 8 * stage, phase);
@@ -212,55 +247,76 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
           const uint32_t b = sbase + OFF_RING + stage * kStageBytes;
 #pragma unroll 4
           for (int ks = 0; ks < Kc; ks += 16) {
-            const uint64_t ad = tc::smem_desc(sbase + a_off + ((kc + ks) >> 3) * 128, 128, a_kt * 16);
             const uint64_t bd = tc::smem_desc(b + (ks >> 3) * 128, 128, Kc * 16);
-            tc::mma_bf16(tmem + d_col, ad, bd, idesc, (acc || kc + ks > 0) ? 1u : 0u);
+            const uint32_t en = (acc || kc + ks > 0) ? 1u : 0u;
+            if (a_tmem)
+              tc::mma_bf16_ta(tmem + d_col, tmem + a_off + ((kc + ks) >> 1), bd, idesc, en);
+            else
+              tc::mma_bf16(tmem + d_col,
+                           tc::smem_desc(sbase + a_off + ((kc + ks) >> 3) * 128, 128, a_kt * 16),
+                           bd, idesc, en);
           }
           tc::mma_commit(bar_empty + 8 * stage);
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
       };
-      // D = A[smem] x B[smem]^T (both operands produced on chip)
-      auto gemm_s = [&](uint32_t a_off, uint32_t a_kt, uint32_t b_off, uint32_t b_kt,
-                        uint32_t d_col, uint32_t N, int K) {
-        const uint32_t idesc = tc::idesc_bf16(128, N);
-        for (int ks = 0; ks < K; ks += 16) {
-          const uint64_t ad = tc::smem_desc(sbase + a_off + (ks >> 3) * 128, 128, a_kt * 16);
-          const uint64_t bd = tc::smem_desc(sbase + b_off + (ks >> 3) * 128, 128, b_kt * 16);
-          tc::mma_bf16(tmem + d_col, ad, bd, idesc, ks > 0 ? 1u : 0u);
-        }
-      };
-      auto done = [&]() { tc::mma_commit(bar_acc); };
       for (int64_t tile = blockIdx.x; tile < a.ntile; tile += gridDim.x) {
-        wait_opnd();                                             // X
-        gemm_w(OFF_R, kKX, T_A, 128, kKX, 32, false); done();    // upsample 0
-        wait_opnd();                                             // U1
-        gemm_w(OFF_R, 128, T_A, kH, 128, 32, false); done();     // upsample 1
-        wait_opnd();                                             // h
+        wait_opnd();                                                      // E0: X
+        gemm_w(false, OFF_X, kKX, T_B, 128, kKX, 32, false);              // up0 -> T_B
+        tc::mma_commit(bar_acc);
+        wait_opnd();                                                      // E1: U1 -> T_Q (bf16)
+        gemm_w(true, T_Q, 0, T_A, kH, 128, 32, false);                    // up1 -> T_A
+        tc::mma_commit(bar_acc);
+        wait_opnd();                                                      // E2: h
         for (int l = 0; l < NA; ++l) {
+          gemm_w(false, OFF_H, kH, T_Q, 96, kH, 64, false);               // QKV_0
+          tc::mma_commit(bar_qkv);
+          wait_opnd();                                                    // E_qkv_0
           for (int j = 0; j < kHeads; ++j) {
-            if (j > 0) gemm_w(OFF_O, kDH, T_A, kH, kDH, 32, j > 1);   // oproj_{j-1}
-            gemm_w(OFF_H, kH, T_B, 96, kH, 64, false); done();        // QKV_j
-            wait_opnd();
-            gemm_s(OFF_Q, kDH, OFF_K, kDH, T_B, kKP, kDH); done();    // S_j
-            wait_opnd();
-            gemm_s(OFF_P, kKP, OFF_V, kKP, T_O, kDH, kKP); done();    // O_j = P_j V_j
-            wait_opnd();
+            {                                                             // S_j = Q_j K_j^T
+              const uint32_t idesc = tc::idesc_bf16(128, kKP);
+              for (int ks = 0; ks < kDH; ks += 16)
+                tc::mma_bf16(tmem + T_B,
+                             tc::smem_desc(sbase + OFF_Q + (ks >> 3) * 128, 128, kDH * 16),
+                             tc::smem_desc(sbase + OFF_K + (ks >> 3) * 128, 128, kDH * 16), idesc,
+                             ks > 0);
+              tc::mma_commit(bar_s);
+            }
+            if (j + 1 < kHeads) {                                          // QKV_{j+1} (T_Q free)
+              gemm_w(false, OFF_H, kH, T_Q, 96, kH, 64, false);
+              tc::mma_commit(bar_qkv);
+            }
+            wait_opnd();                                                  // E_soft_j: P_j in TMEM
+            {                                                             // O_j = P_j V_j
+              const uint32_t idesc = tc::idesc_bf16(128, kDH);
+              for (int ks = 0; ks < kKP; ks += 16)
+                tc::mma_bf16_ta(tmem + T_B + T_PO, tmem + T_B + (ks >> 1),
+                                tc::smem_desc(sbase + OFF_V + (ks >> 3) * 128, 128, kKP * 16),
+                                idesc, ks > 0);
+              tc::mma_commit(bar_pv);
+            }
+            wait_opnd();                                                  // E_o_j: O_j in smem
+            gemm_w(false, OFF_O, kDH, T_A, kH, kDH, 32, j > 0);           // acc += O_j Wo_j
+            if (j + 1 < kHeads) wait_opnd();                              // E_qkv_{j+1}
           }
-          gemm_w(OFF_O, kDH, T_A, kH, kDH, 32, true); done();         // oproj_7
-          wait_opnd();                                                // h += ...
+          tc::mma_commit(bar_acc);
+          wait_opnd();                                                    // E_resid
         }
         for (int r = 0; r < NR; ++r) {
-          gemm_w(OFF_H, kH, T_B, 128, kH, 64, false); done();         // G1 half 0
-          wait_opnd();
-          gemm_w(OFF_R, 128, T_A, kH, 128, 32, false);                // G2 part 0
-          gemm_w(OFF_H, kH, T_B, 128, kH, 64, false); done();         // G1 half 1
-          wait_opnd();
-          gemm_w(OFF_R, 128, T_A, kH, 128, 32, true); done();         // G2 part 1
-          wait_opnd();                                                // h += ...
+          gemm_w(false, OFF_H, kH, T_B, 128, kH, 64, false);              // G1 half 0
+          tc::mma_commit(bar_acc);
+          wait_opnd();                                                    // r_h0 -> T_Q
+          gemm_w(true, T_Q, 0, T_A, kH, 128, 32, false);                  // G2 part 0
+          gemm_w(false, OFF_H, kH, T_B, 128, kH, 64, false);              // G1 half 1
+          tc::mma_commit(bar_acc);
+          wait_opnd();                                                    // r_h1 -> T_Q
+          gemm_w(true, T_Q, 0, T_A, kH, 128, 32, true);                   // G2 part 1
+          tc::mma_commit(bar_acc);
+          wait_opnd();                                                    // E_resid
         }
         for (int t = 0; t < NT; ++t) {
-          gemm_w(OFF_H, kH, T_B, kHD, kH, 64, false); done();         // head t
+          gemm_w(false, OFF_H, kH, T_B, kHD, kH, 64, false);              // head t
+          tc::mma_commit(bar_acc);
           if (t < NT - 1) wait_opnd();
         }
       }
@@ -270,12 +326,11 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
     const uint32_t q = warp & 3;
     const uint32_t r = 32 * q + lane;                  // tile row == TMEM lane
     const uint32_t tl = tmem + ((32 * q) << 16);       // this warp's lane quarter
-    const float* P = a.P;
     float* rowdot = reinterpret_cast<float*>(smem + OFF_DOT);
-    uint32_t acc_phase = 0;
-    auto wait_acc = [&]() {
-      tc::mbar_wait(bar_acc, acc_phase);
-      acc_phase ^= 1;
+    uint32_t ph_acc = 0, ph_qkv = 0, ph_s = 0, ph_pv = 0;
+    auto wait_on = [&](uint32_t bar, uint32_t& ph) {
+      tc::mbar_wait(bar, ph);
+      ph ^= 1;
       tc::tc_fence_after();
     };
     auto signal = [&]() {
@@ -288,10 +343,41 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
     const bool real = r < kCand * kL;
     const uint32_t s_lo = (32 * q) / kL;
     const float sm_scale = 1.4426950408889634f / sqrtf((float)kDH);  // log2(e)/sqrt(d_h)
+
+    auto e_qkv = [&](int l, int j) {
+      wait_on(bar_qkv, ph_qkv);
+      float v[32], b[32];
+      uint32_t pk[16];
+      tc::tmem_ld32(tl + T_Q + 0, v);
+      vec32(vs + a.bq[l] + kDH * j, b);
+      tc::tmem_wait_ld();
+#pragma unroll
+      for (int i = 0; i < 16; ++i) pk[i] = tc::pack_bf16(v[2 * i] + b[2 * i], v[2 * i + 1] + b[2 * i + 1]);
+      store_row32(smem, OFF_Q, r, 0, kDH, pk);
+      tc::tmem_ld32(tl + T_Q + 32, v);
+      vec32(vs + a.bk[l] + kDH * j, b);
+      tc::tmem_wait_ld();
+      if (real) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) pk[i] = tc::pack_bf16(v[2 * i] + b[2 * i], v[2 * i + 1] + b[2 * i + 1]);
+        store_row32(smem, OFF_K, 32 * slot + kk, 0, kDH, pk);
+      }
+      tc::tmem_ld32(tl + T_Q + 64, v);
+      vec32(vs + a.bv[l] + kDH * j, b);
+      tc::tmem_wait_ld();
+      if (real) {
+        const uint32_t kpos = 32 * slot + kk;
+#pragma unroll
+        for (int d = 0; d < kDH; ++d)
+          *reinterpret_cast<__nv_bfloat16*>(smem + OFF_V + tc::canon_off(d, kpos, kKP)) =
+              __float2bfloat16_rn(v[d] + b[d]);
+      }
+      signal();
+    };
+
     for (int64_t tile = blockIdx.x; tile < a.ntile; tile += gridDim.x) {
       const int64_t n = tile * kCand + slot;
-      // E0: X rows -> bf16 [128 x 32]
-      {
+      {  // E0: X rows -> bf16 [128 x 32]
         uint32_t pk[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) pk[i] = 0;
@@ -303,52 +389,28 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
             pk[i] = tc::pack_bf16(x.x, x.y);
           }
         }
-        store_row32(smem, OFF_R, r, 0, kKX, pk);
+        store_row32(smem, OFF_X, r, 0, kKX, pk);
         signal();
       }
-      wait_acc(); epi_bias_relu(smem, tl, T_A, 128, P + a.up_b0, OFF_R, 128, r); signal();
-      wait_acc(); epi_bias_relu(smem, tl, T_A, kH, P + a.up_b1, OFF_H, kH, r); signal();
+      wait_on(bar_acc, ph_acc);
+      epi_relu_to_tmem(tl, T_B, 128, vs + a.up_b0, T_Q);                   // U1 -> TMEM
+      signal();
+      wait_on(bar_acc, ph_acc);
+      epi_relu_to_smem(smem, tl, T_A, kH, vs + a.up_b1, OFF_H, kH, r);     // h
+      signal();
       for (int l = 0; l < NA; ++l) {
+        e_qkv(l, 0);
         for (int j = 0; j < kHeads; ++j) {
-          // ---- Q_j, K_j, V_j -> operand layouts
-          wait_acc();
-          {
-            float v[32], b[32];
-            uint32_t pk[16];
-            tc::tmem_ld32(tl + T_B + 0, v);
-            load_bias32(P + a.bq[l] + kDH * j, b);
-            tc::tmem_wait_ld();
-#pragma unroll
-            for (int i = 0; i < 16; ++i) pk[i] = tc::pack_bf16(v[2 * i] + b[2 * i], v[2 * i + 1] + b[2 * i + 1]);
-            store_row32(smem, OFF_Q, r, 0, kDH, pk);
-            tc::tmem_ld32(tl + T_B + 32, v);
-            load_bias32(P + a.bk[l] + kDH * j, b);
-            tc::tmem_wait_ld();
-            if (real) {
-#pragma unroll
-              for (int i = 0; i < 16; ++i) pk[i] = tc::pack_bf16(v[2 * i] + b[2 * i], v[2 * i + 1] + b[2 * i + 1]);
-              store_row32(smem, OFF_K, 32 * slot + kk, 0, kDH, pk);
-            }
-            tc::tmem_ld32(tl + T_B + 64, v);
-            load_bias32(P + a.bv[l] + kDH * j, b);
-            tc::tmem_wait_ld();
-            if (real) {
-              const uint32_t kpos = 32 * slot + kk;
-#pragma unroll
-              for (int d = 0; d < kDH; ++d) {
-                __nv_bfloat16 hv = __float2bfloat16_rn(v[d] + b[d]);
-                *reinterpret_cast<__nv_bfloat16*>(smem + OFF_V + tc::canon_off(d, kpos, kKP)) = hv;
-              }
-            }
-          }
-          signal();
-          // ---- softmax over the candidate's 25 keys -> P_j
-          wait_acc();
+          // ---- softmax over the candidate's 25 keys; P_j (bf16) in place over S_j
+          wait_on(bar_s, ph_s);
           {
             float va[32], vb[32];
             tc::tmem_ld32(tl + T_B + 32 * s_lo, va);
             tc::tmem_ld32(tl + T_B + 32 * s_lo + 32, vb);
             tc::tmem_wait_ld();
+            uint32_t pk[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) pk[i] = 0;
             if (real) {
               const bool hi = slot != s_lo;
               float x[kL];
@@ -362,22 +424,29 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
 #pragma unroll
               for (int c = 0; c < kL; ++c) { x[c] = exp2f(x[c] - mx); sum += x[c]; }
               const float inv = 1.0f / sum;
-              uint32_t pk[16];
 #pragma unroll
               for (int i = 0; i < 16; ++i) {
                 const float p0 = (2 * i < kL) ? x[(2 * i) % kL] * inv : 0.f;
                 const float p1 = (2 * i + 1 < kL) ? x[(2 * i + 1) % kL] * inv : 0.f;
                 pk[i] = tc::pack_bf16(p0, p1);
               }
-              store_row32(smem, OFF_P, r, 32 * slot, kKP, pk);
             }
+            const uint32_t zero[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+            for (int blk = 0; blk < kCand; ++blk) {
+              uint32_t o[16];
+#pragma unroll
+              for (int i = 0; i < 16; ++i) o[i] = (slot == (uint32_t)blk) ? pk[i] : zero[i];
+              tc::tmem_st16(tl + T_B + 16 * blk, o);
+            }
+            tc::tmem_wait_st();
           }
           signal();
-          // ---- O_j -> bf16 operand
-          wait_acc();
+          // ---- O_j -> bf16 smem operand
+          wait_on(bar_pv, ph_pv);
           {
             float v[32];
-            tc::tmem_ld32(tl + T_O, v);
+            tc::tmem_ld32(tl + T_B + T_PO, v);
             tc::tmem_wait_ld();
             uint32_t pk[16];
 #pragma unroll
@@ -385,22 +454,31 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
             store_row32(smem, OFF_O, r, 0, kDH, pk);
           }
           signal();
+          if (j + 1 < kHeads) e_qkv(l, j + 1);
         }
-        wait_acc(); epi_residual(smem, tl, P + a.bo[l], r); signal();
+        wait_on(bar_acc, ph_acc);
+        epi_residual(smem, tl, vs + a.bo[l], r);
+        signal();
       }
       for (int rb = 0; rb < NR; ++rb) {
-        wait_acc(); epi_bias_relu(smem, tl, T_B, 128, P + a.ra[rb], OFF_R, 128, r); signal();
-        wait_acc(); epi_bias_relu(smem, tl, T_B, 128, P + a.ra[rb] + 128, OFF_R, 128, r); signal();
-        wait_acc(); epi_residual(smem, tl, P + a.rb[rb], r); signal();
+        wait_on(bar_acc, ph_acc);
+        epi_relu_to_tmem(tl, T_B, 128, vs + a.ra[rb], T_Q);
+        signal();
+        wait_on(bar_acc, ph_acc);
+        epi_relu_to_tmem(tl, T_B, 128, vs + a.ra[rb] + 128, T_Q);
+        signal();
+        wait_on(bar_acc, ph_acc);
+        epi_residual(smem, tl, vs + a.rb[rb], r);
+        signal();
       }
       for (int t = 0; t < NT; ++t) {
-        wait_acc();
+        wait_on(bar_acc, ph_acc);
         float dot = 0.f;
         for (int c = 0; c < kHD; c += 32) {
           float v[32], b[32], w[32];
           tc::tmem_ld32(tl + T_B + c, v);
-          load_bias32(P + a.c1[t] + c, b);
-          load_bias32(P + a.w2[t] + c, w);
+          vec32(vs + a.c1[t] + c, b);
+          vec32(vs + a.w2[t] + c, w);
           tc::tmem_wait_ld();
 #pragma unroll
           for (int i = 0; i < 32; ++i) dot = fmaf(fmaxf(v[i] + b[i], 0.f), w[i], dot);
@@ -412,8 +490,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
           const int64_t nn = tile * kCand + r;
           if (nn < a.N) {
             float s = 0.f;
-            for (int l2 = 0; l2 < kL; ++l2) s += rowdot[r * kL + l2];  // fixed order (batch invariance)
-            a.scores[nn * NT + t] = s + (float)kL * __ldg(P + a.c2[t]);
+            for (int l2 = 0; l2 < kL; ++l2) s += rowdot[r * kL + l2];  // fixed order (R34)
+            a.scores[nn * NT + t] = s + (float)kL * vs[a.c2[t]];
           }
         }
         if (t < NT - 1) signal();
@@ -438,6 +516,8 @@ struct PackChunk {
   int seg_col[3];
 };
 
+// B operand chunk (N x Kc bf16, canonical K-major layout) from fp32 W [in, out]:
+// B[n][k] = W[k0 + k][col(n)], zero beyond Kreal (the 22 -> 32 padding).
 __global__ void pack_kernel(const PackChunk* __restrict__ pcs, const float* __restrict__ P,
                             uint8_t* __restrict__ out) {
   const PackChunk c = pcs[blockIdx.x];
@@ -462,11 +542,13 @@ struct TcWeights {
   int nchunks = 0;
   size_t bytes = 0;
   std::vector<PackChunk> host;
-  // epilogue vectors (biases, w2, c2) copied to 16-byte aligned slots so the
-  // epilogue can use float4 loads (flat R24 offsets are not all aligned)
+  // epilogue vectors (biases, w2, c2) copied to 16-byte aligned slots; staged
+  // into shared memory by every CTA (flat R24 offsets are not all aligned)
   float* vec = nullptr;
+  int vec_floats = 0;
   std::vector<std::array<int64_t, 3>> vec_copies;  // {src flat offset, dst offset, n}
   TcArgs slots{};                                  // offsets into `vec`
+  uint32_t smem = 0;
 };
 
 bool tc_supported(const tlp_config& c) {
@@ -475,6 +557,7 @@ bool tc_supported(const tlp_config& c) {
          c.head_dim == kHD && c.n_tasks <= TLP_MAX_TASKS;
 }
 
+// The weight chunks in the exact order tc_forward_kernel's MMA issuer consumes them.
 static std::vector<PackChunk> build_schedule(const tlp_ctx* ctx) {
   const tlp_config& c = ctx->cfg;
   const ParamOffsets& o = ctx->off;
@@ -491,14 +574,19 @@ static std::vector<PackChunk> build_schedule(const tlp_ctx* ctx) {
     dst += (uint32_t)(N * Kc * 2);
     v.push_back(p);
   };
-  add(128, 32, 0, kE, {{0, o.up_W[0], 128, 0}});
-  for (int k0 = 0; k0 < 128; k0 += 32) add(256, 32, k0, 128, {{0, o.up_W[1], 256, 0}});
-  for (int l = 0; l < c.n_attn; ++l)
-    for (int j = 0; j < kHeads; ++j) {
+  add(128, 32, 0, kE, {{0, o.up_W[0], 128, 0}});                                 // up0
+  for (int k0 = 0; k0 < 128; k0 += 32) add(256, 32, k0, 128, {{0, o.up_W[1], 256, 0}});  // up1
+  for (int l = 0; l < c.n_attn; ++l) {
+    auto qkv = [&](int j) {
       for (int k0 = 0; k0 < kH; k0 += 64)
         add(96, 64, k0, kH, {{0, o.Wq[l], kH, kDH * j}, {32, o.Wk[l], kH, kDH * j}, {64, o.Wv[l], kH, kDH * j}});
-      add(256, 32, kDH * j, kH, {{0, o.Wo[l], kH, 0}});
+    };
+    qkv(0);
+    for (int j = 0; j < kHeads; ++j) {
+      if (j + 1 < kHeads) qkv(j + 1);                      // issued right after S_j
+      add(256, 32, kDH * j, kH, {{0, o.Wo[l], kH, 0}});     // oproj_j after PV_j
     }
+  }
   for (int r = 0; r < c.n_res; ++r) {
     for (int k0 = 0; k0 < kH; k0 += 64) add(128, 64, k0, kH, {{0, o.Wa[r], kH, 0}});
     for (int k0 = 0; k0 < 128; k0 += 32) add(256, 32, k0, kH, {{0, o.Wb[r], kH, 0}});
@@ -513,8 +601,8 @@ static std::vector<PackChunk> build_schedule(const tlp_ctx* ctx) {
 tlp_status tc_prepare(tlp_ctx* ctx, cudaStream_t s) {
   if (!ctx->tc) {
     ctx->tc = new TcWeights();
-    ctx->tc->host = build_schedule(ctx);
     TcWeights& w = *ctx->tc;
+    w.host = build_schedule(ctx);
     w.nchunks = (int)w.host.size();
     w.bytes = w.host.back().dst + (size_t)w.host.back().N * w.host.back().Kc * 2;
     std::vector<ChunkRef> refs(w.nchunks);
@@ -526,16 +614,7 @@ tlp_status tc_prepare(tlp_ctx* ctx, cudaStream_t s) {
         return TLP_ERR_STATE;
       }
     }
-    TLP_CUDA_TRY(cudaMalloc(&w.wstream, w.bytes));
-    TLP_CUDA_TRY(cudaMalloc(&w.chunks, w.nchunks * sizeof(ChunkRef)));
-    TLP_CUDA_TRY(cudaMalloc(&w.pack, w.nchunks * sizeof(PackChunk)));
-    TLP_CUDA_TRY(cudaMemcpy(w.chunks, refs.data(), w.nchunks * sizeof(ChunkRef), cudaMemcpyHostToDevice));
-    TLP_CUDA_TRY(cudaMemcpy(w.pack, w.host.data(), w.nchunks * sizeof(PackChunk), cudaMemcpyHostToDevice));
-    TLP_CUDA_TRY(cudaFuncSetAttribute(tc_forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)SMEM_BYTES));
-  }
-  TcWeights& w = *ctx->tc;
-  if (!w.vec) {
+    // epilogue vector slots
     const tlp_config& c = ctx->cfg;
     const ParamOffsets& o = ctx->off;
     int64_t dst = 0;
@@ -556,9 +635,23 @@ tlp_status tc_prepare(tlp_ctx* ctx, cudaStream_t s) {
     for (int k = 0; k < c.n_tasks; ++k) {
       t.c1[k] = slot(o.c1[k], kHD); t.w2[k] = slot(o.w2[k], kHD); t.c2[k] = slot(o.c2[k], 1);
     }
+    w.vec_floats = (int)dst;
+    w.smem = OFF_VEC + (uint32_t)dst * 4u;
+    if (w.smem > kMaxSmem) {
+      ctx->last_error = "tc path: too many layers/tasks for the shared-memory budget";
+      return TLP_ERR_UNSUPPORTED;
+    }
     TLP_CUDA_TRY(cudaMalloc(&w.vec, dst * sizeof(float)));
     TLP_CUDA_TRY(cudaMemset(w.vec, 0, dst * sizeof(float)));
+    TLP_CUDA_TRY(cudaMalloc(&w.wstream, w.bytes));
+    TLP_CUDA_TRY(cudaMalloc(&w.chunks, w.nchunks * sizeof(ChunkRef)));
+    TLP_CUDA_TRY(cudaMalloc(&w.pack, w.nchunks * sizeof(PackChunk)));
+    TLP_CUDA_TRY(cudaMemcpy(w.chunks, refs.data(), w.nchunks * sizeof(ChunkRef), cudaMemcpyHostToDevice));
+    TLP_CUDA_TRY(cudaMemcpy(w.pack, w.host.data(), w.nchunks * sizeof(PackChunk), cudaMemcpyHostToDevice));
+    TLP_CUDA_TRY(cudaFuncSetAttribute(tc_forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)kMaxSmem));
   }
+  TcWeights& w = *ctx->tc;
   for (const auto& cp : w.vec_copies)
     TLP_CUDA_TRY(cudaMemcpyAsync(w.vec + cp[1], ctx->d_params + cp[0], cp[2] * sizeof(float),
                                  cudaMemcpyDeviceToDevice, s));
@@ -569,15 +662,14 @@ tlp_status tc_prepare(tlp_ctx* ctx, cudaStream_t s) {
 
 tlp_status tc_forward(tlp_ctx* ctx, const float* feats, int64_t N, float* scores, cudaStream_t s) {
   const tlp_config& c = ctx->cfg;
-  const ParamOffsets& o = ctx->off;
   TcWeights& w = *ctx->tc;
   TcArgs a = w.slots;  // epilogue vector offsets into w.vec
   a.X = feats; a.scores = scores; a.N = N; a.ntile = cdiv(N, kCand);
-  a.wstream = w.wstream; a.chunks = w.chunks; a.nchunks = w.nchunks; a.P = w.vec;
-  (void)o;
+  a.wstream = w.wstream; a.chunks = w.chunks; a.nchunks = w.nchunks;
+  a.vec = w.vec; a.vec_floats = w.vec_floats;
   a.n_attn = c.n_attn; a.n_res = c.n_res; a.n_tasks = c.n_tasks;
   const int grid = (int)std::min<int64_t>(a.ntile, ctx->num_sms);
-  tc_forward_kernel<<<grid, kThreads, SMEM_BYTES, s>>>(a);
+  tc_forward_kernel<<<grid, kThreads, w.smem, s>>>(a);
   TLP_LAUNCH_CHECK();
   return TLP_OK;
 }
@@ -594,8 +686,11 @@ void tc_free(tlp_ctx* ctx) {
 
 // ---------------------------------------------------------------- test hook
 namespace {
-// D[128 x N] = A[128 x K] * B[N x K]^T through one UMMA chain (descriptor test).
-__global__ void umma_test_kernel(const float* A, const float* B, float* D, int N, int K) {
+// D[128 x N] = A[128 x K] * B[N x K]^T through one UMMA chain.  a_tmem != 0:
+// the A operand is first written to TMEM (bf16 pairs) with tcgen05.st and the
+// MMA reads it from there (the form used for U1, r-halves and P_j).
+__global__ void umma_test_kernel(const float* A, const float* B, float* D, int N, int K,
+                                 int a_tmem) {
   extern __shared__ __align__(128) uint8_t sm[];
   const uint32_t sb = tc::smem_u32(sm);
   const uint32_t offA = 0, offB = 128 * K * 2, offBar = offB + N * K * 2, offT = offBar + 8;
@@ -605,22 +700,39 @@ __global__ void umma_test_kernel(const float* A, const float* B, float* D, int N
     *reinterpret_cast<__nv_bfloat16*>(sm + offB + tc::canon_off(e / K, e % K, K)) = __float2bfloat16_rn(B[e]);
   uint32_t* tp = reinterpret_cast<uint32_t*>(sm + offT);
   if (threadIdx.x == 0) { tc::mbar_init(sb + offBar, 1); tc::fence_barrier_init(); }
-  if (threadIdx.x < 32) tc::tmem_alloc(tc::smem_u32(tp), 256);
+  if (threadIdx.x < 32) tc::tmem_alloc(tc::smem_u32(tp), 512);
   tc::fence_proxy_async_smem();
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tm = *tp;
+  const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
+  const uint32_t a_col = 256;  // A staged at TMEM columns [256, 256 + K/2)
+  if (a_tmem) {
+    const int r = 32 * w + ln;
+    for (int c = 0; c < K; c += 32) {
+      uint32_t pk[16];
+      for (int i = 0; i < 16; ++i) pk[i] = tc::pack_bf16(A[r * K + c + 2 * i], A[r * K + c + 2 * i + 1]);
+      tc::tmem_st16(tm + ((32 * w) << 16) + a_col + c / 2, pk);
+    }
+    tc::tmem_wait_st();
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::tc_fence_after();
+  }
   if (threadIdx.x == 0) {
     const uint32_t id = tc::idesc_bf16(128, N);
-    for (int ks = 0; ks < K; ks += 16)
-      tc::mma_bf16(tm, tc::smem_desc(sb + offA + (ks >> 3) * 128, 128, K * 16),
-                   tc::smem_desc(sb + offB + (ks >> 3) * 128, 128, K * 16), id, ks > 0);
+    for (int ks = 0; ks < K; ks += 16) {
+      const uint64_t bd = tc::smem_desc(sb + offB + (ks >> 3) * 128, 128, K * 16);
+      if (a_tmem)
+        tc::mma_bf16_ta(tm, tm + a_col + ks / 2, bd, id, ks > 0);
+      else
+        tc::mma_bf16(tm, tc::smem_desc(sb + offA + (ks >> 3) * 128, 128, K * 16), bd, id, ks > 0);
+    }
     tc::mma_commit(sb + offBar);
   }
   tc::mbar_wait(sb + offBar, 0);
   tc::tc_fence_after();
-  const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
   for (int c = 0; c < N; c += 32) {
     float v[32];
     tc::tmem_ld32(tm + ((32 * w) << 16) + c, v);
@@ -629,15 +741,15 @@ __global__ void umma_test_kernel(const float* A, const float* B, float* D, int N
   }
   tc::tc_fence_before();
   __syncthreads();
-  if (threadIdx.x < 32) { tc::tc_fence_after(); tc::tmem_dealloc(tm, 256); }
+  if (threadIdx.x < 32) { tc::tc_fence_after(); tc::tmem_dealloc(tm, 512); }
 }
 }  // namespace
 
 extern "C" tlp_status tlp_debug_umma(const float* A, const float* B, float* D, int32_t N,
-                                     int32_t K, void* stream) {
-  if (N < 16 || N > 256 || N % 16 || K < 16 || K % 16 || K > 256) return TLP_ERR_ARG;
+                                     int32_t K, int32_t a_in_tmem, void* stream) {
+  if (N < 16 || N > 256 || N % 16 || K < 32 || K % 32 || K > 256) return TLP_ERR_ARG;
   const size_t smem = (size_t)128 * K * 2 + (size_t)N * K * 2 + 64;
   cudaFuncSetAttribute(umma_test_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  umma_test_kernel<<<1, 128, smem, reinterpret_cast<cudaStream_t>(stream)>>>(A, B, D, N, K);
+  umma_test_kernel<<<1, 128, smem, reinterpret_cast<cudaStream_t>(stream)>>>(A, B, D, N, K, a_in_tmem);
   return cudaGetLastError() == cudaSuccess ? TLP_OK : TLP_ERR_CUDA;
 }

@@ -301,8 +301,9 @@ def test_train_step_adam_parity(tp, tokscale):
 
 
 # ---------------------------------------------------------------- bf16 tcgen05 path
-@pytest.mark.parametrize("N,K", [(16, 16), (96, 64), (160, 32), (32, 160), (256, 256)])
-def test_umma_building_block(tp, N, K):
+@pytest.mark.parametrize("N,K,a_tmem", [(16, 32, 0), (96, 64, 0), (160, 32, 0), (32, 160, 0),
+                                         (256, 256, 0), (32, 160, 1), (256, 128, 1), (16, 32, 1)])
+def test_umma_building_block(tp, N, K, a_tmem):
     """One tcgen05.mma chain (descriptors, TMEM, tcgen05.ld) vs an fp64 matmul of
     the same bf16-rounded operands: products are exact, accumulation fp32."""
     rng = np.random.default_rng(N * 1000 + K)
@@ -311,7 +312,7 @@ def test_umma_building_block(tp, N, K):
     D = torch.zeros((128, N), dtype=torch.float32, device="cuda")
     lib = tp._lib.load()
     Ad, Bd = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()  # keep alive until sync
-    st = lib.tlp_debug_umma(Ad.data_ptr(), Bd.data_ptr(), D.data_ptr(), N, K,
+    st = lib.tlp_debug_umma(Ad.data_ptr(), Bd.data_ptr(), D.data_ptr(), N, K, a_tmem,
                             torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
     assert st == 0
