@@ -1,37 +1,41 @@
-// bf16 tcgen05 fused forward of the TLP network (the scoring hot path).
+// bf16 tensor-core fused forward of the TLP network (the scoring hot path).
 //
 // One persistent CTA per SM walks tiles of 5 candidates = 125 rows (+3 pad
 // rows) = one M=128 UMMA tile, and runs the WHOLE network on chip for the tile
 // (readings R8-R14, R28, R33, R34 in DESIGN.md):
 //   X (fp32 [5,25,22] from HBM) -> bf16 smem
-//   U1 = relu(X W1 + b1)            -> bf16 in TMEM (A operand of the next GEMM)
-//   h  = relu(U1 W2 + b2)           -> bf16 smem (A operand + residual stream)
+//   U1 = relu(X W1 + b1)             tcgen05, -> bf16 in TMEM (A operand of the next GEMM)
+//   h  = relu(U1 W2 + b2)            tcgen05, -> bf16 smem (A operand + residual stream)
 //   per attention layer, per head j (8 heads, d_h = 32):
-//     [Q_j|K_j|V_j] = h W_qkv_j + b                          GEMM N=96 (issued one head ahead)
-//     S_j = Q_j K_j^T   keys at padded positions 32*slot+kk  GEMM N=160
-//     P_j = softmax(S_j / sqrt(32)) over the candidate's 25 keys, written
-//           in place over S_j in TMEM as bf16                 (epilogue, fp32 math)
-//     O_j = P_j V_j     (A = P_j from TMEM, K = 160)         GEMM N=32
-//     acc += O_j Wo[32j:32j+32, :]                            GEMM (accumulated in TMEM)
+//     [Q_j|K_j|V_j] = h W_qkv_j + b  tcgen05 N=96, issued two heads ahead (TMEM double buffer)
+//     O_j = softmax(Q_j K_j^T / sqrt(32)) V_j   block-diagonal per candidate, on the
+//           epilogue warps with warp-level mma.sync (FA2-style register reuse of P)
+//     acc += O_j Wo[32j:32j+32, :]   tcgen05, accumulated in TMEM
 //   h = h + acc + bo
 //   per residual block: r = relu(h Wa + a) in two N-halves (bf16 in TMEM as the
-//     A operand), h = h + r Wb + b
+//     A operand), h = h + r Wb + b       tcgen05
 //   per task t: s_t = sum_l relu(h_l W1_t + c1_t) . w2_t + 25 c2_t (fixed-order row sum)
 // Only X (2,200 B/candidate) is read from HBM and n_tasks floats are written.
 // Weights (bf16, UMMA canonical layout, consumption order) stream from L2
-// through a 6-stage x 16 KB ring filled by 1-D bulk TMA (cp.async.bulk);
+// through a 5-stage x 16 KB ring filled by 1-D bulk TMA (cp.async.bulk);
 // biases / w2 / c2 are staged once per CTA in shared memory.
 //
 // Warp roles: warp 0 = TMA producer (one lane), warp 1 = tcgen05.mma issuer
-// (one lane) and TMEM owner, warps 2..5 = epilogue (thread = tile row = TMEM
-// lane).  MMA -> epilogue: tcgen05.commit on one of four mbarriers (acc, qkv,
-// s, pv) so that the QKV GEMM of head j+1 overlaps the softmax of head j;
-// epilogue -> MMA: 128 arrivals on `opnd` after fence.proxy.async / wait::st.
+// (one lane) and TMEM owner, warps 2..9 = epilogue: two warps per TMEM lane
+// quarter (thread = tile row = TMEM lane), splitting every epilogue's columns
+// (and the attention's two 16-row m-tiles) between them for 2x latency
+// hiding.  MMA -> epilogue: tcgen05.commit on `acc` (generic) or `qkv`;
+// epilogue -> MMA: 256 arrivals on `opnd` after fence.proxy.async / wait::st.
 //
-// Batch invariance (R34): a candidate's keys sit at K positions
-// 32*slot..32*slot+24 (zero padded to 32), so the PV accumulation grouping is
-// identical for every slot; everything else is row-local and the 25-row head
-// sum runs in a fixed order.
+// The attention core is 1.5% of the FLOPs (0.64 of 44 MFLOP/candidate) and is
+// block-diagonal 25x25 per candidate; doing it in registers removes two
+// MMA<->epilogue round trips per head, which dominated v2 (ncu: TC 43% busy).
+//
+// Batch invariance (R34): a candidate's keys sit at positions 32*slot+kk
+// (kk < 25, pad zero / masked), every row's softmax sums the same nonzero
+// terms in the same order whatever its slot, and the PV k-steps of the other
+// candidate contribute exact zeros; everything else is row-local and the
+// 25-row head sum runs in a fixed order.
 #include "tlp_internal.cuh"
 #include "tc_ptx.cuh"
 
@@ -46,19 +50,21 @@ constexpr int kL = 25, kE = 22, kH = 256, kHeads = 8, kDH = 32, kHD = 128;
 constexpr int kCand = 5;            // candidates per tile
 constexpr int kKX = 32;             // padded K of the first GEMM (22 -> 32)
 constexpr int kKP = 160;            // padded key positions (5 x 32)
-constexpr int kStages = 6;
+constexpr int kStages = 5;
 constexpr uint32_t kStageBytes = 16384;
-constexpr int kThreads = 192;
+constexpr int kThreads = 320;   // warp 0 TMA, warp 1 MMA, warps 2..9 epilogue
+constexpr int kEpi = 256;       // epilogue threads (2 warps per TMEM lane quarter)
+constexpr uint32_t kRowB = 80;      // row stride (bytes) of the mma.sync Q/K/V tiles (64 + 16 pad)
 
 // shared memory map (bytes)
-constexpr uint32_t OFF_H = 0;                       // h      [128 x 256] bf16, Kt=256
-constexpr uint32_t OFF_X = OFF_H + 65536;           // X      [128 x 32]
-constexpr uint32_t OFF_Q = OFF_X + 8192;            // Q_j    [128 x 32]
-constexpr uint32_t OFF_O = OFF_Q + 8192;            // O_j    [128 x 32]
-constexpr uint32_t OFF_K = OFF_O + 8192;            // K_j    [160 x 32]  (B operand, padded keys)
-constexpr uint32_t OFF_V = OFF_K + 10240;           // V_j^T  [32 x 160]  (B operand)
-constexpr uint32_t OFF_DOT = OFF_V + 10240;         // 128 fp32 row dots
-constexpr uint32_t OFF_BAR = OFF_DOT + 512;         // mbarriers (<= 32)
+constexpr uint32_t OFF_H = 0;                       // h      [128 x 256] bf16, canonical Kt=256
+constexpr uint32_t OFF_X = OFF_H + 65536;           // X      [128 x 32]  canonical
+constexpr uint32_t OFF_Q = OFF_X + 8192;            // Q_j    [128][32] row-major, 80 B rows
+constexpr uint32_t OFF_K = OFF_Q + 128 * kRowB;     // K_j    [160][32] (padded key positions)
+constexpr uint32_t OFF_V = OFF_K + kKP * kRowB;     // V_j    [160][32]
+constexpr uint32_t OFF_O = OFF_V + kKP * kRowB;     // O_j    2 x [128 x 32] canonical (A of oproj)
+constexpr uint32_t OFF_DOT = OFF_O + 2 * 8192;      // 2 x 128 fp32 row dots
+constexpr uint32_t OFF_BAR = OFF_DOT + 1024;        // mbarriers (<= 32)
 constexpr uint32_t OFF_TPTR = OFF_BAR + 256;
 constexpr uint32_t OFF_RING = OFF_TPTR + 128;       // kStages x 16 KB
 constexpr uint32_t OFF_VEC = OFF_RING + kStages * kStageBytes;  // epilogue vectors (fp32)
@@ -66,11 +72,10 @@ constexpr uint32_t kMaxSmem = 232448;
 static_assert(OFF_RING % 128 == 0, "ring alignment");
 
 // TMEM column map (512 allocated)
-constexpr uint32_t T_A = 0;    // 256: up1 / sum_j O_j Wo_j / residual-block output accumulators
-constexpr uint32_t T_B = 256;  // 160: up0, S_j -> P_j (bf16, cols 0..79) + O_j (cols 96..127),
-                               //      residual-block first GEMM halves, head
-constexpr uint32_t T_Q = 416;  // 96:  QKV_j accumulator; bf16 A operands U1 / r-half (64 cols)
-constexpr uint32_t T_PO = 96;  // O_j offset inside T_B
+constexpr uint32_t T_A = 0;      // 256: up1 / sum_j O_j Wo_j / residual-block output accumulator
+constexpr uint32_t T_B = 256;    // 128: up0, residual-block first GEMM halves, head (scratch)
+constexpr uint32_t T_QKV = 256;  // 2 x 96: QKV_j double buffer (attention phase only)
+constexpr uint32_t T_AOP = 448;  // 64:  bf16 A operand (U1, residual-block half)
 
 struct ChunkRef {
   uint32_t off16;  // byte offset / 16 into the weight stream
@@ -104,6 +109,14 @@ __device__ __forceinline__ void store_row32(uint8_t* smem, uint32_t base, uint32
   }
 }
 
+// 32 bf16 (packed) -> plain row of the mma.sync tiles
+__device__ __forceinline__ void store_plain32(uint8_t* smem, uint32_t off, const uint32_t (&pk)[16]) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    *reinterpret_cast<uint4*>(smem + off + 16 * i) =
+        make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+}
+
 // 32 consecutive fp32 from shared memory (same address across the warp: broadcast)
 __device__ __forceinline__ void vec32(const float* v, float (&o)[32]) {
 #pragma unroll
@@ -114,9 +127,9 @@ __device__ __forceinline__ void vec32(const float* v, float (&o)[32]) {
 }
 
 // relu(acc + bias) -> bf16 A operand in TMEM (two bf16 per column)
-__device__ __forceinline__ void epi_relu_to_tmem(uint32_t tl, uint32_t src, int ncol,
+__device__ __forceinline__ void epi_relu_to_tmem(uint32_t tl, uint32_t src, int c0, int c1,
                                                  const float* bias, uint32_t dst) {
-  for (int c = 0; c < ncol; c += 32) {
+  for (int c = c0; c < c1; c += 32) {
     float v[32], b[32];
     tc::tmem_ld32(tl + src + c, v);
     vec32(bias + c, b);
@@ -132,9 +145,9 @@ __device__ __forceinline__ void epi_relu_to_tmem(uint32_t tl, uint32_t src, int 
 
 // relu(acc + bias) -> bf16 smem operand (row r)
 __device__ __forceinline__ void epi_relu_to_smem(uint8_t* smem, uint32_t tl, uint32_t src,
-                                                 int ncol, const float* bias, uint32_t dst,
+                                                 int c0, int c1, const float* bias, uint32_t dst,
                                                  uint32_t Kt, uint32_t r) {
-  for (int c = 0; c < ncol; c += 32) {
+  for (int c = c0; c < c1; c += 32) {
     float v[32], b[32];
     tc::tmem_ld32(tl + src + c, v);
     vec32(bias + c, b);
@@ -149,8 +162,8 @@ __device__ __forceinline__ void epi_relu_to_smem(uint8_t* smem, uint32_t tl, uin
 
 // h[r, :] = bf16(h[r, :] + acc[r, :] + bias)   (R10 / R12 residual, R33)
 __device__ __forceinline__ void epi_residual(uint8_t* smem, uint32_t tl, const float* bias,
-                                             uint32_t r) {
-  for (int c = 0; c < kH; c += 32) {
+                                             uint32_t r, int c0, int c1) {
+  for (int c = c0; c < c1; c += 32) {
     float v[32], b[32];
     tc::tmem_ld32(tl + T_A + c, v);
     vec32(bias + c, b);
@@ -171,6 +184,107 @@ __device__ __forceinline__ void epi_residual(uint8_t* smem, uint32_t tl, const f
   }
 }
 
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));  // R29: bf16 path may use ex2.approx
+  return y;
+}
+
+// Block-diagonal attention of one head for 16 query rows (m-tile `mt` of this
+// lane quarter q).  Keys of the quarter's two candidates are the 64 padded
+// positions [32*s_lo, 32*s_lo + 64); S = Q K^T (8 n-tiles x 2 k-steps),
+// masked softmax per row (quad shuffles), P reused from registers as the A
+// fragments of O = P V (4 n-tiles x 4 k-steps), O scaled by 1/rowsum;
+// O_j -> canonical bf16 [128 x 32] (A operand of the output projection).
+__device__ __forceinline__ void attn_head_mma(uint8_t* smem, uint32_t sbase, uint32_t q,
+                                              uint32_t mt, uint32_t lane, float sm_scale,
+                                              uint32_t o_off) {
+  const uint32_t s_lo = (32 * q) / kL;
+  const uint32_t kp0 = 32 * s_lo;
+  const uint32_t g = lane >> 2, tig = lane & 3;
+  uint32_t qa[2][4];  // Q A-fragments per k-step
+#pragma unroll
+  for (int ks = 0; ks < 2; ++ks) {
+    const uint32_t row = 32 * q + 16 * mt + (lane & 15);
+    const uint32_t col = 16 * ks + 8 * (lane >> 4);
+    tc::ldsm_x4(sbase + OFF_Q + row * kRowB + col * 2, qa[ks]);
+  }
+  float s[8][4];
+#pragma unroll
+  for (int nt = 0; nt < 8; ++nt) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) s[nt][i] = 0.f;
+    uint32_t kb[4];  // (ks0: b0,b1) (ks1: b0,b1)
+    tc::ldsm_x4(sbase + OFF_K + (kp0 + 8 * nt + (lane & 7)) * kRowB + 16 * (lane >> 3), kb);
+    tc::mma16816(s[nt], qa[0], kb[0], kb[1]);
+    tc::mma16816(s[nt], qa[1], kb[2], kb[3]);
+  }
+  // masked softmax (unnormalised); rows 32q + 16mt + g (+8)
+  float inv[2];
+#pragma unroll
+  for (int half = 0; half < 2; ++half) {
+    const uint32_t row = 32 * q + 16 * mt + g + 8 * half;
+    const int lo = 32 * (int)(row / kL) - (int)kp0;  // window-relative first valid key
+    float mx = -INFINITY;
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int c = 8 * nt + 2 * tig + e;
+        if (c >= lo && c < lo + kL) mx = fmaxf(mx, s[nt][2 * half + e]);
+      }
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+    const float off = (mx == -INFINITY) ? 0.f : mx * sm_scale;
+    float sum = 0.f;
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int c = 8 * nt + 2 * tig + e;
+        const float p = (c >= lo && c < lo + kL) ? ex2_approx(fmaf(s[nt][2 * half + e], sm_scale, -off)) : 0.f;
+        s[nt][2 * half + e] = p;
+        sum += p;
+      }
+    sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+    sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+    inv[half] = sum > 0.f ? 1.0f / sum : 0.f;
+  }
+  uint32_t pa[4][4];  // P as A fragments per 16-key block
+#pragma unroll
+  for (int kbk = 0; kbk < 4; ++kbk) {
+    pa[kbk][0] = tc::pack_bf16(s[2 * kbk][0], s[2 * kbk][1]);
+    pa[kbk][1] = tc::pack_bf16(s[2 * kbk][2], s[2 * kbk][3]);
+    pa[kbk][2] = tc::pack_bf16(s[2 * kbk + 1][0], s[2 * kbk + 1][1]);
+    pa[kbk][3] = tc::pack_bf16(s[2 * kbk + 1][2], s[2 * kbk + 1][3]);
+  }
+  float o[4][4];
+#pragma unroll
+  for (int dn = 0; dn < 4; ++dn)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) o[dn][i] = 0.f;
+#pragma unroll
+  for (int kbk = 0; kbk < 4; ++kbk)
+#pragma unroll
+    for (int dp = 0; dp < 2; ++dp) {  // pairs of d n-tiles
+      uint32_t vb[4];                 // (dn=2dp: b0,b1) (dn=2dp+1: b0,b1)
+      const uint32_t krow = kp0 + 16 * kbk + (lane & 7) + 8 * ((lane >> 3) & 1);
+      const uint32_t dcol = 8 * (2 * dp + (lane >> 4));
+      tc::ldsm_x4_t(sbase + OFF_V + krow * kRowB + dcol * 2, vb);
+      tc::mma16816(o[2 * dp], pa[kbk], vb[0], vb[1]);
+      tc::mma16816(o[2 * dp + 1], pa[kbk], vb[2], vb[3]);
+    }
+#pragma unroll
+  for (int dn = 0; dn < 4; ++dn)
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      const uint32_t row = 32 * q + 16 * mt + g + 8 * half;
+      const uint32_t d = 8 * dn + 2 * tig;
+      *reinterpret_cast<uint32_t*>(smem + o_off + tc::canon_off(row, d, kDH)) =
+          tc::pack_bf16(o[dn][2 * half] * inv[half], o[dn][2 * half + 1] * inv[half]);
+    }
+}
+
 __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -179,14 +293,12 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
   const uint32_t bar_empty = bar_full + 8 * kStages;     // kStages
   const uint32_t bar_acc = bar_empty + 8 * kStages;      // generic GEMM done
   const uint32_t bar_qkv = bar_acc + 8;                  // QKV_j done
-  const uint32_t bar_s = bar_qkv + 8;                    // S_j done
-  const uint32_t bar_pv = bar_s + 8;                     // O_j done
-  const uint32_t bar_opnd = bar_pv + 8;                  // epilogue -> MMA (128 arrivals)
+  const uint32_t bar_opnd = bar_qkv + 8;                 // epilogue -> MMA (kEpi arrivals)
   uint32_t* tptr = reinterpret_cast<uint32_t*>(smem + OFF_TPTR);
   float* vs = reinterpret_cast<float*>(smem + OFF_VEC);
 
-  // V_j^T and K_j pad entries must stay exactly 0 / finite: zero them once.
-  for (uint32_t o = OFF_K + threadIdx.x * 16; o < OFF_DOT; o += kThreads * 16)
+  // K/V pad key positions must stay exactly 0: zero Q/K/V once.
+  for (uint32_t o = OFF_Q + threadIdx.x * 16; o < OFF_O; o += kThreads * 16)
     *reinterpret_cast<uint4*>(smem + o) = make_uint4(0, 0, 0, 0);
   for (int i = threadIdx.x; i < a.vec_floats / 4; i += kThreads)
     reinterpret_cast<float4*>(vs)[i] = __ldg(reinterpret_cast<const float4*>(a.vec) + i);
@@ -197,9 +309,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
     }
     tc::mbar_init(bar_acc, 1);
     tc::mbar_init(bar_qkv, 1);
-    tc::mbar_init(bar_s, 1);
-    tc::mbar_init(bar_pv, 1);
-    tc::mbar_init(bar_opnd, 128);
+    tc::mbar_init(bar_opnd, kEpi);
     tc::fence_barrier_init();
   }
   if (warp == 1) tc::tmem_alloc(tc::smem_u32(tptr), 512);
@@ -236,8 +346,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
         op_phase ^= 1;
         tc::tc_fence_after();
       };
-      // D (+)= A x (ring chunks of N x Kc)^T over K.  A in smem (a_tmem == 0:
-      // canonical layout with Kt = a_kt at a_off) or in TMEM (column a_off).
+      // D (+)= A x (ring chunks of N x Kc)^T over K.  A in smem (canonical
+      // layout with Kt = a_kt at byte offset a_off) or in TMEM (column a_off).
       auto gemm_w = [&](bool a_tmem, uint32_t a_off, uint32_t a_kt, uint32_t d_col, uint32_t N,
                         int K, int Kc, bool acc) {
         const uint32_t idesc = tc::idesc_bf16(128, N);
@@ -264,40 +374,22 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
         wait_opnd();                                                      // E0: X
         gemm_w(false, OFF_X, kKX, T_B, 128, kKX, 32, false);              // up0 -> T_B
         tc::mma_commit(bar_acc);
-        wait_opnd();                                                      // E1: U1 -> T_Q (bf16)
-        gemm_w(true, T_Q, 0, T_A, kH, 128, 32, false);                    // up1 -> T_A
+        wait_opnd();                                                      // E1: U1 -> T_AOP
+        gemm_w(true, T_AOP, 0, T_A, kH, 128, 32, false);                  // up1 -> T_A
         tc::mma_commit(bar_acc);
         wait_opnd();                                                      // E2: h
         for (int l = 0; l < NA; ++l) {
-          gemm_w(false, OFF_H, kH, T_Q, 96, kH, 64, false);               // QKV_0
+          gemm_w(false, OFF_H, kH, T_QKV, 96, kH, 64, false);             // QKV_0 -> buf 0
           tc::mma_commit(bar_qkv);
-          wait_opnd();                                                    // E_qkv_0
+          gemm_w(false, OFF_H, kH, T_QKV + 96, 96, kH, 64, false);        // QKV_1 -> buf 1
+          tc::mma_commit(bar_qkv);
           for (int j = 0; j < kHeads; ++j) {
-            {                                                             // S_j = Q_j K_j^T
-              const uint32_t idesc = tc::idesc_bf16(128, kKP);
-              for (int ks = 0; ks < kDH; ks += 16)
-                tc::mma_bf16(tmem + T_B,
-                             tc::smem_desc(sbase + OFF_Q + (ks >> 3) * 128, 128, kDH * 16),
-                             tc::smem_desc(sbase + OFF_K + (ks >> 3) * 128, 128, kDH * 16), idesc,
-                             ks > 0);
-              tc::mma_commit(bar_s);
-            }
-            if (j + 1 < kHeads) {                                          // QKV_{j+1} (T_Q free)
-              gemm_w(false, OFF_H, kH, T_Q, 96, kH, 64, false);
+            wait_opnd();                                                  // O_j ready, buf j%2 free
+            gemm_w(false, OFF_O + 8192 * (j & 1), kDH, T_A, kH, kDH, 32, j > 0);  // acc += O_j Wo_j
+            if (j + 2 < kHeads) {
+              gemm_w(false, OFF_H, kH, T_QKV + 96 * (j & 1), 96, kH, 64, false);  // QKV_{j+2}
               tc::mma_commit(bar_qkv);
             }
-            wait_opnd();                                                  // E_soft_j: P_j in TMEM
-            {                                                             // O_j = P_j V_j
-              const uint32_t idesc = tc::idesc_bf16(128, kDH);
-              for (int ks = 0; ks < kKP; ks += 16)
-                tc::mma_bf16_ta(tmem + T_B + T_PO, tmem + T_B + (ks >> 1),
-                                tc::smem_desc(sbase + OFF_V + (ks >> 3) * 128, 128, kKP * 16),
-                                idesc, ks > 0);
-              tc::mma_commit(bar_pv);
-            }
-            wait_opnd();                                                  // E_o_j: O_j in smem
-            gemm_w(false, OFF_O, kDH, T_A, kH, kDH, 32, j > 0);           // acc += O_j Wo_j
-            if (j + 1 < kHeads) wait_opnd();                              // E_qkv_{j+1}
           }
           tc::mma_commit(bar_acc);
           wait_opnd();                                                    // E_resid
@@ -305,12 +397,12 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
         for (int r = 0; r < NR; ++r) {
           gemm_w(false, OFF_H, kH, T_B, 128, kH, 64, false);              // G1 half 0
           tc::mma_commit(bar_acc);
-          wait_opnd();                                                    // r_h0 -> T_Q
-          gemm_w(true, T_Q, 0, T_A, kH, 128, 32, false);                  // G2 part 0
+          wait_opnd();                                                    // r_h0 -> T_AOP
+          gemm_w(true, T_AOP, 0, T_A, kH, 128, 32, false);                // G2 part 0
           gemm_w(false, OFF_H, kH, T_B, 128, kH, 64, false);              // G1 half 1
           tc::mma_commit(bar_acc);
-          wait_opnd();                                                    // r_h1 -> T_Q
-          gemm_w(true, T_Q, 0, T_A, kH, 128, 32, true);                   // G2 part 1
+          wait_opnd();                                                    // r_h1 -> T_AOP
+          gemm_w(true, T_AOP, 0, T_A, kH, 128, 32, true);                 // G2 part 1
           tc::mma_commit(bar_acc);
           wait_opnd();                                                    // E_resid
         }
@@ -322,12 +414,13 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
       }
     }
   } else {
-    // ------------------------------------------------ epilogue (128 threads)
-    const uint32_t q = warp & 3;
+    // ------------------------------------------------ epilogue (256 threads)
+    const uint32_t q = warp & 3;                       // TMEM lane quarter
+    const uint32_t hh = (warp - 2) >> 2;               // which of the quarter's two warps
     const uint32_t r = 32 * q + lane;                  // tile row == TMEM lane
     const uint32_t tl = tmem + ((32 * q) << 16);       // this warp's lane quarter
-    float* rowdot = reinterpret_cast<float*>(smem + OFF_DOT);
-    uint32_t ph_acc = 0, ph_qkv = 0, ph_s = 0, ph_pv = 0;
+    float* rowdot = reinterpret_cast<float*>(smem + OFF_DOT);   // [2][128]
+    uint32_t ph_acc = 0, ph_qkv = 0;
     auto wait_on = [&](uint32_t bar, uint32_t& ph) {
       tc::mbar_wait(bar, ph);
       ph ^= 1;
@@ -338,46 +431,17 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
       tc::tc_fence_before();
       tc::mbar_arrive(bar_opnd);
     };
+    // column split between the quarter's two warps
+    auto lo_of = [&](int n) { return (int)hh * (n / 2); };
+    auto hi_of = [&](int n) { return ((int)hh + 1) * (n / 2); };
     const uint32_t slot = r / kL;                      // candidate slot (5 = pad rows)
     const uint32_t kk = r - slot * kL;
     const bool real = r < kCand * kL;
-    const uint32_t s_lo = (32 * q) / kL;
     const float sm_scale = 1.4426950408889634f / sqrtf((float)kDH);  // log2(e)/sqrt(d_h)
-
-    auto e_qkv = [&](int l, int j) {
-      wait_on(bar_qkv, ph_qkv);
-      float v[32], b[32];
-      uint32_t pk[16];
-      tc::tmem_ld32(tl + T_Q + 0, v);
-      vec32(vs + a.bq[l] + kDH * j, b);
-      tc::tmem_wait_ld();
-#pragma unroll
-      for (int i = 0; i < 16; ++i) pk[i] = tc::pack_bf16(v[2 * i] + b[2 * i], v[2 * i + 1] + b[2 * i + 1]);
-      store_row32(smem, OFF_Q, r, 0, kDH, pk);
-      tc::tmem_ld32(tl + T_Q + 32, v);
-      vec32(vs + a.bk[l] + kDH * j, b);
-      tc::tmem_wait_ld();
-      if (real) {
-#pragma unroll
-        for (int i = 0; i < 16; ++i) pk[i] = tc::pack_bf16(v[2 * i] + b[2 * i], v[2 * i + 1] + b[2 * i + 1]);
-        store_row32(smem, OFF_K, 32 * slot + kk, 0, kDH, pk);
-      }
-      tc::tmem_ld32(tl + T_Q + 64, v);
-      vec32(vs + a.bv[l] + kDH * j, b);
-      tc::tmem_wait_ld();
-      if (real) {
-        const uint32_t kpos = 32 * slot + kk;
-#pragma unroll
-        for (int d = 0; d < kDH; ++d)
-          *reinterpret_cast<__nv_bfloat16*>(smem + OFF_V + tc::canon_off(d, kpos, kKP)) =
-              __float2bfloat16_rn(v[d] + b[d]);
-      }
-      signal();
-    };
 
     for (int64_t tile = blockIdx.x; tile < a.ntile; tile += gridDim.x) {
       const int64_t n = tile * kCand + slot;
-      {  // E0: X rows -> bf16 [128 x 32]
+      if (hh == 0) {  // E0: X rows -> bf16 [128 x 32]
         uint32_t pk[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) pk[i] = 0;
@@ -390,91 +454,68 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
           }
         }
         store_row32(smem, OFF_X, r, 0, kKX, pk);
-        signal();
       }
-      wait_on(bar_acc, ph_acc);
-      epi_relu_to_tmem(tl, T_B, 128, vs + a.up_b0, T_Q);                   // U1 -> TMEM
       signal();
       wait_on(bar_acc, ph_acc);
-      epi_relu_to_smem(smem, tl, T_A, kH, vs + a.up_b1, OFF_H, kH, r);     // h
+      epi_relu_to_tmem(tl, T_B, lo_of(128), hi_of(128), vs + a.up_b0, T_AOP);   // U1 -> TMEM
+      signal();
+      wait_on(bar_acc, ph_acc);
+      epi_relu_to_smem(smem, tl, T_A, lo_of(kH), hi_of(kH), vs + a.up_b1, OFF_H, kH, r);  // h
       signal();
       for (int l = 0; l < NA; ++l) {
-        e_qkv(l, 0);
         for (int j = 0; j < kHeads; ++j) {
-          // ---- softmax over the candidate's 25 keys; P_j (bf16) in place over S_j
-          wait_on(bar_s, ph_s);
-          {
-            float va[32], vb[32];
-            tc::tmem_ld32(tl + T_B + 32 * s_lo, va);
-            tc::tmem_ld32(tl + T_B + 32 * s_lo + 32, vb);
-            tc::tmem_wait_ld();
+          wait_on(bar_qkv, ph_qkv);
+          asm volatile("bar.sync 2, 256;" ::: "memory");  // all warps done reading head j-1
+          {  // QKV_j (TMEM) + bias -> Q, K (warp 0 of the quarter) / V (warp 1) tiles
+            const uint32_t tq = tl + T_QKV + 96 * (j & 1);
+            const uint32_t kpos = 32 * slot + kk;
+            float v[32], b[32];
             uint32_t pk[16];
+            if (hh == 0) {
+              tc::tmem_ld32(tq + 0, v);
+              vec32(vs + a.bq[l] + kDH * j, b);
+              tc::tmem_wait_ld();
 #pragma unroll
-            for (int i = 0; i < 16; ++i) pk[i] = 0;
-            if (real) {
-              const bool hi = slot != s_lo;
-              float x[kL];
-              float mx = -INFINITY;
+              for (int i = 0; i < 16; ++i) pk[i] = tc::pack_bf16(v[2 * i] + b[2 * i], v[2 * i + 1] + b[2 * i + 1]);
+              store_plain32(smem, OFF_Q + r * kRowB, pk);
+              tc::tmem_ld32(tq + 32, v);
+              vec32(vs + a.bk[l] + kDH * j, b);
+              tc::tmem_wait_ld();
 #pragma unroll
-              for (int c = 0; c < kL; ++c) {
-                x[c] = (hi ? vb[c] : va[c]) * sm_scale;
-                mx = fmaxf(mx, x[c]);
-              }
-              float sum = 0.f;
+              for (int i = 0; i < 16; ++i) pk[i] = tc::pack_bf16(v[2 * i] + b[2 * i], v[2 * i + 1] + b[2 * i + 1]);
+              if (real) store_plain32(smem, OFF_K + kpos * kRowB, pk);
+            } else {
+              tc::tmem_ld32(tq + 64, v);
+              vec32(vs + a.bv[l] + kDH * j, b);
+              tc::tmem_wait_ld();
 #pragma unroll
-              for (int c = 0; c < kL; ++c) { x[c] = exp2f(x[c] - mx); sum += x[c]; }
-              const float inv = 1.0f / sum;
-#pragma unroll
-              for (int i = 0; i < 16; ++i) {
-                const float p0 = (2 * i < kL) ? x[(2 * i) % kL] * inv : 0.f;
-                const float p1 = (2 * i + 1 < kL) ? x[(2 * i + 1) % kL] * inv : 0.f;
-                pk[i] = tc::pack_bf16(p0, p1);
-              }
+              for (int i = 0; i < 16; ++i) pk[i] = tc::pack_bf16(v[2 * i] + b[2 * i], v[2 * i + 1] + b[2 * i + 1]);
+              if (real) store_plain32(smem, OFF_V + kpos * kRowB, pk);
             }
-            const uint32_t zero[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
-#pragma unroll
-            for (int blk = 0; blk < kCand; ++blk) {
-              uint32_t o[16];
-#pragma unroll
-              for (int i = 0; i < 16; ++i) o[i] = (slot == (uint32_t)blk) ? pk[i] : zero[i];
-              tc::tmem_st16(tl + T_B + 16 * blk, o);
-            }
-            tc::tmem_wait_st();
           }
-          signal();
-          // ---- O_j -> bf16 smem operand
-          wait_on(bar_pv, ph_pv);
-          {
-            float v[32];
-            tc::tmem_ld32(tl + T_B + T_PO, v);
-            tc::tmem_wait_ld();
-            uint32_t pk[16];
-#pragma unroll
-            for (int i = 0; i < 16; ++i) pk[i] = tc::pack_bf16(v[2 * i], v[2 * i + 1]);
-            store_row32(smem, OFF_O, r, 0, kDH, pk);
-          }
-          signal();
-          if (j + 1 < kHeads) e_qkv(l, j + 1);
+          asm volatile("bar.sync 2, 256;" ::: "memory");  // Q/K/V of head j complete
+          attn_head_mma(smem, sbase, q, hh, lane, sm_scale, OFF_O + 8192 * (j & 1));
+          signal();                                       // O_j ready; QKV buffer j%2 free
         }
         wait_on(bar_acc, ph_acc);
-        epi_residual(smem, tl, vs + a.bo[l], r);
+        epi_residual(smem, tl, vs + a.bo[l], r, lo_of(kH), hi_of(kH));
         signal();
       }
       for (int rb = 0; rb < NR; ++rb) {
         wait_on(bar_acc, ph_acc);
-        epi_relu_to_tmem(tl, T_B, 128, vs + a.ra[rb], T_Q);
+        epi_relu_to_tmem(tl, T_B, lo_of(128), hi_of(128), vs + a.ra[rb], T_AOP);
         signal();
         wait_on(bar_acc, ph_acc);
-        epi_relu_to_tmem(tl, T_B, 128, vs + a.ra[rb] + 128, T_Q);
+        epi_relu_to_tmem(tl, T_B, lo_of(128), hi_of(128), vs + a.ra[rb] + 128, T_AOP);
         signal();
         wait_on(bar_acc, ph_acc);
-        epi_residual(smem, tl, vs + a.rb[rb], r);
+        epi_residual(smem, tl, vs + a.rb[rb], r, lo_of(kH), hi_of(kH));
         signal();
       }
       for (int t = 0; t < NT; ++t) {
         wait_on(bar_acc, ph_acc);
         float dot = 0.f;
-        for (int c = 0; c < kHD; c += 32) {
+        for (int c = lo_of(kHD); c < hi_of(kHD); c += 32) {
           float v[32], b[32], w[32];
           tc::tmem_ld32(tl + T_B + c, v);
           vec32(vs + a.c1[t] + c, b);
@@ -483,15 +524,16 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
 #pragma unroll
           for (int i = 0; i < 32; ++i) dot = fmaf(fmaxf(v[i] + b[i], 0.f), w[i], dot);
         }
-        rowdot[r] = dot;
+        rowdot[hh * 128 + r] = dot;
         tc::tc_fence_before();
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (r < kCand) {
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        if (hh == 0 && r < kCand) {
           const int64_t nn = tile * kCand + r;
           if (nn < a.N) {
-            float s = 0.f;
-            for (int l2 = 0; l2 < kL; ++l2) s += rowdot[r * kL + l2];  // fixed order (R34)
-            a.scores[nn * NT + t] = s + (float)kL * vs[a.c2[t]];
+            float s2 = 0.f;
+            for (int l2 = 0; l2 < kL; ++l2)  // fixed order (R34)
+              s2 += rowdot[r * kL + l2] + rowdot[128 + r * kL + l2];
+            a.scores[nn * NT + t] = s2 + (float)kL * vs[a.c2[t]];
           }
         }
         if (t < NT - 1) signal();
@@ -582,9 +624,10 @@ static std::vector<PackChunk> build_schedule(const tlp_ctx* ctx) {
         add(96, 64, k0, kH, {{0, o.Wq[l], kH, kDH * j}, {32, o.Wk[l], kH, kDH * j}, {64, o.Wv[l], kH, kDH * j}});
     };
     qkv(0);
+    qkv(1);
     for (int j = 0; j < kHeads; ++j) {
-      if (j + 1 < kHeads) qkv(j + 1);                      // issued right after S_j
-      add(256, 32, kDH * j, kH, {{0, o.Wo[l], kH, 0}});     // oproj_j after PV_j
+      add(256, 32, kDH * j, kH, {{0, o.Wo[l], kH, 0}});     // oproj_j once O_j is ready
+      if (j + 2 < kHeads) qkv(j + 2);                      // then QKV two heads ahead
     }
   }
   for (int r = 0; r < c.n_res; ++r) {
