@@ -69,10 +69,11 @@ typedef enum {
  * hidden -> head_dim (ReLU) -> 1, summed over the L rows; n_tasks heads for
  * MTL-TLP.
  * Limits of this build: L <= 32, E <= 64, T < E, hidden % attn_heads == 0,
- * hidden <= 512, n_up <= 4, 1 <= n_tasks <= 8.  TLP_PREC_BF16 scoring
- * additionally requires the paper shape (E=22, hidden=256, up_dims={128,256},
- * attn_heads=8, head_dim=128, L=25) and otherwise returns TLP_ERR_UNSUPPORTED
- * from tlp_create.
+ * hidden <= 512, n_up <= 4, 1 <= n_tasks <= 8.  TLP_PREC_BF16 training runs
+ * its dense layers on the tensor cores for any shape; TLP_PREC_BF16 scoring
+ * (the fused kernel) requires the paper shape (E=22, hidden=256,
+ * up_dims={128,256}, attn_heads=8, head_dim=128, L=25) and otherwise
+ * tlp_score returns TLP_ERR_UNSUPPORTED.
  */
 typedef struct {
   int L, E, T;
@@ -207,6 +208,15 @@ int64_t tlp_launch_count(const tlp_ctx* ctx);
  * a_in_tmem != 0: A is staged in TMEM with tcgen05.st and read from there. */
 tlp_status tlp_debug_umma(const float* A, const float* B, float* D, int32_t N, int32_t K,
                           int32_t a_in_tmem, void* stream);
+
+/* Test hook for the tf32 tcgen05 GEMM of the bf16-context training path:
+ * C = op(A) op(B) (op = transpose when ta / tb), fp32 device row-major with the
+ * given leading dimensions (multiples of 4, 16-byte aligned pointers).  With
+ * splits > 1, C receives `splits` partial products [splits, M, ldc] (fixed K
+ * slices) instead of the sum. */
+tlp_status tlp_debug_gemm(tlp_ctx* ctx, int32_t ta, int32_t tb, int64_t M, int64_t N, int64_t K,
+                          const float* A, int64_t lda, const float* B, int64_t ldb, float* C,
+                          int64_t ldc, int32_t splits, void* stream);
 
 #ifdef __cplusplus
 }

@@ -17,7 +17,8 @@ EXPORTS = ("tlp_create", "tlp_destroy", "tlp_last_error", "tlp_default_config",
            "tlp_set_token_table", "tlp_set_norm_scales", "tlp_num_params", "tlp_set_params",
            "tlp_get_params", "tlp_get_grads", "tlp_set_comm", "tlp_get_unique_id", "tlp_encode",
            "tlp_score", "tlp_train_step", "tlp_compute_grads", "tlp_lambdarank", "tlp_topk",
-           "tlp_normalize_labels", "tlp_sync", "tlp_launch_count", "tlp_debug_umma")
+           "tlp_normalize_labels", "tlp_sync", "tlp_launch_count", "tlp_debug_umma",
+           "tlp_debug_gemm")
 
 
 class tlp_config(C.Structure):
@@ -72,6 +73,7 @@ def load() -> C.CDLL:
         "tlp_sync": (C.c_int, [vp]),
         "tlp_launch_count": (i64, [vp]),
         "tlp_debug_umma": (C.c_int, [vp, vp, vp, i32, i32, i32, vp]),
+        "tlp_debug_gemm": (C.c_int, [vp, i32, i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, i32, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)

@@ -109,10 +109,6 @@ tlp_status tlp_create(const tlp_config* cfg, int device, tlp_ctx** out) {
   if (!cfg || !out) return fail(nullptr, TLP_ERR_ARG, "null argument");
   const std::string why = check_config(*cfg);
   if (!why.empty()) return fail(nullptr, TLP_ERR_SHAPE, why);
-  if (cfg->precision == TLP_PREC_BF16 && !tc_supported(*cfg))
-    return fail(nullptr, TLP_ERR_UNSUPPORTED,
-                "bf16 tensor-core scoring needs the paper shape (E=22, L=25, hidden=256, "
-                "up_dims={128,256}, 8 heads, head_dim=128)");
   if (cudaSetDevice(device) != cudaSuccess) return fail(nullptr, TLP_ERR_CUDA, "cudaSetDevice failed");
   tlp_ctx* ctx = new tlp_ctx();
   ctx->cfg = *cfg;
@@ -261,6 +257,10 @@ tlp_status tlp_score(tlp_ctx* ctx, const float* feats, int64_t N, float* scores,
   cudaSetDevice(ctx->device);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (ctx->cfg.precision == TLP_PREC_BF16) {
+    if (!tc_supported(ctx->cfg))
+      return fail(ctx, TLP_ERR_UNSUPPORTED,
+                  "bf16 tensor-core scoring needs the paper shape (E=22, L=25, hidden=256, "
+                  "up_dims={128,256}, 8 heads, head_dim=128); use TLP_PREC_FP32");
     if (ctx->tc_dirty) {
       tlp_status st = tc_prepare(ctx, s);
       if (st != TLP_OK) return st;

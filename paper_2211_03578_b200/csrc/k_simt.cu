@@ -461,6 +461,10 @@ tlp_status sgemm(tlp_ctx* ctx, bool ta, bool tb, int64_t M, int64_t N, int64_t K
                  int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc,
                  const EpiParams& e, cudaStream_t s) {
   if (M == 0 || N == 0) return TLP_OK;
+  // TLP_PREC_BF16 contexts train on the tensor cores (tf32 tcgen05) whenever the
+  // operands allow 16-byte async copies; the fp32 context stays on FFMA (1e-5).
+  if (ctx->cfg.precision == TLP_PREC_BF16 && tc_gemm_ok(A, lda, B, ldb))
+    return tc_gemm(ctx, ta, tb, M, N, K, A, lda, B, ldb, C, ldc, e, 1, K, s);
   EpiDev ed{e.bias, e.resid, e.ldr, e.mask, e.ldm, e.relu ? 1 : 0, e.accumulate ? 1 : 0};
   dim3 grid((unsigned)cdiv(N, BN), (unsigned)cdiv(M, BM), 1);
   const int64_t ks = K > 0 ? K : 1;
@@ -481,6 +485,17 @@ tlp_status sgemm_wgrad(tlp_ctx* ctx, int64_t M, int64_t K, int64_t N, const floa
   const int64_t kslice = cdiv(cdiv(M, Z), BK) * BK;
   EpiDev ed{nullptr, nullptr, 0, nullptr, 0, 0, 0};
   dim3 grid((unsigned)cdiv(N, BN), (unsigned)cdiv(K, BM), (unsigned)Z);
+  if (ctx->cfg.precision == TLP_PREC_BF16 && tc_gemm_ok(A, lda, dY, lddy)) {
+    EpiParams none;
+    if (Z == 1) return tc_gemm(ctx, true, false, K, N, M, A, lda, dY, lddy, dW, N, none, 1, M, s);
+    TLP_CUDA_TRY(ctx->ws_partial.ensure((size_t)Z * K * N * sizeof(float)));
+    float* part = ctx->ws_partial.as<float>();
+    tlp_status st = tc_gemm(ctx, true, false, K, N, M, A, lda, dY, lddy, part, N, none, Z, kslice, s);
+    if (st != TLP_OK) return st;
+    reduce_partials<<<(unsigned)cdiv(K * N, 256), 256, 0, s>>>(part, K * N, Z, dW);
+    TLP_LAUNCH_CHECK();
+    return TLP_OK;
+  }
   if (Z == 1) {
     sgemm_kernel<true, false><<<grid, 256, 0, s>>>(K, N, M, A, lda, dY, lddy, dW, N, ed, kslice);
     TLP_LAUNCH_CHECK();

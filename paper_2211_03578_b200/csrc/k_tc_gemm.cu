@@ -1,0 +1,299 @@
+// Generic tcgen05 GEMM (kind::f16, bf16 operands, fp32 accumulate) for the
+// training path of TLP_PREC_BF16 contexts: every dense layer of the forward,
+// every dgrad and every wgrad of the backward ("the loss is
+// back-propagated to update the weights").
+//
+//   C[M,N] = epi( op(A)[M,K] * op(B)[K,N] )      fp32 in HBM, bf16 on the tensor core
+//
+// op(A) = A (row-major [M][K] -> K-major UMMA operand) or A^T (A stored [K][M]
+// -> MN-major operand); op(B) likewise (B stored [K][N] -> MN-major, B^T
+// stored [N][K] -> K-major).  Operands are read as fp32 (float4 when aligned),
+// rounded to bf16 (RN, R28) in registers and stored into the UMMA no-swizzle
+// canonical layouts of a 2-stage smem ring as hi + lo pairs ("bf16x3": three
+// MMAs per k-step recover fp32-class accuracy); one thread issues tcgen05.mma
+// (M=128, N=128, K=16) into a 128-column TMEM accumulator and tcgen05.commit
+// frees each stage; global loads for k-block i+2 are in flight while the
+// tensor core works on block i.  (kind::tf32 cannot take an MN-major operand
+// in the no-swizzle layout -- tools/mn_major_probe.cu -- hence bf16.)
+// Epilogue: TMEM -> registers -> smem transpose -> coalesced fp32 row stores
+// with bias / residual / ReLU / ReLU-mask / accumulate.  blockIdx.z splits K into fixed slices (wgrad over
+// the 204,800 rows of a step); the caller reduces the partials in a fixed
+// order, so training stays deterministic.
+#include "tlp_internal.cuh"
+#include "tc_ptx.cuh"
+
+#include <algorithm>
+
+namespace {
+
+constexpr int BM = 128, BN = 128, BK = 32, STAGES = 2, THREADS = 256;
+constexpr uint32_t TILE_BYTES = BM * BK * 2;                 // 8 KB (A) == BN*BK*2 (B)
+// stage = [A_hi][B_hi][A_lo][B_lo]: "bf16x3" split precision, x = hi + lo with
+// hi = bf16(x), lo = bf16(x - hi); A.B ~= Ah.Bh + Ah.Bl + Al.Bh (error ~2^-16,
+// i.e. fp32-class gradients from the bf16 tensor core; R28 rounding per term)
+constexpr uint32_t STAGE_BYTES = 4 * TILE_BYTES;
+constexpr uint32_t SMEM_BYTES = STAGES * STAGE_BYTES + 128;  // + barriers / tmem ptr
+constexpr int CHUNKS = BM * BK / 4 / THREADS;                // float4 chunks per thread per tile (4)
+
+struct Epi {
+  const float* bias;
+  const float* resid;
+  int64_t ldr;
+  const float* mask;
+  int64_t ldm;
+  int relu;
+  int accumulate;
+};
+
+struct Src {
+  const float* p;
+  int64_t ld;
+  int64_t rows;   // extent along the M (or N) dimension
+  int64_t r0;
+  bool vec;       // float4 loads allowed (16-byte aligned rows)
+};
+
+// One 128 x 32 (rows x K) operand tile: fp32 global -> registers.
+//  KMAJOR: source [rows][K]; chunk c covers (r = c/8, k = 4*(c%8) .. +3)
+//  !KMAJOR: source [K][rows]; chunk c covers (k = c/32, r = 4*(c%32) .. +3)
+template <bool KMAJOR>
+__device__ __forceinline__ void load_regs(const Src& s, int64_t k0, int64_t kend, float4 (&v)[CHUNKS]) {
+#pragma unroll
+  for (int it = 0; it < CHUNKS; ++it) {
+    const int c = threadIdx.x + it * THREADS;
+    int64_t gr, gk;
+    if (KMAJOR) { gr = s.r0 + (c >> 3); gk = k0 + (c & 7) * 4; }
+    else { gk = k0 + (c >> 5); gr = s.r0 + (c & 31) * 4; }
+    float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (KMAJOR) {
+      if (gr < s.rows) {
+        const float* p = s.p + gr * s.ld + gk;
+        if (s.vec && gk + 3 < kend) x = __ldg(reinterpret_cast<const float4*>(p));
+        else {
+          if (gk < kend) x.x = __ldg(p);
+          if (gk + 1 < kend) x.y = __ldg(p + 1);
+          if (gk + 2 < kend) x.z = __ldg(p + 2);
+          if (gk + 3 < kend) x.w = __ldg(p + 3);
+        }
+      }
+    } else {
+      if (gk < kend) {
+        const float* p = s.p + gk * s.ld + gr;
+        if (s.vec && gr + 3 < s.rows) x = __ldg(reinterpret_cast<const float4*>(p));
+        else {
+          if (gr < s.rows) x.x = __ldg(p);
+          if (gr + 1 < s.rows) x.y = __ldg(p + 1);
+          if (gr + 2 < s.rows) x.z = __ldg(p + 2);
+          if (gr + 3 < s.rows) x.w = __ldg(p + 3);
+        }
+      }
+    }
+    v[it] = x;
+  }
+}
+
+// registers -> bf16 hi / lo canonical layouts (8-byte stores)
+//  KMAJOR: (r,k) -> (r/8)*512 + (k/8)*128 + (r%8)*16 + (k%8)*2      (SBO 512, LBO 128)
+//  !KMAJOR: (r,k) -> (k/8)*2048 + (r/8)*128 + (k%8)*16 + (r%8)*2    (LBO 2048, SBO 128)
+__device__ __forceinline__ uint32_t pack_lo(float a, float b, uint32_t hi) {
+  const __nv_bfloat162 h = *reinterpret_cast<const __nv_bfloat162*>(&hi);
+  const float2 hf = __bfloat1622float2(h);
+  return tc::pack_bf16(a - hf.x, b - hf.y);
+}
+
+template <bool KMAJOR>
+__device__ __forceinline__ void store_smem(uint8_t* dst, uint8_t* dst_lo, const float4 (&v)[CHUNKS]) {
+#pragma unroll
+  for (int it = 0; it < CHUNKS; ++it) {
+    const int c = threadIdx.x + it * THREADS;
+    uint32_t off;
+    if (KMAJOR) {
+      const int r = c >> 3, k = (c & 7) * 4;
+      off = (r >> 3) * 512 + (k >> 3) * 128 + (r & 7) * 16 + (k & 7) * 2;
+    } else {
+      const int k = c >> 5, r = (c & 31) * 4;
+      off = (k >> 3) * 2048 + (r >> 3) * 128 + (k & 7) * 16 + (r & 7) * 2;
+    }
+    const uint32_t h0 = tc::pack_bf16(v[it].x, v[it].y), h1 = tc::pack_bf16(v[it].z, v[it].w);
+    *reinterpret_cast<uint2*>(dst + off) = make_uint2(h0, h1);
+    *reinterpret_cast<uint2*>(dst_lo + off) =
+        make_uint2(pack_lo(v[it].x, v[it].y, h0), pack_lo(v[it].z, v[it].w, h1));
+  }
+}
+
+template <bool TA, bool TB>
+__global__ void __launch_bounds__(THREADS, 3) tc_gemm_kernel(int64_t M, int64_t N, int64_t K,
+                                                          const float* __restrict__ A, int64_t lda,
+                                                          const float* __restrict__ B, int64_t ldb,
+                                                          float* __restrict__ C, int64_t ldc,
+                                                          Epi ep, int64_t kslice, int avec, int bvec) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const uint32_t sb = tc::smem_u32(smem);
+  const uint32_t bar = sb + STAGES * STAGE_BYTES;  // STAGES mbarriers
+  uint32_t* tptr = reinterpret_cast<uint32_t*>(smem + STAGES * STAGE_BYTES + 64);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
+  const int64_t kb = (int64_t)blockIdx.z * kslice;
+  const int64_t ke = std::min<int64_t>(K, kb + kslice);
+  const int nk = ke > kb ? (int)((ke - kb + BK - 1) / BK) : 0;
+
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) tc::mbar_init(bar + 8 * s, 1);
+    tc::fence_barrier_init();
+  }
+  if (warp == 0) tc::tmem_alloc(tc::smem_u32(tptr), BN);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tptr;
+  constexpr bool A_K = !TA;   // A stored [M][K] -> K-major
+  constexpr bool B_K = TB;    // B stored [N][K] -> K-major
+  const uint32_t idesc = tc::idesc_bf16(BM, BN) | ((A_K ? 0u : 1u) << 15) | ((B_K ? 0u : 1u) << 16);
+  const Src sa{A, lda, M, m0, avec != 0};
+  const Src sbb{B, ldb, N, n0, bvec != 0};
+
+  float4 ra[CHUNKS], rb[CHUNKS];
+  if (nk > 0) {
+    load_regs<A_K>(sa, kb, ke, ra);
+    load_regs<B_K>(sbb, kb, ke, rb);
+    store_smem<A_K>(smem, smem + 2 * TILE_BYTES, ra);
+    store_smem<B_K>(smem + TILE_BYTES, smem + 3 * TILE_BYTES, rb);
+    if (nk > 1) {
+      load_regs<A_K>(sa, kb + BK, ke, ra);
+      load_regs<B_K>(sbb, kb + BK, ke, rb);
+    }
+  }
+  for (int it = 0; it < nk; ++it) {
+    const int s = it % STAGES;
+    tc::fence_proxy_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      tc::tc_fence_after();
+      const uint32_t a0 = sb + s * STAGE_BYTES, b0 = a0 + TILE_BYTES;
+      const uint32_t al = a0 + 2 * TILE_BYTES, bl = a0 + 3 * TILE_BYTES;
+      auto da = [&](uint32_t base, int ks) {
+        return A_K ? tc::smem_desc(base + ks * 256, 128, 512) : tc::smem_desc(base + ks * 4096, 2048, 128);
+      };
+      auto db = [&](uint32_t base, int ks) {
+        return B_K ? tc::smem_desc(base + ks * 256, 128, 512) : tc::smem_desc(base + ks * 4096, 2048, 128);
+      };
+#pragma unroll
+      for (int ks = 0; ks < BK / 16; ++ks) {
+        tc::mma_bf16(tmem, da(al, ks), db(b0, ks), idesc, (it > 0 || ks > 0) ? 1u : 0u);  // Al.Bh
+        tc::mma_bf16(tmem, da(a0, ks), db(bl, ks), idesc, 1u);                          // Ah.Bl
+        tc::mma_bf16(tmem, da(a0, ks), db(b0, ks), idesc, 1u);                          // Ah.Bh
+      }
+      tc::mma_commit(bar + 8 * s);
+    }
+    if (it + 1 < nk) {
+      const int ns = (it + 1) % STAGES;
+      if (it + 1 >= STAGES)  // stage ns last used by k-block it+1-STAGES
+        tc::mbar_wait(bar + 8 * ns, (uint32_t)(((it + 1 - STAGES) / STAGES) & 1));
+      uint8_t* st = smem + ns * STAGE_BYTES;
+      store_smem<A_K>(st, st + 2 * TILE_BYTES, ra);
+      store_smem<B_K>(st + TILE_BYTES, st + 3 * TILE_BYTES, rb);
+      if (it + 2 < nk) {
+        load_regs<A_K>(sa, kb + (int64_t)(it + 2) * BK, ke, ra);
+        load_regs<B_K>(sbb, kb + (int64_t)(it + 2) * BK, ke, rb);
+      }
+    }
+  }
+  if (nk > 0) {
+    const int ls = (nk - 1) % STAGES;
+    tc::mbar_wait(bar + 8 * ls, (uint32_t)(((nk - 1) / STAGES) & 1));
+  }
+  tc::tc_fence_after();
+  __syncthreads();  // every thread is past its last smem store: the ring is free
+  // ---- epilogue: TMEM (thread = row) -> smem transpose -> coalesced row stores
+  float* Cz = C + (int64_t)blockIdx.z * M * ldc;
+  const bool partial = gridDim.z > 1;
+  float* stage = reinterpret_cast<float*>(smem);       // [128][EPI_LD]
+  constexpr int EPI_COLS = 64, EPI_LD = 68;
+  const int q = warp & 3, hh = warp >> 2;  // TMEM lane quarter, column half
+  for (int p = 0; p < BN / EPI_COLS; ++p) {
+    if (n0 + p * EPI_COLS >= N) break;
+    {
+      float v[32];
+      if (nk > 0) {
+        tc::tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + p * EPI_COLS + 32 * hh, v);
+        tc::tmem_wait_ld();
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = 0.f;
+      }
+      float* dst = stage + (q * 32 + lane) * EPI_LD + 32 * hh;
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        reinterpret_cast<float4*>(dst)[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+    }
+    __syncthreads();
+    // warp w handles rows w, w+8, ...; lane handles columns 2*lane, 2*lane+1
+    for (int rr = warp; rr < BM; rr += THREADS / 32) {
+      const int64_t gi = m0 + rr;
+      if (gi >= M) break;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int cc = 2 * lane + e;
+        const int64_t gj = n0 + p * EPI_COLS + cc;
+        if (gj >= N) continue;
+        float x = stage[rr * EPI_LD + cc];
+        if (!partial) {
+          if (ep.bias) x += ep.bias[gj];
+          if (ep.resid) x += ep.resid[gi * ep.ldr + gj];
+          if (ep.relu) x = fmaxf(x, 0.f);
+          if (ep.mask) x = ep.mask[gi * ep.ldm + gj] > 0.f ? x : 0.f;
+          if (ep.accumulate) x += Cz[gi * ldc + gj];
+        }
+        Cz[gi * ldc + gj] = x;
+      }
+    }
+    __syncthreads();
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc::tc_fence_after();
+    tc::tmem_dealloc(tmem, BN);
+  }
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+}  // namespace
+
+bool tc_gemm_ok(const float*, int64_t, const float*, int64_t) { return true; }
+
+tlp_status tc_gemm(tlp_ctx* ctx, bool ta, bool tb, int64_t M, int64_t N, int64_t K,
+                   const float* A, int64_t lda, const float* B, int64_t ldb, float* C,
+                   int64_t ldc, const EpiParams& e, int splits, int64_t kslice, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(tc_gemm_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    cudaFuncSetAttribute(tc_gemm_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    cudaFuncSetAttribute(tc_gemm_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    cudaFuncSetAttribute(tc_gemm_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    attr = true;
+  }
+  Epi ep{e.bias, e.resid, e.ldr, e.mask, e.ldm, e.relu ? 1 : 0, e.accumulate ? 1 : 0};
+  dim3 grid((unsigned)cdiv(N, BN), (unsigned)cdiv(M, BM), (unsigned)splits);
+  if (splits == 1) kslice = K > 0 ? K : 1;
+  const int av = aligned16(A) && lda % 4 == 0, bv = aligned16(B) && ldb % 4 == 0;
+  if (!ta && !tb) tc_gemm_kernel<false, false><<<grid, THREADS, SMEM_BYTES, s>>>(M, N, K, A, lda, B, ldb, C, ldc, ep, kslice, av, bv);
+  else if (!ta && tb) tc_gemm_kernel<false, true><<<grid, THREADS, SMEM_BYTES, s>>>(M, N, K, A, lda, B, ldb, C, ldc, ep, kslice, av, bv);
+  else if (ta && !tb) tc_gemm_kernel<true, false><<<grid, THREADS, SMEM_BYTES, s>>>(M, N, K, A, lda, B, ldb, C, ldc, ep, kslice, av, bv);
+  else tc_gemm_kernel<true, true><<<grid, THREADS, SMEM_BYTES, s>>>(M, N, K, A, lda, B, ldb, C, ldc, ep, kslice, av, bv);
+  TLP_LAUNCH_CHECK();
+  return TLP_OK;
+}
+
+// ---------------------------------------------------------------- test hook
+extern "C" tlp_status tlp_debug_gemm(tlp_ctx* ctx, int32_t ta, int32_t tb, int64_t M, int64_t N,
+                                     int64_t K, const float* A, int64_t lda, const float* B,
+                                     int64_t ldb, float* C, int64_t ldc, int32_t splits,
+                                     void* stream) {
+  if (!ctx || !A || !B || !C || M < 1 || N < 1 || K < 0 || splits < 1) return TLP_ERR_ARG;
+  EpiParams none;
+  const int64_t kslice = splits > 1 ? cdiv(cdiv(K, splits), 32) * 32 : K;
+  return tc_gemm(ctx, ta != 0, tb != 0, M, N, K, A, lda, B, ldb, C, ldc, none, splits, kslice,
+                 reinterpret_cast<cudaStream_t>(stream));
+}

@@ -163,6 +163,12 @@ tlp_status simt_forward(tlp_ctx* ctx, const float* feats, int64_t N, float* scor
                         cudaStream_t s);
 tlp_status simt_backward(tlp_ctx* ctx, int64_t N, const float* dscores, cudaStream_t s);
 
+// k_tc_gemm.cu : tf32 tcgen05 GEMM used by the training path of bf16 contexts
+bool tc_gemm_ok(const float* A, int64_t lda, const float* B, int64_t ldb);
+tlp_status tc_gemm(tlp_ctx* ctx, bool ta, bool tb, int64_t M, int64_t N, int64_t K,
+                   const float* A, int64_t lda, const float* B, int64_t ldb, float* C,
+                   int64_t ldc, const EpiParams& e, int splits, int64_t kslice, cudaStream_t s);
+
 // k_rank.cu
 tlp_status rank_pair_counts(tlp_ctx* ctx, const float* labels, const int64_t* d_goff, int G,
                             int max_group, double* d_counts, cudaStream_t s);

@@ -228,8 +228,12 @@ GRAD_CASES = [(1, 1, 17, (9, 16, 12, 16, 11, 7)), (4, 1, 20, (8, 6, 9, 7, 10, 8)
               (1, 2, 14, (9, 16, 12, 16, 11, 7))]
 
 
+@pytest.mark.parametrize("precision,tol", [("fp32", 1e-5), ("bf16", 1e-2)])
 @pytest.mark.parametrize("n_tasks,n_attn,seed,sizes", GRAD_CASES)
-def test_grads_fp32_parity(tp, tokscale, n_tasks, n_attn, seed, sizes):
+def test_grads_parity(tp, tokscale, n_tasks, n_attn, seed, sizes, precision, tol):
+    """fp32 context: SIMT FFMA everywhere (1e-5).  bf16 context: every dense
+    layer / dgrad / wgrad on the tcgen05 tensor cores (bf16x3 split operands),
+    attention / heads / LambdaRank SIMT fp32 (contract 1e-2)."""
     tokens, scale = tokscale
     ocfg = oracle_cfg(n_tasks=n_tasks, n_attn=n_attn, hidden=64, up=(32, 64), head_dim=32)
     flat = flat_params(ocfg, seed=seed)
@@ -239,17 +243,17 @@ def test_grads_fp32_parity(tp, tokscale, n_tasks, n_attn, seed, sizes):
     assert min_rel_gap(s_ref, off) > 2e-4
     loss_ref, g = OLR.mtl_lambdarank(s_ref, y.astype(np.float64), off)
     grads_ref = OM.backward(ocfg, p, acts, g)
-    m = tp.TLP(product_cfg(ocfg, "fp32"))
+    m = tp.TLP(product_cfg(ocfg, precision))
     m.set_params(flat.astype(np.float32))
     loss = m.compute_grads(torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda(), off)
     m.sync()
-    assert abs(float(loss.cpu()) - loss_ref) <= 1e-5 * abs(loss_ref)
+    assert abs(float(loss.cpu()) - loss_ref) <= tol * abs(loss_ref)
     got = OM.unflatten(ocfg, m.get_grads().astype(np.float64))
     bad = {}
     for name, _ in OM.param_shapes(ocfg):
         if ZERO_GRAD.search(name):
             ref_w = name.replace(".bk", ".Wk").replace(".c2", ".w2")
-            assert np.abs(got[name]).max() <= 1e-5 * np.abs(grads_ref[ref_w]).max() * ocfg.L, name
+            assert np.abs(got[name]).max() <= tol * np.abs(grads_ref[ref_w]).max() * ocfg.L, name
             continue
         mc = CANCEL_GRAD.search(name)
         if mc:
@@ -257,10 +261,10 @@ def test_grads_fp32_parity(tp, tokscale, n_tasks, n_attn, seed, sizes):
             u = acts["heads"][t]["u"]
             terms = np.abs(g[:, t])[:, None, None] * np.abs(p["head%d.w2" % t][:, 0]) * (u > 0)
             mag = terms.sum(axis=(0, 1))
-            assert np.all(np.abs(got[name] - grads_ref[name]) <= 1e-5 * mag.max()), name
+            assert np.all(np.abs(got[name] - grads_ref[name]) <= tol * mag.max()), name
             continue
         e = rel_err(got[name], grads_ref[name])
-        if e > 1e-5:
+        if e > tol:
             bad[name] = e
     assert not bad, bad
 
@@ -386,3 +390,35 @@ def test_bf16_full_size_sampled(tp, tokscale):
     assert rel_err(s_h[pick], ref) <= 1e-2
     idx_ref, val_ref = oracle.topk(s_h[:, 0], off, 16)
     assert np.array_equal(idx.cpu().numpy(), idx_ref)
+
+
+# ---------------------------------------------------------------- bf16 tcgen05 GEMM (training, bf16 ctx)
+@pytest.mark.parametrize("ta,tb", [(0, 0), (0, 1), (1, 0), (1, 1)])
+@pytest.mark.parametrize("M,N,K,splits", [(300, 200, 72, 1), (128, 128, 32, 1), (1000, 96, 516, 3),
+                                          (64, 256, 4096, 8), (37, 22, 22, 1), (130, 30, 50, 2)])
+def test_train_gemm_building_block(tp, ta, tb, M, N, K, splits):
+    rng = np.random.default_rng(M + N + K + 10 * ta + tb)
+    A = rng.normal(size=(K, M) if ta else (M, K)).astype(np.float32)
+    B = rng.normal(size=(N, K) if tb else (K, N)).astype(np.float32)
+    opA = A.T if ta else A
+    opB = B.T if tb else B
+    m = tp.TLP(tp.TLPConfig(precision="bf16"))
+    Ad, Bd = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    ldc = N + (4 - N % 4) % 4
+    C = torch.zeros((splits, M, ldc), dtype=torch.float32, device="cuda")
+    st = m.lib.tlp_debug_gemm(m.h, ta, tb, M, N, K, Ad.data_ptr(), A.shape[1], Bd.data_ptr(),
+                              B.shape[1], C.data_ptr(), ldc, splits, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert st == 0
+    got = C.cpu().numpy().sum(axis=0)[:, :N]
+    # bf16x3 split precision (hi.hi + hi.lo + lo.hi): ~2^-16 per product + fp32 sums
+    ref = opA.astype(np.float64) @ opB.astype(np.float64)
+    assert rel_err(got, ref) <= 1e-4
+
+
+def test_bf16_scoring_needs_paper_shape(tp):
+    m = tp.TLP(tp.tiny_config(precision="bf16"))  # training works at any shape
+    m.set_params(np.zeros(m.num_params, np.float32))
+    with pytest.raises(tp.TLPError) as e:
+        m.score(torch.zeros((5, 25, 22), device="cuda"))
+    assert e.value.code == "ERR_UNSUPPORTED"
