@@ -189,6 +189,14 @@ tlp_status tlp_topk(tlp_ctx* ctx, const float* scores, int32_t score_stride, int
                     const int64_t* task_off, int32_t T, int32_t k, int64_t shard_base,
                     int64_t* idx_out, float* val_out, void* stream);
 
+/* Merge of per-shard top-k lists (the second half of the sharded tlp_topk,
+ * exposed for callers that gather the shards themselves): vals / idx are
+ * [W, T, k] device arrays (shard r's tlp_topk output with its shard_base; pad
+ * entries (-1, -inf) allowed); idx_out / val_out [T, k] device receive the
+ * global top-k per task under the same total order (R21). */
+tlp_status tlp_topk_merge(tlp_ctx* ctx, const float* vals, const int64_t* idx, int32_t W,
+                          int32_t T, int32_t k, int64_t* idx_out, float* val_out, void* stream);
+
 /* ---- training-data preparation, P:295-296 -------------------------------
  * label_i = min_{j in g} latency_j / latency_i per group g (fp64 quotient,
  * rounded to fp32).  latency [M] fp32 device > 0; group_off [G+1] HOST int64;

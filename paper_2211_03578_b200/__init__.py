@@ -287,6 +287,20 @@ class TLP:
                                       _stream_ptr(stream)))
         return idx_out, val_out
 
+    def topk_merge(self, vals: torch.Tensor, idx: torch.Tensor, idx_out=None, val_out=None,
+                   stream=None):
+        """Merge per-shard top-k lists vals/idx [W, T, k] into the global [T, k]."""
+        W, T, k = vals.shape
+        vals, idx = vals.contiguous(), idx.contiguous()
+        if idx_out is None:
+            idx_out = torch.empty((T, k), dtype=torch.int64, device=vals.device)
+        if val_out is None:
+            val_out = torch.empty((T, k), dtype=torch.float32, device=vals.device)
+        self._check(self.lib.tlp_topk_merge(self.h, vals.data_ptr(), idx.data_ptr(), W, T, k,
+                                            idx_out.data_ptr(), val_out.data_ptr(),
+                                            _stream_ptr(stream)))
+        return idx_out, val_out
+
     def normalize_labels(self, latency: torch.Tensor, group_off, out=None, stream=None):
         goff = np.ascontiguousarray(group_off, np.int64)
         if out is None:

@@ -16,7 +16,7 @@ TLP_STATUS = {0: "OK", -1: "ERR_ARG", -2: "ERR_SHAPE", -3: "ERR_EMPTY_SEQ",
 EXPORTS = ("tlp_create", "tlp_destroy", "tlp_last_error", "tlp_default_config",
            "tlp_set_token_table", "tlp_set_norm_scales", "tlp_num_params", "tlp_set_params",
            "tlp_get_params", "tlp_get_grads", "tlp_set_comm", "tlp_get_unique_id", "tlp_encode",
-           "tlp_score", "tlp_train_step", "tlp_compute_grads", "tlp_lambdarank", "tlp_topk",
+           "tlp_score", "tlp_train_step", "tlp_compute_grads", "tlp_lambdarank", "tlp_topk", "tlp_topk_merge",
            "tlp_normalize_labels", "tlp_sync", "tlp_launch_count", "tlp_debug_umma",
            "tlp_debug_gemm")
 
@@ -69,6 +69,7 @@ def load() -> C.CDLL:
         "tlp_compute_grads": (C.c_int, [vp, vp, vp, vp, i32, i32, vp, vp]),
         "tlp_lambdarank": (C.c_int, [vp, vp, vp, vp, i32, i32, vp, vp, vp]),
         "tlp_topk": (C.c_int, [vp, vp, i32, i32, vp, i32, i32, i64, vp, vp, vp]),
+        "tlp_topk_merge": (C.c_int, [vp, vp, vp, i32, i32, i32, vp, vp, vp]),
         "tlp_normalize_labels": (C.c_int, [vp, vp, vp, i32, vp, vp]),
         "tlp_sync": (C.c_int, [vp]),
         "tlp_launch_count": (i64, [vp]),

@@ -146,7 +146,7 @@ void tlp_destroy(tlp_ctx* ctx) {
   cudaFree(ctx->d_hkeys); cudaFree(ctx->d_hval); cudaFree(ctx->d_hstr);
   cudaFree(ctx->d_tblob); cudaFree(ctx->d_toff);
   for (DevBuf* b : {&ctx->ws_tokens, &ctx->ws_act, &ctx->ws_train, &ctx->ws_rank, &ctx->ws_topk,
-                    &ctx->ws_misc, &ctx->ws_partial})
+                    &ctx->ws_misc, &ctx->ws_partial, &ctx->ws_merge})
     b->release();
   delete ctx;
 }
@@ -346,6 +346,23 @@ tlp_status grads_impl(tlp_ctx* ctx, const float* feats, const float* labels,
   return TLP_OK;
 }
 
+// [W, T, k] per-shard top-k lists (scores + global indices) -> the global top-k
+// per task, by the same deterministic tournament as tlp_topk (R21).
+tlp_status merge_gathered(tlp_ctx* ctx, const float* gs, const int64_t* gi, float* ts, int64_t* ti,
+                          int W, int T, int k, int64_t* idx_out, float* val_out, cudaStream_t s) {
+  const size_t loc = (size_t)T * k;
+  // [W, T, k] -> [T, W, k] so every segment's candidates are contiguous
+  for (int r = 0; r < W; ++r) {
+    TLP_CUDA_TRY(cudaMemcpy2DAsync(ts + (size_t)r * k, (size_t)W * k * sizeof(float),
+                                   gs + (size_t)r * loc, (size_t)k * sizeof(float),
+                                   (size_t)k * sizeof(float), T, cudaMemcpyDeviceToDevice, s));
+    TLP_CUDA_TRY(cudaMemcpy2DAsync(ti + (size_t)r * k, (size_t)W * k * sizeof(int64_t),
+                                   gi + (size_t)r * loc, (size_t)k * sizeof(int64_t),
+                                   (size_t)k * sizeof(int64_t), T, cudaMemcpyDeviceToDevice, s));
+  }
+  return topk_merge_launch(ctx, ts, ti, T, (int64_t)W * k, k, idx_out, val_out, s);
+}
+
 }  // namespace
 
 tlp_status tlp_compute_grads(tlp_ctx* ctx, const float* feats, const float* labels,
@@ -420,16 +437,21 @@ tlp_status tlp_topk(tlp_ctx* ctx, const float* scores, int32_t score_stride, int
       ncclAllGather(li, gi, loc, ncclInt64, comm, s) != ncclSuccess ||
       ncclGroupEnd() != ncclSuccess)
     return fail(ctx, TLP_ERR_NCCL, "top-k allgather failed");
-  // [W, T, k] -> [T, W, k] so every segment's candidates are contiguous
-  for (int r = 0; r < W; ++r) {
-    TLP_CUDA_TRY(cudaMemcpy2DAsync(ts + (size_t)r * k, (size_t)W * k * sizeof(float),
-                                   gs + (size_t)r * loc, (size_t)k * sizeof(float),
-                                   (size_t)k * sizeof(float), T, cudaMemcpyDeviceToDevice, s));
-    TLP_CUDA_TRY(cudaMemcpy2DAsync(ti + (size_t)r * k, (size_t)W * k * sizeof(int64_t),
-                                   gi + (size_t)r * loc, (size_t)k * sizeof(int64_t),
-                                   (size_t)k * sizeof(int64_t), T, cudaMemcpyDeviceToDevice, s));
-  }
-  return topk_merge_launch(ctx, ts, ti, T, (int64_t)W * k, k, idx_out, val_out, s);
+  return merge_gathered(ctx, gs, gi, ts, ti, W, T, k, idx_out, val_out, s);
+}
+
+tlp_status tlp_topk_merge(tlp_ctx* ctx, const float* vals, const int64_t* idx, int32_t W, int32_t T,
+                          int32_t k, int64_t* idx_out, float* val_out, void* stream) {
+  CHECK_CTX();
+  if (!vals || !idx || !idx_out || !val_out || W < 1 || T < 1 || k < 1)
+    return fail(ctx, TLP_ERR_ARG, "bad top-k merge arguments");
+  cudaSetDevice(ctx->device);
+  const size_t n = (size_t)W * T * k;
+  TLP_CUDA_TRY(ctx->ws_merge.ensure(n * (sizeof(float) + sizeof(int64_t)) + 256));
+  int64_t* ti = ctx->ws_merge.as<int64_t>();
+  float* ts = reinterpret_cast<float*>(ti + n);
+  return merge_gathered(ctx, vals, idx, ts, ti, W, T, k, idx_out, val_out,
+                        reinterpret_cast<cudaStream_t>(stream));
 }
 
 tlp_status tlp_normalize_labels(tlp_ctx* ctx, const float* latency, const int64_t* group_off,

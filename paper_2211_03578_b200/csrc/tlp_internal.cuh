@@ -83,7 +83,7 @@ struct tlp_ctx {
   uint32_t* d_err = nullptr;
 
   // workspaces
-  DevBuf ws_tokens, ws_act, ws_train, ws_rank, ws_topk, ws_misc, ws_partial;
+  DevBuf ws_tokens, ws_act, ws_train, ws_rank, ws_topk, ws_misc, ws_partial, ws_merge;
 
   // bf16 tensor-core path
   TcWeights* tc = nullptr;

@@ -422,3 +422,30 @@ def test_bf16_scoring_needs_paper_shape(tp):
     with pytest.raises(tp.TLPError) as e:
         m.score(torch.zeros((5, 25, 22), device="cuda"))
     assert e.value.code == "ERR_UNSUPPORTED"
+
+
+def test_sharded_topk_merge_bitwise(tp, tokscale):
+    """C-2 on one GPU: 4 shards (5-aligned, paper.dist.shard_range) scored and
+    selected separately with their shard_base, then tlp_topk_merge == the
+    unsharded tlp_topk bit for bit (needs batch-invariant bf16 scoring, R34)."""
+    from paper_2211_03578_b200 import dist as D
+    tokens, scale = tokscale
+    ocfg = oracle_cfg(n_attn=2)
+    flat = flat_params(ocfg, seed=9)
+    _, X = encoded_batch(26, 2003, tokens, scale)
+    off = np.array([0, 400, 401, 1500, 2003], np.int64)
+    m = tp.TLP(product_cfg(ocfg, "bf16"))
+    m.set_params(flat.astype(np.float32))
+    Xd = torch.from_numpy(X).cuda()
+    full = m.score(Xd)
+    idx_ref, val_ref = m.topk(full, off, 16)
+    vs, is_ = [], []
+    for r in range(4):
+        lo, hi = D.shard_range(2003, 4, r)
+        s = m.score(Xd[lo:hi].contiguous())
+        i, v = m.topk(s, D.local_task_off(off, lo, hi), 16, shard_base=lo)
+        vs.append(v); is_.append(i)
+    idx, val = m.topk_merge(torch.stack(vs), torch.stack(is_))
+    m.sync()
+    assert np.array_equal(idx.cpu().numpy(), idx_ref.cpu().numpy())
+    assert np.array_equal(val.cpu().numpy().view(np.uint32), val_ref.cpu().numpy().view(np.uint32))
