@@ -58,36 +58,52 @@ __global__ void resolve_tokens(const uint8_t* __restrict__ blob, const int64_t* 
   tokens[u] = tok;
 }
 
-template <int L_, int E_, int T_>
-__global__ void __launch_bounds__(256) encode_kernel_fixed(
-    int64_t total, const int64_t* __restrict__ seq_off, const uint8_t* __restrict__ prim_type,
+// One warp per candidate: lane r < min(len, L) builds row r (one-hot, then its
+// arguments in order, / scale) in shared memory; the warp then streams the
+// candidate's L*E floats to HBM with coalesced 8-byte stores (a candidate
+// block is 2,200 B, 8-byte aligned).
+constexpr int kEncWarps = 8;
+constexpr int kEncMaxElems = 32 * 64;  // L <= 32, E <= 64
+
+template <int E_, int T_>
+__global__ void __launch_bounds__(32 * kEncWarps) encode_warp_kernel(
+    int64_t N, const int64_t* __restrict__ seq_off, const uint8_t* __restrict__ prim_type,
     const int64_t* __restrict__ arg_off, const uint8_t* __restrict__ arg_kind,
     const double* __restrict__ arg_num, const int32_t* __restrict__ arg_name,
     const int32_t* __restrict__ tokens, const float* __restrict__ scale, float* __restrict__ out,
     uint32_t* __restrict__ err, int L, int E, int T) {
-  const int Lr = L_ ? L_ : L, Er = E_ ? E_ : E, Tr = T_ ? T_ : T;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
-    const int64_t n = e / (Lr * Er);
-    const int rc = (int)(e - n * (Lr * Er));
-    const int r = rc / Er;
-    const int c = rc - r * Er;
+  const int Er = E_ ? E_ : E, Tr = T_ ? T_ : T;
+  extern __shared__ float enc_sm[];  // [kEncWarps][L*E] + scale[E]
+  const int LE = L * Er;
+  float* s_scale = enc_sm + kEncWarps * LE;
+  if (threadIdx.x < Er) s_scale[threadIdx.x] = scale[threadIdx.x];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  float* buf = enc_sm + w * LE;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t n = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; n < N; n += nwarps) {
     const int64_t s0 = seq_off[n];
     const int64_t len = seq_off[n + 1] - s0;
-    float v = 0.f;
-    if (len <= 0) {
-      if (rc == 0) atomicOr(err, DERR_EMPTY_SEQ);
-    } else if (r < len) {
-      const int64_t p = s0 + r;
-      const int tau = prim_type[p];
-      if (tau >= Tr) {
-        if (c == 0) atomicOr(err, DERR_UNKNOWN_TYPE);
-      } else if (c < Tr) {
-        v = (c == tau) ? 1.f : 0.f;  // F1 one-hot
-      } else {
-        const int64_t a0 = arg_off[p];
-        const int a = c - Tr;
-        if (a < arg_off[p + 1] - a0) {
+    if (len <= 0 && lane == 0) atomicOr(err, DERR_EMPTY_SEQ);
+    if (lane < L) {
+      float* row = buf + lane * Er;
+      int tau = -1, na = 0;
+      int64_t a0 = 0;
+      if (lane < len) {
+        const int64_t p = s0 + lane;
+        tau = prim_type[p];
+        a0 = arg_off[p];
+        na = (int)(arg_off[p + 1] - a0);
+        if (tau >= Tr) {
+          atomicOr(err, DERR_UNKNOWN_TYPE);
+          tau = -1;  // row left zero
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < Tr; ++c) row[c] = __fdiv_rn((tau >= 0 && c == tau) ? 1.f : 0.f, s_scale[c]);
+      for (int a = 0; a < Er - Tr; ++a) {
+        float v = 0.f;
+        if (tau >= 0 && a < na) {
           const int64_t ai = a0 + a;
           if (arg_kind[ai]) {
             v = (float)tokens[arg_name[ai]];  // F2 (tokens < 2^24: exact)
@@ -97,9 +113,18 @@ __global__ void __launch_bounds__(256) encode_kernel_fixed(
             if (!isfinite(d) || !isfinite(v)) atomicOr(err, DERR_NONFINITE);
           }
         }
+        row[Tr + a] = __fdiv_rn(v, s_scale[Tr + a]);  // R3: IEEE round-to-nearest division
       }
     }
-    out[e] = __fdiv_rn(v, scale[c]);  // R3: IEEE round-to-nearest division
+    __syncwarp();
+    float* o = out + n * (int64_t)LE;
+    if ((LE & 1) == 0) {
+      for (int j = lane; j < LE / 2; j += 32)
+        reinterpret_cast<float2*>(o)[j] = reinterpret_cast<const float2*>(buf)[j];
+    } else {
+      for (int j = lane; j < LE; j += 32) o[j] = buf[j];
+    }
+    __syncwarp();
   }
 }
 
@@ -167,17 +192,17 @@ tlp_status encode_launch(tlp_ctx* ctx, const tlp_seq_batch* in, int64_t N, float
         ctx->d_toff, ctx->hcap, tokens);
     TLP_LAUNCH_CHECK();
   }
-  const int64_t total = N * (int64_t)c.L * c.E;
-  if (total == 0) return TLP_OK;
-  const int64_t want = cdiv(total, 256);
-  const unsigned grid = (unsigned)(want < (int64_t)ctx->num_sms * 64 ? want : (int64_t)ctx->num_sms * 64);
-  if (c.L == 25 && c.E == 22 && c.T == 11) {
-    encode_kernel_fixed<25, 22, 11><<<grid, 256, 0, s>>>(
-        total, in->seq_off, in->prim_type, in->arg_off, in->arg_kind, in->arg_num, in->arg_name,
+  if (N == 0) return TLP_OK;
+  const int64_t want = cdiv(N, kEncWarps);  // one warp per candidate
+  const unsigned grid = (unsigned)(want < (int64_t)ctx->num_sms * 16 ? want : (int64_t)ctx->num_sms * 16);
+  const size_t smem = ((size_t)kEncWarps * c.L * c.E + c.E) * sizeof(float);
+  if (c.E == 22 && c.T == 11) {
+    encode_warp_kernel<22, 11><<<grid, 32 * kEncWarps, smem, s>>>(
+        N, in->seq_off, in->prim_type, in->arg_off, in->arg_kind, in->arg_num, in->arg_name,
         tokens, ctx->d_scale, feats, ctx->d_err, c.L, c.E, c.T);
   } else {
-    encode_kernel_fixed<0, 0, 0><<<grid, 256, 0, s>>>(
-        total, in->seq_off, in->prim_type, in->arg_off, in->arg_kind, in->arg_num, in->arg_name,
+    encode_warp_kernel<0, 0><<<grid, 32 * kEncWarps, smem, s>>>(
+        N, in->seq_off, in->prim_type, in->arg_off, in->arg_kind, in->arg_num, in->arg_name,
         tokens, ctx->d_scale, feats, ctx->d_err, c.L, c.E, c.T);
   }
   TLP_LAUNCH_CHECK();
