@@ -42,6 +42,17 @@ TRAIN_GROUPS, TRAIN_PER_GROUP = 16, 512
 B_TRAIN = TRAIN_GROUPS * TRAIN_PER_GROUP
 
 
+def _traffic(kernel: str):
+    """DRAM bytes per launch of `kernel` from the newest profiles/*_traffic.json."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_traffic.json")))
+    for f in reversed(files):
+        d = json.load(open(f))
+        if kernel in d:
+            return d[kernel]["dram_read_bytes"] + d[kernel]["dram_write_bytes"]
+    return None
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -256,10 +267,12 @@ def run_ours(args):
     if precision == "bf16":
         achieved = fl * N_ROUND / (score_launch_ms / 1e3) / 1e12
         peak = peaks["bf16_tflops_sustained"]
-        roof = {"bound": "tensor", "kernel": "tc_fused_forward (tlp_score, 1 launch/round)",
+        roof = {"bound": "tensor", "kernel": "tc_forward_kernel (tlp_score, 1 launch/round)",
                 "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                "traffic": None, "peak_kind": peaks_kind + " bf16 sustained",
-                "flops_per_launch": fl * N_ROUND}
+                "traffic": _traffic("tc_forward_kernel"), "peak_kind": peaks_kind + " bf16 sustained",
+                "flops_per_launch": fl * N_ROUND,
+                "traffic_note": "dram__bytes_read+write per launch from profiles/*_traffic.json "
+                                "(ncu --set full of the same command); algorithmic input 2,200 B/cand"}
     else:
         achieved = fl * N_ROUND / (score_launch_ms / 1e3) / 1e12
         sm_mhz = peaks.get("sm_max_mhz", 1965.0)

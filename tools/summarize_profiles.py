@@ -1,0 +1,116 @@
+"""Summarise a round's ncu captures (gpurun_out/<tag>_*) into profiles/<tag>_*.
+
+    python tools/summarize_profiles.py r01
+
+Writes profiles/<tag>_launches.csv (kernel, ms, share of the step) and
+profiles/<tag>_kernels.md (per kernel: duration, DRAM bytes, tensor-pipe %,
+achieved occupancy, top stall reasons) and profiles/<tag>_traffic.json (DRAM
+bytes per launch of each captured kernel, read by bench.py's roofline).
+"""
+from __future__ import annotations
+
+import collections
+import csv
+import io
+import json
+import os
+import re
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+GO = os.path.join(ROOT, "gpurun_out")
+PR = os.path.join(ROOT, "profiles")
+
+
+def short(name: str) -> str:
+    m = re.search(r"(\w+_kernel\w*|\w+_partial\w*|reduce_partials|label_kernel|finalize_\w+|sum_counts|resolve_tokens|pack_kernel)", name)
+    k = m.group(1) if m else name.split("(")[0][:40]
+    t = re.search(r"<([^>]*)>", name)
+    if t and ("gemm" in k or "attn" in k or "encode" in k):
+        k += "<" + t.group(1) + ">"
+    return k
+
+
+def launches(tag: str):
+    path = os.path.join(GO, tag + "_launches.csv")
+    rows = list(csv.reader(open(path)))
+    start = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
+    hdr = rows[start]
+    ik, iv = hdr.index("Kernel Name"), hdr.index("Metric Value")
+    data = rows[start + 1:]
+    agg, cnt = collections.OrderedDict(), collections.Counter()
+    # the bench does 3 warm-up steps + 1 timed step (+ the e2e passes); take
+    # the launches of the last training/scoring step: the 4th tc_forward onward
+    fwd = [i for i, r in enumerate(data) if "tc_forward_kernel" in r[ik]]
+    lo = fwd[3] if len(fwd) > 3 else 0
+    hi = fwd[4] if len(fwd) > 4 else len(data)
+    # extend to the end of the training step that follows the 4th round
+    for r in data[lo:hi]:
+        k = short(r[ik])
+        agg[k] = agg.get(k, 0.0) + float(r[iv].replace(",", ""))
+        cnt[k] += 1
+    tot = sum(agg.values())
+    out = io.StringIO()
+    w = csv.writer(out)
+    w.writerow(["kernel", "launches", "total_ms", "share_of_step"])
+    for k, v in sorted(agg.items(), key=lambda kv: -kv[1]):
+        w.writerow([k, cnt[k], "%.4f" % (v / 1e6), "%.4f" % (v / tot)])
+    return out.getvalue(), tot
+
+
+def raw_metrics(rep: str):
+    txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(txt)))
+    if len(rows) < 3:
+        return {}
+    return {h: (u, v) for h, u, v in zip(rows[0], rows[1], rows[2])}
+
+
+def to_bytes(u, v):
+    x = float(v.replace(",", ""))
+    return x * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
+
+
+def kernels(tag: str):
+    md = ["# %s ncu --set full summaries (one launch each, --clock-control none)\n" % tag,
+          "| kernel | duration | DRAM read | DRAM write | DRAM GB/s | tensor pipe % | occupancy % | top stalls |",
+          "|---|---|---|---|---|---|---|---|"]
+    traffic = {}
+    for f in sorted(os.listdir(GO)):
+        if not (f.startswith(tag + "_prof_") and f.endswith(".ncu-rep")):
+            continue
+        k = f[len(tag + "_prof_"):-len(".ncu-rep")]
+        m = raw_metrics(os.path.join(GO, f))
+        if not m:
+            continue
+        dur_u, dur_v = m.get("gpu__time_duration.sum", ("", "0"))
+        dur_s = float(dur_v.replace(",", "")) * {"ns": 1e-9, "us": 1e-6, "usecond": 1e-6, "ms": 1e-3, "msecond": 1e-3}.get(dur_u, 1e-9)
+        rd = to_bytes(*m.get("dram__bytes_read.sum", ("byte", "0")))
+        wr = to_bytes(*m.get("dram__bytes_write.sum", ("byte", "0")))
+        tp = m.get("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", ("", "n/a"))[1]
+        occ = m.get("sm__warps_active.avg.pct_of_peak_sustained_active", ("", "n/a"))[1]
+        st = [(h.replace("smsp__pcsamp_warps_issue_stalled_", ""), float(v[1] or 0)) for h, v in m.items()
+              if h.startswith("smsp__pcsamp_warps_issue_stalled_") and not h.endswith("not_issued")]
+        tots = sum(x for _, x in st) or 1.0
+        top = ", ".join("%s %.0f%%" % (a, 100 * b / tots) for a, b in sorted(st, key=lambda x: -x[1])[:3])
+        md.append("| %s | %.3f ms | %.1f MB | %.1f MB | %.0f | %s | %s | %s |" % (
+            k, dur_s * 1e3, rd / 1e6, wr / 1e6, (rd + wr) / max(dur_s, 1e-12) / 1e9, tp, occ, top))
+        traffic[k] = {"dram_read_bytes": rd, "dram_write_bytes": wr, "duration_s": dur_s}
+    return "\n".join(md) + "\n", traffic
+
+
+def main():
+    tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
+    os.makedirs(PR, exist_ok=True)
+    csv_txt, tot = launches(tag)
+    open(os.path.join(PR, tag + "_launches.csv"), "w").write(csv_txt)
+    md, traffic = kernels(tag)
+    open(os.path.join(PR, tag + "_kernels.md"), "w").write(md)
+    json.dump(traffic, open(os.path.join(PR, tag + "_traffic.json"), "w"), indent=1)
+    print(csv_txt)
+    print(md)
+
+
+if __name__ == "__main__":
+    main()
