@@ -97,6 +97,7 @@ struct TcArgs {
   int64_t ra[TLP_MAX_RES], rb[TLP_MAX_RES];
   int64_t c1[TLP_MAX_TASKS], w2[TLP_MAX_TASKS], c2[TLP_MAX_TASKS];
   int n_attn, n_res, n_tasks;
+  long long* trace;  // diagnostics (TLP_TC_TRACE=1): CTA 0 epilogue phase timestamps
 };
 
 // ---------------------------------------------------------------- epilogue helpers
@@ -127,18 +128,30 @@ __device__ __forceinline__ void vec32(const float* v, float (&o)[32]) {
 }
 
 // relu(acc + bias) -> bf16 A operand in TMEM (two bf16 per column)
+// The epilogue helpers below walk their column range 64 columns at a time:
+// two tcgen05.ld in flight per tcgen05.wait::ld.
+__device__ __forceinline__ void relu_pack32(const float (&v)[32], const float* bias,
+                                            uint32_t (&pk)[16]) {
+  float b[32];
+  vec32(bias, b);
+#pragma unroll
+  for (int i = 0; i < 16; ++i)
+    pk[i] = tc::pack_bf16(fmaxf(v[2 * i] + b[2 * i], 0.f), fmaxf(v[2 * i + 1] + b[2 * i + 1], 0.f));
+}
+
+// relu(acc + bias) -> bf16 A operand in TMEM (two bf16 per column)
 __device__ __forceinline__ void epi_relu_to_tmem(uint32_t tl, uint32_t src, int c0, int c1,
                                                  const float* bias, uint32_t dst) {
-  for (int c = c0; c < c1; c += 32) {
-    float v[32], b[32];
-    tc::tmem_ld32(tl + src + c, v);
-    vec32(bias + c, b);
-    tc::tmem_wait_ld();
+  for (int c = c0; c < c1; c += 64) {
+    float v0[32], v1[32];
     uint32_t pk[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i)
-      pk[i] = tc::pack_bf16(fmaxf(v[2 * i] + b[2 * i], 0.f), fmaxf(v[2 * i + 1] + b[2 * i + 1], 0.f));
+    tc::tmem_ld32(tl + src + c, v0);
+    tc::tmem_ld32(tl + src + c + 32, v1);
+    tc::tmem_wait_ld();
+    relu_pack32(v0, bias + c, pk);
     tc::tmem_st16(tl + dst + c / 2, pk);
+    relu_pack32(v1, bias + c + 32, pk);
+    tc::tmem_st16(tl + dst + c / 2 + 16, pk);
   }
   tc::tmem_wait_st();
 }
@@ -147,40 +160,48 @@ __device__ __forceinline__ void epi_relu_to_tmem(uint32_t tl, uint32_t src, int 
 __device__ __forceinline__ void epi_relu_to_smem(uint8_t* smem, uint32_t tl, uint32_t src,
                                                  int c0, int c1, const float* bias, uint32_t dst,
                                                  uint32_t Kt, uint32_t r) {
-  for (int c = c0; c < c1; c += 32) {
-    float v[32], b[32];
-    tc::tmem_ld32(tl + src + c, v);
-    vec32(bias + c, b);
-    tc::tmem_wait_ld();
+  for (int c = c0; c < c1; c += 64) {
+    float v0[32], v1[32];
     uint32_t pk[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i)
-      pk[i] = tc::pack_bf16(fmaxf(v[2 * i] + b[2 * i], 0.f), fmaxf(v[2 * i + 1] + b[2 * i + 1], 0.f));
+    tc::tmem_ld32(tl + src + c, v0);
+    tc::tmem_ld32(tl + src + c + 32, v1);
+    tc::tmem_wait_ld();
+    relu_pack32(v0, bias + c, pk);
     store_row32(smem, dst, r, c, Kt, pk);
+    relu_pack32(v1, bias + c + 32, pk);
+    store_row32(smem, dst, r, c + 32, Kt, pk);
   }
 }
 
-// h[r, :] = bf16(h[r, :] + acc[r, :] + bias)   (R10 / R12 residual, R33)
+// h[r, c..c+32) = bf16(h + acc + bias)   (R10 / R12 residual, R33)
+__device__ __forceinline__ void residual32(uint8_t* smem, const float (&v)[32], const float* bias,
+                                           uint32_t r, int c) {
+  float b[32];
+  vec32(bias + c, b);
+  uint4 old[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    old[i] = *reinterpret_cast<const uint4*>(smem + OFF_H + tc::canon_off(r, c + 8 * i, kH));
+  uint32_t pk[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const uint32_t w = (&old[i >> 2].x)[i & 3];
+    __nv_bfloat162 hb = *reinterpret_cast<const __nv_bfloat162*>(&w);
+    const float2 hf = __bfloat1622float2(hb);
+    pk[i] = tc::pack_bf16(hf.x + (v[2 * i] + b[2 * i]), hf.y + (v[2 * i + 1] + b[2 * i + 1]));
+  }
+  store_row32(smem, OFF_H, r, c, kH, pk);
+}
+
 __device__ __forceinline__ void epi_residual(uint8_t* smem, uint32_t tl, const float* bias,
                                              uint32_t r, int c0, int c1) {
-  for (int c = c0; c < c1; c += 32) {
-    float v[32], b[32];
-    tc::tmem_ld32(tl + T_A + c, v);
-    vec32(bias + c, b);
-    uint4 old[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-      old[i] = *reinterpret_cast<const uint4*>(smem + OFF_H + tc::canon_off(r, c + 8 * i, kH));
+  for (int c = c0; c < c1; c += 64) {
+    float v0[32], v1[32];
+    tc::tmem_ld32(tl + T_A + c, v0);
+    tc::tmem_ld32(tl + T_A + c + 32, v1);
     tc::tmem_wait_ld();
-    uint32_t pk[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const uint32_t w = (&old[i >> 2].x)[i & 3];
-      __nv_bfloat162 hb = *reinterpret_cast<const __nv_bfloat162*>(&w);
-      const float2 hf = __bfloat1622float2(hb);
-      pk[i] = tc::pack_bf16(hf.x + (v[2 * i] + b[2 * i]), hf.y + (v[2 * i + 1] + b[2 * i + 1]));
-    }
-    store_row32(smem, OFF_H, r, c, kH, pk);
+    residual32(smem, v0, bias, r, c);
+    residual32(smem, v1, bias, r, c + 32);
   }
 }
 
@@ -220,30 +241,39 @@ __device__ __forceinline__ void attn_head_mma(uint8_t* smem, uint32_t sbase, uin
     tc::mma16816(s[nt], qa[1], kb[2], kb[3]);
   }
   // masked softmax (unnormalised); rows 32q + 16mt + g (+8)
+  // Each row only attends to its own candidate's block of 4 n-tiles (block 0 =
+  // s_lo, 1 = s_lo + 1): select that block (8 values per thread), exponentiate
+  // only those, and zero the other block -- half the MUFU work of a masked
+  // 64-wide row, same values and summation order (batch invariance, R34).
   float inv[2];
 #pragma unroll
   for (int half = 0; half < 2; ++half) {
     const uint32_t row = 32 * q + 16 * mt + g + 8 * half;
-    const int lo = 32 * (int)(row / kL) - (int)kp0;  // window-relative first valid key
+    const int blk = (int)(row / kL) - (int)s_lo;  // 0, 1; >= 2 for pad rows
+    const bool hi = blk == 1, any = blk <= 1;
+    float x[8];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) x[2 * i + e] = hi ? s[4 + i][2 * half + e] : s[i][2 * half + e];
     float mx = -INFINITY;
 #pragma unroll
-    for (int nt = 0; nt < 8; ++nt)
+    for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int c = 8 * nt + 2 * tig + e;
-        if (c >= lo && c < lo + kL) mx = fmaxf(mx, s[nt][2 * half + e]);
-      }
+      for (int e = 0; e < 2; ++e)
+        if (any && 8 * i + 2 * (int)tig + e < kL) mx = fmaxf(mx, x[2 * i + e]);
     mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
     mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
     const float off = (mx == -INFINITY) ? 0.f : mx * sm_scale;
     float sum = 0.f;
 #pragma unroll
-    for (int nt = 0; nt < 8; ++nt)
+    for (int i = 0; i < 4; ++i)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        const int c = 8 * nt + 2 * tig + e;
-        const float p = (c >= lo && c < lo + kL) ? ex2_approx(fmaf(s[nt][2 * half + e], sm_scale, -off)) : 0.f;
-        s[nt][2 * half + e] = p;
+        const bool ok = any && 8 * i + 2 * (int)tig + e < kL;
+        const float p = ok ? ex2_approx(fmaf(x[2 * i + e], sm_scale, -off)) : 0.f;
+        s[i][2 * half + e] = hi ? 0.f : p;
+        s[4 + i][2 * half + e] = hi ? p : 0.f;
         sum += p;
       }
     sum += __shfl_xor_sync(0xffffffffu, sum, 1);
@@ -421,15 +451,23 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
     const uint32_t tl = tmem + ((32 * q) << 16);       // this warp's lane quarter
     float* rowdot = reinterpret_cast<float*>(smem + OFF_DOT);   // [2][128]
     uint32_t ph_acc = 0, ph_qkv = 0;
+    int titer = 0, tev = 0;
+    auto tr = [&]() {  // diagnostics only (a.trace == nullptr in production)
+      if (a.trace && blockIdx.x == 0 && threadIdx.x == 64 && titer < 8 && tev < 64)
+        a.trace[titer * 64 + tev] = clock64();
+      ++tev;
+    };
     auto wait_on = [&](uint32_t bar, uint32_t& ph) {
       tc::mbar_wait(bar, ph);
       ph ^= 1;
       tc::tc_fence_after();
+      tr();
     };
     auto signal = [&]() {
       tc::fence_proxy_async_smem();
       tc::tc_fence_before();
       tc::mbar_arrive(bar_opnd);
+      tr();
     };
     // column split between the quarter's two warps
     auto lo_of = [&](int n) { return (int)hh * (n / 2); };
@@ -439,7 +477,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
     const bool real = r < kCand * kL;
     const float sm_scale = 1.4426950408889634f / sqrtf((float)kDH);  // log2(e)/sqrt(d_h)
 
-    for (int64_t tile = blockIdx.x; tile < a.ntile; tile += gridDim.x) {
+    for (int64_t tile = blockIdx.x; tile < a.ntile; tile += gridDim.x, ++titer) {
+      tev = 0;
+      tr();
       const int64_t n = tile * kCand + slot;
       if (hh == 0) {  // E0: X rows -> bf16 [128 x 32]
         uint32_t pk[16];
@@ -469,28 +509,32 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
           {  // QKV_j (TMEM) + bias -> Q, K (warp 0 of the quarter) / V (warp 1) tiles
             const uint32_t tq = tl + T_QKV + 96 * (j & 1);
             const uint32_t kpos = 32 * slot + kk;
-            float v[32], b[32];
-            uint32_t pk[16];
-            if (hh == 0) {
-              tc::tmem_ld32(tq + 0, v);
-              vec32(vs + a.bq[l] + kDH * j, b);
-              tc::tmem_wait_ld();
+            // balanced split, 48 columns per warp: warp 0 of the quarter converts Q
+            // and K[0:16), warp 1 converts K[16:32) and V; both loads in flight
+            // before one wait
+            float v[32], v2[16], b[32], b2[16];
+            uint32_t pk[16], pk2[8];
+            const uint32_t c32 = hh == 0 ? 0u : 64u;       // Q or V (32 columns)
+            const uint32_t c16 = hh == 0 ? 32u : 48u;      // K half (16 columns)
+            tc::tmem_ld32(tq + c32, v);
+            tc::tmem_ld16(tq + c16, v2);
+            vec32(vs + (hh == 0 ? a.bq[l] : a.bv[l]) + kDH * j, b);
 #pragma unroll
-              for (int i = 0; i < 16; ++i) pk[i] = tc::pack_bf16(v[2 * i] + b[2 * i], v[2 * i + 1] + b[2 * i + 1]);
-              store_plain32(smem, OFF_Q + r * kRowB, pk);
-              tc::tmem_ld32(tq + 32, v);
-              vec32(vs + a.bk[l] + kDH * j, b);
-              tc::tmem_wait_ld();
+            for (int i = 0; i < 4; ++i) {
+              const float4 x = reinterpret_cast<const float4*>(vs + a.bk[l] + kDH * j + 16 * hh)[i];
+              b2[4 * i] = x.x; b2[4 * i + 1] = x.y; b2[4 * i + 2] = x.z; b2[4 * i + 3] = x.w;
+            }
+            tc::tmem_wait_ld();
 #pragma unroll
-              for (int i = 0; i < 16; ++i) pk[i] = tc::pack_bf16(v[2 * i] + b[2 * i], v[2 * i + 1] + b[2 * i + 1]);
-              if (real) store_plain32(smem, OFF_K + kpos * kRowB, pk);
-            } else {
-              tc::tmem_ld32(tq + 64, v);
-              vec32(vs + a.bv[l] + kDH * j, b);
-              tc::tmem_wait_ld();
+            for (int i = 0; i < 16; ++i) pk[i] = tc::pack_bf16(v[2 * i] + b[2 * i], v[2 * i + 1] + b[2 * i + 1]);
 #pragma unroll
-              for (int i = 0; i < 16; ++i) pk[i] = tc::pack_bf16(v[2 * i] + b[2 * i], v[2 * i + 1] + b[2 * i + 1]);
-              if (real) store_plain32(smem, OFF_V + kpos * kRowB, pk);
+            for (int i = 0; i < 8; ++i) pk2[i] = tc::pack_bf16(v2[2 * i] + b2[2 * i], v2[2 * i + 1] + b2[2 * i + 1]);
+            if (hh == 0) store_plain32(smem, OFF_Q + r * kRowB, pk);
+            else if (real) store_plain32(smem, OFF_V + kpos * kRowB, pk);
+            if (real) {
+              uint8_t* kd = smem + OFF_K + kpos * kRowB + 32 * hh;
+              *reinterpret_cast<uint4*>(kd) = make_uint4(pk2[0], pk2[1], pk2[2], pk2[3]);
+              *reinterpret_cast<uint4*>(kd + 16) = make_uint4(pk2[4], pk2[5], pk2[6], pk2[7]);
             }
           }
           asm volatile("bar.sync 2, 256;" ::: "memory");  // Q/K/V of head j complete
@@ -712,8 +756,28 @@ tlp_status tc_forward(tlp_ctx* ctx, const float* feats, int64_t N, float* scores
   a.vec = w.vec; a.vec_floats = w.vec_floats;
   a.n_attn = c.n_attn; a.n_res = c.n_res; a.n_tasks = c.n_tasks;
   const int grid = (int)std::min<int64_t>(a.ntile, ctx->num_sms);
+  // Diagnostics: TLP_TC_TRACE=1 prints CTA 0's epilogue phase timeline (cycles
+  // between successive waits/signals) for its first tiles to stderr.
+  static const bool trace = getenv("TLP_TC_TRACE") != nullptr;
+  long long* d_trace = nullptr;
+  if (trace) {
+    TLP_CUDA_TRY(cudaMalloc(&d_trace, 8 * 64 * sizeof(long long)));
+    TLP_CUDA_TRY(cudaMemset(d_trace, 0, 8 * 64 * sizeof(long long)));
+  }
+  a.trace = d_trace;
   tc_forward_kernel<<<grid, kThreads, w.smem, s>>>(a);
   TLP_LAUNCH_CHECK();
+  if (trace) {
+    std::vector<long long> h(8 * 64);
+    TLP_CUDA_TRY(cudaStreamSynchronize(s));
+    TLP_CUDA_TRY(cudaMemcpy(h.data(), d_trace, h.size() * sizeof(long long), cudaMemcpyDeviceToHost));
+    cudaFree(d_trace);
+    for (int t = 1; t < 4; ++t) {
+      fprintf(stderr, "tile %d:", t);
+      for (int e = 1; e < 64 && h[t * 64 + e]; ++e) fprintf(stderr, " %lld", h[t * 64 + e] - h[t * 64 + e - 1]);
+      fprintf(stderr, " | total %lld\n", h[(t + 1) * 64] ? h[(t + 1) * 64] - h[t * 64] : 0LL);
+    }
+  }
   return TLP_OK;
 }
 
