@@ -233,15 +233,15 @@ def run_ours(args):
         dist.all_reduce(times, op=dist.ReduceOp.MAX)
     total_ms, round_ms, train_ms, score_ms, enc_ms, topk_ms = times.tolist()
 
-    # --- e2e: public API with host buffers (pinned H2D of the packed round, D2H of top-k) ---
+    # --- e2e: one C-ABI call per round from host buffers (tlp_search_round: pinned
+    # H2D of the packed round in chunks overlapped with encode + score, top-k,
+    # D2H of the top-k) ---
     hbatch = tp.DeviceBatch.from_packed(packed, pin=True)
     idx_host = torch.empty((T_TASKS, TOPK), dtype=torch.int64).pin_memory()
+    val_host = torch.empty((T_TASKS, TOPK), dtype=torch.float32).pin_memory()
     def e2e_step():
-        db = hbatch.to(dev, non_blocking=True)
-        scorer.encode(db, out=feats, stream=stream)
-        scorer.score(feats, out=scores, stream=stream)
-        scorer.topk(scores, task_off, TOPK, shard_base=shard_base, idx_out=idx, val_out=val, stream=stream)
-        idx_host.copy_(idx, non_blocking=True)
+        scorer.search_round(hbatch, task_off, TOPK, shard_base=shard_base, chunks=args.chunks,
+                            idx_out=idx_host, val_out=val_host, stream=stream)
     for _ in range(max(1, args.warmup)):
         e2e_step()
     torch.cuda.synchronize()
@@ -297,7 +297,8 @@ def run_ours(args):
                               "train": train_ms / K},
         "roofline": roof,
         "e2e": {"value": world * N_ROUND * K / (e2e_ms / 1e3), "unit": "candidates/s",
-                "h2d_bytes_per_step": hbatch.nbytes(), "d2h_bytes_per_step": T_TASKS * TOPK * 8},
+                "h2d_bytes_per_step": hbatch.nbytes(), "d2h_bytes_per_step": T_TASKS * TOPK * 12,
+                "call": "tlp_search_round, %d chunks" % args.chunks},
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
@@ -381,6 +382,7 @@ def main():
     ap.add_argument("--precision", default=os.environ.get("TLP_BENCH_PRECISION", "bf16"),
                     choices=["bf16", "fp32"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--chunks", type=int, default=16, help="tlp_search_round chunks (e2e leg)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -197,6 +197,36 @@ tlp_status tlp_topk(tlp_ctx* ctx, const float* scores, int32_t score_stride, int
 tlp_status tlp_topk_merge(tlp_ctx* ctx, const float* vals, const int64_t* idx, int32_t W,
                           int32_t T, int32_t k, int64_t* idx_out, float* val_out, void* stream);
 
+/* ---- one search round from host memory: (1) -> (2) -> (4) ---------------
+ * The per-round call of the search loop ("the cost model ... predicts the
+ * top-k candidates"): tlp_encode, tlp_score and tlp_topk over a batch of
+ * N candidates held in HOST memory, with the top-k returned to HOST memory.
+ *   host_in      tlp_seq_batch whose pointers are all HOST memory (page-locked
+ *                for the copies to overlap the kernels; pageable is accepted
+ *                and copied synchronously by the driver).  Not modified.
+ *                Offsets as for tlp_encode; seq_off is checked in full
+ *                (SHAPE), arg_off at the chunk boundaries.
+ *   task_off     HOST int64 [T+1], candidate segments per task (as tlp_topk).
+ *   head         score column ranked (0 <= head < n_tasks).
+ *   shard_base   global index of candidate 0 (sharded rounds, as tlp_topk).
+ *   chunks       1..64: the candidates are cut into `chunks` ranges (multiples
+ *                of 5 candidates); chunk c+1's host->device copy runs on an
+ *                internal copy stream while chunk c is encoded and scored on
+ *                `stream`.  The result does not depend on `chunks` (batch
+ *                invariance, R34).
+ *   idx_out / val_out  HOST [T, k] int64 / fp32 (page-locked for an
+ *                asynchronous read-back), written by a copy ordered on `stream`.
+ * Asynchronous on `stream`: outputs and the reuse of host_in are safe after
+ * stream synchronisation or tlp_sync.  Device memory (a copy of the batch, one
+ * chunk of features, N * n_tasks scores) is owned by the ctx and grows to the
+ * largest round seen.  With a communicator the top-k is the merged global one
+ * (as tlp_topk).  Errors: as tlp_encode / tlp_score / tlp_topk; ARG for chunks
+ * outside [1, 64] or a null pointer. */
+tlp_status tlp_search_round(tlp_ctx* ctx, const tlp_seq_batch* host_in, int64_t N,
+                            const int64_t* task_off, int32_t T, int32_t k, int32_t head,
+                            int64_t shard_base, int32_t chunks, int64_t* idx_out, float* val_out,
+                            void* stream);
+
 /* ---- training-data preparation, P:295-296 -------------------------------
  * label_i = min_{j in g} latency_j / latency_i per group g (fp64 quotient,
  * rounded to fp32).  latency [M] fp32 device > 0; group_off [G+1] HOST int64;

@@ -287,6 +287,25 @@ class TLP:
                                       _stream_ptr(stream)))
         return idx_out, val_out
 
+    def search_round(self, host_batch: DeviceBatch, task_off, k: int, head: int = 0,
+                     shard_base: int = 0, chunks: int = 16, idx_out=None, val_out=None, stream=None):
+        """One search round from host memory (tlp_search_round): encode -> score ->
+        per-task top-k of a HOST batch (DeviceBatch.from_packed(..., pin=True)),
+        the chunked host->device copy overlapped with the kernels.  Returns host
+        (pinned) idx [T, k] int64 and val [T, k] fp32, valid after stream sync."""
+        toff = np.ascontiguousarray(task_off, np.int64)
+        T = len(toff) - 1
+        if idx_out is None:
+            idx_out = torch.empty((T, k), dtype=torch.int64).pin_memory()
+        if val_out is None:
+            val_out = torch.empty((T, k), dtype=torch.float32).pin_memory()
+        assert not idx_out.is_cuda and not val_out.is_cuda
+        cs = host_batch.c_struct()
+        self._check(self.lib.tlp_search_round(self.h, C.byref(cs), host_batch.N, toff.ctypes.data, T, k,
+                                              head, shard_base, chunks, idx_out.data_ptr(),
+                                              val_out.data_ptr(), _stream_ptr(stream)))
+        return idx_out, val_out
+
     def topk_merge(self, vals: torch.Tensor, idx: torch.Tensor, idx_out=None, val_out=None,
                    stream=None):
         """Merge per-shard top-k lists vals/idx [W, T, k] into the global [T, k]."""

@@ -146,8 +146,12 @@ void tlp_destroy(tlp_ctx* ctx) {
   cudaFree(ctx->d_hkeys); cudaFree(ctx->d_hval); cudaFree(ctx->d_hstr);
   cudaFree(ctx->d_tblob); cudaFree(ctx->d_toff);
   for (DevBuf* b : {&ctx->ws_tokens, &ctx->ws_act, &ctx->ws_train, &ctx->ws_rank, &ctx->ws_topk,
-                    &ctx->ws_misc, &ctx->ws_partial, &ctx->ws_merge})
+                    &ctx->ws_misc, &ctx->ws_partial, &ctx->ws_merge, &ctx->ws_round_in,
+                    &ctx->ws_round_feats, &ctx->ws_round_scores})
     b->release();
+  for (cudaEvent_t& e : ctx->round_ev)
+    if (e) cudaEventDestroy(e);
+  if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
   delete ctx;
 }
 
@@ -253,14 +257,19 @@ tlp_status tlp_score(tlp_ctx* ctx, const float* feats, int64_t N, float* scores,
   CHECK_CTX();
   if (N < 0 || (N > 0 && (!feats || !scores))) return fail(ctx, TLP_ERR_ARG, "null buffer");
   if (!ctx->have_params) return fail(ctx, TLP_ERR_STATE, "tlp_set_params first");
+  if (ctx->cfg.precision == TLP_PREC_BF16 && !tc_supported(ctx->cfg))
+    return fail(ctx, TLP_ERR_UNSUPPORTED,
+                "bf16 tensor-core scoring needs the paper shape (E=22, L=25, hidden=256, "
+                "up_dims={128,256}, 8 heads, head_dim=128); use TLP_PREC_FP32");
   if (N == 0) return TLP_OK;
   cudaSetDevice(ctx->device);
-  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  return score_launch(ctx, feats, N, scores, reinterpret_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"
+
+tlp_status score_launch(tlp_ctx* ctx, const float* feats, int64_t N, float* scores, cudaStream_t s) {
   if (ctx->cfg.precision == TLP_PREC_BF16) {
-    if (!tc_supported(ctx->cfg))
-      return fail(ctx, TLP_ERR_UNSUPPORTED,
-                  "bf16 tensor-core scoring needs the paper shape (E=22, L=25, hidden=256, "
-                  "up_dims={128,256}, 8 heads, head_dim=128); use TLP_PREC_FP32");
     if (ctx->tc_dirty) {
       tlp_status st = tc_prepare(ctx, s);
       if (st != TLP_OK) return st;
@@ -270,6 +279,8 @@ tlp_status tlp_score(tlp_ctx* ctx, const float* feats, int64_t N, float* scores,
   }
   return simt_forward(ctx, feats, N, scores, false, s);
 }
+
+extern "C" {
 
 namespace {
 

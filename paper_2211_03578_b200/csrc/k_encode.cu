@@ -180,18 +180,27 @@ tlp_status build_token_table(tlp_ctx* ctx, const uint8_t* blob, const int64_t* o
   return TLP_OK;
 }
 
+tlp_status encode_resolve(tlp_ctx* ctx, const tlp_seq_batch* in, cudaStream_t s) {
+  if (in->U <= 0) return TLP_OK;
+  TLP_CUDA_TRY(ctx->ws_tokens.ensure(sizeof(int32_t) * (size_t)in->U));
+  resolve_tokens<<<(unsigned)cdiv(in->U, 128), 128, 0, s>>>(
+      in->str_blob, in->str_off, in->U, ctx->d_hkeys, ctx->d_hval, ctx->d_hstr, ctx->d_tblob,
+      ctx->d_toff, ctx->hcap, ctx->ws_tokens.as<int32_t>());
+  TLP_LAUNCH_CHECK();
+  return TLP_OK;
+}
+
 tlp_status encode_launch(tlp_ctx* ctx, const tlp_seq_batch* in, int64_t N, float* feats,
                          cudaStream_t s) {
+  tlp_status st = encode_resolve(ctx, in, s);
+  if (st != TLP_OK) return st;
+  return encode_rows(ctx, in, N, feats, s);
+}
+
+tlp_status encode_rows(tlp_ctx* ctx, const tlp_seq_batch* in, int64_t N, float* feats,
+                       cudaStream_t s) {
   const tlp_config& c = ctx->cfg;
-  int32_t* tokens = nullptr;
-  if (in->U > 0) {
-    TLP_CUDA_TRY(ctx->ws_tokens.ensure(sizeof(int32_t) * (size_t)in->U));
-    tokens = ctx->ws_tokens.as<int32_t>();
-    resolve_tokens<<<(unsigned)cdiv(in->U, 128), 128, 0, s>>>(
-        in->str_blob, in->str_off, in->U, ctx->d_hkeys, ctx->d_hval, ctx->d_hstr, ctx->d_tblob,
-        ctx->d_toff, ctx->hcap, tokens);
-    TLP_LAUNCH_CHECK();
-  }
+  const int32_t* tokens = in->U > 0 ? ctx->ws_tokens.as<int32_t>() : nullptr;
   if (N == 0) return TLP_OK;
   const int64_t want = cdiv(N, kEncWarps);  // one warp per candidate
   const unsigned grid = (unsigned)(want < (int64_t)ctx->num_sms * 16 ? want : (int64_t)ctx->num_sms * 16);

@@ -15,6 +15,7 @@
 #define TLP_MAX_ATTN 4
 #define TLP_MAX_RES 4
 #define TLP_MAX_TASKS 8
+#define TLP_MAX_ROUND_CHUNKS 64
 
 // Sticky device error bits (ctx->d_err), surfaced by tlp_sync.
 enum : uint32_t {
@@ -89,6 +90,12 @@ struct tlp_ctx {
   TcWeights* tc = nullptr;
   bool tc_dirty = true;
 
+  // tlp_search_round (round.cu): device copy of the host batch (same offsets),
+  // one chunk of features, all scores; copy stream + per-chunk events
+  DevBuf ws_round_in, ws_round_feats, ws_round_scores;
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t round_ev[TLP_MAX_ROUND_CHUNKS + 1] = {};
+
   // NCCL
   void* comm = nullptr;  // ncclComm_t
   int rank = 0, world = 1;
@@ -132,6 +139,13 @@ static inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 // k_encode.cu
 tlp_status encode_launch(tlp_ctx* ctx, const tlp_seq_batch* in, int64_t N, float* feats,
                          cudaStream_t s);
+// the two halves of encode_launch: batch strings -> tokens (ctx->ws_tokens), and
+// rows of candidates [0, N) of `in` (seq_off may be a shifted view: offsets are absolute)
+tlp_status encode_resolve(tlp_ctx* ctx, const tlp_seq_batch* in, cudaStream_t s);
+tlp_status encode_rows(tlp_ctx* ctx, const tlp_seq_batch* in, int64_t N, float* feats,
+                       cudaStream_t s);
+// api.cu: the bf16 / fp32 scoring dispatch behind tlp_score (no argument checks)
+tlp_status score_launch(tlp_ctx* ctx, const float* feats, int64_t N, float* scores, cudaStream_t s);
 tlp_status build_token_table(tlp_ctx* ctx, const uint8_t* blob, const int64_t* off, int32_t n);
 
 // k_select.cu

@@ -449,3 +449,75 @@ def test_sharded_topk_merge_bitwise(tp, tokscale):
     m.sync()
     assert np.array_equal(idx.cpu().numpy(), idx_ref.cpu().numpy())
     assert np.array_equal(val.cpu().numpy().view(np.uint32), val_ref.cpu().numpy().view(np.uint32))
+
+
+# ---------------------------------------------------------------- one search round from host memory
+ROUND_OFF = np.array([0, 400, 401, 401, 1500, 2003], np.int64)  # an empty and a 1-candidate task
+
+
+def _round_model(tp, tokens, scale, precision):
+    ocfg = oracle_cfg(n_attn=2, n_tasks=2)
+    flat = flat_params(ocfg, seed=21)
+    m = tp.TLP(product_cfg(ocfg, precision))
+    m.set_token_table(sorted(tokens, key=tokens.get))
+    m.set_norm_scales(scale)
+    m.set_params(flat.astype(np.float32))
+    return m, ocfg, flat
+
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_search_round_host_pipeline(tp, tokscale, precision):
+    """tlp_search_round (host batch; chunked host->device copy overlapped with
+    encode + score) equals tlp_encode -> tlp_score -> tlp_topk on a device copy
+    bit for bit, for every chunk count and for pinned and pageable host memory;
+    its top-k is the oracle top-k of the GPU's scores and sampled scores match
+    the oracle forward."""
+    tokens, scale = tokscale
+    m, ocfg, flat = _round_model(tp, tokens, scale, precision)
+    N = 2003
+    b = synth.generate(41, N)
+    X = m.encode(tp.DeviceBatch.from_packed(b))
+    s = m.score(X)
+    idx_ref, val_ref = m.topk(s, ROUND_OFF, 16, head=1, shard_base=7)
+    m.sync()
+    idx_ref, val_ref = idx_ref.cpu().numpy(), val_ref.cpu().numpy()
+    s_h = s.cpu().numpy()
+    o_idx, o_val = oracle.topk(s_h[:, 1], ROUND_OFF, 16)
+    assert np.array_equal(idx_ref, np.where(o_idx >= 0, o_idx + 7, o_idx))
+    pick = np.array([0, 1, 399, 400, 1004, 2002])
+    Xs = oracle.encode([b.slice(int(i), int(i) + 1).to_lists()[0] for i in pick], tokens, scale)
+    tol = 1e-5 if precision == "fp32" else 1e-2
+    assert rel_err(s_h[pick], OM.forward(ocfg, OM.unflatten(ocfg, flat), Xs)) <= tol
+    for pin in (True, False):
+        hb = tp.DeviceBatch.from_packed(b, pin=True) if pin else tp.DeviceBatch.from_packed(b, device="cpu")
+        for chunks in ((1, 2, 7, 64) if pin else (3,)):
+            idx, val = m.search_round(hb, ROUND_OFF, 16, head=1, shard_base=7, chunks=chunks)
+            m.sync()
+            assert np.array_equal(idx.numpy(), idx_ref), (pin, chunks)
+            assert np.array_equal(val.numpy().view(np.uint32), val_ref.view(np.uint32)), (pin, chunks)
+
+
+def test_search_round_errors(tp, tokscale):
+    tokens, scale = tokscale
+    m, _, _ = _round_model(tp, tokens, scale, "bf16")
+    b = synth.generate(42, 50)
+    hb = tp.DeviceBatch.from_packed(b, device="cpu")
+    off = np.array([0, 20, 50], np.int64)
+    for kw, code in ((dict(chunks=0), "ERR_ARG"), (dict(chunks=65), "ERR_ARG"),
+                     (dict(head=2), "ERR_ARG")):
+        with pytest.raises(tp.TLPError) as e:
+            m.search_round(hb, off, 4, **kw)
+        assert e.value.code == code
+    with pytest.raises(tp.TLPError) as e:
+        m.search_round(hb, np.array([0, 20, 51], np.int64), 4)
+    assert e.value.code == "ERR_SHAPE"
+    bad = hb.seq_off.clone()
+    bad[3] = bad[2] - 1
+    hb_bad = tp.DeviceBatch(bad, hb.prim_type, hb.arg_off, hb.arg_kind, hb.arg_num, hb.arg_name,
+                            hb.str_blob, hb.str_off, hb.N, hb.P, hb.A, hb.U)
+    with pytest.raises(tp.TLPError) as e:
+        m.search_round(hb_bad, off, 4)
+    assert e.value.code == "ERR_SHAPE"
+    idx, _ = m.search_round(hb, off, 4)  # the ctx is still usable after the refusals
+    m.sync()
+    assert (idx.numpy()[:, :4] >= 0).all()
