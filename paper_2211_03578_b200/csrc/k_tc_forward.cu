@@ -8,8 +8,8 @@
 //   h  = relu(U1 W2 + b2)            tcgen05, -> bf16 smem (A operand + residual stream)
 //   per attention layer, per head j (8 heads, d_h = 32):
 //     [Q_j|K_j|V_j] = h W_qkv_j + b  tcgen05 N=96, issued two heads ahead (TMEM double buffer)
-//     O_j = softmax(Q_j K_j^T / sqrt(32)) V_j   block-diagonal per candidate, on the
-//           epilogue warps with warp-level mma.sync (FA2-style register reuse of P)
+//     O_j = softmax(Q_j K_j^T / sqrt(32)) V_j   per candidate (25 x 25 in a padded
+//           32 x 32 block), on 10 epilogue warps with warp-level mma.sync
 //     acc += O_j Wo[32j:32j+32, :]   tcgen05, accumulated in TMEM
 //   h = h + acc + bo
 //   per residual block: r = relu(h Wa + a) in two N-halves (bf16 in TMEM as the
@@ -17,25 +17,26 @@
 //   per task t: s_t = sum_l relu(h_l W1_t + c1_t) . w2_t + 25 c2_t (fixed-order row sum)
 // Only X (2,200 B/candidate) is read from HBM and n_tasks floats are written.
 // Weights (bf16, UMMA canonical layout, consumption order) stream from L2
-// through a 5-stage x 16 KB ring filled by 1-D bulk TMA (cp.async.bulk);
+// through a 4-stage x 16 KB ring filled by 1-D bulk TMA (cp.async.bulk);
 // biases / w2 / c2 are staged once per CTA in shared memory.
 //
 // Warp roles: warp 0 = TMA producer (one lane), warp 1 = tcgen05.mma issuer
-// (one lane) and TMEM owner, warps 2..9 = epilogue: two warps per TMEM lane
-// quarter (thread = tile row = TMEM lane), splitting every epilogue's columns
-// (and the attention's two 16-row m-tiles) between them for 2x latency
-// hiding.  MMA -> epilogue: tcgen05.commit on `acc` (generic) or `qkv`;
-// epilogue -> MMA: 256 arrivals on `opnd` after fence.proxy.async / wait::st.
+// (one lane) and TMEM owner, warps 2..11 = epilogue.  Row-wise epilogues run on
+// warps 2..9, two per TMEM lane quarter (thread = tile row = TMEM lane),
+// splitting the columns.  The attention runs on all ten: QKV_j is converted by
+// the warps of each lane quarter (2 or 3), and warp 2 + u computes the unit u =
+// (candidate u/2, query half u%2).  MMA -> epilogue: tcgen05.commit on `acc`
+// (generic) or `qkv[j%2]`; epilogue -> MMA: arrivals on `opnd` (256) or
+// `attn[j%2]` (320) after fence.proxy.async / wait::st.
 //
 // The attention core is 1.5% of the FLOPs (0.64 of 44 MFLOP/candidate) and is
 // block-diagonal 25x25 per candidate; doing it in registers removes two
 // MMA<->epilogue round trips per head, which dominated v2 (ncu: TC 43% busy).
 //
-// Batch invariance (R34): a candidate's keys sit at positions 32*slot+kk
-// (kk < 25, pad zero / masked), every row's softmax sums the same nonzero
-// terms in the same order whatever its slot, and the PV k-steps of the other
-// candidate contribute exact zeros; everything else is row-local and the
-// 25-row head sum runs in a fixed order.
+// Batch invariance (R34): Q, K, V of a candidate sit at padded positions
+// 32*slot+kk (kk < 25, pad zero / masked); a unit only touches its candidate's
+// block, at the same relative positions whatever the slot; everything else is
+// row-local and the 25-row head sum runs in a fixed order.
 #include "tlp_internal.cuh"
 #include "tc_ptx.cuh"
 
@@ -50,17 +51,18 @@ constexpr int kL = 25, kE = 22, kH = 256, kHeads = 8, kDH = 32, kHD = 128;
 constexpr int kCand = 5;            // candidates per tile
 constexpr int kKX = 32;             // padded K of the first GEMM (22 -> 32)
 constexpr int kKP = 160;            // padded key positions (5 x 32)
-constexpr int kStages = 5;
+constexpr int kStages = 4;
 constexpr uint32_t kStageBytes = 16384;
-constexpr int kThreads = 320;   // warp 0 TMA, warp 1 MMA, warps 2..9 epilogue
-constexpr int kEpi = 256;       // epilogue threads (2 warps per TMEM lane quarter)
+constexpr int kThreads = 384;   // warp 0 TMA, warp 1 MMA, warps 2..11 epilogue
+constexpr int kEpi = 256;       // row-wise epilogue threads: warps 2..9, 2 per TMEM lane quarter
+constexpr int kAttn = 320;      // attention threads: warps 2..11, one (candidate, query half) each
 constexpr uint32_t kRowB = 80;      // row stride (bytes) of the mma.sync Q/K/V tiles (64 + 16 pad)
 
 // shared memory map (bytes)
 constexpr uint32_t OFF_H = 0;                       // h      [128 x 256] bf16, canonical Kt=256
 constexpr uint32_t OFF_X = OFF_H + 65536;           // X      [128 x 32]  canonical
-constexpr uint32_t OFF_Q = OFF_X + 8192;            // Q_j    [128][32] row-major, 80 B rows
-constexpr uint32_t OFF_K = OFF_Q + 128 * kRowB;     // K_j    [160][32] (padded key positions)
+constexpr uint32_t OFF_Q = OFF_X + 8192;            // Q_j    [160][32] row-major, 80 B rows (padded positions)
+constexpr uint32_t OFF_K = OFF_Q + kKP * kRowB;     // K_j    [160][32] (padded key positions)
 constexpr uint32_t OFF_V = OFF_K + kKP * kRowB;     // V_j    [160][32]
 constexpr uint32_t OFF_O = OFF_V + kKP * kRowB;     // O_j    2 x [128 x 32] canonical (A of oproj)
 constexpr uint32_t OFF_DOT = OFF_O + 2 * 8192;      // 2 x 128 fp32 row dots
@@ -211,78 +213,63 @@ __device__ __forceinline__ float ex2_approx(float x) {
   return y;
 }
 
-// Block-diagonal attention of one head for 16 query rows (m-tile `mt` of this
-// lane quarter q).  Keys of the quarter's two candidates are the 64 padded
-// positions [32*s_lo, 32*s_lo + 64); S = Q K^T (8 n-tiles x 2 k-steps),
-// masked softmax per row (quad shuffles), P reused from registers as the A
-// fragments of O = P V (4 n-tiles x 4 k-steps), O scaled by 1/rowsum;
-// O_j -> canonical bf16 [128 x 32] (A operand of the output projection).
-__device__ __forceinline__ void attn_head_mma(uint8_t* smem, uint32_t sbase, uint32_t q,
-                                              uint32_t mt, uint32_t lane, float sm_scale,
+// Attention core of one head for one unit = (candidate c, query half mh): the
+// 16 queries at padded positions 32c + 16mh .. +15 against the candidate's own
+// 32 padded key positions (25 real), on one warp with mma.sync m16n8k16 bf16:
+// S = Q K^T (4 n-tiles x 2 k-steps), masked softmax in registers (exp2 with the
+// log2(e)/sqrt(d_h) scale folded in), P packed as A fragments (FA2-style register
+// reuse), O = P V (4 d-tiles x 2 k-steps), O scaled by 1/rowsum and stored to
+// the canonical bf16 [128 x 32] A operand of the output projection at tile rows
+// 25c + kk.  Every candidate sees exactly its own block, at the same relative
+// positions whatever its slot (batch invariance, R34).
+__device__ __forceinline__ void attn_unit_mma(uint8_t* smem, uint32_t sbase, uint32_t c,
+                                              uint32_t mh, uint32_t lane, float sm_scale,
                                               uint32_t o_off) {
-  const uint32_t s_lo = (32 * q) / kL;
-  const uint32_t kp0 = 32 * s_lo;
   const uint32_t g = lane >> 2, tig = lane & 3;
-  uint32_t qa[2][4];  // Q A-fragments per k-step
+  const uint32_t q0 = 32 * c + 16 * mh, k0 = 32 * c;
+  uint32_t qa[2][4];  // Q A-fragments per k-step (d 0..15, 16..31)
 #pragma unroll
-  for (int ks = 0; ks < 2; ++ks) {
-    const uint32_t row = 32 * q + 16 * mt + (lane & 15);
-    const uint32_t col = 16 * ks + 8 * (lane >> 4);
-    tc::ldsm_x4(sbase + OFF_Q + row * kRowB + col * 2, qa[ks]);
-  }
-  float s[8][4];
+  for (int ks = 0; ks < 2; ++ks)
+    tc::ldsm_x4(sbase + OFF_Q + (q0 + (lane & 15)) * kRowB + (16 * ks + 8 * (lane >> 4)) * 2, qa[ks]);
+  float s[4][4];
 #pragma unroll
-  for (int nt = 0; nt < 8; ++nt) {
+  for (int nt = 0; nt < 4; ++nt) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) s[nt][i] = 0.f;
     uint32_t kb[4];  // (ks0: b0,b1) (ks1: b0,b1)
-    tc::ldsm_x4(sbase + OFF_K + (kp0 + 8 * nt + (lane & 7)) * kRowB + 16 * (lane >> 3), kb);
+    tc::ldsm_x4(sbase + OFF_K + (k0 + 8 * nt + (lane & 7)) * kRowB + 16 * (lane >> 3), kb);
     tc::mma16816(s[nt], qa[0], kb[0], kb[1]);
     tc::mma16816(s[nt], qa[1], kb[2], kb[3]);
   }
-  // masked softmax (unnormalised); rows 32q + 16mt + g (+8)
-  // Each row only attends to its own candidate's block of 4 n-tiles (block 0 =
-  // s_lo, 1 = s_lo + 1): select that block (8 values per thread), exponentiate
-  // only those, and zero the other block -- half the MUFU work of a masked
-  // 64-wide row, same values and summation order (batch invariance, R34).
   float inv[2];
 #pragma unroll
-  for (int half = 0; half < 2; ++half) {
-    const uint32_t row = 32 * q + 16 * mt + g + 8 * half;
-    const int blk = (int)(row / kL) - (int)s_lo;  // 0, 1; >= 2 for pad rows
-    const bool hi = blk == 1, any = blk <= 1;
-    float x[8];
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) x[2 * i + e] = hi ? s[4 + i][2 * half + e] : s[i][2 * half + e];
+  for (int half = 0; half < 2; ++half) {  // rows q0 + g (+8)
     float mx = -INFINITY;
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
       for (int e = 0; e < 2; ++e)
-        if (any && 8 * i + 2 * (int)tig + e < kL) mx = fmaxf(mx, x[2 * i + e]);
+        if (8 * nt + 2 * (int)tig + e < kL) mx = fmaxf(mx, s[nt][2 * half + e]);
     mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
     mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-    const float off = (mx == -INFINITY) ? 0.f : mx * sm_scale;
+    const float off = mx * sm_scale;  // key 0 is always real: mx finite
     float sum = 0.f;
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        const bool ok = any && 8 * i + 2 * (int)tig + e < kL;
-        const float p = ok ? ex2_approx(fmaf(x[2 * i + e], sm_scale, -off)) : 0.f;
-        s[i][2 * half + e] = hi ? 0.f : p;
-        s[4 + i][2 * half + e] = hi ? p : 0.f;
+        const float p = (8 * nt + 2 * (int)tig + e < kL)
+                            ? ex2_approx(fmaf(s[nt][2 * half + e], sm_scale, -off)) : 0.f;
+        s[nt][2 * half + e] = p;
         sum += p;
       }
     sum += __shfl_xor_sync(0xffffffffu, sum, 1);
     sum += __shfl_xor_sync(0xffffffffu, sum, 2);
-    inv[half] = sum > 0.f ? 1.0f / sum : 0.f;
+    inv[half] = 1.0f / sum;
   }
-  uint32_t pa[4][4];  // P as A fragments per 16-key block
+  uint32_t pa[2][4];  // P as A fragments per 16-key block
 #pragma unroll
-  for (int kbk = 0; kbk < 4; ++kbk) {
+  for (int kbk = 0; kbk < 2; ++kbk) {
     pa[kbk][0] = tc::pack_bf16(s[2 * kbk][0], s[2 * kbk][1]);
     pa[kbk][1] = tc::pack_bf16(s[2 * kbk][2], s[2 * kbk][3]);
     pa[kbk][2] = tc::pack_bf16(s[2 * kbk + 1][0], s[2 * kbk + 1][1]);
@@ -294,25 +281,27 @@ __device__ __forceinline__ void attn_head_mma(uint8_t* smem, uint32_t sbase, uin
 #pragma unroll
     for (int i = 0; i < 4; ++i) o[dn][i] = 0.f;
 #pragma unroll
-  for (int kbk = 0; kbk < 4; ++kbk)
+  for (int kbk = 0; kbk < 2; ++kbk)
 #pragma unroll
     for (int dp = 0; dp < 2; ++dp) {  // pairs of d n-tiles
       uint32_t vb[4];                 // (dn=2dp: b0,b1) (dn=2dp+1: b0,b1)
-      const uint32_t krow = kp0 + 16 * kbk + (lane & 7) + 8 * ((lane >> 3) & 1);
+      const uint32_t krow = k0 + 16 * kbk + (lane & 7) + 8 * ((lane >> 3) & 1);
       const uint32_t dcol = 8 * (2 * dp + (lane >> 4));
       tc::ldsm_x4_t(sbase + OFF_V + krow * kRowB + dcol * 2, vb);
       tc::mma16816(o[2 * dp], pa[kbk], vb[0], vb[1]);
       tc::mma16816(o[2 * dp + 1], pa[kbk], vb[2], vb[3]);
     }
 #pragma unroll
-  for (int dn = 0; dn < 4; ++dn)
+  for (int half = 0; half < 2; ++half) {
+    const uint32_t kk = 16 * mh + g + 8 * half;
+    if (kk < (uint32_t)kL) {
+      const uint32_t row = kL * c + kk;
 #pragma unroll
-    for (int half = 0; half < 2; ++half) {
-      const uint32_t row = 32 * q + 16 * mt + g + 8 * half;
-      const uint32_t d = 8 * dn + 2 * tig;
-      *reinterpret_cast<uint32_t*>(smem + o_off + tc::canon_off(row, d, kDH)) =
-          tc::pack_bf16(o[dn][2 * half] * inv[half], o[dn][2 * half + 1] * inv[half]);
+      for (int dn = 0; dn < 4; ++dn)
+        *reinterpret_cast<uint32_t*>(smem + o_off + tc::canon_off(row, 8 * dn + 2 * tig, kDH)) =
+            tc::pack_bf16(o[dn][2 * half] * inv[half], o[dn][2 * half + 1] * inv[half]);
     }
+  }
 }
 
 __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a) {
@@ -322,13 +311,17 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
   const uint32_t bar_full = sbase + OFF_BAR;             // kStages
   const uint32_t bar_empty = bar_full + 8 * kStages;     // kStages
   const uint32_t bar_acc = bar_empty + 8 * kStages;      // generic GEMM done
-  const uint32_t bar_qkv = bar_acc + 8;                  // QKV_j done
-  const uint32_t bar_opnd = bar_qkv + 8;                 // epilogue -> MMA (kEpi arrivals)
+  // Per head-parity barriers: phase n+1 of bar_qkv[p] / bar_attn[p] cannot
+  // complete before every waiter has observed phase n (QKV_{j+2} is issued only
+  // after O_j, O_{j+2} needs QKV_{j+2}), so a parity wait can never miss a phase.
+  const uint32_t bar_qkv = bar_acc + 8;                  // [2] QKV_j done (j % 2)
+  const uint32_t bar_opnd = bar_qkv + 16;                // epilogue -> MMA (kEpi arrivals)
+  const uint32_t bar_attn = bar_opnd + 8;                // [2] O_j ready (kAttn arrivals, j % 2)
   uint32_t* tptr = reinterpret_cast<uint32_t*>(smem + OFF_TPTR);
   float* vs = reinterpret_cast<float*>(smem + OFF_VEC);
 
-  // K/V pad key positions must stay exactly 0: zero Q/K/V once.
-  for (uint32_t o = OFF_Q + threadIdx.x * 16; o < OFF_O; o += kThreads * 16)
+  // Q/K/V pad positions must stay exactly 0 (and O's pad rows finite): zero once.
+  for (uint32_t o = OFF_Q + threadIdx.x * 16; o < OFF_O + 2 * 8192; o += kThreads * 16)
     *reinterpret_cast<uint4*>(smem + o) = make_uint4(0, 0, 0, 0);
   for (int i = threadIdx.x; i < a.vec_floats / 4; i += kThreads)
     reinterpret_cast<float4*>(vs)[i] = __ldg(reinterpret_cast<const float4*>(a.vec) + i);
@@ -339,7 +332,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
     }
     tc::mbar_init(bar_acc, 1);
     tc::mbar_init(bar_qkv, 1);
+    tc::mbar_init(bar_qkv + 8, 1);
     tc::mbar_init(bar_opnd, kEpi);
+    tc::mbar_init(bar_attn, kAttn);
+    tc::mbar_init(bar_attn + 8, kAttn);
     tc::fence_barrier_init();
   }
   if (warp == 1) tc::tmem_alloc(tc::smem_u32(tptr), 512);
@@ -370,7 +366,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
     // ------------------------------------------------ MMA issuer
     if (lane == 0) {
       int stage = 0;
-      uint32_t phase = 0, op_phase = 0;
+      uint32_t phase = 0, op_phase = 0, at_phase[2] = {0, 0};
       auto wait_opnd = [&]() {
         tc::mbar_wait(bar_opnd, op_phase);
         op_phase ^= 1;
@@ -412,13 +408,15 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
           gemm_w(false, OFF_H, kH, T_QKV, 96, kH, 64, false);             // QKV_0 -> buf 0
           tc::mma_commit(bar_qkv);
           gemm_w(false, OFF_H, kH, T_QKV + 96, 96, kH, 64, false);        // QKV_1 -> buf 1
-          tc::mma_commit(bar_qkv);
+          tc::mma_commit(bar_qkv + 8);
           for (int j = 0; j < kHeads; ++j) {
-            wait_opnd();                                                  // O_j ready, buf j%2 free
+            tc::mbar_wait(bar_attn + 8 * (j & 1), at_phase[j & 1]);       // O_j ready, buf j%2 free
+            at_phase[j & 1] ^= 1;
+            tc::tc_fence_after();
             gemm_w(false, OFF_O + 8192 * (j & 1), kDH, T_A, kH, kDH, 32, j > 0);  // acc += O_j Wo_j
             if (j + 2 < kHeads) {
               gemm_w(false, OFF_H, kH, T_QKV + 96 * (j & 1), 96, kH, 64, false);  // QKV_{j+2}
-              tc::mma_commit(bar_qkv);
+              tc::mma_commit(bar_qkv + 8 * (j & 1));
             }
           }
           tc::mma_commit(bar_acc);
@@ -444,13 +442,15 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
       }
     }
   } else {
-    // ------------------------------------------------ epilogue (256 threads)
+    // ------------------------------------------------ epilogue (warps 2..11)
     const uint32_t q = warp & 3;                       // TMEM lane quarter
-    const uint32_t hh = (warp - 2) >> 2;               // which of the quarter's two warps
+    const uint32_t hh = (warp - 2) >> 2;               // 0, 1 (row-wise phases) or 2 (quarters 2, 3)
+    const bool rowwise = hh < 2;                       // warps 2..9 run the row-wise epilogues
+    const uint32_t unit = warp - 2;                    // attention unit: candidate unit/2, query half unit%2
     const uint32_t r = 32 * q + lane;                  // tile row == TMEM lane
     const uint32_t tl = tmem + ((32 * q) << 16);       // this warp's lane quarter
     float* rowdot = reinterpret_cast<float*>(smem + OFF_DOT);   // [2][128]
-    uint32_t ph_acc = 0, ph_qkv = 0;
+    uint32_t ph_acc = 0, ph_qkv[2] = {0, 0};
     int titer = 0, tev = 0;
     auto tr = [&]() {  // diagnostics only (a.trace == nullptr in production)
       if (a.trace && blockIdx.x == 0 && threadIdx.x == 64 && titer < 8 && tev < 64)
@@ -481,70 +481,85 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
       tev = 0;
       tr();
       const int64_t n = tile * kCand + slot;
-      if (hh == 0) {  // E0: X rows -> bf16 [128 x 32]
-        uint32_t pk[16];
+      if (rowwise) {
+        if (hh == 0) {  // E0: X rows -> bf16 [128 x 32]
+          uint32_t pk[16];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) pk[i] = 0;
-        if (real && n < a.N) {
-          const float2* src = reinterpret_cast<const float2*>(a.X + (tile * kCand * kL + r) * kE);
+          for (int i = 0; i < 16; ++i) pk[i] = 0;
+          if (real && n < a.N) {
+            const float2* src = reinterpret_cast<const float2*>(a.X + (tile * kCand * kL + r) * kE);
 #pragma unroll
-          for (int i = 0; i < kE / 2; ++i) {
-            const float2 x = __ldg(src + i);
-            pk[i] = tc::pack_bf16(x.x, x.y);
-          }
-        }
-        store_row32(smem, OFF_X, r, 0, kKX, pk);
-      }
-      signal();
-      wait_on(bar_acc, ph_acc);
-      epi_relu_to_tmem(tl, T_B, lo_of(128), hi_of(128), vs + a.up_b0, T_AOP);   // U1 -> TMEM
-      signal();
-      wait_on(bar_acc, ph_acc);
-      epi_relu_to_smem(smem, tl, T_A, lo_of(kH), hi_of(kH), vs + a.up_b1, OFF_H, kH, r);  // h
-      signal();
-      for (int l = 0; l < NA; ++l) {
-        for (int j = 0; j < kHeads; ++j) {
-          wait_on(bar_qkv, ph_qkv);
-          asm volatile("bar.sync 2, 256;" ::: "memory");  // all warps done reading head j-1
-          {  // QKV_j (TMEM) + bias -> Q, K (warp 0 of the quarter) / V (warp 1) tiles
-            const uint32_t tq = tl + T_QKV + 96 * (j & 1);
-            const uint32_t kpos = 32 * slot + kk;
-            // balanced split, 48 columns per warp: warp 0 of the quarter converts Q
-            // and K[0:16), warp 1 converts K[16:32) and V; both loads in flight
-            // before one wait
-            float v[32], v2[16], b[32], b2[16];
-            uint32_t pk[16], pk2[8];
-            const uint32_t c32 = hh == 0 ? 0u : 64u;       // Q or V (32 columns)
-            const uint32_t c16 = hh == 0 ? 32u : 48u;      // K half (16 columns)
-            tc::tmem_ld32(tq + c32, v);
-            tc::tmem_ld16(tq + c16, v2);
-            vec32(vs + (hh == 0 ? a.bq[l] : a.bv[l]) + kDH * j, b);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const float4 x = reinterpret_cast<const float4*>(vs + a.bk[l] + kDH * j + 16 * hh)[i];
-              b2[4 * i] = x.x; b2[4 * i + 1] = x.y; b2[4 * i + 2] = x.z; b2[4 * i + 3] = x.w;
-            }
-            tc::tmem_wait_ld();
-#pragma unroll
-            for (int i = 0; i < 16; ++i) pk[i] = tc::pack_bf16(v[2 * i] + b[2 * i], v[2 * i + 1] + b[2 * i + 1]);
-#pragma unroll
-            for (int i = 0; i < 8; ++i) pk2[i] = tc::pack_bf16(v2[2 * i] + b2[2 * i], v2[2 * i + 1] + b2[2 * i + 1]);
-            if (hh == 0) store_plain32(smem, OFF_Q + r * kRowB, pk);
-            else if (real) store_plain32(smem, OFF_V + kpos * kRowB, pk);
-            if (real) {
-              uint8_t* kd = smem + OFF_K + kpos * kRowB + 32 * hh;
-              *reinterpret_cast<uint4*>(kd) = make_uint4(pk2[0], pk2[1], pk2[2], pk2[3]);
-              *reinterpret_cast<uint4*>(kd + 16) = make_uint4(pk2[4], pk2[5], pk2[6], pk2[7]);
+            for (int i = 0; i < kE / 2; ++i) {
+              const float2 x = __ldg(src + i);
+              pk[i] = tc::pack_bf16(x.x, x.y);
             }
           }
-          asm volatile("bar.sync 2, 256;" ::: "memory");  // Q/K/V of head j complete
-          attn_head_mma(smem, sbase, q, hh, lane, sm_scale, OFF_O + 8192 * (j & 1));
-          signal();                                       // O_j ready; QKV buffer j%2 free
+          store_row32(smem, OFF_X, r, 0, kKX, pk);
         }
+        signal();
         wait_on(bar_acc, ph_acc);
-        epi_residual(smem, tl, vs + a.bo[l], r, lo_of(kH), hi_of(kH));
+        epi_relu_to_tmem(tl, T_B, lo_of(128), hi_of(128), vs + a.up_b0, T_AOP);   // U1 -> TMEM
+        signal();
+        wait_on(bar_acc, ph_acc);
+        epi_relu_to_smem(smem, tl, T_A, lo_of(kH), hi_of(kH), vs + a.up_b1, OFF_H, kH, r);  // h
         signal();
       }
+      for (int l = 0; l < NA; ++l) {
+        for (int j = 0; j < kHeads; ++j) {
+          wait_on(bar_qkv + 8 * (j & 1), ph_qkv[j & 1]);
+          asm volatile("bar.sync 2, 320;" ::: "memory");  // all warps done reading head j-1
+          {  // QKV_j (TMEM) + bias -> Q, K, V tiles at padded positions 32 slot + kk
+            const uint32_t tq = tl + T_QKV + 96 * (j & 1);
+            const uint32_t pos = (32 * slot + kk) * kRowB;
+            if (q >= 2) {  // three warps in this quarter: Q, K, V (32 columns each)
+              float v[32], b[32];
+              uint32_t pk[16];
+              tc::tmem_ld32(tq + 32 * hh, v);
+              vec32(vs + (hh == 0 ? a.bq[l] : hh == 1 ? a.bk[l] : a.bv[l]) + kDH * j, b);
+              tc::tmem_wait_ld();
+#pragma unroll
+              for (int i = 0; i < 16; ++i) pk[i] = tc::pack_bf16(v[2 * i] + b[2 * i], v[2 * i + 1] + b[2 * i + 1]);
+              if (real) store_plain32(smem, (hh == 0 ? OFF_Q : hh == 1 ? OFF_K : OFF_V) + pos, pk);
+            } else {  // two warps: Q + K[0:16) / K[16:32) + V, both loads before one wait
+              float v[32], v2[16], b[32], b2[16];
+              uint32_t pk[16], pk2[8];
+              const uint32_t c32 = hh == 0 ? 0u : 64u;       // Q or V (32 columns)
+              const uint32_t c16 = hh == 0 ? 32u : 48u;      // K half (16 columns)
+              tc::tmem_ld32(tq + c32, v);
+              tc::tmem_ld16(tq + c16, v2);
+              vec32(vs + (hh == 0 ? a.bq[l] : a.bv[l]) + kDH * j, b);
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const float4 x = reinterpret_cast<const float4*>(vs + a.bk[l] + kDH * j + 16 * hh)[i];
+                b2[4 * i] = x.x; b2[4 * i + 1] = x.y; b2[4 * i + 2] = x.z; b2[4 * i + 3] = x.w;
+              }
+              tc::tmem_wait_ld();
+#pragma unroll
+              for (int i = 0; i < 16; ++i) pk[i] = tc::pack_bf16(v[2 * i] + b[2 * i], v[2 * i + 1] + b[2 * i + 1]);
+#pragma unroll
+              for (int i = 0; i < 8; ++i) pk2[i] = tc::pack_bf16(v2[2 * i] + b2[2 * i], v2[2 * i + 1] + b2[2 * i + 1]);
+              if (real) {
+                store_plain32(smem, (hh == 0 ? OFF_Q : OFF_V) + pos, pk);
+                uint8_t* kd = smem + OFF_K + pos + 32 * hh;
+                *reinterpret_cast<uint4*>(kd) = make_uint4(pk2[0], pk2[1], pk2[2], pk2[3]);
+                *reinterpret_cast<uint4*>(kd + 16) = make_uint4(pk2[4], pk2[5], pk2[6], pk2[7]);
+              }
+            }
+          }
+          asm volatile("bar.sync 2, 320;" ::: "memory");  // Q/K/V of head j complete
+          attn_unit_mma(smem, sbase, unit >> 1, unit & 1, lane, sm_scale, OFF_O + 8192 * (j & 1));
+          tc::fence_proxy_async_smem();                   // O_j ready; QKV buffer j%2 free
+          tc::tc_fence_before();
+          tc::mbar_arrive(bar_attn + 8 * (j & 1));
+          tr();
+        }
+        if (rowwise) {
+          wait_on(bar_acc, ph_acc);
+          epi_residual(smem, tl, vs + a.bo[l], r, lo_of(kH), hi_of(kH));
+          signal();
+        }
+      }
+      if (!rowwise) continue;
       for (int rb = 0; rb < NR; ++rb) {
         wait_on(bar_acc, ph_acc);
         epi_relu_to_tmem(tl, T_B, lo_of(128), hi_of(128), vs + a.ra[rb], T_AOP);
