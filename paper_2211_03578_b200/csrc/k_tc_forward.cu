@@ -64,8 +64,8 @@ constexpr uint32_t OFF_X = OFF_H + 65536;           // X      [128 x 32]  canoni
 constexpr uint32_t OFF_Q = OFF_X + 8192;            // Q_j    [160][32] row-major, 80 B rows (padded positions)
 constexpr uint32_t OFF_K = OFF_Q + kKP * kRowB;     // K_j    [160][32] (padded key positions)
 constexpr uint32_t OFF_V = OFF_K + kKP * kRowB;     // V_j    [160][32]
-constexpr uint32_t OFF_O = OFF_V + kKP * kRowB;     // O_j    2 x [128 x 32] canonical (A of oproj)
-constexpr uint32_t OFF_DOT = OFF_O + 2 * 8192;      // 2 x 128 fp32 row dots
+constexpr uint32_t OFF_O = OFF_V + kKP * kRowB;     // O_j    3 x [128 x 32] canonical (A of oproj), j % 3
+constexpr uint32_t OFF_DOT = OFF_O + 3 * 8192;      // 2 x 128 fp32 row dots
 constexpr uint32_t OFF_BAR = OFF_DOT + 1024;        // mbarriers (<= 32)
 constexpr uint32_t OFF_TPTR = OFF_BAR + 256;
 constexpr uint32_t OFF_RING = OFF_TPTR + 128;       // kStages x 16 KB
@@ -311,17 +311,19 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
   const uint32_t bar_full = sbase + OFF_BAR;             // kStages
   const uint32_t bar_empty = bar_full + 8 * kStages;     // kStages
   const uint32_t bar_acc = bar_empty + 8 * kStages;      // generic GEMM done
-  // Per head-parity barriers: phase n+1 of bar_qkv[p] / bar_attn[p] cannot
-  // complete before every waiter has observed phase n (QKV_{j+2} is issued only
-  // after O_j, O_{j+2} needs QKV_{j+2}), so a parity wait can never miss a phase.
+  // Attention-phase barriers, indexed so that phase n+1 of a barrier cannot
+  // complete before every waiter has observed phase n (a parity wait can never
+  // miss a phase): QKV_{j+2} is issued after conv_j is observed, O_{j+4} needs
+  // QKV_{j+4}, issued after attn_j is observed.
   const uint32_t bar_qkv = bar_acc + 8;                  // [2] QKV_j done (j % 2)
   const uint32_t bar_opnd = bar_qkv + 16;                // epilogue -> MMA (kEpi arrivals)
-  const uint32_t bar_attn = bar_opnd + 8;                // [2] O_j ready (kAttn arrivals, j % 2)
+  const uint32_t bar_conv = bar_opnd + 8;                // [2] QKV_j read, TMEM buffer free (j % 2)
+  const uint32_t bar_attn = bar_conv + 16;               // [4] O_j ready (j % 4)
   uint32_t* tptr = reinterpret_cast<uint32_t*>(smem + OFF_TPTR);
   float* vs = reinterpret_cast<float*>(smem + OFF_VEC);
 
   // Q/K/V pad positions must stay exactly 0 (and O's pad rows finite): zero once.
-  for (uint32_t o = OFF_Q + threadIdx.x * 16; o < OFF_O + 2 * 8192; o += kThreads * 16)
+  for (uint32_t o = OFF_Q + threadIdx.x * 16; o < OFF_O + 3 * 8192; o += kThreads * 16)
     *reinterpret_cast<uint4*>(smem + o) = make_uint4(0, 0, 0, 0);
   for (int i = threadIdx.x; i < a.vec_floats / 4; i += kThreads)
     reinterpret_cast<float4*>(vs)[i] = __ldg(reinterpret_cast<const float4*>(a.vec) + i);
@@ -334,8 +336,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
     tc::mbar_init(bar_qkv, 1);
     tc::mbar_init(bar_qkv + 8, 1);
     tc::mbar_init(bar_opnd, kEpi);
-    tc::mbar_init(bar_attn, kAttn);
-    tc::mbar_init(bar_attn + 8, kAttn);
+    for (int i = 0; i < 2; ++i) tc::mbar_init(bar_conv + 8 * i, kAttn);
+    for (int i = 0; i < 4; ++i) tc::mbar_init(bar_attn + 8 * i, kAttn);
     tc::fence_barrier_init();
   }
   if (warp == 1) tc::tmem_alloc(tc::smem_u32(tptr), 512);
@@ -366,9 +368,18 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
     // ------------------------------------------------ MMA issuer
     if (lane == 0) {
       int stage = 0;
-      uint32_t phase = 0, op_phase = 0, at_phase[2] = {0, 0};
+      uint32_t phase = 0, op_phase = 0, cv_phase[2] = {0, 0}, at_phase[4] = {0, 0, 0, 0};
+      // diagnostics (a.trace, CTA 0): cycles the issuer spends waiting per tile on
+      // weight chunks / QKV reads / O_j / other epilogue operands
+      const bool trc = a.trace != nullptr && blockIdx.x == 0;
+      long long wt[4] = {0, 0, 0, 0};
+      auto timed_wait = [&](int k, uint32_t bar, uint32_t ph) {
+        const long long t0 = trc ? clock64() : 0;
+        tc::mbar_wait(bar, ph);
+        if (trc) wt[k] += clock64() - t0;
+      };
       auto wait_opnd = [&]() {
-        tc::mbar_wait(bar_opnd, op_phase);
+        timed_wait(3, bar_opnd, op_phase);
         op_phase ^= 1;
         tc::tc_fence_after();
       };
@@ -378,7 +389,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
                         int K, int Kc, bool acc) {
         const uint32_t idesc = tc::idesc_bf16(128, N);
         for (int kc = 0; kc < K; kc += Kc) {
-          tc::mbar_wait(bar_full + 8 * stage, phase);
+          timed_wait(0, bar_full + 8 * stage, phase);
           tc::tc_fence_after();
           const uint32_t b = sbase + OFF_RING + stage * kStageBytes;
 #pragma unroll 4
@@ -396,7 +407,12 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
       };
-      for (int64_t tile = blockIdx.x; tile < a.ntile; tile += gridDim.x) {
+      int mt = 0;
+      for (int64_t tile = blockIdx.x; tile < a.ntile; tile += gridDim.x, ++mt) {
+        if (trc && mt < 8) {
+          for (int k = 0; k < 4; ++k) wt[k] = 0;
+          a.trace[512 + mt * 8 + 4] = clock64();
+        }
         wait_opnd();                                                      // E0: X
         gemm_w(false, OFF_X, kKX, T_B, 128, kKX, 32, false);              // up0 -> T_B
         tc::mma_commit(bar_acc);
@@ -410,14 +426,17 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
           gemm_w(false, OFF_H, kH, T_QKV + 96, 96, kH, 64, false);        // QKV_1 -> buf 1
           tc::mma_commit(bar_qkv + 8);
           for (int j = 0; j < kHeads; ++j) {
-            tc::mbar_wait(bar_attn + 8 * (j & 1), at_phase[j & 1]);       // O_j ready, buf j%2 free
-            at_phase[j & 1] ^= 1;
-            tc::tc_fence_after();
-            gemm_w(false, OFF_O + 8192 * (j & 1), kDH, T_A, kH, kDH, 32, j > 0);  // acc += O_j Wo_j
             if (j + 2 < kHeads) {
+              timed_wait(1, bar_conv + 8 * (j & 1), cv_phase[j & 1]);     // QKV_j read: buf j%2 free
+              cv_phase[j & 1] ^= 1;
+              tc::tc_fence_after();
               gemm_w(false, OFF_H, kH, T_QKV + 96 * (j & 1), 96, kH, 64, false);  // QKV_{j+2}
               tc::mma_commit(bar_qkv + 8 * (j & 1));
             }
+            timed_wait(2, bar_attn + 8 * (j & 3), at_phase[j & 3]);       // O_j ready
+            at_phase[j & 3] ^= 1;
+            tc::tc_fence_after();
+            gemm_w(false, OFF_O + 8192 * (j % 3), kDH, T_A, kH, kDH, 32, j > 0);  // acc += O_j Wo_j
           }
           tc::mma_commit(bar_acc);
           wait_opnd();                                                    // E_resid
@@ -439,6 +458,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
           tc::mma_commit(bar_acc);
           if (t < NT - 1) wait_opnd();
         }
+        if (trc && mt < 8)
+          for (int k = 0; k < 4; ++k) a.trace[512 + mt * 8 + k] = wt[k];
       }
     }
   } else {
@@ -546,11 +567,13 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
               }
             }
           }
+          tc::tc_fence_before();                          // QKV_j read: TMEM buffer j%2 free
+          if (j + 2 < kHeads) tc::mbar_arrive(bar_conv + 8 * (j & 1));
           asm volatile("bar.sync 2, 320;" ::: "memory");  // Q/K/V of head j complete
-          attn_unit_mma(smem, sbase, unit >> 1, unit & 1, lane, sm_scale, OFF_O + 8192 * (j & 1));
-          tc::fence_proxy_async_smem();                   // O_j ready; QKV buffer j%2 free
+          attn_unit_mma(smem, sbase, unit >> 1, unit & 1, lane, sm_scale, OFF_O + 8192 * (j % 3));
+          tc::fence_proxy_async_smem();                   // O_j ready
           tc::tc_fence_before();
-          tc::mbar_arrive(bar_attn + 8 * (j & 1));
+          tc::mbar_arrive(bar_attn + 8 * (j & 3));
           tr();
         }
         if (rowwise) {
@@ -685,8 +708,8 @@ static std::vector<PackChunk> build_schedule(const tlp_ctx* ctx) {
     qkv(0);
     qkv(1);
     for (int j = 0; j < kHeads; ++j) {
+      if (j + 2 < kHeads) qkv(j + 2);                      // QKV two heads ahead once QKV_j is read
       add(256, 32, kDH * j, kH, {{0, o.Wo[l], kH, 0}});     // oproj_j once O_j is ready
-      if (j + 2 < kHeads) qkv(j + 2);                      // then QKV two heads ahead
     }
   }
   for (int r = 0; r < c.n_res; ++r) {
@@ -776,14 +799,14 @@ tlp_status tc_forward(tlp_ctx* ctx, const float* feats, int64_t N, float* scores
   static const bool trace = getenv("TLP_TC_TRACE") != nullptr;
   long long* d_trace = nullptr;
   if (trace) {
-    TLP_CUDA_TRY(cudaMalloc(&d_trace, 8 * 64 * sizeof(long long)));
-    TLP_CUDA_TRY(cudaMemset(d_trace, 0, 8 * 64 * sizeof(long long)));
+    TLP_CUDA_TRY(cudaMalloc(&d_trace, 8 * 72 * sizeof(long long)));
+    TLP_CUDA_TRY(cudaMemset(d_trace, 0, 8 * 72 * sizeof(long long)));
   }
   a.trace = d_trace;
   tc_forward_kernel<<<grid, kThreads, w.smem, s>>>(a);
   TLP_LAUNCH_CHECK();
   if (trace) {
-    std::vector<long long> h(8 * 64);
+    std::vector<long long> h(8 * 72);
     TLP_CUDA_TRY(cudaStreamSynchronize(s));
     TLP_CUDA_TRY(cudaMemcpy(h.data(), d_trace, h.size() * sizeof(long long), cudaMemcpyDeviceToHost));
     cudaFree(d_trace);
@@ -791,6 +814,9 @@ tlp_status tc_forward(tlp_ctx* ctx, const float* feats, int64_t N, float* scores
       fprintf(stderr, "tile %d:", t);
       for (int e = 1; e < 64 && h[t * 64 + e]; ++e) fprintf(stderr, " %lld", h[t * 64 + e] - h[t * 64 + e - 1]);
       fprintf(stderr, " | total %lld\n", h[(t + 1) * 64] ? h[(t + 1) * 64] - h[t * 64] : 0LL);
+      const long long* m = &h[512 + t * 8];
+      fprintf(stderr, "  mma issuer waits: chunks %lld, qkv-read %lld, O_j %lld, operands %lld (tile %lld)\n",
+              m[0], m[1], m[2], m[3], m[12] ? m[12] - m[4] : 0LL);
     }
   }
   return TLP_OK;
