@@ -342,7 +342,7 @@ def cpu_baseline(seconds_hint=15.0):
     n = 256
     dt = oracle_sample(n)
     # scale the sample to ~seconds_hint of CPU work
-    n2 = int(min(4096, max(256, n * seconds_hint / max(dt, 1e-3))))
+    n2 = int(min(16384, max(256, n * seconds_hint / max(dt, 1e-3))))
     dt2 = oracle_sample(n2, seed=1)
     return {"value": n2 / dt2, "unit": "candidates/s", "cores": _oracle_threads(), "kind": "oracle",
             "sample": "%d candidates of the C2 round (1 task): oracle encode + fp64 forward (2 attention "
