@@ -4,11 +4,12 @@
 // concurrent 1-D bulk-TMA stream into another shared-memory region.
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o tools/ubench_umma tools/ubench_umma.cu -lcuda
 #include <cstdio>
+#include <vector>
 #include <cstdint>
 #include <cuda_bf16.h>
 #include "../paper_2211_03578_b200/csrc/tc_ptx.cuh"
 
-constexpr uint32_t kA = 0, kB = 65536, kRing = 65536 + 65536, kBar = kRing + 4 * 16384;
+constexpr uint32_t kA = 0, kB = 65536, kRing = 65536 + 16384, kBar = kRing + 16384;
 
 __device__ __forceinline__ bool elect_one() {
   uint32_t pred = 0;
@@ -21,7 +22,7 @@ __device__ __forceinline__ bool elect_one() {
 }
 
 __global__ void __launch_bounds__(128, 1) umma_bench(int N, int a_tmem, int tma, int iters, int nacc,
-                                                     const uint8_t* gsrc, long long* out) {
+                                                     const uint8_t* gsrc, long long* out, int nis, int ncols) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint32_t tptr;
   const uint32_t sb = tc::smem_u32(smem);
@@ -29,10 +30,10 @@ __global__ void __launch_bounds__(128, 1) umma_bench(int N, int a_tmem, int tma,
   for (int i = threadIdx.x; i < (int)(kRing / 16); i += blockDim.x)
     reinterpret_cast<uint4*>(smem)[i] = make_uint4(0x3f803f80u, 0, 0x3f803f80u, 0);
   if (threadIdx.x == 0) {
-    for (int i = 0; i < 6; ++i) tc::mbar_init(sb + kBar + 8 * i, 1);
+    for (int i = 0; i < 10; ++i) tc::mbar_init(sb + kBar + 8 * i, 1);
     tc::fence_barrier_init();
   }
-  if (warp == 0) tc::tmem_alloc(tc::smem_u32(&tptr), 512);
+  if (warp == 0) tc::tmem_alloc(tc::smem_u32(&tptr), ncols);
   tc::fence_proxy_async_smem();
   tc::tc_fence_before();
   __syncthreads();
@@ -41,7 +42,7 @@ __global__ void __launch_bounds__(128, 1) umma_bench(int N, int a_tmem, int tma,
   volatile int* stop = reinterpret_cast<volatile int*>(smem + kBar + 64);
   if (threadIdx.x == 0) *stop = 0;
   __syncthreads();
-  if (warp == 0) {  // whole warp runs the issue loop (warp-uniform values), one elected lane issues
+  if (warp < nis) {  // whole warp runs the issue loop (warp-uniform values), one elected lane issues
     const uint32_t idesc = tc::idesc_bf16(128, N);
     const uint64_t a0 = tc::smem_desc(sb + kA, 128, 256 * 16);
     const uint64_t b0 = tc::smem_desc(sb + kB, 128, 64 * 16);
@@ -51,25 +52,25 @@ __global__ void __launch_bounds__(128, 1) umma_bench(int N, int a_tmem, int tma,
 #pragma unroll
       for (int ks = 0; ks < 16; ++ks) {
         const uint64_t bd = b0 + (uint64_t)(((ks & 3) * 2 * 128) >> 4);
-        const uint32_t d = tmem + (nacc == 1 ? 0u : (uint32_t)((ks % 2) * 256));
+        const uint32_t d = tmem + (uint32_t)(warp * (ncols / nis)) + (nacc == 1 ? 0u : (uint32_t)((ks % 2) * 256));
         if (elect_one()) {
           if (a_tmem)
-            tc::mma_bf16_ta(d + 256 * 0, tmem + 384 + ks * 8, bd, idesc, (i + ks) >= nacc);
+            tc::mma_bf16_ta(d, tmem + (ncols - 128) + ks * 8, bd, idesc, (i + ks) >= nacc);
           else
             tc::mma_bf16(d, a0 + (uint64_t)((ks * 2 * 128) >> 4), bd, idesc, (i + ks) >= nacc);
         }
         __syncwarp();
       }
     }
-    if (elect_one()) tc::mma_commit(sb + kBar + 40);
+    if (elect_one()) tc::mma_commit(sb + kBar + 40 + 8 * warp);
     __syncwarp();
-    tc::mbar_wait(sb + kBar + 40, 0);
+    tc::mbar_wait(sb + kBar + 40 + 8 * warp, 0);
     const long long t1 = clock64();
     if (lane == 0) {
-      out[blockIdx.x] = t1 - t0;
+      out[blockIdx.x * 4 + warp] = t1 - t0;
       *stop = 1;
     }
-  } else if (warp == 1 && lane == 0 && tma) {
+  } else if (warp == 3 && lane == 0 && tma) {
     uint32_t cnt[4] = {0, 0, 0, 0};
     long long bytes = 0;
     for (int i = 0; !*stop; ++i) {
@@ -86,35 +87,39 @@ __global__ void __launch_bounds__(128, 1) umma_bench(int N, int a_tmem, int tma,
   }
   tc::tc_fence_before();
   __syncthreads();
-  if (warp == 0) tc::tmem_dealloc(tmem, 512);
+  if (warp == 0) tc::tmem_dealloc(tmem, ncols);
 }
 
 int main() {
   long long* out;
   uint8_t* src;
-  cudaMalloc(&out, 2 * 148 * sizeof(long long));
+  cudaMalloc(&out, 8 * 4 * 148 * sizeof(long long));
   cudaMalloc(&src, 64 * 16384);
   cudaMemset(src, 0, 64 * 16384);
-  const int smem = kBar + 128;
-  cudaFuncSetAttribute(umma_bench, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const int iters = 4096;
-  for (int nacc : {1, 2})
+  // (ctas per SM, issuers per CTA)
+  const int cfgs[4][2] = {{1, 1}, {1, 2}, {2, 1}, {1, 4}};
+  for (auto& cf : cfgs) {
+    const int cps = cf[0], nis = cf[1];
+    const int smem = cps == 1 ? 160 * 1024 : 100 * 1024;
+    cudaFuncSetAttribute(umma_bench, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    const int ncols = cps == 1 ? 512 : 256;
     for (int a_tmem : {0, 1})
-      for (int N : {32, 64, 96, 128, 192, 256}) {
-        const int tma = 0;
-        if (a_tmem && nacc > 1 && N > 128) continue;
-        umma_bench<<<148, 128, smem>>>(N, a_tmem, tma, iters, nacc, src, out);
-        umma_bench<<<148, 128, smem>>>(N, a_tmem, tma, iters, nacc, src, out);
+      for (int N : {64, 96, 128, 256}) {
+        if (N * nis + (a_tmem ? 128 : 0) > ncols) continue;
+        const int grid = 148 * cps;
+        umma_bench<<<grid, 128, smem>>>(N, a_tmem, 0, iters, 1, src, out, nis, ncols);
+        umma_bench<<<grid, 128, smem>>>(N, a_tmem, 0, iters, 1, src, out, nis, ncols);
         cudaError_t e = cudaDeviceSynchronize();
-        long long h[296];
-        cudaMemcpy(h, out, sizeof(h), cudaMemcpyDeviceToHost);
-        long long mx = 0, by = 0;
-        for (int b = 0; b < 148; ++b) { mx = h[b] > mx ? h[b] : mx; by += h[148 + b]; }
-        const double floor_c = 128.0 * N / 256.0;
-        printf("acc=%d A=%s N=%3d: %.1f cyc/MMA (floor %.0f, %.0f%%)  %s\n", nacc,
-               a_tmem ? "tmem" : "smem", N, (double)mx / iters, floor_c, 100.0 * floor_c * iters / mx,
-               cudaGetErrorString(e));
-        (void)by;
+        std::vector<long long> h(grid * 4);
+        cudaMemcpy(h.data(), out, h.size() * sizeof(long long), cudaMemcpyDeviceToHost);
+        long long mx = 0;
+        for (int b = 0; b < grid; ++b)
+          for (int w = 0; w < nis; ++w) mx = h[b * 4 + w] > mx ? h[b * 4 + w] : mx;
+        const double per_sm = (double)mx / (iters * (double)nis * cps);  // cycles per MMA per SM
+        printf("ctas/SM=%d issuers=%d A=%s N=%3d: %.1f cyc per MMA per SM (floor %.0f)  %s\n", cps, nis,
+               a_tmem ? "tmem" : "smem", N, per_sm, 128.0 * N / 256.0, cudaGetErrorString(e));
       }
+  }
   return 0;
 }
