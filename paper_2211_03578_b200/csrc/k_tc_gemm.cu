@@ -53,17 +53,32 @@ struct Src {
   bool vec;       // float4 loads allowed (16-byte aligned rows)
 };
 
+// Which 4 elements (r, k..k+3 for K-major; r..r+3, k for MN-major) thread
+// `tid` moves in iteration `it`: every warp store covers two whole 8 x 16-byte
+// core matrices (256 contiguous bytes: bank-conflict free), and every warp load
+// reads 8 rows x 64 contiguous bytes.
+template <bool KMAJOR>
+__device__ __forceinline__ void chunk_rk(int it, int& r, int& k) {
+  const int w = threadIdx.x >> 5, t = threadIdx.x & 31;
+  const int task = it * (THREADS / 32) + w;
+  if (KMAJOR) {  // task = (row group, pair of K groups)
+    r = (task >> 1) * 8 + ((t >> 1) & 7);
+    k = (2 * (task & 1) + (t >> 4)) * 8 + 4 * (t & 1);
+  } else {       // task = (K group, pair of row groups)
+    k = (task >> 3) * 8 + ((t >> 1) & 7);
+    r = (2 * (task & 7) + (t >> 4)) * 8 + 4 * (t & 1);
+  }
+}
+
 // One 128 x 32 (rows x K) operand tile: fp32 global -> registers.
-//  KMAJOR: source [rows][K]; chunk c covers (r = c/8, k = 4*(c%8) .. +3)
-//  !KMAJOR: source [K][rows]; chunk c covers (k = c/32, r = 4*(c%32) .. +3)
+//  KMAJOR: source [rows][K], chunk = (r, k..k+3);  !KMAJOR: source [K][rows], chunk = (r..r+3, k)
 template <bool KMAJOR>
 __device__ __forceinline__ void load_regs(const Src& s, int64_t k0, int64_t kend, float4 (&v)[CHUNKS]) {
 #pragma unroll
   for (int it = 0; it < CHUNKS; ++it) {
-    const int c = threadIdx.x + it * THREADS;
-    int64_t gr, gk;
-    if (KMAJOR) { gr = s.r0 + (c >> 3); gk = k0 + (c & 7) * 4; }
-    else { gk = k0 + (c >> 5); gr = s.r0 + (c & 31) * 4; }
+    int r, k;
+    chunk_rk<KMAJOR>(it, r, k);
+    const int64_t gr = s.r0 + r, gk = k0 + k;
     float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
     if (KMAJOR) {
       if (gr < s.rows) {
@@ -105,15 +120,11 @@ template <bool KMAJOR>
 __device__ __forceinline__ void store_smem(uint8_t* dst, uint8_t* dst_lo, const float4 (&v)[CHUNKS]) {
 #pragma unroll
   for (int it = 0; it < CHUNKS; ++it) {
-    const int c = threadIdx.x + it * THREADS;
+    int r, k;
+    chunk_rk<KMAJOR>(it, r, k);
     uint32_t off;
-    if (KMAJOR) {
-      const int r = c >> 3, k = (c & 7) * 4;
-      off = (r >> 3) * 512 + (k >> 3) * 128 + (r & 7) * 16 + (k & 7) * 2;
-    } else {
-      const int k = c >> 5, r = (c & 31) * 4;
-      off = (k >> 3) * 2048 + (r >> 3) * 128 + (k & 7) * 16 + (r & 7) * 2;
-    }
+    if (KMAJOR) off = (r >> 3) * 512 + (k >> 3) * 128 + (r & 7) * 16 + (k & 7) * 2;
+    else off = (k >> 3) * 2048 + (r >> 3) * 128 + (k & 7) * 16 + (r & 7) * 2;
     const uint32_t h0 = tc::pack_bf16(v[it].x, v[it].y), h1 = tc::pack_bf16(v[it].z, v[it].w);
     *reinterpret_cast<uint2*>(dst + off) = make_uint2(h0, h1);
     *reinterpret_cast<uint2*>(dst_lo + off) =
