@@ -268,6 +268,162 @@ __global__ void __launch_bounds__(THREADS, 3) tc_gemm_kernel(int64_t M, int64_t 
   }
 }
 
+// ---------------------------------------------------------------- B-image variant
+// For the N in (128, 256] layers with a row-major activation A (every dense
+// forward layer and every dgrad of the bf16-context training path): the weight
+// operand op(B) is split into bf16 hi / lo ONCE per call into a K-major
+// canonical image [K/32 blocks][hi 16 KB | lo 16 KB] (bimg_kernel), and each
+// stage receives its 32 KB block by one 1-D bulk copy (no LSU traffic, no
+// per-CTA re-splitting); A (read from HBM exactly once: one 128 x 256 tile per
+// row block) keeps the conflict-free register-staged split.
+constexpr int BNI = 256;
+constexpr uint32_t IMG_HALF = BNI * BK * 2;                       // 16 KB
+constexpr uint32_t ISTAGE = 2 * (BM * BK * 2) + 2 * IMG_HALF;     // A hi | A lo | B hi | B lo = 48 KB
+constexpr uint32_t ISMEM = STAGES * ISTAGE + 128;
+
+__global__ void bimg_kernel(const float* __restrict__ B, int64_t ldb, int tb, int64_t N, int64_t K,
+                            uint8_t* __restrict__ img) {
+  const int64_t kb = blockIdx.x;
+  uint8_t* dst = img + kb * 2 * IMG_HALF;
+  for (int e = threadIdx.x; e < BNI * BK; e += blockDim.x) {
+    const int n = e / BK, k = e % BK;
+    const int64_t gk = kb * BK + k;
+    float x = 0.f;
+    if (n < N && gk < K) x = tb ? B[(int64_t)n * ldb + gk] : B[gk * ldb + n];
+    const uint32_t off = (n >> 3) * 512 + (k >> 3) * 128 + (n & 7) * 16 + (k & 7) * 2;
+    const __nv_bfloat16 h = __float2bfloat16_rn(x);
+    *reinterpret_cast<__nv_bfloat16*>(dst + off) = h;
+    *reinterpret_cast<__nv_bfloat16*>(dst + IMG_HALF + off) = __float2bfloat16_rn(x - __bfloat162float(h));
+  }
+}
+
+__global__ void __launch_bounds__(THREADS, 2) tc_gemm_bimg_kernel(int64_t M, int64_t N, int64_t K,
+                                                                   const float* __restrict__ A, int64_t lda,
+                                                                   const uint8_t* __restrict__ img,
+                                                                   float* __restrict__ C, int64_t ldc,
+                                                                   Epi ep, int avec) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const uint32_t sb = tc::smem_u32(smem);
+  const uint32_t bar = sb + STAGES * ISTAGE;   // [STAGES] MMA done
+  const uint32_t bfull = bar + 8 * STAGES;     // [STAGES] B block landed
+  uint32_t* tptr = reinterpret_cast<uint32_t*>(smem + STAGES * ISTAGE + 64);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t m0 = (int64_t)blockIdx.y * BM;
+  const int nk = K > 0 ? (int)((K + BK - 1) / BK) : 0;
+  constexpr uint32_t AB = BM * BK * 2;
+
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      tc::mbar_init(bar + 8 * s, 1);
+      tc::mbar_init(bfull + 8 * s, 1);
+    }
+    tc::fence_barrier_init();
+  }
+  if (warp == 0) tc::tmem_alloc(tc::smem_u32(tptr), BNI);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tptr;
+  const uint32_t idesc = tc::idesc_bf16(BM, BNI);
+  const Src sa{A, lda, M, m0, avec != 0};
+  auto copy_b = [&](int kblk, int st) {
+    tc::mbar_arrive_expect_tx(bfull + 8 * st, 2 * IMG_HALF);
+    tc::bulk_g2s(sb + st * ISTAGE + 2 * AB, img + (size_t)kblk * 2 * IMG_HALF, 2 * IMG_HALF, bfull + 8 * st);
+  };
+
+  float4 ra[CHUNKS];
+  if (nk > 0) {
+    if (tid == 0) {
+      copy_b(0, 0);
+      if (nk > 1) copy_b(1, 1);
+    }
+    load_regs<true>(sa, 0, K, ra);
+    store_smem<true>(smem, smem + AB, ra);
+    if (nk > 1) load_regs<true>(sa, BK, K, ra);
+  }
+  for (int it = 0; it < nk; ++it) {
+    const int s = it % STAGES;
+    tc::fence_proxy_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      tc::mbar_wait(bfull + 8 * s, (uint32_t)((it / STAGES) & 1));
+      tc::tc_fence_after();
+      const uint32_t a0 = sb + s * ISTAGE, al = a0 + AB, b0 = a0 + 2 * AB, bl = b0 + IMG_HALF;
+#pragma unroll
+      for (int ks = 0; ks < BK / 16; ++ks) {
+        const uint64_t dah = tc::smem_desc(a0 + ks * 256, 128, 512), dal = tc::smem_desc(al + ks * 256, 128, 512);
+        const uint64_t dbh = tc::smem_desc(b0 + ks * 256, 128, 512), dbl = tc::smem_desc(bl + ks * 256, 128, 512);
+        tc::mma_bf16(tmem, dal, dbh, idesc, (it > 0 || ks > 0) ? 1u : 0u);  // Al.Bh
+        tc::mma_bf16(tmem, dah, dbl, idesc, 1u);                          // Ah.Bl
+        tc::mma_bf16(tmem, dah, dbh, idesc, 1u);                          // Ah.Bh
+      }
+      tc::mma_commit(bar + 8 * s);
+    }
+    if (it + 1 < nk) {
+      const int ns = (it + 1) % STAGES;
+      if (it + 1 >= STAGES) {  // stage ns last used by k-block it+1-STAGES
+        tc::mbar_wait(bar + 8 * ns, (uint32_t)(((it + 1 - STAGES) / STAGES) & 1));
+        if (tid == 0) copy_b(it + 1, ns);
+      }
+      uint8_t* st = smem + ns * ISTAGE;
+      store_smem<true>(st, st + AB, ra);
+      if (it + 2 < nk) load_regs<true>(sa, (int64_t)(it + 2) * BK, K, ra);
+    }
+  }
+  if (nk > 0) {
+    const int ls = (nk - 1) % STAGES;
+    tc::mbar_wait(bar + 8 * ls, (uint32_t)(((nk - 1) / STAGES) & 1));
+  }
+  tc::tc_fence_after();
+  __syncthreads();
+  // ---- epilogue (as tc_gemm_kernel): TMEM -> smem transpose -> coalesced row stores
+  float* stage = reinterpret_cast<float*>(smem);
+  constexpr int EPI_COLS = 64, EPI_LD = 68;
+  const int q = warp & 3, hh = warp >> 2;
+  for (int p = 0; p < BNI / EPI_COLS; ++p) {
+    if (p * EPI_COLS >= N) break;
+    {
+      float v[32];
+      if (nk > 0) {
+        tc::tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + p * EPI_COLS + 32 * hh, v);
+        tc::tmem_wait_ld();
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = 0.f;
+      }
+      float* dst = stage + (q * 32 + lane) * EPI_LD + 32 * hh;
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        reinterpret_cast<float4*>(dst)[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+    }
+    __syncthreads();
+    for (int rr = warp; rr < BM; rr += THREADS / 32) {
+      const int64_t gi = m0 + rr;
+      if (gi >= M) break;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int cc = 2 * lane + e;
+        const int64_t gj = p * EPI_COLS + cc;
+        if (gj >= N) continue;
+        float x = stage[rr * EPI_LD + cc];
+        if (ep.bias) x += ep.bias[gj];
+        if (ep.resid) x += ep.resid[gi * ep.ldr + gj];
+        if (ep.relu) x = fmaxf(x, 0.f);
+        if (ep.mask) x = ep.mask[gi * ep.ldm + gj] > 0.f ? x : 0.f;
+        if (ep.accumulate) x += C[gi * ldc + gj];
+        C[gi * ldc + gj] = x;
+      }
+    }
+    __syncthreads();
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc::tc_fence_after();
+    tc::tmem_dealloc(tmem, BNI);
+  }
+}
+
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 }  // namespace
@@ -286,6 +442,23 @@ tlp_status tc_gemm(tlp_ctx* ctx, bool ta, bool tb, int64_t M, int64_t N, int64_t
     attr = true;
   }
   Epi ep{e.bias, e.resid, e.ldr, e.mask, e.ldm, e.relu ? 1 : 0, e.accumulate ? 1 : 0};
+  if (!ta && splits == 1 && N > BN && N <= BNI && K > 0) {
+    static bool iattr = false;
+    if (!iattr) {
+      cudaFuncSetAttribute(tc_gemm_bimg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, ISMEM);
+      iattr = true;
+    }
+    const int64_t nkb = cdiv(K, BK);
+    TLP_CUDA_TRY(ctx->ws_bimg.ensure((size_t)nkb * 2 * IMG_HALF));
+    uint8_t* img = ctx->ws_bimg.as<uint8_t>();
+    bimg_kernel<<<(unsigned)nkb, 256, 0, s>>>(B, ldb, tb ? 1 : 0, N, K, img);
+    TLP_LAUNCH_CHECK();
+    const int av = aligned16(A) && lda % 4 == 0;
+    tc_gemm_bimg_kernel<<<dim3(1, (unsigned)cdiv(M, BM), 1), THREADS, ISMEM, s>>>(M, N, K, A, lda, img, C,
+                                                                                ldc, ep, av);
+    TLP_LAUNCH_CHECK();
+    return TLP_OK;
+  }
   dim3 grid((unsigned)cdiv(N, BN), (unsigned)cdiv(M, BM), (unsigned)splits);
   if (splits == 1) kslice = K > 0 ? K : 1;
   const int av = aligned16(A) && lda % 4 == 0, bv = aligned16(B) && ldb % 4 == 0;
