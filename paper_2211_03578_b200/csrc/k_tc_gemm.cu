@@ -132,6 +132,70 @@ __device__ __forceinline__ void store_smem(uint8_t* dst, uint8_t* dst_lo, const 
   }
 }
 
+// Epilogue stores of one 64-column slab staged in smem ([128][ld] fp32): warp w
+// handles rows w, w+8, ..; lane l columns 2l, 2l+1 (8-byte accesses, coalesced
+// rows).  Four rows per round with every global read (bias, residual, mask,
+// accumulate) issued before the stores, so the slab streams at memory-level
+// parallelism 4 per warp instead of one dependent round trip per row.
+__device__ __forceinline__ void epi_store_slab(const float* stage, int ld, int64_t m0, int64_t M,
+                                               int64_t col0, int64_t N, float* __restrict__ Cz,
+                                               int64_t ldc, const Epi& ep, bool partial) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int cc = 2 * lane;
+  const int64_t gj = col0 + cc;
+  const bool c0 = gj < N, c1 = gj + 1 < N;
+  const float* __restrict__ bias = ep.bias;
+  const float* __restrict__ resid = ep.resid;
+  const float* __restrict__ mask = ep.mask;
+  float2 b = make_float2(0.f, 0.f);
+  if (!partial && bias) {
+    if (c0) b.x = __ldg(bias + gj);
+    if (c1) b.y = __ldg(bias + gj + 1);
+  }
+  const uintptr_t al = reinterpret_cast<uintptr_t>(Cz) | reinterpret_cast<uintptr_t>(resid) |
+                       reinterpret_cast<uintptr_t>(mask);
+  const bool vec = c1 && (al & 7) == 0 && ((ldc | (resid ? ep.ldr : 0) | (mask ? ep.ldm : 0)) % 2 == 0);
+  for (int r0 = warp; r0 < BM; r0 += 4 * (THREADS / 32)) {
+    float2 x[4], rv[4], mv[4], cv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int rr = r0 + u * (THREADS / 32);
+      const int64_t gi = m0 + rr;
+      x[u] = *reinterpret_cast<const float2*>(stage + rr * ld + cc);
+      rv[u] = mv[u] = cv[u] = make_float2(0.f, 0.f);
+      if (partial || gi >= M || !c0) continue;
+      if (vec) {
+        if (resid) rv[u] = __ldg(reinterpret_cast<const float2*>(resid + gi * ep.ldr + gj));
+        if (mask) mv[u] = __ldg(reinterpret_cast<const float2*>(mask + gi * ep.ldm + gj));
+        if (ep.accumulate) cv[u] = *reinterpret_cast<const float2*>(Cz + gi * ldc + gj);
+      } else {
+        if (resid) { rv[u].x = resid[gi * ep.ldr + gj]; if (c1) rv[u].y = resid[gi * ep.ldr + gj + 1]; }
+        if (mask) { mv[u].x = mask[gi * ep.ldm + gj]; if (c1) mv[u].y = mask[gi * ep.ldm + gj + 1]; }
+        if (ep.accumulate) { cv[u].x = Cz[gi * ldc + gj]; if (c1) cv[u].y = Cz[gi * ldc + gj + 1]; }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int rr = r0 + u * (THREADS / 32);
+      const int64_t gi = m0 + rr;
+      if (gi >= M || !c0) continue;
+      float2 y = x[u];
+      if (!partial) {
+        y.x += b.x; y.y += b.y;
+        y.x += rv[u].x; y.y += rv[u].y;
+        if (ep.relu) { y.x = fmaxf(y.x, 0.f); y.y = fmaxf(y.y, 0.f); }
+        if (mask) { y.x = mv[u].x > 0.f ? y.x : 0.f; y.y = mv[u].y > 0.f ? y.y : 0.f; }
+        y.x += cv[u].x; y.y += cv[u].y;
+      }
+      if (vec) *reinterpret_cast<float2*>(Cz + gi * ldc + gj) = y;
+      else {
+        Cz[gi * ldc + gj] = y.x;
+        if (c1) Cz[gi * ldc + gj + 1] = y.y;
+      }
+    }
+  }
+}
+
 template <bool TA, bool TB>
 __global__ void __launch_bounds__(THREADS, 3) tc_gemm_kernel(int64_t M, int64_t N, int64_t K,
                                                           const float* __restrict__ A, int64_t lda,
@@ -238,26 +302,7 @@ __global__ void __launch_bounds__(THREADS, 3) tc_gemm_kernel(int64_t M, int64_t 
         reinterpret_cast<float4*>(dst)[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
     }
     __syncthreads();
-    // warp w handles rows w, w+8, ...; lane handles columns 2*lane, 2*lane+1
-    for (int rr = warp; rr < BM; rr += THREADS / 32) {
-      const int64_t gi = m0 + rr;
-      if (gi >= M) break;
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int cc = 2 * lane + e;
-        const int64_t gj = n0 + p * EPI_COLS + cc;
-        if (gj >= N) continue;
-        float x = stage[rr * EPI_LD + cc];
-        if (!partial) {
-          if (ep.bias) x += ep.bias[gj];
-          if (ep.resid) x += ep.resid[gi * ep.ldr + gj];
-          if (ep.relu) x = fmaxf(x, 0.f);
-          if (ep.mask) x = ep.mask[gi * ep.ldm + gj] > 0.f ? x : 0.f;
-          if (ep.accumulate) x += Cz[gi * ldc + gj];
-        }
-        Cz[gi * ldc + gj] = x;
-      }
-    }
+    epi_store_slab(stage, EPI_LD, m0, M, n0 + p * EPI_COLS, N, Cz, ldc, ep, partial);
     __syncthreads();
   }
   tc::tc_fence_before();
@@ -397,23 +442,7 @@ __global__ void __launch_bounds__(THREADS, 2) tc_gemm_bimg_kernel(int64_t M, int
         reinterpret_cast<float4*>(dst)[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
     }
     __syncthreads();
-    for (int rr = warp; rr < BM; rr += THREADS / 32) {
-      const int64_t gi = m0 + rr;
-      if (gi >= M) break;
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int cc = 2 * lane + e;
-        const int64_t gj = p * EPI_COLS + cc;
-        if (gj >= N) continue;
-        float x = stage[rr * EPI_LD + cc];
-        if (ep.bias) x += ep.bias[gj];
-        if (ep.resid) x += ep.resid[gi * ep.ldr + gj];
-        if (ep.relu) x = fmaxf(x, 0.f);
-        if (ep.mask) x = ep.mask[gi * ep.ldm + gj] > 0.f ? x : 0.f;
-        if (ep.accumulate) x += C[gi * ldc + gj];
-        C[gi * ldc + gj] = x;
-      }
-    }
+    epi_store_slab(stage, EPI_LD, m0, M, p * EPI_COLS, N, C, ldc, ep, false);
     __syncthreads();
   }
   tc::tc_fence_before();
