@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(256) sgemm_kernel(int64_t M, int64_t N, int64_
   }
 }
 
-// out[j] (=|+=) sum_z part[z][j], fixed order.
+// out[j] = sum_z part[z][j], fixed order.
 __global__ void reduce_partials(const float* __restrict__ part, int64_t n, int Z,
                                 float* __restrict__ out) {
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -152,14 +152,38 @@ __global__ void reduce_partials(const float* __restrict__ part, int64_t n, int Z
   out[j] = s;
 }
 
+// Same sum for few outputs and many partials (column sums): one warp per
+// output, lane-strided partial sums combined by a fixed butterfly
+// (deterministic for given n, Z).
+__global__ void reduce_partials_warp(const float* __restrict__ part, int64_t n, int Z,
+                                     float* __restrict__ out) {
+  const int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (j >= n) return;
+  float s = 0.f;
+  for (int z = lane; z < Z; z += 32) s += part[(int64_t)z * n + j];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) out[j] = s;
+}
+
 __global__ void colsum_partial(int64_t M, int64_t N, const float* __restrict__ X, int64_t ldx,
                                int64_t rows, float* __restrict__ part) {
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= N) return;
   const int64_t r0 = (int64_t)blockIdx.y * rows, r1 = std::min<int64_t>(M, r0 + rows);
-  float s = 0.f;
-  for (int64_t i = r0; i < r1; ++i) s += X[i * ldx + j];
-  part[(int64_t)blockIdx.y * N + j] = s;
+  // four interleaved partial sums (rows i, i+1, i+2, i+3 mod 4) for memory-level
+  // parallelism, combined in a fixed order: deterministic for a given M
+  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+  int64_t i = r0;
+  for (; i + 3 < r1; i += 4) {
+    a0 += X[i * ldx + j];
+    a1 += X[(i + 1) * ldx + j];
+    a2 += X[(i + 2) * ldx + j];
+    a3 += X[(i + 3) * ldx + j];
+  }
+  for (; i < r1; ++i) a0 += X[i * ldx + j];
+  part[(int64_t)blockIdx.y * N + j] = (a0 + a1) + (a2 + a3);
 }
 
 // ---------------------------------------------------------------------------
@@ -266,12 +290,15 @@ __global__ void __launch_bounds__(64) attn_bwd_kernel(const float* __restrict__ 
     const int l = lane;
     float dA[32];
     float rowdot = 0.f;
+    float dor[DH];  // this lane's dO row in registers (row reads of dOs would be 32-way bank conflicts)
+#pragma unroll
+    for (int d = 0; d < DH; ++d) dor[d] = dO[(row0 + l) * H + hd * DH + d];
 #pragma unroll
     for (int m = 0; m < 32; ++m) {
       if (m < L) {
         float a = 0.f;
 #pragma unroll
-        for (int d = 0; d < DH; ++d) a = fmaf(dOs[l * DH + d], Vs[m * DH + d], a);
+        for (int d = 0; d < DH; ++d) a = fmaf(dor[d], Vs[m * DH + d], a);
         dA[m] = a;
         rowdot = fmaf(a, As[l * 33 + m], rowdot);
       }
@@ -512,13 +539,13 @@ tlp_status sgemm_wgrad(tlp_ctx* ctx, int64_t M, int64_t K, int64_t N, const floa
 
 tlp_status colsum(tlp_ctx* ctx, int64_t M, int64_t N, const float* X, int64_t ldx, float* out,
                   cudaStream_t s) {
-  const int64_t rows = 1024;
+  const int64_t rows = 256;
   const int Z = (int)std::max<int64_t>(1, cdiv(M, rows));
   TLP_CUDA_TRY(ctx->ws_misc.ensure((size_t)Z * N * sizeof(float) + 4096));
   float* part = ctx->ws_misc.as<float>();
   colsum_partial<<<dim3((unsigned)cdiv(N, 128), (unsigned)Z), 128, 0, s>>>(M, N, X, ldx, rows, part);
   TLP_LAUNCH_CHECK();
-  reduce_partials<<<(unsigned)cdiv(N, 256), 256, 0, s>>>(part, N, Z, out);
+  reduce_partials_warp<<<(unsigned)cdiv(N * 32, 256), 256, 0, s>>>(part, N, Z, out);
   TLP_LAUNCH_CHECK();
   return TLP_OK;
 }

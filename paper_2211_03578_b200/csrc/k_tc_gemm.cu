@@ -57,7 +57,7 @@ struct Src {
 // `tid` moves in iteration `it`: every warp store covers two whole 8 x 16-byte
 // core matrices (256 contiguous bytes: bank-conflict free), and every warp load
 // reads 8 rows x 64 contiguous bytes.
-template <bool KMAJOR>
+template <bool KMAJOR, int ROWS = BM>
 __device__ __forceinline__ void chunk_rk(int it, int& r, int& k) {
   const int w = threadIdx.x >> 5, t = threadIdx.x & 31;
   const int task = it * (THREADS / 32) + w;
@@ -65,19 +65,21 @@ __device__ __forceinline__ void chunk_rk(int it, int& r, int& k) {
     r = (task >> 1) * 8 + ((t >> 1) & 7);
     k = (2 * (task & 1) + (t >> 4)) * 8 + 4 * (t & 1);
   } else {       // task = (K group, pair of row groups)
-    k = (task >> 3) * 8 + ((t >> 1) & 7);
-    r = (2 * (task & 7) + (t >> 4)) * 8 + 4 * (t & 1);
+    constexpr int RP = ROWS / 16;  // row-group pairs per K group
+    k = (task / RP) * 8 + ((t >> 1) & 7);
+    r = (2 * (task % RP) + (t >> 4)) * 8 + 4 * (t & 1);
   }
 }
 
 // One 128 x 32 (rows x K) operand tile: fp32 global -> registers.
 //  KMAJOR: source [rows][K], chunk = (r, k..k+3);  !KMAJOR: source [K][rows], chunk = (r..r+3, k)
-template <bool KMAJOR>
-__device__ __forceinline__ void load_regs(const Src& s, int64_t k0, int64_t kend, float4 (&v)[CHUNKS]) {
+template <bool KMAJOR, int ROWS = BM>
+__device__ __forceinline__ void load_regs(const Src& s, int64_t k0, int64_t kend,
+                                          float4 (&v)[ROWS * BK / 4 / THREADS]) {
 #pragma unroll
-  for (int it = 0; it < CHUNKS; ++it) {
+  for (int it = 0; it < ROWS * BK / 4 / THREADS; ++it) {
     int r, k;
-    chunk_rk<KMAJOR>(it, r, k);
+    chunk_rk<KMAJOR, ROWS>(it, r, k);
     const int64_t gr = s.r0 + r, gk = k0 + k;
     float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
     if (KMAJOR) {
@@ -116,15 +118,16 @@ __device__ __forceinline__ uint32_t pack_lo(float a, float b, uint32_t hi) {
   return tc::pack_bf16(a - hf.x, b - hf.y);
 }
 
-template <bool KMAJOR>
-__device__ __forceinline__ void store_smem(uint8_t* dst, uint8_t* dst_lo, const float4 (&v)[CHUNKS]) {
+template <bool KMAJOR, int ROWS = BM>
+__device__ __forceinline__ void store_smem(uint8_t* dst, uint8_t* dst_lo,
+                                           const float4 (&v)[ROWS * BK / 4 / THREADS]) {
 #pragma unroll
-  for (int it = 0; it < CHUNKS; ++it) {
+  for (int it = 0; it < ROWS * BK / 4 / THREADS; ++it) {
     int r, k;
-    chunk_rk<KMAJOR>(it, r, k);
+    chunk_rk<KMAJOR, ROWS>(it, r, k);
     uint32_t off;
     if (KMAJOR) off = (r >> 3) * 512 + (k >> 3) * 128 + (r & 7) * 16 + (k & 7) * 2;
-    else off = (k >> 3) * 2048 + (r >> 3) * 128 + (k & 7) * 16 + (r & 7) * 2;
+    else off = (k >> 3) * (ROWS * 16) + (r >> 3) * 128 + (k & 7) * 16 + (r & 7) * 2;
     const uint32_t h0 = tc::pack_bf16(v[it].x, v[it].y), h1 = tc::pack_bf16(v[it].z, v[it].w);
     *reinterpret_cast<uint2*>(dst + off) = make_uint2(h0, h1);
     *reinterpret_cast<uint2*>(dst_lo + off) =
@@ -453,6 +456,135 @@ __global__ void __launch_bounds__(THREADS, 2) tc_gemm_bimg_kernel(int64_t M, int
   }
 }
 
+// ---------------------------------------------------------------- wgrad variant
+// dW[M<=256, N<=256] = A^T B over a slice of the K = 204,800 rows (A = X
+// [rows][M], B = dY [rows][N], both MN-major operands): ONE CTA per slice owns
+// the whole 256 x 256 output (two M=128 accumulators, 512 TMEM columns), so X
+// and dY are each read from HBM exactly once (the 128 x 128 tiling read both
+// twice).  Partials [Z][M][N] are reduced in a fixed order by the caller.
+constexpr int WROWS = 256;
+constexpr uint32_t WT = WROWS * BK * 2;                  // one 256 x 32 bf16 operand tile (16 KB)
+constexpr uint32_t WSTAGE = 4 * WT;                      // A hi | A lo | B hi | B lo = 64 KB
+constexpr uint32_t WSMEM = STAGES * WSTAGE + 128;
+constexpr int WCH = WROWS * BK / 4 / THREADS;            // float4 chunks per operand per thread (8)
+
+__global__ void __launch_bounds__(THREADS, 1) tc_wgrad_kernel(int64_t M, int64_t N, int64_t K,
+                                                               const float* __restrict__ A, int64_t lda,
+                                                               const float* __restrict__ B, int64_t ldb,
+                                                               float* __restrict__ part, int64_t ldc,
+                                                               int64_t kslice, int avec, int bvec) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const uint32_t sb = tc::smem_u32(smem);
+  const uint32_t bar = sb + STAGES * WSTAGE;
+  uint32_t* tptr = reinterpret_cast<uint32_t*>(smem + STAGES * WSTAGE + 64);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t kb = (int64_t)blockIdx.z * kslice;
+  const int64_t ke = std::min<int64_t>(K, kb + kslice);
+  const int nk = ke > kb ? (int)((ke - kb + BK - 1) / BK) : 0;
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) tc::mbar_init(bar + 8 * s, 1);
+    tc::fence_barrier_init();
+  }
+  if (warp == 0) tc::tmem_alloc(tc::smem_u32(tptr), 512);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tptr;
+  // both operands MN-major: a_major = b_major = 1; M = 128 per MMA, N = 256
+  const uint32_t idesc = tc::idesc_bf16(BM, WROWS) | (1u << 15) | (1u << 16);
+  const Src sa{A, lda, M, 0, avec != 0};
+  const Src sbb{B, ldb, N, 0, bvec != 0};
+  float4 ra[WCH], rb[WCH];
+  if (nk > 0) {
+    load_regs<false, WROWS>(sa, kb, ke, ra);
+    load_regs<false, WROWS>(sbb, kb, ke, rb);
+    store_smem<false, WROWS>(smem, smem + WT, ra);
+    store_smem<false, WROWS>(smem + 2 * WT, smem + 3 * WT, rb);
+    if (nk > 1) {
+      load_regs<false, WROWS>(sa, kb + BK, ke, ra);
+      load_regs<false, WROWS>(sbb, kb + BK, ke, rb);
+    }
+  }
+  for (int it = 0; it < nk; ++it) {
+    const int s = it % STAGES;
+    tc::fence_proxy_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      tc::tc_fence_after();
+      const uint32_t ah = sb + s * WSTAGE, al = ah + WT, bh = ah + 2 * WT, bl = ah + 3 * WT;
+      // MN-major 256-row tile: K group stride (LBO) = 256 * 16, 8-row group stride (SBO) = 128;
+      // the second M half starts 16 row groups (2 KB) in
+#pragma unroll
+      for (int ks = 0; ks < BK / 16; ++ks) {
+        const uint32_t ko = ks * 2 * WROWS * 16;
+        const uint64_t dbh = tc::smem_desc(bh + ko, WROWS * 16, 128), dbl = tc::smem_desc(bl + ko, WROWS * 16, 128);
+#pragma unroll
+        for (int mh = 0; mh < 2; ++mh) {
+          const uint32_t mo = ko + mh * 2048;
+          const uint64_t dah = tc::smem_desc(ah + mo, WROWS * 16, 128), dal = tc::smem_desc(al + mo, WROWS * 16, 128);
+          const uint32_t d = tmem + 256 * mh;
+          tc::mma_bf16(d, dal, dbh, idesc, (it > 0 || ks > 0) ? 1u : 0u);  // Al.Bh
+          tc::mma_bf16(d, dah, dbl, idesc, 1u);                          // Ah.Bl
+          tc::mma_bf16(d, dah, dbh, idesc, 1u);                          // Ah.Bh
+        }
+      }
+      tc::mma_commit(bar + 8 * s);
+    }
+    if (it + 1 < nk) {
+      const int ns = (it + 1) % STAGES;
+      if (it + 1 >= STAGES) tc::mbar_wait(bar + 8 * ns, (uint32_t)(((it + 1 - STAGES) / STAGES) & 1));
+      uint8_t* st = smem + ns * WSTAGE;
+      store_smem<false, WROWS>(st, st + WT, ra);
+      store_smem<false, WROWS>(st + 2 * WT, st + 3 * WT, rb);
+      if (it + 2 < nk) {
+        load_regs<false, WROWS>(sa, kb + (int64_t)(it + 2) * BK, ke, ra);
+        load_regs<false, WROWS>(sbb, kb + (int64_t)(it + 2) * BK, ke, rb);
+      }
+    }
+  }
+  if (nk > 0) {
+    const int ls = (nk - 1) % STAGES;
+    tc::mbar_wait(bar + 8 * ls, (uint32_t)(((nk - 1) / STAGES) & 1));
+  }
+  tc::tc_fence_after();
+  __syncthreads();
+  // epilogue: raw partial sums, TMEM -> smem transpose -> coalesced rows of part[z]
+  float* Pz = part + (int64_t)blockIdx.z * M * ldc;
+  float* stage = reinterpret_cast<float*>(smem);
+  constexpr int EPI_COLS = 64, EPI_LD = 68;
+  const int q = warp & 3, hh = warp >> 2;
+  Epi none{nullptr, nullptr, 0, nullptr, 0, 0, 0};
+  for (int mh = 0; mh < 2; ++mh) {
+    if (mh * BM >= M) break;
+    for (int p = 0; p < WROWS / EPI_COLS; ++p) {
+      if (p * EPI_COLS >= N) break;
+      {
+        float v[32];
+        if (nk > 0) {
+          tc::tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + 256 * mh + p * EPI_COLS + 32 * hh, v);
+          tc::tmem_wait_ld();
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = 0.f;
+        }
+        float* dst = stage + (q * 32 + lane) * EPI_LD + 32 * hh;
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          reinterpret_cast<float4*>(dst)[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+      }
+      __syncthreads();
+      epi_store_slab(stage, EPI_LD, mh * BM, M, p * EPI_COLS, N, Pz, ldc, none, true);
+      __syncthreads();
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc::tc_fence_after();
+    tc::tmem_dealloc(tmem, 512);
+  }
+}
+
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 }  // namespace
@@ -471,6 +603,18 @@ tlp_status tc_gemm(tlp_ctx* ctx, bool ta, bool tb, int64_t M, int64_t N, int64_t
     attr = true;
   }
   Epi ep{e.bias, e.resid, e.ldr, e.mask, e.ldm, e.relu ? 1 : 0, e.accumulate ? 1 : 0};
+  if (ta && !tb && splits > 1 && M > BM && M <= WROWS && N > BN && N <= WROWS) {
+    static bool wattr = false;
+    if (!wattr) {
+      cudaFuncSetAttribute(tc_wgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, WSMEM);
+      wattr = true;
+    }
+    const int av = aligned16(A) && lda % 4 == 0, bv = aligned16(B) && ldb % 4 == 0;
+    tc_wgrad_kernel<<<dim3(1, 1, (unsigned)splits), THREADS, WSMEM, s>>>(M, N, K, A, lda, B, ldb, C,
+                                                                         ldc, kslice, av, bv);
+    TLP_LAUNCH_CHECK();
+    return TLP_OK;
+  }
   if (!ta && splits == 1 && N > BN && N <= BNI && K > 0) {
     static bool iattr = false;
     if (!iattr) {
