@@ -112,12 +112,6 @@ __device__ __forceinline__ void load_regs(const Src& s, int64_t k0, int64_t kend
 // registers -> bf16 hi / lo canonical layouts (8-byte stores)
 //  KMAJOR: (r,k) -> (r/8)*512 + (k/8)*128 + (r%8)*16 + (k%8)*2      (SBO 512, LBO 128)
 //  !KMAJOR: (r,k) -> (k/8)*2048 + (r/8)*128 + (k%8)*16 + (r%8)*2    (LBO 2048, SBO 128)
-__device__ __forceinline__ uint32_t pack_lo(float a, float b, uint32_t hi) {
-  const __nv_bfloat162 h = *reinterpret_cast<const __nv_bfloat162*>(&hi);
-  const float2 hf = __bfloat1622float2(h);
-  return tc::pack_bf16(a - hf.x, b - hf.y);
-}
-
 template <bool KMAJOR, int ROWS = BM>
 __device__ __forceinline__ void store_smem(uint8_t* dst, uint8_t* dst_lo,
                                            const float4 (&v)[ROWS * BK / 4 / THREADS]) {
@@ -128,10 +122,17 @@ __device__ __forceinline__ void store_smem(uint8_t* dst, uint8_t* dst_lo,
     uint32_t off;
     if (KMAJOR) off = (r >> 3) * 512 + (k >> 3) * 128 + (r & 7) * 16 + (k & 7) * 2;
     else off = (k >> 3) * (ROWS * 16) + (r >> 3) * 128 + (k & 7) * 16 + (r & 7) * 2;
-    const uint32_t h0 = tc::pack_bf16(v[it].x, v[it].y), h1 = tc::pack_bf16(v[it].z, v[it].w);
+    // hi = x truncated to its upper 16 bits (one PRMT per pair), lo = RN_bf16(x - hi)
+    // (x - hi is exact in fp32): |x - hi - lo| <= 2^-8 |x - hi| < 2^-15 |x|
+    const uint32_t x0 = __float_as_uint(v[it].x), x1 = __float_as_uint(v[it].y);
+    const uint32_t x2 = __float_as_uint(v[it].z), x3 = __float_as_uint(v[it].w);
+    const uint32_t h0 = __byte_perm(x0, x1, 0x7632), h1 = __byte_perm(x2, x3, 0x7632);
+    const uint32_t l0 = tc::pack_bf16(v[it].x - __uint_as_float(x0 & 0xffff0000u),
+                                      v[it].y - __uint_as_float(x1 & 0xffff0000u));
+    const uint32_t l1 = tc::pack_bf16(v[it].z - __uint_as_float(x2 & 0xffff0000u),
+                                      v[it].w - __uint_as_float(x3 & 0xffff0000u));
     *reinterpret_cast<uint2*>(dst + off) = make_uint2(h0, h1);
-    *reinterpret_cast<uint2*>(dst_lo + off) =
-        make_uint2(pack_lo(v[it].x, v[it].y, h0), pack_lo(v[it].z, v[it].w, h1));
+    *reinterpret_cast<uint2*>(dst_lo + off) = make_uint2(l0, l1);
   }
 }
 
