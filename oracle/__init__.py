@@ -25,6 +25,8 @@ Pins (tests/test_oracle_*.py, ``-m "not gpu"``):
   labels     -- SPEC example, range (0,1], one label == 1 per group.
   adam       -- torch.optim.Adam.
   dp         -- R-rank emulation equals the unsharded step.
+  dataset    -- (NEXT-2) SPEC duplicate-rate / dedup / top-k-score examples,
+                brute-force pairwise classes, permutation invariance.
 """
 from .tokenizer import build_token_table, extract_rows, fit_scales, encode  # noqa: F401
 from .model import Config, param_shapes, unflatten, flatten, forward, backward  # noqa: F401
@@ -32,3 +34,4 @@ from .rank_loss import lambdarank, strict_pair_counts, mtl_lambdarank  # noqa: F
 from .select import topk, normalize_labels  # noqa: F401
 from .optim import adam_step, AdamState  # noqa: F401
 from .dp import dp_emulate  # noqa: F401
+from .dataset import feature_classes, duplicate_rate, dedup_labels, topk_score  # noqa: F401
