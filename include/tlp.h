@@ -227,6 +227,39 @@ tlp_status tlp_search_round(tlp_ctx* ctx, const tlp_seq_batch* host_in, int64_t 
                             int64_t shard_base, int32_t chunks, int64_t* idx_out, float* val_out,
                             void* stream);
 
+/* ---- NEXT-2 dataset scans: duplicates, P:276-278 ---------
+ * Duplicate classes of feature matrices (§4.3 "8.56 million
+ * different schedule primitive sequences in a total of 8.65 million tensor
+ * programs"; R39): samples i, j are duplicates iff they lie in the same group
+ * and their rows feats[i*row_len .. +row_len) are bitwise equal.
+ *   feats      device fp32 [N, row_len] (row_len = L*E for tlp_encode output)
+ *   group_off  HOST int64 [G+1], 0 = group_off[0] <= ... <= group_off[G] = N;
+ *              pass G = 1, {0, N} for the global duplicate rate
+ *   labels     device fp32 [N] finite and >= 0, or NULL (NONFINITE device error
+ *              otherwise, returned by tlp_sync)
+ *   keep_out   device int32 [N]: 1 iff i is the lowest index of its class
+ *   label_out  device fp32 [N] or NULL (requires labels): the maximum label of
+ *              i's class ("the optimal value of the labels ... can be used as
+ *              the label") -- the kept sample carries it
+ *   n_distinct_out  HOST: number of classes; duplicate rate = 1 - n/N.
+ * Synchronous (returns after the count is on the host).  A 64-bit row hash
+ * with full verification; collisions are detected and re-hashed, so the
+ * result never depends on the hash. */
+tlp_status tlp_dedup(tlp_ctx* ctx, const float* feats, int64_t N, int32_t row_len,
+                     const int64_t* group_off, int32_t G, const float* labels, int32_t* keep_out,
+                     float* label_out, int64_t* n_distinct_out, void* stream);
+
+/* The top-k score metric (§6.1, R40):
+ *   sum_g w_g min_{i in g} lat_i / sum_g w_g min_{i in topk_g} lat_i
+ * with topk_g the min(k, |g|) best of group g by (score desc, index asc) as in
+ * tlp_topk.  scores: column `head` of a row-major [N, score_stride] device
+ * array; latency device fp32 [N] > 0; group_off HOST int64 [G+1]; weight HOST
+ * fp64 [G]; 1 <= k <= 1024; empty groups contribute nothing.  *out (HOST) in
+ * (0, 1].  Synchronous.  NaN score -> NONFINITE device error (as tlp_topk). */
+tlp_status tlp_topk_score(tlp_ctx* ctx, const float* scores, int32_t score_stride, int32_t head,
+                          const float* latency, const int64_t* group_off, const double* weight,
+                          int32_t G, int32_t k, double* out, void* stream);
+
 /* ---- training-data preparation, P:295-296 -------------------------------
  * label_i = min_{j in g} latency_j / latency_i per group g (fp64 quotient,
  * rounded to fp32).  latency [M] fp32 device > 0; group_off [G+1] HOST int64;

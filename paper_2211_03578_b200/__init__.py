@@ -306,6 +306,41 @@ class TLP:
                                               val_out.data_ptr(), _stream_ptr(stream)))
         return idx_out, val_out
 
+    def dedup(self, feats: torch.Tensor, group_off, labels: Optional[torch.Tensor] = None,
+              stream=None):
+        """tlp_dedup: duplicate classes of the rows of `feats` ([N, ...] fp32 device)
+        within groups.  Returns (keep int32 [N], label_out fp32 [N] or None,
+        n_distinct)."""
+        assert feats.dtype == torch.float32 and feats.is_contiguous()
+        N = feats.shape[0]
+        row_len = feats.numel() // N if N else 1
+        goff = np.ascontiguousarray(group_off, np.int64)
+        keep = torch.empty(N, dtype=torch.int32, device=feats.device)
+        lab = None
+        if labels is not None:
+            assert labels.dtype == torch.float32 and labels.is_contiguous()
+            lab = torch.empty(N, dtype=torch.float32, device=feats.device)
+        n = C.c_int64(0)
+        self._check(self.lib.tlp_dedup(self.h, feats.data_ptr() if N else None, N, row_len,
+                                       goff.ctypes.data, len(goff) - 1,
+                                       labels.data_ptr() if labels is not None else None,
+                                       keep.data_ptr() if N else None,
+                                       lab.data_ptr() if lab is not None else None,
+                                       C.byref(n), _stream_ptr(stream)))
+        return keep, lab, int(n.value)
+
+    def topk_score(self, scores: torch.Tensor, latency: torch.Tensor, group_off, weight, k: int,
+                   head: int = 0, stream=None) -> float:
+        """tlp_topk_score: the paper's top-k score metric."""
+        goff = np.ascontiguousarray(group_off, np.int64)
+        w = np.ascontiguousarray(weight, np.float64)
+        stride = scores.shape[1] if scores.dim() == 2 else 1
+        out = C.c_double(0.0)
+        self._check(self.lib.tlp_topk_score(self.h, scores.data_ptr(), stride, head, latency.data_ptr(),
+                                            goff.ctypes.data, w.ctypes.data, len(goff) - 1, k,
+                                            C.byref(out), _stream_ptr(stream)))
+        return float(out.value)
+
     def topk_merge(self, vals: torch.Tensor, idx: torch.Tensor, idx_out=None, val_out=None,
                    stream=None):
         """Merge per-shard top-k lists vals/idx [W, T, k] into the global [T, k]."""

@@ -17,7 +17,7 @@ EXPORTS = ("tlp_create", "tlp_destroy", "tlp_last_error", "tlp_default_config",
            "tlp_set_token_table", "tlp_set_norm_scales", "tlp_num_params", "tlp_set_params",
            "tlp_get_params", "tlp_get_grads", "tlp_set_comm", "tlp_get_unique_id", "tlp_encode",
            "tlp_score", "tlp_train_step", "tlp_compute_grads", "tlp_lambdarank", "tlp_topk", "tlp_topk_merge",
-           "tlp_search_round", "tlp_normalize_labels", "tlp_sync", "tlp_launch_count", "tlp_debug_umma",
+           "tlp_search_round", "tlp_dedup", "tlp_topk_score", "tlp_normalize_labels", "tlp_sync", "tlp_launch_count", "tlp_debug_umma",
            "tlp_debug_gemm")
 
 
@@ -72,6 +72,8 @@ def load() -> C.CDLL:
         "tlp_topk_merge": (C.c_int, [vp, vp, vp, i32, i32, i32, vp, vp, vp]),
         "tlp_search_round": (C.c_int, [vp, C.POINTER(tlp_seq_batch), i64, vp, i32, i32, i32, i64,
                                        i32, vp, vp, vp]),
+        "tlp_dedup": (C.c_int, [vp, vp, i64, i32, vp, i32, vp, vp, vp, vp, vp]),
+        "tlp_topk_score": (C.c_int, [vp, vp, i32, i32, vp, vp, vp, i32, i32, vp, vp]),
         "tlp_normalize_labels": (C.c_int, [vp, vp, vp, i32, vp, vp]),
         "tlp_sync": (C.c_int, [vp]),
         "tlp_launch_count": (i64, [vp]),
