@@ -258,6 +258,10 @@ def run_ours(args):
         dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
     e2e_ms = float(e2e_ms.item())
 
+    # --- NEXT-2 rows: duplicate scan of this round's features and
+    # the §6.1 top-k score of its scores against synthetic latencies ---
+    next_rows = next2_measure(scorer, feats, scores, task_off, args, stream, dev)
+
     K = args.steps
     cand_s = world * N_ROUND * K / (round_ms / 1e3)
     train_s = world * B_TRAIN * K / (train_ms / 1e3)
@@ -300,6 +304,7 @@ def run_ours(args):
                 "h2d_bytes_per_step": hbatch.nbytes(), "d2h_bytes_per_step": T_TASKS * TOPK * 12,
                 "call": "tlp_search_round, %d chunks" % args.chunks},
         "gpu_launches": launches,
+        "next_rows": next_rows,
         "clocks": clk.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -311,6 +316,57 @@ def run_ours(args):
 
 
 # ------------------------------------------------------------------ oracle arm
+def next2_measure(m, feats, scores, task_off, args, stream, dev):
+    """Time tlp_dedup over the round's 409,600 feature matrices (1% planted
+    duplicates inside the 100 groups = the round's tasks) and tlp_topk_score (k=1, 5) over
+    its scores, CUDA events on the launching stream, W warm-up + K timed calls.
+    dedup roofline: HBM, algorithmic bytes = each 2,200-byte row read once + a
+    duplicate's row re-read for verification + 8 B key + 16 B table slot per
+    row."""
+    import torch
+    N = feats.shape[0]
+    rng = np.random.default_rng(11)
+    X = feats.clone()
+    goff = np.asarray(task_off, np.int64)
+    per = int(goff[1] - goff[0])  # uniform task segments: plant duplicates inside groups
+    src_h = rng.integers(0, N, N // 100)
+    dst_h = (src_h // per) * per + rng.integers(0, per, N // 100)
+    X[torch.from_numpy(dst_h).to(dev)] = X[torch.from_numpy(src_h).to(dev)]
+    lat = torch.from_numpy(np.random.default_rng(5).lognormal(0.0, 0.7, N).astype(np.float32)).to(dev)
+    w = np.random.default_rng(6).integers(1, 6, len(goff) - 1).astype(np.float64)
+
+    def timed(fn):
+        for _ in range(args.warmup):
+            fn()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / args.steps
+
+    res = {}
+    ms = timed(lambda: m.dedup(X, goff, stream=stream))
+    _, _, n = m.dedup(X, goff, stream=stream)
+    peaks, kind = load_peaks()
+    dup = N - n
+    bytes_alg = N * (2200 + 8 + 16) + dup * 2200
+    res["dedup"] = {"value": N / (ms / 1e3), "unit": "candidates/s", "ms_per_call": ms,
+                    "duplicate_rate": dup / N, "distinct": n,
+                    "roofline": {"bound": "hbm", "achieved": bytes_alg / (ms / 1e3) / 1e9,
+                                 "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                                 "frac": bytes_alg / (ms / 1e3) / 1e9 / peaks["hbm_gbs"],
+                                 "peak_kind": kind + " HBM copy bandwidth"},
+                    "note": "synchronous call: includes the host read-back of the distinct count"}
+    for k in (1, 5):
+        ms = timed(lambda: m.topk_score(scores, lat, goff, w, k, stream=stream))
+        res["topk_score_k%d" % k] = {"value": N / (ms / 1e3), "unit": "candidates/s", "ms_per_call": ms,
+                                     "score": m.topk_score(scores, lat, goff, w, k, stream=stream)}
+    return res
+
+
 def _oracle_threads():
     try:
         from threadpoolctl import threadpool_info
