@@ -42,10 +42,16 @@ __global__ void hash_rows(const float* __restrict__ X, int64_t N, int row_len,
   const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (i >= N) return;
-  const uint32_t* row = reinterpret_cast<const uint32_t*>(X + i * row_len);
   uint64_t h = seed ^ (0x9e3779b97f4a7c15ull * (uint64_t)(lane + 1));
-  for (int w = lane; w < row_len; w += 32)
-    h = mix64(h ^ (((uint64_t)w << 32) | __ldg(row + w)));
+  if (((row_len & 1) == 0) && ((reinterpret_cast<uintptr_t>(X) & 7) == 0)) {
+    // 8-byte loads (rows of an even number of floats are 8-byte aligned)
+    const uint64_t* row = reinterpret_cast<const uint64_t*>(X + i * row_len);
+    for (int w = lane; w < row_len / 2; w += 32) h = mix64(h ^ __ldg(row + w) ^ ((uint64_t)w * 0xd6e8feb86659fd93ull));
+  } else {
+    const uint32_t* row = reinterpret_cast<const uint32_t*>(X + i * row_len);
+    for (int w = lane; w < row_len; w += 32)
+      h = mix64(h ^ (((uint64_t)w << 32) | __ldg(row + w)));
+  }
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {  // fixed butterfly: every lane ends with the same value
     const uint64_t other = __shfl_xor_sync(0xffffffffu, h, o);
@@ -231,23 +237,20 @@ extern "C" tlp_status tlp_dedup(tlp_ctx* ctx, const float* feats, int64_t N, int
     TLP_LAUNCH_CHECK();
     verify_rows<<<wb, 256, 0, s>>>(feats, N, row_len, rep, reinterpret_cast<unsigned int*>(cnt));
     TLP_LAUNCH_CHECK();
-    unsigned int coll = 0;
-    TLP_CUDA_TRY(cudaMemcpyAsync(&coll, cnt, sizeof(coll), cudaMemcpyDeviceToHost, s));
+    if (labels) {
+      TLP_CUDA_TRY(cudaMemsetAsync(acc, 0, N * sizeof(int), s));
+      label_max<<<tb, 256, 0, s>>>(labels, rep, N, acc, ctx->d_err);
+      TLP_LAUNCH_CHECK();
+    }
+    finish<<<tb, 256, 0, s>>>(rep, N, acc, keep_out, labels ? label_out : nullptr, cnt + 1);
+    TLP_LAUNCH_CHECK();
+    unsigned long long hc[2] = {0, 0};  // [0] collisions (low 32 bits), [1] distinct
+    TLP_CUDA_TRY(cudaMemcpyAsync(hc, cnt, sizeof(hc), cudaMemcpyDeviceToHost, s));
     TLP_CUDA_TRY(cudaStreamSynchronize(s));
-    ok = coll == 0;
+    ok = (hc[0] & 0xffffffffull) == 0;  // a collision invalidates the pass: re-hash
+    *n_distinct_out = (int64_t)hc[1];
   }
   if (!ok) return fail_msg(ctx, TLP_ERR_STATE, "tlp_dedup: persistent 64-bit hash collisions");
-  if (labels) {
-    TLP_CUDA_TRY(cudaMemsetAsync(acc, 0, N * sizeof(int), s));
-    label_max<<<tb, 256, 0, s>>>(labels, rep, N, acc, ctx->d_err);
-    TLP_LAUNCH_CHECK();
-  }
-  finish<<<tb, 256, 0, s>>>(rep, N, acc, keep_out, labels ? label_out : nullptr, cnt + 1);
-  TLP_LAUNCH_CHECK();
-  unsigned long long distinct = 0;
-  TLP_CUDA_TRY(cudaMemcpyAsync(&distinct, cnt + 1, sizeof(distinct), cudaMemcpyDeviceToHost, s));
-  TLP_CUDA_TRY(cudaStreamSynchronize(s));
-  *n_distinct_out = (int64_t)distinct;
   return TLP_OK;
 }
 
