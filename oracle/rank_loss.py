@@ -143,3 +143,42 @@ def mtl_lambdarank(scores: np.ndarray, labels: np.ndarray, group_off: np.ndarray
         total += lt
         grad[:, t] = gt
     return total, grad
+
+
+# ---------------------------------------------------------------- NEXT-3: MSE
+# P:296 "We use the Mean Square Error (MSE) loss function or the rank loss";
+# P:393 "the label of TLP is a normalization value in the range of (0,1], so MSE
+# loss is an option"; mean of squared residuals, gradient
+# 2 (score - label) / B.  MTL: sum over tasks of the
+# per-task mean over its present labels; absent labels give zero loss and zero
+# gradient.  R41: a task with no present label contributes 0 (as R16's P = 0).
+def mse_counts(labels: np.ndarray) -> np.ndarray:
+    """Present labels per task (the MSE denominator; global under DP)."""
+    labels = np.asarray(labels, np.float64)
+    if labels.ndim == 1:
+        labels = labels[:, None]
+    return (~np.isnan(labels)).sum(axis=0).astype(np.int64)
+
+
+def mtl_mse(scores: np.ndarray, labels: np.ndarray, counts: Optional[np.ndarray] = None):
+    """Returns (loss, grad [B, n_tasks]) of sum_t mean_{i present} (s_it - y_it)^2."""
+    scores = np.asarray(scores, np.float64)
+    labels = np.asarray(labels, np.float64)
+    if scores.ndim == 1:
+        scores, labels = scores[:, None], labels[:, None]
+    B, nt = scores.shape
+    if counts is None:
+        counts = mse_counts(labels)
+    grad = np.zeros((B, nt))
+    total = 0.0
+    for t in range(nt):
+        n = float(counts[t])
+        if n == 0:
+            continue
+        for i in range(B):
+            if np.isnan(labels[i, t]):
+                continue
+            r = scores[i, t] - labels[i, t]
+            total += r * r / n
+            grad[i, t] = 2.0 * r / n
+    return total, grad

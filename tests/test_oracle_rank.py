@@ -213,3 +213,37 @@ def test_dp_emulation_equals_unsharded(R):
     l_dp, g_dp = dp_emulate(cfg, flat, X, lab, off, R, seed=R)
     assert abs(l_full - l_dp) < 1e-12 * abs(l_full)
     assert np.abs(g_full - g_dp).max() < 1e-12 * np.abs(g_full).max()
+
+
+# ---------------------------------------------------------------- NEXT-3: MSE
+def test_mse_spec_examples():
+    from oracle.rank_loss import mtl_mse
+    # S:305 scores [0.5], labels [1.0] -> 0.25
+    assert mtl_mse(np.array([0.5]), np.array([1.0]))[0] == 0.25
+    # S:306 scores == labels -> 0.0
+    y = np.array([0.3, 0.7, 1.0])
+    assert mtl_mse(y, y)[0] == 0.0
+    # S:392 labels [None, 0.5], preds [0.3, 0.5], MSE both tasks -> 0.0 (one sample, two tasks)
+    loss, g = mtl_mse(np.array([[0.3, 0.5]]), np.array([[np.nan, 0.5]]))
+    assert loss == 0.0 and g[0, 0] == 0.0
+    # S:393 labels [1.0, None], preds [0.5, 0.9] -> 0.25
+    assert mtl_mse(np.array([[0.5, 0.9]]), np.array([[1.0, np.nan]]))[0] == 0.25
+
+
+def test_mse_gradient_finite_differences():
+    from oracle.rank_loss import mtl_mse
+    rng = np.random.default_rng(0)
+    s = rng.normal(size=(13, 3))
+    y = rng.uniform(0.1, 1.0, (13, 3))
+    y[rng.random((13, 3)) < 0.3] = np.nan
+    _, g = mtl_mse(s, y)
+    h = 1e-6
+    for i in range(13):
+        for t in range(3):
+            sp, sm = s.copy(), s.copy()
+            sp[i, t] += h
+            sm[i, t] -= h
+            fd = (mtl_mse(sp, y)[0] - mtl_mse(sm, y)[0]) / (2 * h)
+            assert abs(fd - g[i, t]) <= 1e-7 * max(1.0, abs(fd))
+            if np.isnan(y[i, t]):
+                assert g[i, t] == 0.0  # S:394 masked task: exactly zero gradient
