@@ -88,7 +88,13 @@ typedef struct {
   int precision;              /* tlp_precision */
   float lr, beta1, beta2, eps; /* Adam (R23 / S:356: 1e-3, 0.9, 0.999, 1e-8) */
   unsigned long long seed;    /* reserved */
+  int loss;                   /* tlp_loss: training loss ("MSE loss function or the rank loss") */
 } tlp_config;
+
+typedef enum {
+  TLP_LOSS_LAMBDARANK = 0,  /* R16 (the paper's choice) */
+  TLP_LOSS_MSE = 1          /* NEXT-3: per-task mean squared residual over present labels (R41) */
+} tlp_loss;
 
 /* Packed abstract schedule primitives (S ::= p*, p ::= tau (id|num)*).
  * Structure of arrays; ALL pointers are device memory owned by the caller. */
@@ -156,8 +162,9 @@ tlp_status tlp_score(tlp_ctx* ctx, const float* feats, int64_t N, float* scores,
  * One optimizer step on a batch of B candidates grouped into G contiguous
  * groups (subgraphs, R18): feats [B, L, E] device; labels [B, n_tasks] device
  * fp32 in (0,1], NaN = absent (MTL); group_off [G+1] HOST int64.
- * Forward, LambdaRank (R16, mean over the global strict-pair count per task),
- * backward, gradient allreduce when a communicator is set, Adam (R23).
+ * Forward, the configured loss (cfg.loss: LambdaRank R16, mean over the global
+ * strict-pair count per task; or MSE, mean over the global present-label count
+ * per task), backward, gradient allreduce when a communicator is set, Adam (R23).
  * loss_out: device fp32 scalar (sum over tasks of the per-task means; with a
  * communicator every rank receives the global loss). */
 tlp_status tlp_train_step(tlp_ctx* ctx, const float* feats, const float* labels,
@@ -173,6 +180,15 @@ tlp_status tlp_compute_grads(tlp_ctx* ctx, const float* feats, const float* labe
 tlp_status tlp_lambdarank(tlp_ctx* ctx, const float* scores, const float* labels,
                           const int64_t* group_off, int32_t B, int32_t G,
                           float* loss_out, float* dscores_out, void* stream);
+
+/* The MSE unit alone (NEXT-3, MTL S:386-394, R41):
+ * loss = sum_t (1/n_t) sum_{i: label present} (s_it - y_it)^2, n_t = present
+ * labels of task t in the batch (a task with none contributes 0);
+ * dscores = 2 (s - y) / n_t, 0 where the label is absent.  scores / labels /
+ * dscores_out [B, n_tasks] device fp32, loss_out device fp32 scalar.  Counts
+ * are local (no communicator). */
+tlp_status tlp_mse(tlp_ctx* ctx, const float* scores, const float* labels, int32_t B,
+                   float* loss_out, float* dscores_out, void* stream);
 
 /* ---- (4) per-task top-k, P:182 + P:390 ----------------------------------
  * For task segment t = [task_off[t], task_off[t+1]) of `scores` (column `head`

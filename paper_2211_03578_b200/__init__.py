@@ -47,6 +47,7 @@ class TLPConfig:
     beta1: float = 0.9
     beta2: float = 0.999
     eps: float = 1e-8
+    loss: str = "lambdarank"  # "lambdarank" (R16, the paper's choice) | "mse" (NEXT-3)
 
     def to_c(self) -> tlp_config:
         c = tlp_config()
@@ -58,6 +59,7 @@ class TLPConfig:
         c.head_dim, c.n_tasks = self.head_dim, self.n_tasks
         c.precision = {"fp32": 0, "bf16": 1}[self.precision]
         c.lr, c.beta1, c.beta2, c.eps = self.lr, self.beta1, self.beta2, self.eps
+        c.loss = {"lambdarank": 0, "mse": 1}[self.loss]
         return c
 
 
@@ -271,6 +273,15 @@ class TLP:
         self._check(self.lib.tlp_lambdarank(self.h, scores.data_ptr(), labels.data_ptr(),
                                             goff.ctypes.data, B, len(goff) - 1, loss.data_ptr(),
                                             ds.data_ptr(), _stream_ptr(stream)))
+        return loss, ds
+
+    def mse(self, scores, labels, stream=None):
+        """tlp_mse: the NEXT-3 MSE unit (loss [1], dscores like scores)."""
+        B = scores.shape[0]
+        loss = torch.empty(1, dtype=torch.float32, device=scores.device)
+        ds = torch.empty_like(scores)
+        self._check(self.lib.tlp_mse(self.h, scores.data_ptr(), labels.data_ptr(), B, loss.data_ptr(),
+                                     ds.data_ptr(), _stream_ptr(stream)))
         return loss, ds
 
     def topk(self, scores: torch.Tensor, task_off, k: int, head: int = 0, shard_base: int = 0,

@@ -16,7 +16,7 @@ TLP_STATUS = {0: "OK", -1: "ERR_ARG", -2: "ERR_SHAPE", -3: "ERR_EMPTY_SEQ",
 EXPORTS = ("tlp_create", "tlp_destroy", "tlp_last_error", "tlp_default_config",
            "tlp_set_token_table", "tlp_set_norm_scales", "tlp_num_params", "tlp_set_params",
            "tlp_get_params", "tlp_get_grads", "tlp_set_comm", "tlp_get_unique_id", "tlp_encode",
-           "tlp_score", "tlp_train_step", "tlp_compute_grads", "tlp_lambdarank", "tlp_topk", "tlp_topk_merge",
+           "tlp_score", "tlp_train_step", "tlp_compute_grads", "tlp_lambdarank", "tlp_mse", "tlp_topk", "tlp_topk_merge",
            "tlp_search_round", "tlp_dedup", "tlp_topk_score", "tlp_normalize_labels", "tlp_sync", "tlp_launch_count", "tlp_debug_umma",
            "tlp_debug_gemm")
 
@@ -27,7 +27,7 @@ class tlp_config(C.Structure):
                 ("n_attn", C.c_int), ("n_res", C.c_int), ("head_dim", C.c_int),
                 ("n_tasks", C.c_int), ("precision", C.c_int), ("lr", C.c_float),
                 ("beta1", C.c_float), ("beta2", C.c_float), ("eps", C.c_float),
-                ("seed", C.c_ulonglong)]
+                ("seed", C.c_ulonglong), ("loss", C.c_int)]
 
 
 class tlp_seq_batch(C.Structure):
@@ -70,6 +70,7 @@ def load() -> C.CDLL:
         "tlp_lambdarank": (C.c_int, [vp, vp, vp, vp, i32, i32, vp, vp, vp]),
         "tlp_topk": (C.c_int, [vp, vp, i32, i32, vp, i32, i32, i64, vp, vp, vp]),
         "tlp_topk_merge": (C.c_int, [vp, vp, vp, i32, i32, i32, vp, vp, vp]),
+        "tlp_mse": (C.c_int, [vp, vp, vp, i32, vp, vp, vp]),
         "tlp_search_round": (C.c_int, [vp, C.POINTER(tlp_seq_batch), i64, vp, i32, i32, i32, i64,
                                        i32, vp, vp, vp]),
         "tlp_dedup": (C.c_int, [vp, vp, i64, i32, vp, i32, vp, vp, vp, vp, vp]),

@@ -59,6 +59,7 @@ std::string check_config(const tlp_config& c) {
   if (c.E < 2 || c.E > 64) return "E must be in [2, 64]";
   if (c.T < 1 || c.T >= c.E) return "T must be in [1, E)";
   if (c.n_up < 1 || c.n_up > TLP_MAX_UP) return "n_up must be in [1, 4]";
+  if (c.loss != TLP_LOSS_LAMBDARANK && c.loss != TLP_LOSS_MSE) return "loss must be 0 (LambdaRank) or 1 (MSE)";
   if (c.hidden < 8 || c.hidden > 512) return "hidden must be in [8, 512]";
   if (c.up_dims[c.n_up - 1] != c.hidden) return "up_dims[n_up-1] must equal hidden";
   for (int i = 0; i < c.n_up; ++i)
@@ -334,17 +335,22 @@ tlp_status grads_impl(tlp_ctx* ctx, const float* feats, const float* labels,
   if ((st = train_ws(ctx, B, G, &w)) != TLP_OK) return st;
   TLP_CUDA_TRY(cudaMemcpyAsync(w.goff, group_off, (G + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
   const int nt = ctx->cfg.n_tasks;
-  // C-0: per-task strict-pair counts (labels only), summed over ranks.
-  if ((st = rank_pair_counts(ctx, labels, w.goff, G, max_group, w.counts, s)) != TLP_OK) return st;
+  // C-0: per-task loss denominators (labels only), summed over ranks: strict
+  // pairs for LambdaRank (R16), present labels for MSE (R41).
+  const bool mse = ctx->cfg.loss == TLP_LOSS_MSE;
+  st = mse ? mse_counts(ctx, labels, B, w.counts, s)
+           : rank_pair_counts(ctx, labels, w.goff, G, max_group, w.counts, s);
+  if (st != TLP_OK) return st;
   ncclComm_t comm = reinterpret_cast<ncclComm_t>(ctx->comm);
   if (comm) {
     if (ncclAllReduce(w.counts, w.counts, nt, ncclFloat64, ncclSum, comm, s) != ncclSuccess)
-      return fail(ctx, TLP_ERR_NCCL, "pair-count allreduce failed");
+      return fail(ctx, TLP_ERR_NCCL, "loss-count allreduce failed");
   }
   if ((st = simt_forward(ctx, feats, B, w.scores, true, s)) != TLP_OK) return st;
-  if ((st = rank_loss_grad(ctx, w.scores, labels, w.goff, G, B, max_group, w.counts, loss_out,
-                           w.dscores, s)) != TLP_OK)
-    return st;
+  st = mse ? mse_loss_grad(ctx, w.scores, labels, B, w.counts, loss_out, w.dscores, s)
+           : rank_loss_grad(ctx, w.scores, labels, w.goff, G, B, max_group, w.counts, loss_out,
+                            w.dscores, s);
+  if (st != TLP_OK) return st;
   if ((st = simt_backward(ctx, B, w.dscores, s)) != TLP_OK) return st;
   if (comm) {
     // C-1: gradient allreduce (sum); every rank then applies the same Adam step.
@@ -410,6 +416,19 @@ tlp_status tlp_lambdarank(tlp_ctx* ctx, const float* scores, const float* labels
   if ((st = rank_pair_counts(ctx, labels, w.goff, G, max_group, w.counts, s)) != TLP_OK) return st;
   return rank_loss_grad(ctx, scores, labels, w.goff, G, B, max_group, w.counts, loss_out,
                         dscores_out, s);
+}
+
+tlp_status tlp_mse(tlp_ctx* ctx, const float* scores, const float* labels, int32_t B,
+                   float* loss_out, float* dscores_out, void* stream) {
+  CHECK_CTX();
+  if (!scores || !labels || !loss_out || !dscores_out || B < 1) return fail(ctx, TLP_ERR_ARG, "bad MSE arguments");
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  TrainWs w;
+  tlp_status st = train_ws(ctx, B, 1, &w);
+  if (st != TLP_OK) return st;
+  if ((st = mse_counts(ctx, labels, B, w.counts, s)) != TLP_OK) return st;
+  return mse_loss_grad(ctx, scores, labels, B, w.counts, loss_out, dscores_out, s);
 }
 
 tlp_status tlp_topk(tlp_ctx* ctx, const float* scores, int32_t score_stride, int32_t head,

@@ -189,7 +189,94 @@ __global__ void finalize_rank(const float* __restrict__ loss_part, int G, int nt
   }
 }
 
+// ---- NEXT-3: MSE (MTL masking S:386-394; R41)
+constexpr int kMseBlocks = 64;
+
+// present labels per task (exact integer counts, summed into doubles)
+__global__ void mse_count_kernel(const float* __restrict__ labels, int64_t B, int nt,
+                                 unsigned long long* __restrict__ cnt) {
+  const int t = blockIdx.y;
+  unsigned long long c = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < B; i += (int64_t)gridDim.x * blockDim.x)
+    c += !isnan(labels[i * nt + t]);
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(cnt + t, c);
+}
+
+__global__ void mse_counts_to_double(const unsigned long long* __restrict__ cnt, int nt,
+                                     double* __restrict__ counts) {
+  if (threadIdx.x < nt) counts[threadIdx.x] = (double)cnt[threadIdx.x];
+}
+
+// gradient 2 r / n_t and per-(block, task) partial sums of r^2 in a fixed order
+__global__ void mse_kernel(const float* __restrict__ scores, const float* __restrict__ labels,
+                           int64_t B, int nt, const double* __restrict__ counts,
+                           float* __restrict__ dscores, double* __restrict__ part) {
+  const int t = blockIdx.y;
+  const double n = counts[t];
+  __shared__ double red[256];
+  double acc = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < B; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = i * nt + t;
+    const float y = labels[e];
+    float g = 0.f;
+    if (!isnan(y) && n > 0) {
+      const double r = (double)scores[e] - (double)y;
+      acc += r * r;
+      g = (float)(2.0 * r / n);
+    }
+    dscores[e] = g;
+  }
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int o = 128; o; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[(int64_t)t * gridDim.x + blockIdx.x] = red[0];
+}
+
+__global__ void mse_finalize(const double* __restrict__ part, int nblk, int nt,
+                             const double* __restrict__ counts, float* __restrict__ loss_out,
+                             uint32_t* err) {
+  double tot = 0.0;
+  for (int t = 0; t < nt; ++t) {
+    if (!(counts[t] > 0)) continue;
+    double lt = 0.0;
+    for (int b = 0; b < nblk; ++b) lt += part[(int64_t)t * nblk + b];
+    tot += lt / counts[t];
+  }
+  const float lf = (float)tot;
+  if (isnan(lf)) atomicOr(err, DERR_NAN_LOSS);
+  *loss_out = lf;
+}
+
 }  // namespace
+
+tlp_status mse_counts(tlp_ctx* ctx, const float* labels, int64_t B, double* d_counts, cudaStream_t s) {
+  const int nt = ctx->cfg.n_tasks;
+  TLP_CUDA_TRY(ctx->ws_rank.ensure((size_t)nt * kMseBlocks * sizeof(double) + 64 * sizeof(unsigned long long)));
+  unsigned long long* cnt = reinterpret_cast<unsigned long long*>(
+      ctx->ws_rank.as<char>() + (size_t)nt * kMseBlocks * sizeof(double));
+  TLP_CUDA_TRY(cudaMemsetAsync(cnt, 0, nt * sizeof(unsigned long long), s));
+  mse_count_kernel<<<dim3(kMseBlocks, nt), 256, 0, s>>>(labels, B, nt, cnt);
+  TLP_LAUNCH_CHECK();
+  mse_counts_to_double<<<1, 32, 0, s>>>(cnt, nt, d_counts);
+  TLP_LAUNCH_CHECK();
+  return TLP_OK;
+}
+
+tlp_status mse_loss_grad(tlp_ctx* ctx, const float* scores, const float* labels, int64_t B,
+                         const double* d_counts, float* loss_out, float* dscores, cudaStream_t s) {
+  const int nt = ctx->cfg.n_tasks;
+  TLP_CUDA_TRY(ctx->ws_rank.ensure((size_t)nt * kMseBlocks * sizeof(double) + 64 * sizeof(unsigned long long)));
+  double* part = ctx->ws_rank.as<double>();
+  mse_kernel<<<dim3(kMseBlocks, nt), 256, 0, s>>>(scores, labels, B, nt, d_counts, dscores, part);
+  TLP_LAUNCH_CHECK();
+  mse_finalize<<<1, 1, 0, s>>>(part, kMseBlocks, nt, d_counts, loss_out, ctx->d_err);
+  TLP_LAUNCH_CHECK();
+  return TLP_OK;
+}
 
 static size_t rank_ws_bytes(int G, int nt) {
   return (size_t)G * nt * (sizeof(double) + sizeof(float)) + 64;

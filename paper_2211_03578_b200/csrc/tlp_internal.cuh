@@ -184,6 +184,10 @@ tlp_status tc_gemm(tlp_ctx* ctx, bool ta, bool tb, int64_t M, int64_t N, int64_t
                    const float* A, int64_t lda, const float* B, int64_t ldb, float* C,
                    int64_t ldc, const EpiParams& e, int splits, int64_t kslice, cudaStream_t s);
 
+// k_rank.cu: MSE (NEXT-3): present-label counts per task, then loss + dscores
+tlp_status mse_counts(tlp_ctx* ctx, const float* labels, int64_t B, double* d_counts, cudaStream_t s);
+tlp_status mse_loss_grad(tlp_ctx* ctx, const float* scores, const float* labels, int64_t B,
+                         const double* d_counts, float* loss_out, float* dscores, cudaStream_t s);
 // k_rank.cu
 tlp_status rank_pair_counts(tlp_ctx* ctx, const float* labels, const int64_t* d_goff, int G,
                             int max_group, double* d_counts, cudaStream_t s);

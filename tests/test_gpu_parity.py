@@ -269,6 +269,79 @@ def test_grads_parity(tp, tokscale, n_tasks, n_attn, seed, sizes, precision, tol
     assert not bad, bad
 
 
+def test_mse_unit_parity(tp):
+    """NEXT-3 MSE unit (tlp_mse) vs oracle mtl_mse on MTL labels with absent tasks."""
+    rng = np.random.default_rng(4)
+    s = rng.normal(size=(777, 3)).astype(np.float32)
+    y = rng.uniform(0.05, 1.0, (777, 3)).astype(np.float32)
+    y[rng.random((777, 3)) < 0.3] = np.nan
+    y[:, 2] = np.nan  # a task with no labels contributes nothing (R41)
+    loss_ref, g_ref = OLR.mtl_mse(s.astype(np.float64), y.astype(np.float64))
+    m = tp.TLP(tp.TLPConfig(precision="fp32", n_tasks=3, loss="mse"))
+    loss, g = m.mse(torch.from_numpy(s).cuda(), torch.from_numpy(y).cuda())
+    m.sync()
+    assert abs(float(loss.cpu()) - loss_ref) <= 1e-6 * loss_ref
+    assert rel_err(g.cpu().numpy(), g_ref) <= 1e-6
+    assert not g.cpu().numpy()[np.isnan(y)].any()
+
+
+@pytest.mark.parametrize("precision,tol", [("fp32", 1e-5), ("bf16", 1e-2)])
+def test_grads_parity_mse(tp, tokscale, precision, tol):
+    """NEXT-3: the whole training gradient with the MSE loss (cfg.loss = MSE),
+    MTL with absent labels.  Only attn*.bk is identically zero here (softmax
+    shift invariance, R32); c1 / c2 carry real MSE gradients."""
+    tokens, scale = tokscale
+    ocfg = oracle_cfg(n_tasks=2, n_attn=1, hidden=64, up=(32, 64), head_dim=32)
+    flat = flat_params(ocfg, seed=23)
+    X, y, off = train_inputs(tokens, scale, 2, sizes=(9, 16, 12, 16, 11, 7))
+    p = OM.unflatten(ocfg, flat)
+    s_ref, acts = OM.forward(ocfg, p, X, save=True)
+    loss_ref, g = OLR.mtl_mse(s_ref, y.astype(np.float64))
+    grads_ref = OM.backward(ocfg, p, acts, g)
+    cfg = product_cfg(ocfg, precision)
+    cfg.loss = "mse"
+    m = tp.TLP(cfg)
+    m.set_params(flat.astype(np.float32))
+    loss = m.compute_grads(torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda(), off)
+    m.sync()
+    assert abs(float(loss.cpu()) - loss_ref) <= tol * abs(loss_ref)
+    got = OM.unflatten(ocfg, m.get_grads().astype(np.float64))
+    bad = {}
+    for name, _ in OM.param_shapes(ocfg):
+        if re.search(r"attn\d+\.bk$", name):
+            assert np.abs(got[name]).max() <= tol * np.abs(grads_ref[name.replace(".bk", ".Wk")]).max() * ocfg.L
+            continue
+        e = rel_err(got[name], grads_ref[name])
+        if e > tol:
+            bad[name] = e
+    assert not bad, bad
+
+
+def test_finetune_from_checkpoint(tp, tokscale):
+    """NEXT-3 fine-tuning (P:518 transfer): parameters saved from one ctx
+    (tlp_get_params) and loaded into a fresh ctx (tlp_set_params) continue
+    training exactly like the original ctx after a re-load of the same state
+    (Adam restarts, R23)."""
+    tokens, scale = tokscale
+    ocfg = oracle_cfg(hidden=64, up=(32, 64), head_dim=32)
+    X, y, off = train_inputs(tokens, scale)
+    Xd, yd = torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda()
+    a = tp.TLP(product_cfg(ocfg, "fp32"))
+    a.set_params(flat_params(ocfg, seed=17).astype(np.float32))
+    for _ in range(3):
+        a.train_step(Xd, yd, off)
+    ckpt = a.get_params()
+    b = tp.TLP(product_cfg(ocfg, "fp32"))
+    b.set_params(ckpt)
+    a.set_params(ckpt)  # both restart Adam from the checkpoint
+    for _ in range(2):
+        a.train_step(Xd, yd, off)
+        b.train_step(Xd, yd, off)
+    a.sync(); b.sync()
+    assert np.array_equal(a.get_params().view(np.uint32), b.get_params().view(np.uint32))
+    assert not np.array_equal(a.get_params(), ckpt)
+
+
 def test_train_step_adam_parity(tp, tokscale):
     tokens, scale = tokscale
     ocfg = oracle_cfg(hidden=64, up=(32, 64), head_dim=32)
