@@ -8,6 +8,8 @@ Paper (P:295 [§4.4], P:431 [§6.1.3], P:355 [§5.2]):
    with "8 heads", "one layer of the self-attention module is enough"
    -> n_attn layers of 8-head self-attention; R8 no mask, R9 no positional
    encoding, R10 identity residual and no LayerNorm, R14 scale 1/sqrt(d_h).
+   NEXT-3 variant (cfg.attn_mask, R42): keys that are padding rows (all-zero
+   rows of X, R7) are masked out of every softmax; queries are unchanged.
   "Then two residual blocks follow" -> R12: h + relu(h Wa + a) Wb + b.
   "Finally, multiple linear layers and a sum operation are used to obtain a
    prediction score" -> R13: per position relu(h W1 + c1) w2 + c2, summed over
@@ -38,6 +40,7 @@ class Config:
     n_res: int = 2
     head_dim: int = 128
     n_tasks: int = 1
+    attn_mask: bool = False  # NEXT-3 / R42: mask padding keys (the paper: no mask, R8)
 
     def __post_init__(self):
         self.up_dims = tuple(self.up_dims)
@@ -105,6 +108,8 @@ def forward(cfg: Config, p: Dict[str, np.ndarray], X: np.ndarray, save: bool = F
     h = np.asarray(X, np.float64)
     N, L = h.shape[0], h.shape[1]
     nh, dh, H = cfg.attn_heads, cfg.d_h, cfg.hidden
+    # R42: a key is valid unless its input row is all zeros (a padding row)
+    key_valid = (h != 0).any(axis=2) if cfg.attn_mask else None
     acts = {"up_in": [], "up_pre": [], "attn": [], "res": []}
     for i in range(len(cfg.up_dims)):
         acts["up_in"].append(h)
@@ -120,7 +125,9 @@ def forward(cfg: Config, p: Dict[str, np.ndarray], X: np.ndarray, save: bool = F
         Kh = K.reshape(N, L, nh, dh).transpose(0, 2, 1, 3)
         Vh = V.reshape(N, L, nh, dh).transpose(0, 2, 1, 3)
         S = Qh @ Kh.transpose(0, 1, 3, 2) / np.sqrt(dh)      # R14
-        A = softmax_rows(S)                                    # R8: no mask
+        if key_valid is not None:
+            S = np.where(key_valid[:, None, None, :], S, -np.inf)
+        A = softmax_rows(S)                                    # R8: no mask (R42 optional)
         Oh = A @ Vh
         O = Oh.transpose(0, 2, 1, 3).reshape(N, L, H)
         acts["attn"].append(dict(h=h, Qh=Qh, Kh=Kh, Vh=Vh, A=A, O=O))

