@@ -89,6 +89,8 @@ typedef struct {
   float lr, beta1, beta2, eps; /* Adam (R23 / S:356: 1e-3, 0.9, 0.999, 1e-8) */
   unsigned long long seed;    /* reserved */
   int loss;                   /* tlp_loss: training loss ("MSE loss function or the rank loss") */
+  int attn_mask;              /* NEXT-3 / R42: 1 = padding keys (all-zero input rows) are masked
+                                 out of every attention softmax; 0 = no mask (the paper, R8) */
 } tlp_config;
 
 typedef enum {

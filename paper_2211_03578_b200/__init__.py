@@ -48,6 +48,7 @@ class TLPConfig:
     beta2: float = 0.999
     eps: float = 1e-8
     loss: str = "lambdarank"  # "lambdarank" (R16, the paper's choice) | "mse" (NEXT-3)
+    attn_mask: bool = False   # NEXT-3 / R42: mask padding keys (the paper: no mask, R8)
 
     def to_c(self) -> tlp_config:
         c = tlp_config()
@@ -60,6 +61,7 @@ class TLPConfig:
         c.precision = {"fp32": 0, "bf16": 1}[self.precision]
         c.lr, c.beta1, c.beta2, c.eps = self.lr, self.beta1, self.beta2, self.eps
         c.loss = {"lambdarank": 0, "mse": 1}[self.loss]
+        c.attn_mask = 1 if self.attn_mask else 0
         return c
 
 

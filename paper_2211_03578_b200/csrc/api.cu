@@ -60,6 +60,7 @@ std::string check_config(const tlp_config& c) {
   if (c.T < 1 || c.T >= c.E) return "T must be in [1, E)";
   if (c.n_up < 1 || c.n_up > TLP_MAX_UP) return "n_up must be in [1, 4]";
   if (c.loss != TLP_LOSS_LAMBDARANK && c.loss != TLP_LOSS_MSE) return "loss must be 0 (LambdaRank) or 1 (MSE)";
+  if (c.attn_mask != 0 && c.attn_mask != 1) return "attn_mask must be 0 or 1";
   if (c.hidden < 8 || c.hidden > 512) return "hidden must be in [8, 512]";
   if (c.up_dims[c.n_up - 1] != c.hidden) return "up_dims[n_up-1] must equal hidden";
   for (int i = 0; i < c.n_up; ++i)

@@ -188,11 +188,22 @@ __global__ void colsum_partial(int64_t M, int64_t N, const float* __restrict__ X
 
 // ---------------------------------------------------------------------------
 // attention, one warp per (candidate, head); lane = query row (L <= 32)
+// R42 (NEXT-3): kvalid[r] = 1 unless input row r is all zeros (a padding row)
+__global__ void row_valid_kernel(const float* __restrict__ X, int64_t M, int E,
+                                 float* __restrict__ kvalid) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= M) return;
+  bool v = false;
+  for (int c = 0; c < E; ++c) v |= X[r * E + c] != 0.f;
+  kvalid[r] = v ? 1.f : 0.f;
+}
+
 template <int DH>
 __global__ void __launch_bounds__(128) attn_fwd_kernel(const float* __restrict__ QKV, int L,
                                                        int H, int nh, int64_t pairs,
                                                        float* __restrict__ O,
-                                                       float* __restrict__ Asave) {
+                                                       float* __restrict__ Asave,
+                                                       const float* __restrict__ kvalid) {
   extern __shared__ float sm[];
   const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int64_t pair = (int64_t)blockIdx.x * (blockDim.x / 32) + w;
@@ -222,9 +233,15 @@ __global__ void __launch_bounds__(128) attn_fwd_kernel(const float* __restrict__
         float a = 0.f;
 #pragma unroll
         for (int d = 0; d < DH; ++d) a = fmaf(q[d], Ks[m * DH + d], a);
-        s[m] = a * scale;
+        s[m] = (kvalid && kvalid[row0 + m] == 0.f) ? -INFINITY : a * scale;  // R42 mask
         mx = fmaxf(mx, s[m]);
       }
+    }
+    if (mx == -INFINITY) {  // no valid key (cannot come from tlp_encode): attend uniformly
+#pragma unroll
+      for (int m = 0; m < 32; ++m)
+        if (m < L) s[m] = 0.f;
+      mx = 0.f;
     }
     float sum = 0.f;
 #pragma unroll
@@ -399,6 +416,7 @@ struct ActLayout {
   int64_t qkv[TLP_MAX_ATTN], A[TLP_MAX_ATTN], O[TLP_MAX_ATTN], hattn[TLP_MAX_ATTN];
   int64_t r[TLP_MAX_RES], hres[TLP_MAX_RES];
   int64_t U[TLP_MAX_TASKS], pooled[TLP_MAX_TASKS];
+  int64_t kvalid;  // R42 key-validity flags (attn_mask)
   // backward scratch
   int64_t dh, dtmp, dqkv, dU;
   int64_t total_fwd, total;
@@ -418,6 +436,7 @@ ActLayout act_layout(const tlp_config& c, int64_t N) {
   }
   for (int r = 0; r < c.n_res; ++r) { a.r[r] = take(M * H); a.hres[r] = take(M * H); }
   for (int t = 0; t < c.n_tasks; ++t) { a.U[t] = take(M * c.head_dim); a.pooled[t] = take(N * c.head_dim); }
+  a.kvalid = take(M);
   a.total_fwd = o;
   a.dh = take(M * H);
   a.dtmp = take(M * std::max<int64_t>(H, c.up_dims[0]));
@@ -429,13 +448,13 @@ ActLayout act_layout(const tlp_config& c, int64_t N) {
 
 template <int DH>
 tlp_status launch_attn_fwd(tlp_ctx* ctx, const float* qkv, int64_t N, float* O, float* A,
-                           cudaStream_t s) {
+                           const float* kvalid, cudaStream_t s) {
   const tlp_config& c = ctx->cfg;
   const int64_t pairs = N * c.attn_heads;
   const int warps = 4;
   const size_t smem = (size_t)warps * 2 * 32 * DH * sizeof(float);
   attn_fwd_kernel<DH><<<(unsigned)cdiv(pairs, warps), warps * 32, smem, s>>>(
-      qkv, c.L, c.hidden, c.attn_heads, pairs, O, A);
+      qkv, c.L, c.hidden, c.attn_heads, pairs, O, A, kvalid);
   TLP_LAUNCH_CHECK();
   return TLP_OK;
 }
@@ -460,12 +479,12 @@ tlp_status launch_attn_bwd(tlp_ctx* ctx, const float* qkv, const float* A, const
 }
 
 tlp_status attn_fwd(tlp_ctx* ctx, const float* qkv, int64_t N, float* O, float* A,
-                    cudaStream_t s) {
+                    const float* kvalid, cudaStream_t s) {
   switch (ctx->cfg.hidden / ctx->cfg.attn_heads) {
-    case 8: return launch_attn_fwd<8>(ctx, qkv, N, O, A, s);
-    case 16: return launch_attn_fwd<16>(ctx, qkv, N, O, A, s);
-    case 32: return launch_attn_fwd<32>(ctx, qkv, N, O, A, s);
-    case 64: return launch_attn_fwd<64>(ctx, qkv, N, O, A, s);
+    case 8: return launch_attn_fwd<8>(ctx, qkv, N, O, A, kvalid, s);
+    case 16: return launch_attn_fwd<16>(ctx, qkv, N, O, A, kvalid, s);
+    case 32: return launch_attn_fwd<32>(ctx, qkv, N, O, A, kvalid, s);
+    case 64: return launch_attn_fwd<64>(ctx, qkv, N, O, A, kvalid, s);
     default: ctx->last_error = "head dim must be 8/16/32/64"; return TLP_ERR_UNSUPPORTED;
   }
 }
@@ -567,6 +586,12 @@ tlp_status simt_forward(tlp_ctx* ctx, const float* X, int64_t N, float* scores, 
     const int64_t n = std::min(chunk, N - n0);
     const int64_t M = n * c.L;
     const float* h = X + n0 * c.L * c.E;
+    const float* kvalid = nullptr;
+    if (c.attn_mask && c.n_attn > 0) {
+      row_valid_kernel<<<(unsigned)cdiv(M, 256), 256, 0, s>>>(h, M, c.E, W + lay.kvalid);
+      TLP_LAUNCH_CHECK();
+      kvalid = W + lay.kvalid;
+    }
     int64_t din = c.E;
     for (int i = 0; i < c.n_up; ++i) {
       EpiParams e; e.bias = P + o.up_b[i]; e.relu = true;
@@ -582,7 +607,7 @@ tlp_status simt_forward(tlp_ctx* ctx, const float* X, int64_t N, float* scores, 
         EpiParams e; e.bias = P + bq[j];
         TRY(sgemm(ctx, false, false, M, H, H, h, H, P + wq[j], H, qkv + j * H, 3 * H, e, s));
       }
-      TRY(attn_fwd(ctx, qkv, n, W + lay.O[l], save ? W + lay.A[l] : nullptr, s));
+      TRY(attn_fwd(ctx, qkv, n, W + lay.O[l], save ? W + lay.A[l] : nullptr, kvalid, s));
       EpiParams e; e.bias = P + o.bo[l]; e.resid = h; e.ldr = H;
       TRY(sgemm(ctx, false, false, M, H, H, W + lay.O[l], H, P + o.Wo[l], H, W + lay.hattn[l], H, e, s));
       h = W + lay.hattn[l];

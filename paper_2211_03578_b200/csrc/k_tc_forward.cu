@@ -68,7 +68,8 @@ constexpr uint32_t OFF_O = OFF_V + kKP * kRowB;     // O_j    3 x [128 x 32] can
 constexpr uint32_t OFF_DOT = OFF_O + 3 * 8192;      // 2 x 128 fp32 row dots
 constexpr uint32_t OFF_BAR = OFF_DOT + 1024;        // mbarriers (<= 32)
 constexpr uint32_t OFF_TPTR = OFF_BAR + 256;
-constexpr uint32_t OFF_RING = OFF_TPTR + 128;       // kStages x 16 KB
+constexpr uint32_t OFF_KV = OFF_TPTR + 128;         // R42: key-valid byte per tile row (attn_mask)
+constexpr uint32_t OFF_RING = OFF_KV + 128;         // kStages x 16 KB
 constexpr uint32_t OFF_VEC = OFF_RING + kStages * kStageBytes;  // epilogue vectors (fp32)
 constexpr uint32_t kMaxSmem = 232448;
 static_assert(OFF_RING % 128 == 0, "ring alignment");
@@ -99,6 +100,7 @@ struct TcArgs {
   int64_t ra[TLP_MAX_RES], rb[TLP_MAX_RES];
   int64_t c1[TLP_MAX_TASKS], w2[TLP_MAX_TASKS], c2[TLP_MAX_TASKS];
   int n_attn, n_res, n_tasks;
+  int attn_mask;     // R42: mask padding keys (all-zero X rows)
   long long* trace;  // diagnostics (TLP_TC_TRACE=1): CTA 0 epilogue phase timestamps
 };
 
@@ -222,9 +224,10 @@ __device__ __forceinline__ float ex2_approx(float x) {
 // the canonical bf16 [128 x 32] A operand of the output projection at tile rows
 // 25c + kk.  Every candidate sees exactly its own block, at the same relative
 // positions whatever its slot (batch invariance, R34).
+template <bool MASK>
 __device__ __forceinline__ void attn_unit_mma(uint8_t* smem, uint32_t sbase, uint32_t c,
                                               uint32_t mh, uint32_t lane, float sm_scale,
-                                              uint32_t o_off) {
+                                              uint32_t o_off, uint32_t kmask) {
   const uint32_t g = lane >> 2, tig = lane & 3;
   const uint32_t q0 = 32 * c + 16 * mh, k0 = 32 * c;
   uint32_t qa[2][4];  // Q A-fragments per k-step (d 0..15, 16..31)
@@ -249,17 +252,18 @@ __device__ __forceinline__ void attn_unit_mma(uint8_t* smem, uint32_t sbase, uin
     for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
       for (int e = 0; e < 2; ++e)
-        if (8 * nt + 2 * (int)tig + e < kL) mx = fmaxf(mx, s[nt][2 * half + e]);
+        if (MASK ? ((kmask >> (8 * nt + 2 * tig + e)) & 1u) : (8 * nt + 2 * (int)tig + e < kL))
+          mx = fmaxf(mx, s[nt][2 * half + e]);
     mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
     mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-    const float off = mx * sm_scale;  // key 0 is always real: mx finite
+    const float off = mx * sm_scale;  // kmask is never empty: mx finite
     float sum = 0.f;
 #pragma unroll
     for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        const float p = (8 * nt + 2 * (int)tig + e < kL)
-                            ? ex2_approx(fmaf(s[nt][2 * half + e], sm_scale, -off)) : 0.f;
+        const bool ok = MASK ? ((kmask >> (8 * nt + 2 * tig + e)) & 1u) : (8 * nt + 2 * (int)tig + e < kL);
+        const float p = ok ? ex2_approx(fmaf(s[nt][2 * half + e], sm_scale, -off)) : 0.f;
         s[nt][2 * half + e] = p;
         sum += p;
       }
@@ -507,15 +511,18 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
           uint32_t pk[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) pk[i] = 0;
+          bool nz = false;
           if (real && n < a.N) {
             const float2* src = reinterpret_cast<const float2*>(a.X + (tile * kCand * kL + r) * kE);
 #pragma unroll
             for (int i = 0; i < kE / 2; ++i) {
               const float2 x = __ldg(src + i);
               pk[i] = tc::pack_bf16(x.x, x.y);
+              nz |= (x.x != 0.f) | (x.y != 0.f);
             }
           }
           store_row32(smem, OFF_X, r, 0, kKX, pk);
+          smem[OFF_KV + r] = nz ? 1 : 0;  // R42 key validity (read after barrier 2 of head 0)
         }
         signal();
         wait_on(bar_acc, ph_acc);
@@ -570,7 +577,14 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
           tc::tc_fence_before();                          // QKV_j read: TMEM buffer j%2 free
           if (j + 2 < kHeads) tc::mbar_arrive(bar_conv + 8 * (j & 1));
           asm volatile("bar.sync 2, 320;" ::: "memory");  // Q/K/V of head j complete
-          attn_unit_mma(smem, sbase, unit >> 1, unit & 1, lane, sm_scale, OFF_O + 8192 * (j % 3));
+          if (a.attn_mask) {  // R42: drop padding keys (an all-padding slot keeps every key)
+            const uint32_t cand = unit >> 1;
+            uint32_t kmask = __ballot_sync(0xffffffffu, lane < (uint32_t)kL && smem[OFF_KV + kL * cand + lane]);
+            if (!kmask) kmask = (1u << kL) - 1u;
+            attn_unit_mma<true>(smem, sbase, cand, unit & 1, lane, sm_scale, OFF_O + 8192 * (j % 3), kmask);
+          } else {
+            attn_unit_mma<false>(smem, sbase, unit >> 1, unit & 1, lane, sm_scale, OFF_O + 8192 * (j % 3), 0u);
+          }
           tc::fence_proxy_async_smem();                   // O_j ready
           tc::tc_fence_before();
           tc::mbar_arrive(bar_attn + 8 * (j & 3));
@@ -793,6 +807,7 @@ tlp_status tc_forward(tlp_ctx* ctx, const float* feats, int64_t N, float* scores
   a.wstream = w.wstream; a.chunks = w.chunks; a.nchunks = w.nchunks;
   a.vec = w.vec; a.vec_floats = w.vec_floats;
   a.n_attn = c.n_attn; a.n_res = c.n_res; a.n_tasks = c.n_tasks;
+  a.attn_mask = c.attn_mask;
   const int grid = (int)std::min<int64_t>(a.ntile, ctx->num_sms);
   // Diagnostics: TLP_TC_TRACE=1 prints CTA 0's epilogue phase timeline (cycles
   // between successive waits/signals) for its first tiles to stderr.

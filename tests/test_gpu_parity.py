@@ -317,6 +317,64 @@ def test_grads_parity_mse(tp, tokscale, precision, tol):
     assert not bad, bad
 
 
+# ---------------------------------------------------------------- NEXT-3: padding mask (R42)
+@pytest.mark.parametrize("precision,tol", [("fp32", 1e-5), ("bf16", 1e-2)])
+def test_forward_parity_attn_mask(tp, tokscale, precision, tol):
+    """Encoded TenSet-shaped candidates (most shorter than 25 primitives, so
+    with padding rows) scored with the padding-key mask, 2 layers."""
+    tokens, scale = tokscale
+    ocfg = oracle_cfg(n_attn=2)
+    ocfg.attn_mask = True
+    flat = flat_params(ocfg, seed=31)
+    _, X = encoded_batch(33, 301, tokens, scale)
+    assert ((X == 0).all(axis=2).any(axis=1)).mean() > 0.3  # padding present
+    ref = OM.forward(ocfg, OM.unflatten(ocfg, flat), X)
+    cfg = product_cfg(ocfg, precision)
+    cfg.attn_mask = True
+    m = tp.TLP(cfg)
+    m.set_params(flat.astype(np.float32))
+    Xd = torch.from_numpy(X).cuda()
+    s = m.score(Xd)
+    m.sync()
+    assert rel_err(s.cpu().numpy(), ref) <= tol
+    # the mask changes the result (it is not a no-op on padded inputs)
+    unmasked = OM.forward(oracle_cfg(n_attn=2), OM.unflatten(ocfg, flat), X)
+    assert rel_err(unmasked, ref) > 1e-3
+    if precision == "bf16":  # batch invariance holds with the mask
+        part = m.score(Xd[7:300].contiguous()).cpu().numpy()
+        assert np.array_equal(s.cpu().numpy()[7:300].view(np.uint32), part.view(np.uint32))
+
+
+@pytest.mark.parametrize("precision,tol", [("fp32", 1e-5), ("bf16", 1e-2)])
+def test_grads_parity_attn_mask(tp, tokscale, precision, tol):
+    tokens, scale = tokscale
+    ocfg = oracle_cfg(n_tasks=1, n_attn=1, hidden=64, up=(32, 64), head_dim=32)
+    ocfg.attn_mask = True
+    flat = flat_params(ocfg, seed=25)  # seed with within-group score gaps > 2e-4 (R26)
+    X, y, off = train_inputs(tokens, scale, 1, sizes=(9, 16, 12, 16, 11, 7))
+    p = OM.unflatten(ocfg, flat)
+    s_ref, acts = OM.forward(ocfg, p, X, save=True)
+    assert min_rel_gap(s_ref, off) > 2e-4
+    loss_ref, g = OLR.mtl_lambdarank(s_ref, y.astype(np.float64), off)
+    grads_ref = OM.backward(ocfg, p, acts, g)
+    cfg = product_cfg(ocfg, precision)
+    cfg.attn_mask = True
+    m = tp.TLP(cfg)
+    m.set_params(flat.astype(np.float32))
+    loss = m.compute_grads(torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda(), off)
+    m.sync()
+    assert abs(float(loss.cpu()) - loss_ref) <= tol * abs(loss_ref)
+    got = OM.unflatten(ocfg, m.get_grads().astype(np.float64))
+    bad = {}
+    for name, _ in OM.param_shapes(ocfg):
+        if ZERO_GRAD.search(name) or CANCEL_GRAD.search(name):
+            continue  # as in test_grads_parity (R32)
+        e = rel_err(got[name], grads_ref[name])
+        if e > tol:
+            bad[name] = e
+    assert not bad, bad
+
+
 def test_finetune_from_checkpoint(tp, tokscale):
     """NEXT-3 fine-tuning (P:518 transfer): parameters saved from one ctx
     (tlp_get_params) and loaded into a fresh ctx (tlp_set_params) continue
