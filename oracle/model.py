@@ -10,6 +10,8 @@ Paper (P:295 [§4.4], P:431 [§6.1.3], P:355 [§5.2]):
    encoding, R10 identity residual and no LayerNorm, R14 scale 1/sqrt(d_h).
    NEXT-3 variant (cfg.attn_mask, R42): keys that are padding rows (all-zero
    rows of X, R7) are masked out of every softmax; queries are unchanged.
+   NEXT-3 variant (cfg.pos_enc, R43): a learned positional table pos [L, H]
+   is added to the upsampled rows before the first attention layer.
   "Then two residual blocks follow" -> R12: h + relu(h Wa + a) Wb + b.
   "Finally, multiple linear layers and a sum operation are used to obtain a
    prediction score" -> R13: per position relu(h W1 + c1) w2 + c2, summed over
@@ -41,6 +43,7 @@ class Config:
     head_dim: int = 128
     n_tasks: int = 1
     attn_mask: bool = False  # NEXT-3 / R42: mask padding keys (the paper: no mask, R8)
+    pos_enc: bool = False    # NEXT-3 / R43: learned positional table (the paper: none, R9)
 
     def __post_init__(self):
         self.up_dims = tuple(self.up_dims)
@@ -60,6 +63,8 @@ def param_shapes(cfg: Config) -> List[Tuple[str, Tuple[int, ...]]]:
         out += [("up%d.W" % i, (d_in, d)), ("up%d.b" % i, (d,))]
         d_in = d
     H = cfg.hidden
+    if cfg.pos_enc:
+        out += [("pos", (cfg.L, H))]  # R43: right after the upsample (R24 order)
     for l in range(cfg.n_attn):
         for nm in ("q", "k", "v", "o"):
             out += [("attn%d.W%s" % (l, nm), (H, H)), ("attn%d.b%s" % (l, nm), (H,))]
@@ -116,6 +121,8 @@ def forward(cfg: Config, p: Dict[str, np.ndarray], X: np.ndarray, save: bool = F
         pre = h @ p["up%d.W" % i] + p["up%d.b" % i]
         acts["up_pre"].append(pre)
         h = relu(pre)
+    if cfg.pos_enc:
+        h = h + p["pos"][None, :L, :]                           # R43
     for l in range(cfg.n_attn):
         pre = "attn%d." % l
         Q = h @ p[pre + "Wq"] + p[pre + "bq"]
@@ -201,6 +208,8 @@ def backward(cfg: Config, p: Dict[str, np.ndarray], acts, g: np.ndarray) -> Dict
             grads[pre + "W" + nm] = np.einsum("nli,nlo->io", hin, d)
             grads[pre + "b" + nm] = d.sum(axis=(0, 1))
         dh_ = dh_ + dQ @ p[pre + "Wq"].T + dK @ p[pre + "Wk"].T + dV @ p[pre + "Wv"].T
+    if cfg.pos_enc:
+        grads["pos"] = dh_.sum(axis=0)                         # R43: d h / d pos = identity per row
     for i in reversed(range(len(cfg.up_dims))):
         pre_ = "up%d." % i
         dpre = dh_ * (acts["up_pre"][i] > 0)

@@ -49,6 +49,8 @@ class TorchTLP(torch.nn.Module):
             mha.out_proj.weight.data = torch.tensor(p[pre + "Wo"].T.copy())
             mha.out_proj.bias.data = torch.tensor(p[pre + "bo"])
             self.attn.append(mha)
+        self.pos = (torch.nn.Parameter(torch.tensor(p["pos"].copy()))
+                    if getattr(cfg, "pos_enc", False) else None)
         self.res = torch.nn.ModuleList()
         for r in range(cfg.n_res):
             a = torch.nn.Linear(H, H, dtype=torch.float64)
@@ -69,6 +71,8 @@ class TorchTLP(torch.nn.Module):
         pad = (x == 0).all(dim=-1) if getattr(self.cfg, "attn_mask", False) else None
         for lin in self.ups:
             h = torch.relu(lin(h))
+        if self.pos is not None:
+            h = h + self.pos
         for mha in self.attn:
             h = h + mha(h, h, h, key_padding_mask=pad, need_weights=False)[0]
         for a, b in self.res:
@@ -93,6 +97,8 @@ class TorchTLP(torch.nn.Module):
         for t, (a, b) in enumerate(self.heads):
             g["head%d.W1" % t] = a.weight.grad.T; g["head%d.c1" % t] = a.bias.grad
             g["head%d.w2" % t] = b.weight.grad.T; g["head%d.c2" % t] = b.bias.grad
+        if self.pos is not None:
+            g["pos"] = self.pos.grad
         return {k: v.detach().numpy() for k, v in g.items()}
 
 
@@ -274,3 +280,41 @@ def test_masked_backward_matches_torch_autograd():
     for name, _ in M.param_shapes(cfg):
         a, b = grads[name].reshape(tg[name].shape), tg[name]
         assert np.abs(a - b).max() <= 1e-12 * max(1.0, np.abs(b).max()), name
+
+
+# ---------------------------------------------------------------- NEXT-3: learned positional table (R43)
+POSENC = M.Config(L=6, E=8, T=3, hidden=16, up_dims=(8, 16), attn_heads=2, n_attn=2, n_res=1,
+                  head_dim=8, n_tasks=2, pos_enc=True)
+
+
+def test_posenc_forward_backward_match_torch():
+    cfg = POSENC
+    p = rand_params(cfg, 21)
+    X, _ = _ragged_X(cfg, 5, 22)
+    g = np.random.default_rng(23).normal(size=(5, cfg.n_tasks))
+    s, acts = M.forward(cfg, p, X, save=True)
+    tm = TorchTLP(cfg, p)
+    out = tm(torch.tensor(X))
+    assert np.abs(s - out.detach().numpy()).max() <= 1e-12 * max(1.0, np.abs(s).max())
+    (out * torch.tensor(g)).sum().backward()
+    tg = tm.named_grads()
+    grads = M.backward(cfg, p, acts, g)
+    for name, _ in M.param_shapes(cfg):
+        a, b = grads[name].reshape(tg[name].shape), tg[name]
+        assert np.abs(a - b).max() <= 1e-12 * max(1.0, np.abs(b).max()), name
+
+
+def test_posenc_breaks_permutation_invariance_and_zero_table_is_identity():
+    """with positional encoding off a row-permuted input gives the same
+    score; with a nonzero table it does not; a zero table equals no table."""
+    import dataclasses
+    cfg = POSENC
+    p = rand_params(cfg, 24)
+    X = rand_X(cfg, 3, 25, n_real=cfg.L)
+    perm = np.random.default_rng(26).permutation(cfg.L)
+    assert np.abs(M.forward(cfg, p, X) - M.forward(cfg, p, X[:, perm])).max() > 1e-6
+    plain = dataclasses.replace(cfg, pos_enc=False)
+    q = {k: v for k, v in p.items() if k != "pos"}
+    assert np.allclose(M.forward(plain, q, X), M.forward(plain, q, X[:, perm]), rtol=0, atol=1e-12)
+    p0 = dict(p, pos=np.zeros_like(p["pos"]))
+    assert np.array_equal(M.forward(cfg, p0, X), M.forward(plain, q, X))
