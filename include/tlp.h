@@ -91,6 +91,9 @@ typedef struct {
   int loss;                   /* tlp_loss: training loss ("MSE loss function or the rank loss") */
   int attn_mask;              /* NEXT-3 / R42: 1 = padding keys (all-zero input rows) are masked
                                  out of every attention softmax; 0 = no mask (the paper, R8) */
+  int pos_enc;                /* NEXT-3 / R43: 1 = learned positional table pos [L, hidden] added
+                                 after the upsample (R24: right after the upsample parameters);
+                                 0 = none (the paper, R9) */
 } tlp_config;
 
 typedef enum {

@@ -49,6 +49,7 @@ class TLPConfig:
     eps: float = 1e-8
     loss: str = "lambdarank"  # "lambdarank" (R16, the paper's choice) | "mse" (NEXT-3)
     attn_mask: bool = False   # NEXT-3 / R42: mask padding keys (the paper: no mask, R8)
+    pos_enc: bool = False     # NEXT-3 / R43: learned positional table (the paper: none, R9)
 
     def to_c(self) -> tlp_config:
         c = tlp_config()
@@ -62,6 +63,7 @@ class TLPConfig:
         c.lr, c.beta1, c.beta2, c.eps = self.lr, self.beta1, self.beta2, self.eps
         c.loss = {"lambdarank": 0, "mse": 1}[self.loss]
         c.attn_mask = 1 if self.attn_mask else 0
+        c.pos_enc = 1 if self.pos_enc else 0
         return c
 
 

@@ -36,6 +36,8 @@ ParamOffsets compute_offsets(const tlp_config& c) {
     din = c.up_dims[i];
   }
   const int64_t H = c.hidden;
+  o.pos = -1;
+  if (c.pos_enc) { o.pos = p; p += (int64_t)c.L * H; }  // R43, right after the upsample (R24)
   for (int l = 0; l < c.n_attn; ++l) {
     o.Wq[l] = p; p += H * H; o.bq[l] = p; p += H;
     o.Wk[l] = p; p += H * H; o.bk[l] = p; p += H;
@@ -61,6 +63,7 @@ std::string check_config(const tlp_config& c) {
   if (c.n_up < 1 || c.n_up > TLP_MAX_UP) return "n_up must be in [1, 4]";
   if (c.loss != TLP_LOSS_LAMBDARANK && c.loss != TLP_LOSS_MSE) return "loss must be 0 (LambdaRank) or 1 (MSE)";
   if (c.attn_mask != 0 && c.attn_mask != 1) return "attn_mask must be 0 or 1";
+  if (c.pos_enc != 0 && c.pos_enc != 1) return "pos_enc must be 0 or 1";
   if (c.hidden < 8 || c.hidden > 512) return "hidden must be in [8, 512]";
   if (c.up_dims[c.n_up - 1] != c.hidden) return "up_dims[n_up-1] must equal hidden";
   for (int i = 0; i < c.n_up; ++i)

@@ -188,6 +188,30 @@ __global__ void colsum_partial(int64_t M, int64_t N, const float* __restrict__ X
 
 // ---------------------------------------------------------------------------
 // attention, one warp per (candidate, head); lane = query row (L <= 32)
+// R43 (NEXT-3): out[n*L + l, :] = h[n*L + l, :] + pos[l, :]
+__global__ void add_pos_kernel(const float* __restrict__ h, const float* __restrict__ pos, int64_t M,
+                               int L, int H, float* __restrict__ out) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= M * H) return;
+  const int64_t r = e / H;
+  out[e] = h[e] + pos[(r % L) * H + (e % H)];
+}
+
+// R43: dpos[l, c] = sum_n dh[n*L + l, c], fixed order over n
+__global__ void pos_grad_kernel(const float* __restrict__ dh, int64_t N, int L, int H,
+                                float* __restrict__ dpos) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)L * H) return;
+  float a0 = 0.f, a1 = 0.f;
+  int64_t n = 0;
+  for (; n + 1 < N; n += 2) {
+    a0 += dh[(n * L) * H + e];
+    a1 += dh[((n + 1) * L) * H + e];
+  }
+  if (n < N) a0 += dh[(n * L) * H + e];
+  dpos[e] = a0 + a1;
+}
+
 // R42 (NEXT-3): kvalid[r] = 1 unless input row r is all zeros (a padding row)
 __global__ void row_valid_kernel(const float* __restrict__ X, int64_t M, int E,
                                  float* __restrict__ kvalid) {
@@ -417,6 +441,7 @@ struct ActLayout {
   int64_t r[TLP_MAX_RES], hres[TLP_MAX_RES];
   int64_t U[TLP_MAX_TASKS], pooled[TLP_MAX_TASKS];
   int64_t kvalid;  // R42 key-validity flags (attn_mask)
+  int64_t hpos;    // R43 upsample output + positional table (pos_enc)
   // backward scratch
   int64_t dh, dtmp, dqkv, dU;
   int64_t total_fwd, total;
@@ -437,6 +462,7 @@ ActLayout act_layout(const tlp_config& c, int64_t N) {
   for (int r = 0; r < c.n_res; ++r) { a.r[r] = take(M * H); a.hres[r] = take(M * H); }
   for (int t = 0; t < c.n_tasks; ++t) { a.U[t] = take(M * c.head_dim); a.pooled[t] = take(N * c.head_dim); }
   a.kvalid = take(M);
+  a.hpos = take(M * H);
   a.total_fwd = o;
   a.dh = take(M * H);
   a.dtmp = take(M * std::max<int64_t>(H, c.up_dims[0]));
@@ -600,6 +626,11 @@ tlp_status simt_forward(tlp_ctx* ctx, const float* X, int64_t N, float* scores, 
       h = W + lay.up[i];
       din = c.up_dims[i];
     }
+    if (c.pos_enc) {  // R43
+      add_pos_kernel<<<(unsigned)cdiv(M * H, 256), 256, 0, s>>>(h, P + o.pos, M, c.L, (int)H, W + lay.hpos);
+      TLP_LAUNCH_CHECK();
+      h = W + lay.hpos;
+    }
     for (int l = 0; l < c.n_attn; ++l) {
       float* qkv = W + lay.qkv[l];
       const int64_t wq[3] = {o.Wq[l], o.Wk[l], o.Wv[l]}, bq[3] = {o.bq[l], o.bk[l], o.bv[l]};
@@ -650,7 +681,7 @@ tlp_status simt_backward(tlp_ctx* ctx, int64_t N, const float* g, cudaStream_t s
   float* dqkv = W + lay.dqkv;
   float* dU = W + lay.dU;
   const float* hfin = c.n_res ? W + lay.hres[c.n_res - 1]
-                    : (c.n_attn ? W + lay.hattn[c.n_attn - 1] : W + lay.up[c.n_up - 1]);
+                    : (c.n_attn ? W + lay.hattn[c.n_attn - 1] : (c.pos_enc ? W + lay.hpos : W + lay.up[c.n_up - 1]));
   // heads
   for (int t = 0; t < c.n_tasks; ++t) {
     head_bwd_kernel<<<(unsigned)cdiv(M * hd, 256), 256, 0, s>>>(W + lay.U[t], c.L, hd, N,
@@ -667,7 +698,7 @@ tlp_status simt_backward(tlp_ctx* ctx, int64_t N, const float* g, cudaStream_t s
   // residual blocks
   for (int r = c.n_res - 1; r >= 0; --r) {
     const float* hin = r > 0 ? W + lay.hres[r - 1]
-                     : (c.n_attn ? W + lay.hattn[c.n_attn - 1] : W + lay.up[c.n_up - 1]);
+                     : (c.n_attn ? W + lay.hattn[c.n_attn - 1] : (c.pos_enc ? W + lay.hpos : W + lay.up[c.n_up - 1]));
     const float* rr = W + lay.r[r];
     TRY(sgemm_wgrad(ctx, M, H, H, rr, H, dh, H, G + o.Wb[r], s));
     TRY(colsum(ctx, M, H, dh, H, G + o.b[r], s));
@@ -680,7 +711,7 @@ tlp_status simt_backward(tlp_ctx* ctx, int64_t N, const float* g, cudaStream_t s
   }
   // attention layers
   for (int l = c.n_attn - 1; l >= 0; --l) {
-    const float* hin = l > 0 ? W + lay.hattn[l - 1] : W + lay.up[c.n_up - 1];
+    const float* hin = l > 0 ? W + lay.hattn[l - 1] : (c.pos_enc ? W + lay.hpos : W + lay.up[c.n_up - 1]);
     TRY(sgemm_wgrad(ctx, M, H, H, W + lay.O[l], H, dh, H, G + o.Wo[l], s));
     TRY(colsum(ctx, M, H, dh, H, G + o.bo[l], s));
     EpiParams e0;
@@ -693,6 +724,11 @@ tlp_status simt_backward(tlp_ctx* ctx, int64_t N, const float* g, cudaStream_t s
       EpiParams ea; ea.accumulate = true;
       TRY(sgemm(ctx, false, true, M, H, H, dqkv + j * H, 3 * H, P + wq[j], H, dh, H, ea, s));
     }
+  }
+  // R43: dpos = sum over candidates; d(up_out) = d(up_out + pos) unchanged
+  if (c.pos_enc) {
+    pos_grad_kernel<<<(unsigned)cdiv((int64_t)c.L * H, 256), 256, 0, s>>>(dh, N, c.L, (int)H, G + o.pos);
+    TLP_LAUNCH_CHECK();
   }
   // upsample: dh is d(up_out[n_up-1])
   float* cur = dh;

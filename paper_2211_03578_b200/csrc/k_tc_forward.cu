@@ -101,6 +101,7 @@ struct TcArgs {
   int64_t c1[TLP_MAX_TASKS], w2[TLP_MAX_TASKS], c2[TLP_MAX_TASKS];
   int n_attn, n_res, n_tasks;
   int attn_mask;     // R42: mask padding keys (all-zero X rows)
+  const float* pos;  // R43: positional table [L, 256] (16-byte aligned copy) or null
   long long* trace;  // diagnostics (TLP_TC_TRACE=1): CTA 0 epilogue phase timestamps
 };
 
@@ -161,15 +162,39 @@ __device__ __forceinline__ void epi_relu_to_tmem(uint32_t tl, uint32_t src, int 
 }
 
 // relu(acc + bias) -> bf16 smem operand (row r)
+// R43 (NEXT-3): + pos[row position][c] after the ReLU when `pos_row` is set
+__device__ __forceinline__ void add_row32(float (&v)[32], const float* bias, const float* pos_row) {
+  float b[32];
+  vec32(bias, b);
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i] + b[i], 0.f);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const float4 p = __ldg(reinterpret_cast<const float4*>(pos_row) + i);
+    v[4 * i] += p.x; v[4 * i + 1] += p.y; v[4 * i + 2] += p.z; v[4 * i + 3] += p.w;
+  }
+}
+
 __device__ __forceinline__ void epi_relu_to_smem(uint8_t* smem, uint32_t tl, uint32_t src,
                                                  int c0, int c1, const float* bias, uint32_t dst,
-                                                 uint32_t Kt, uint32_t r) {
+                                                 uint32_t Kt, uint32_t r, const float* pos_row) {
   for (int c = c0; c < c1; c += 64) {
     float v0[32], v1[32];
     uint32_t pk[16];
     tc::tmem_ld32(tl + src + c, v0);
     tc::tmem_ld32(tl + src + c + 32, v1);
     tc::tmem_wait_ld();
+    if (pos_row) {
+      add_row32(v0, bias + c, pos_row + c);
+      add_row32(v1, bias + c + 32, pos_row + c + 32);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) pk[i] = tc::pack_bf16(v0[2 * i], v0[2 * i + 1]);
+      store_row32(smem, dst, r, c, Kt, pk);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) pk[i] = tc::pack_bf16(v1[2 * i], v1[2 * i + 1]);
+      store_row32(smem, dst, r, c + 32, Kt, pk);
+      continue;
+    }
     relu_pack32(v0, bias + c, pk);
     store_row32(smem, dst, r, c, Kt, pk);
     relu_pack32(v1, bias + c + 32, pk);
@@ -529,7 +554,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
         epi_relu_to_tmem(tl, T_B, lo_of(128), hi_of(128), vs + a.up_b0, T_AOP);   // U1 -> TMEM
         signal();
         wait_on(bar_acc, ph_acc);
-        epi_relu_to_smem(smem, tl, T_A, lo_of(kH), hi_of(kH), vs + a.up_b1, OFF_H, kH, r);  // h
+        epi_relu_to_smem(smem, tl, T_A, lo_of(kH), hi_of(kH), vs + a.up_b1, OFF_H, kH, r,
+                         a.pos ? a.pos + kk * kH : nullptr);  // h (+ pos, R43)
         signal();
       }
       for (int l = 0; l < NA; ++l) {
@@ -687,6 +713,7 @@ struct TcWeights {
   std::vector<std::array<int64_t, 3>> vec_copies;  // {src flat offset, dst offset, n}
   TcArgs slots{};                                  // offsets into `vec`
   uint32_t smem = 0;
+  float* pos = nullptr;                            // R43: aligned copy of the positional table
 };
 
 bool tc_supported(const tlp_config& c) {
@@ -791,6 +818,11 @@ tlp_status tc_prepare(tlp_ctx* ctx, cudaStream_t s) {
                                       (int)kMaxSmem));
   }
   TcWeights& w = *ctx->tc;
+  if (ctx->cfg.pos_enc) {  // R43: the table, copied to an aligned buffer (read through L1 in E2)
+    if (!w.pos) TLP_CUDA_TRY(cudaMalloc(&w.pos, (size_t)kL * kH * sizeof(float)));
+    TLP_CUDA_TRY(cudaMemcpyAsync(w.pos, ctx->d_params + ctx->off.pos, (size_t)kL * kH * sizeof(float),
+                                 cudaMemcpyDeviceToDevice, s));
+  }
   for (const auto& cp : w.vec_copies)
     TLP_CUDA_TRY(cudaMemcpyAsync(w.vec + cp[1], ctx->d_params + cp[0], cp[2] * sizeof(float),
                                  cudaMemcpyDeviceToDevice, s));
@@ -806,6 +838,7 @@ tlp_status tc_forward(tlp_ctx* ctx, const float* feats, int64_t N, float* scores
   a.X = feats; a.scores = scores; a.N = N; a.ntile = cdiv(N, kCand);
   a.wstream = w.wstream; a.chunks = w.chunks; a.nchunks = w.nchunks;
   a.vec = w.vec; a.vec_floats = w.vec_floats;
+  a.pos = ctx->cfg.pos_enc ? w.pos : nullptr;
   a.n_attn = c.n_attn; a.n_res = c.n_res; a.n_tasks = c.n_tasks;
   a.attn_mask = c.attn_mask;
   const int grid = (int)std::min<int64_t>(a.ntile, ctx->num_sms);
@@ -843,6 +876,7 @@ void tc_free(tlp_ctx* ctx) {
   cudaFree(ctx->tc->chunks);
   cudaFree(ctx->tc->pack);
   cudaFree(ctx->tc->vec);
+  cudaFree(ctx->tc->pos);
   delete ctx->tc;
   ctx->tc = nullptr;
 }

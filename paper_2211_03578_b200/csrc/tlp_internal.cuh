@@ -28,6 +28,7 @@ enum : uint32_t {
 // R24 flat-parameter offsets (fp32 elements).
 struct ParamOffsets {
   int64_t up_W[TLP_MAX_UP], up_b[TLP_MAX_UP];
+  int64_t pos;  // R43 positional table [L, hidden] (cfg.pos_enc), else -1
   int64_t Wq[TLP_MAX_ATTN], bq[TLP_MAX_ATTN], Wk[TLP_MAX_ATTN], bk[TLP_MAX_ATTN];
   int64_t Wv[TLP_MAX_ATTN], bv[TLP_MAX_ATTN], Wo[TLP_MAX_ATTN], bo[TLP_MAX_ATTN];
   int64_t Wa[TLP_MAX_RES], a[TLP_MAX_RES], Wb[TLP_MAX_RES], b[TLP_MAX_RES];

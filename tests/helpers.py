@@ -21,7 +21,8 @@ def product_cfg(ocfg: OM.Config, precision="fp32"):
     from paper_2211_03578_b200 import TLPConfig
     return TLPConfig(L=ocfg.L, E=ocfg.E, T=ocfg.T, hidden=ocfg.hidden, up_dims=tuple(ocfg.up_dims),
                      attn_heads=ocfg.attn_heads, n_attn=ocfg.n_attn, n_res=ocfg.n_res,
-                     head_dim=ocfg.head_dim, n_tasks=ocfg.n_tasks, precision=precision)
+                     head_dim=ocfg.head_dim, n_tasks=ocfg.n_tasks, precision=precision,
+                     attn_mask=ocfg.attn_mask, pos_enc=ocfg.pos_enc)
 
 
 def flat_params(ocfg: OM.Config, seed: int, scale: float = 1.0, bf16: bool = True) -> np.ndarray:

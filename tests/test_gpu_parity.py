@@ -375,6 +375,54 @@ def test_grads_parity_attn_mask(tp, tokscale, precision, tol):
     assert not bad, bad
 
 
+# ---------------------------------------------------------------- NEXT-3: learned positional table (R43)
+@pytest.mark.parametrize("precision,tol", [("fp32", 1e-5), ("bf16", 1e-2)])
+def test_forward_parity_pos_enc(tp, tokscale, precision, tol):
+    tokens, scale = tokscale
+    ocfg = oracle_cfg(n_attn=2)
+    ocfg.pos_enc = True
+    flat = flat_params(ocfg, seed=41)
+    _, X = encoded_batch(43, 301, tokens, scale)
+    ref = OM.forward(ocfg, OM.unflatten(ocfg, flat), X)
+    m = tp.TLP(product_cfg(ocfg, precision))
+    assert m.num_params == OM.n_params(ocfg)
+    m.set_params(flat.astype(np.float32))
+    s = m.score(torch.from_numpy(X).cuda())
+    m.sync()
+    assert rel_err(s.cpu().numpy(), ref) <= tol
+
+
+@pytest.mark.parametrize("precision,tol", [("fp32", 1e-5), ("bf16", 1e-2)])
+def test_grads_parity_pos_enc(tp, tokscale, precision, tol):
+    tokens, scale = tokscale
+    ocfg = oracle_cfg(n_tasks=1, n_attn=1, hidden=64, up=(32, 64), head_dim=32)
+    ocfg.pos_enc = True
+    ocfg.attn_mask = True
+    X, y, off = train_inputs(tokens, scale, 1, sizes=(9, 16, 12, 16, 11, 7))
+    for seed in range(40, 80):  # a seed with within-group score gaps > 2e-4 (R26)
+        flat = flat_params(ocfg, seed=seed)
+        p = OM.unflatten(ocfg, flat)
+        s_ref, acts = OM.forward(ocfg, p, X, save=True)
+        if min_rel_gap(s_ref, off) > 2e-4:
+            break
+    loss_ref, g = OLR.mtl_lambdarank(s_ref, y.astype(np.float64), off)
+    grads_ref = OM.backward(ocfg, p, acts, g)
+    m = tp.TLP(product_cfg(ocfg, precision))
+    m.set_params(flat.astype(np.float32))
+    loss = m.compute_grads(torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda(), off)
+    m.sync()
+    assert abs(float(loss.cpu()) - loss_ref) <= tol * abs(loss_ref)
+    got = OM.unflatten(ocfg, m.get_grads().astype(np.float64))
+    bad = {}
+    for name, _ in OM.param_shapes(ocfg):
+        if ZERO_GRAD.search(name) or CANCEL_GRAD.search(name):
+            continue
+        e = rel_err(got[name], grads_ref[name])
+        if e > tol:
+            bad[name] = e
+    assert not bad, bad
+
+
 def test_finetune_from_checkpoint(tp, tokscale):
     """NEXT-3 fine-tuning (P:518 transfer): parameters saved from one ctx
     (tlp_get_params) and loaded into a fresh ctx (tlp_set_params) continue
