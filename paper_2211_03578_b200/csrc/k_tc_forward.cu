@@ -78,7 +78,8 @@ static_assert(OFF_RING % 128 == 0, "ring alignment");
 constexpr uint32_t T_A = 0;      // 256: up1 / sum_j O_j Wo_j / residual-block output accumulator
 constexpr uint32_t T_B = 256;    // 128: up0, residual-block first GEMM halves, head (scratch)
 constexpr uint32_t T_QKV = 256;  // 2 x 96: QKV_j double buffer (attention phase only)
-constexpr uint32_t T_AOP = 448;  // 64:  bf16 A operand (U1, residual-block half)
+constexpr uint32_t T_AOP = 448;  // 64:  bf16 A operand (U1, residual-block second half)
+constexpr uint32_t T_AOP0 = 384; // 64:  bf16 A operand (residual-block first half; res phase only)
 
 struct ChunkRef {
   uint32_t off16;  // byte offset / 16 into the weight stream
@@ -471,12 +472,14 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
           wait_opnd();                                                    // E_resid
         }
         for (int r = 0; r < NR; ++r) {
+          // G1 half 1 goes ahead of G2 part 0 so that the epilogue of r_h1 overlaps
+          // G2 part 0 (the two r halves live in separate TMEM operand slots)
           gemm_w(false, OFF_H, kH, T_B, 128, kH, 64, false);              // G1 half 0
           tc::mma_commit(bar_acc);
-          wait_opnd();                                                    // r_h0 -> T_AOP
-          gemm_w(true, T_AOP, 0, T_A, kH, 128, 32, false);                // G2 part 0
+          wait_opnd();                                                    // r_h0 -> T_AOP0
           gemm_w(false, OFF_H, kH, T_B, 128, kH, 64, false);              // G1 half 1
           tc::mma_commit(bar_acc);
+          gemm_w(true, T_AOP0, 0, T_A, kH, 128, 32, false);               // G2 part 0
           wait_opnd();                                                    // r_h1 -> T_AOP
           gemm_w(true, T_AOP, 0, T_A, kH, 128, 32, true);                 // G2 part 1
           tc::mma_commit(bar_acc);
@@ -625,7 +628,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
       if (!rowwise) continue;
       for (int rb = 0; rb < NR; ++rb) {
         wait_on(bar_acc, ph_acc);
-        epi_relu_to_tmem(tl, T_B, lo_of(128), hi_of(128), vs + a.ra[rb], T_AOP);
+        epi_relu_to_tmem(tl, T_B, lo_of(128), hi_of(128), vs + a.ra[rb], T_AOP0);
         signal();
         wait_on(bar_acc, ph_acc);
         epi_relu_to_tmem(tl, T_B, lo_of(128), hi_of(128), vs + a.ra[rb] + 128, T_AOP);
@@ -754,10 +757,10 @@ static std::vector<PackChunk> build_schedule(const tlp_ctx* ctx) {
     }
   }
   for (int r = 0; r < c.n_res; ++r) {
-    for (int k0 = 0; k0 < kH; k0 += 64) add(128, 64, k0, kH, {{0, o.Wa[r], kH, 0}});
-    for (int k0 = 0; k0 < 128; k0 += 32) add(256, 32, k0, kH, {{0, o.Wb[r], kH, 0}});
-    for (int k0 = 0; k0 < kH; k0 += 64) add(128, 64, k0, kH, {{0, o.Wa[r], kH, 128}});
-    for (int k0 = 128; k0 < kH; k0 += 32) add(256, 32, k0, kH, {{0, o.Wb[r], kH, 0}});
+    for (int k0 = 0; k0 < kH; k0 += 64) add(128, 64, k0, kH, {{0, o.Wa[r], kH, 0}});    // G1 half 0
+    for (int k0 = 0; k0 < kH; k0 += 64) add(128, 64, k0, kH, {{0, o.Wa[r], kH, 128}});  // G1 half 1
+    for (int k0 = 0; k0 < 128; k0 += 32) add(256, 32, k0, kH, {{0, o.Wb[r], kH, 0}});   // G2 part 0
+    for (int k0 = 128; k0 < kH; k0 += 32) add(256, 32, k0, kH, {{0, o.Wb[r], kH, 0}});  // G2 part 1
   }
   for (int t = 0; t < c.n_tasks; ++t)
     for (int k0 = 0; k0 < kH; k0 += 64) add(kHD, 64, k0, kH, {{0, o.W1[t], kHD, 0}});
