@@ -1,6 +1,8 @@
 """Small end-to-end run of every kernel for compute-sanitizer (memcheck /
-racecheck / synccheck):  encode -> score (fp32 + bf16 fused) -> top-k ->
-labels -> LambdaRank train step (fp32 and bf16 contexts) -> top-k merge."""
+racecheck / synccheck): encode -> score (fp32 + bf16 fused, with and without the
+padding mask / positional table) -> top-k -> labels -> train steps (LambdaRank
+and MSE; fp32 and bf16 contexts, incl. the B-image and wgrad GEMMs) -> top-k
+merge -> tlp_search_round -> tlp_dedup -> tlp_topk_score."""
 import os
 import sys
 
@@ -18,18 +20,33 @@ names = sorted(tokens, key=tokens.get)
 b = synth.generate(3, 23)
 off = np.array([0, 7, 15, 23], np.int64)
 lat = torch.from_numpy(synth.latencies(b, off, 1).astype(np.float32)).cuda()
-for prec, cfg in (("fp32", OM.Config(hidden=64, up_dims=(32, 64), head_dim=32)),
-                  ("bf16", OM.Config(n_attn=2, n_tasks=2))):
+cases = [("fp32", OM.Config(hidden=64, up_dims=(32, 64), head_dim=32), {}),
+         ("bf16", OM.Config(n_attn=2, n_tasks=2), {}),
+         ("bf16", OM.Config(n_attn=1, n_tasks=1, attn_mask=True, pos_enc=True), {"loss": "mse"})]
+for prec, cfg, extra in cases:
     m = tp.TLP(tp.TLPConfig(hidden=cfg.hidden, up_dims=cfg.up_dims, head_dim=cfg.head_dim,
-                            n_attn=cfg.n_attn, n_tasks=cfg.n_tasks, precision=prec))
+                            n_attn=cfg.n_attn, n_tasks=cfg.n_tasks, precision=prec,
+                            attn_mask=cfg.attn_mask, pos_enc=cfg.pos_enc, **extra))
     m.set_token_table(names)
     m.set_norm_scales(np.full(22, 8.0, np.float32))
     m.set_params(np.concatenate([v.ravel() for v in synth.init_params(1, OM.param_shapes(cfg))]).astype(np.float32))
-    X = m.encode(tp.DeviceBatch.from_packed(b))
+    db = tp.DeviceBatch.from_packed(b)
+    X = m.encode(db)
     s = m.score(X)
     idx, val = m.topk(s, off, 4)
     y = m.normalize_labels(lat, off).view(-1, 1).repeat(1, cfg.n_tasks).contiguous()
     m.train_step(X, y, off)
     m.topk_merge(torch.stack([val, val]), torch.stack([idx, idx]))
+    if prec == "bf16":
+        m.search_round(tp.DeviceBatch.from_packed(b, pin=True), off, 4, chunks=3)
+    m.dedup(X, off, y[:, 0].contiguous())
+    m.topk_score(s, lat, off, [1.0, 2.0, 1.0], 2)
     m.sync()
+# the training GEMM variants at their real shapes (N = 256 tiles, 256 x 256 wgrad)
+big = tp.TLP(tp.TLPConfig(n_attn=1))
+big.set_params(np.concatenate([v.ravel() for v in synth.init_params(2, OM.param_shapes(OM.Config()))]).astype(np.float32))
+Xb = torch.rand((64, 25, 22), device="cuda")
+yb = torch.rand((64, 1), device="cuda") + 0.01
+big.train_step(Xb, yb, np.array([0, 32, 64], np.int64))
+big.sync()
 print("sanitize smoke ok")
