@@ -1,0 +1,300 @@
+// Attention core of the TRAINING path of TLP_PREC_BF16 contexts on the tensor
+// cores: warp-level mma.sync m16n8k8 tf32 (fp32 accumulate), one warp per
+// (candidate, head), d_h = 32, L <= 32 (padded to 32).  Same contract as the
+// fp32 SIMT kernels of k_simt.cu (P:295 / SURVEY §8(a) a4; R14 scale 1/sqrt(d_h);
+// R42 optional padding-key mask); the fp32 context keeps the SIMT kernels (the
+// 1e-5 path).  Operands are split "3xTF32" (x = hi + lo, both tf32; A.B ~=
+// Ah.Bh + Ah.Bl + Al.Bh, ~2^-21 relative): plain tf32 is NOT enough here --
+// dS = A (dA - rowdot) cancels to ~1e-3 of |dA| at the paper's initial scale and
+// the Wq / Wk gradients are ~1e-3 of the Wv one (measured: 53% error on Wk).
+//
+// forward:  S = Q K^T (32 MMAs), masked softmax in registers, A (probabilities,
+//           fp32) saved for the backward, O = A V (32 MMAs; A re-read from smem
+//           in the A-fragment layout)
+// backward: dA = dO V^T, rowdot = sum_m dA A, dS = A (dA - rowdot);
+//           dQ = dS K / sqrt(d_h), dK = dS^T Q / sqrt(d_h), dV = A^T dO
+//           (5 x 32 MMAs; transposed operands are read from smem by index)
+// Operands staged in smem as fp32 [32][36] (row stride 36 floats: the fragment
+// reads (4g + tig) mod 32 are bank-conflict free).
+#include "tlp_internal.cuh"
+
+namespace {
+
+constexpr int DH = 32, LP = 32, LD = 36;
+constexpr int MAT = LP * LD;  // floats per staged matrix
+
+__device__ __forceinline__ uint32_t tf32(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return r;
+}
+
+// x = hi + lo with hi = tf32(x), lo = tf32(x - hi)  ("3xTF32")
+__device__ __forceinline__ void split(float x, uint32_t& hi, uint32_t& lo) {
+  hi = tf32(x);
+  lo = tf32(x - __uint_as_float(hi));
+}
+
+// D (+)= A B: m16n8k8, A row-major tf32, B col-major tf32, fp32 accumulate
+__device__ __forceinline__ void mma_tf32(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
+                                         uint32_t a3, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+// C[32 x 32] = op(X) op(Y): for every (m-tile, n-tile) of 16 x 8, k over 32.
+//   A element (row i, k) = TA ? X[k][i] : X[i][k];  B element (k, col j) = TB ? Y[j][k] : Y[k][j]
+template <bool TA, bool TB>
+__device__ __forceinline__ void gemm32(const float* X, const float* Y, float (&c)[2][4][4], int lane) {
+  const int g = lane >> 2, t = lane & 3;
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) c[mt][nt][i] = 0.f;
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks) {
+    const int k0 = 8 * ks + t, k1 = k0 + 4;
+    uint32_t ah[2][4], al[2][4];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      const int r0 = 16 * mt + g, r1 = r0 + 8;
+      split(TA ? X[k0 * LD + r0] : X[r0 * LD + k0], ah[mt][0], al[mt][0]);
+      split(TA ? X[k0 * LD + r1] : X[r1 * LD + k0], ah[mt][1], al[mt][1]);
+      split(TA ? X[k1 * LD + r0] : X[r0 * LD + k1], ah[mt][2], al[mt][2]);
+      split(TA ? X[k1 * LD + r1] : X[r1 * LD + k1], ah[mt][3], al[mt][3]);
+    }
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+      const int j = 8 * nt + g;
+      uint32_t bh0, bl0, bh1, bl1;
+      split(TB ? Y[j * LD + k0] : Y[k0 * LD + j], bh0, bl0);
+      split(TB ? Y[j * LD + k1] : Y[k1 * LD + j], bh1, bl1);
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        mma_tf32(c[mt][nt], al[mt][0], al[mt][1], al[mt][2], al[mt][3], bh0, bh1);
+        mma_tf32(c[mt][nt], ah[mt][0], ah[mt][1], ah[mt][2], ah[mt][3], bl0, bl1);
+        mma_tf32(c[mt][nt], ah[mt][0], ah[mt][1], ah[mt][2], ah[mt][3], bh0, bh1);
+      }
+    }
+  }
+}
+
+// stage rows [0, L) of a [*, ld] fp32 matrix slice (32 columns from col0), zero pad
+__device__ __forceinline__ void stage(float* dst, const float* src, int64_t ld, int L, int lane) {
+  for (int e = lane; e < LP * DH; e += 32) {
+    const int m = e / DH, d = e % DH;
+    dst[m * LD + d] = m < L ? src[(int64_t)m * ld + d] : 0.f;
+  }
+}
+
+__global__ void __launch_bounds__(128) attn_fwd_tc_kernel(const float* __restrict__ QKV, int L, int H,
+                                                          int nh, int64_t pairs, float* __restrict__ O,
+                                                          float* __restrict__ Asave,
+                                                          const float* __restrict__ kvalid) {
+  extern __shared__ float sm[];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t pair = (int64_t)blockIdx.x * (blockDim.x >> 5) + w;
+  if (pair >= pairs) return;
+  float* Qs = sm + w * 3 * MAT;
+  float* Ks = Qs + MAT;
+  float* Vs = Ks + MAT;  // reused for P after S
+  const int64_t n = pair / nh;
+  const int hd = (int)(pair % nh);
+  const int64_t row0 = n * L, ld = 3 * (int64_t)H;
+  stage(Qs, QKV + row0 * ld + hd * DH, ld, L, lane);
+  stage(Ks, QKV + row0 * ld + H + hd * DH, ld, L, lane);
+  stage(Vs, QKV + row0 * ld + 2 * H + hd * DH, ld, L, lane);
+  __syncwarp();
+  float c[2][4][4];
+  gemm32<false, true>(Qs, Ks, c, lane);  // S = Q K^T
+  const int g = lane >> 2, t = lane & 3;
+  const float scale = 1.0f / sqrtf((float)DH);
+  // key validity for this thread's 8 key columns (2 per n-tile)
+  bool kv[4][2];
+#pragma unroll
+  for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int m = 8 * nt + 2 * t + e;
+      kv[nt][e] = m < L && (!kvalid || kvalid[row0 + m] != 0.f);
+    }
+  float* Ps = Ks;  // K no longer needed: A [32][36] goes here (rows l, cols m)
+  __syncwarp();
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      const int l = 16 * mt + g + 8 * half;
+      float mx = -INFINITY;
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+          if (kv[nt][e]) mx = fmaxf(mx, c[mt][nt][2 * half + e] * scale);
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+      const bool none = mx == -INFINITY;  // no valid key (not produced by tlp_encode): uniform
+      float sum = 0.f;
+      float p[4][2];
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int m = 8 * nt + 2 * t + e;
+          p[nt][e] = none ? (m < L ? 1.f : 0.f)
+                          : (kv[nt][e] ? expf(c[mt][nt][2 * half + e] * scale - mx) : 0.f);
+          sum += p[nt][e];
+        }
+      sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+      sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+      const float inv = 1.0f / sum;
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int m = 8 * nt + 2 * t + e;
+          const float a = l < L ? p[nt][e] * inv : 0.f;
+          Ps[l * LD + m] = a;
+          if (Asave && l < L && m < L) Asave[((n * nh + hd) * L + l) * (int64_t)L + m] = a;
+        }
+    }
+  __syncwarp();
+  gemm32<false, false>(Ps, Vs, c, lane);  // O = A V
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      const int l = 16 * mt + g + 8 * half;
+      if (l >= L) continue;
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+        *reinterpret_cast<float2*>(O + (row0 + l) * H + hd * DH + 8 * nt + 2 * t) =
+            make_float2(c[mt][nt][2 * half], c[mt][nt][2 * half + 1]);
+    }
+}
+
+__global__ void __launch_bounds__(64) attn_bwd_tc_kernel(const float* __restrict__ QKV,
+                                                         const float* __restrict__ Asave,
+                                                         const float* __restrict__ dO, int L, int H,
+                                                         int nh, int64_t pairs, float* __restrict__ dQKV) {
+  extern __shared__ float sm[];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t pair = (int64_t)blockIdx.x * (blockDim.x >> 5) + w;
+  if (pair >= pairs) return;
+  float* Qs = sm + w * 6 * MAT;  // Q, K, V, dO, A, dS
+  float* Ks = Qs + MAT;
+  float* Vs = Ks + MAT;
+  float* dOs = Vs + MAT;
+  float* As = dOs + MAT;  // A, then dS in place
+  const int64_t n = pair / nh;
+  const int hd = (int)(pair % nh);
+  const int64_t row0 = n * L, ld = 3 * (int64_t)H;
+  stage(Qs, QKV + row0 * ld + hd * DH, ld, L, lane);
+  stage(Ks, QKV + row0 * ld + H + hd * DH, ld, L, lane);
+  stage(Vs, QKV + row0 * ld + 2 * H + hd * DH, ld, L, lane);
+  stage(dOs, dO + row0 * H + hd * DH, H, L, lane);
+  const float* Ab = Asave + (n * nh + hd) * (int64_t)L * L;
+  for (int e = lane; e < LP * LP; e += 32) {
+    const int l = e / LP, m = e % LP;
+    As[l * LD + m] = (l < L && m < L) ? Ab[l * L + m] : 0.f;
+  }
+  __syncwarp();
+  const int g = lane >> 2, t = lane & 3;
+  float c[2][4][4];
+  gemm32<false, true>(dOs, Vs, c, lane);  // dA = dO V^T
+  // dS = A (dA - rowdot), rowdot_l = sum_m dA[l,m] A[l,m]
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      const int l = 16 * mt + g + 8 * half;
+      float rd = 0.f;
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) rd += c[mt][nt][2 * half + e] * As[l * LD + 8 * nt + 2 * t + e];
+      rd += __shfl_xor_sync(0xffffffffu, rd, 1);
+      rd += __shfl_xor_sync(0xffffffffu, rd, 2);
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) c[mt][nt][2 * half + e] = As[l * LD + 8 * nt + 2 * t + e] * (c[mt][nt][2 * half + e] - rd);
+    }
+  float* dSs = Qs + 5 * MAT;
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      const int l = 16 * mt + g + 8 * half;
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+        *reinterpret_cast<float2*>(dSs + l * LD + 8 * nt + 2 * t) = make_float2(c[mt][nt][2 * half], c[mt][nt][2 * half + 1]);
+    }
+  __syncwarp();
+  const float scale = 1.0f / sqrtf((float)DH);
+  auto store = [&](const float (&cc)[2][4][4], int64_t col, float f) {
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        const int r = 16 * mt + g + 8 * half;
+        if (r >= L) continue;
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt)
+          *reinterpret_cast<float2*>(dQKV + (row0 + r) * ld + col + 8 * nt + 2 * t) =
+              make_float2(cc[mt][nt][2 * half] * f, cc[mt][nt][2 * half + 1] * f);
+      }
+  };
+  gemm32<false, false>(dSs, Ks, c, lane);  // dQ = dS K
+  store(c, hd * DH, scale);
+  gemm32<true, false>(dSs, Qs, c, lane);   // dK = dS^T Q
+  store(c, H + hd * DH, scale);
+  gemm32<true, false>(As, dOs, c, lane);   // dV = A^T dO
+  store(c, 2 * H + hd * DH, 1.f);
+}
+
+}  // namespace
+
+bool attn_tc_ok(const tlp_ctx* ctx) {
+  return ctx->cfg.precision == TLP_PREC_BF16 && ctx->cfg.hidden / ctx->cfg.attn_heads == DH &&
+         ctx->cfg.L <= LP;
+}
+
+tlp_status attn_fwd_tc(tlp_ctx* ctx, const float* qkv, int64_t N, float* O, float* A,
+                       const float* kvalid, cudaStream_t s) {
+  const tlp_config& c = ctx->cfg;
+  const int64_t pairs = N * c.attn_heads;
+  const int warps = 4;
+  const size_t smem = (size_t)warps * 3 * MAT * sizeof(float);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(attn_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  attn_fwd_tc_kernel<<<(unsigned)cdiv(pairs, warps), warps * 32, smem, s>>>(qkv, c.L, c.hidden,
+                                                                           c.attn_heads, pairs, O, A, kvalid);
+  TLP_LAUNCH_CHECK();
+  return TLP_OK;
+}
+
+tlp_status attn_bwd_tc(tlp_ctx* ctx, const float* qkv, const float* A, const float* dO, int64_t N,
+                       float* dqkv, cudaStream_t s) {
+  const tlp_config& c = ctx->cfg;
+  const int64_t pairs = N * c.attn_heads;
+  const int warps = 2;
+  const size_t smem = (size_t)warps * 6 * MAT * sizeof(float);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(attn_bwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  attn_bwd_tc_kernel<<<(unsigned)cdiv(pairs, warps), warps * 32, smem, s>>>(qkv, A, dO, c.L, c.hidden,
+                                                                           c.attn_heads, pairs, dqkv);
+  TLP_LAUNCH_CHECK();
+  return TLP_OK;
+}

@@ -506,6 +506,7 @@ tlp_status launch_attn_bwd(tlp_ctx* ctx, const float* qkv, const float* A, const
 
 tlp_status attn_fwd(tlp_ctx* ctx, const float* qkv, int64_t N, float* O, float* A,
                     const float* kvalid, cudaStream_t s) {
+  if (attn_tc_ok(ctx)) return attn_fwd_tc(ctx, qkv, N, O, A, kvalid, s);  // bf16 ctx: tensor cores
   switch (ctx->cfg.hidden / ctx->cfg.attn_heads) {
     case 8: return launch_attn_fwd<8>(ctx, qkv, N, O, A, kvalid, s);
     case 16: return launch_attn_fwd<16>(ctx, qkv, N, O, A, kvalid, s);
@@ -517,6 +518,7 @@ tlp_status attn_fwd(tlp_ctx* ctx, const float* qkv, int64_t N, float* O, float* 
 
 tlp_status attn_bwd(tlp_ctx* ctx, const float* qkv, const float* A, const float* dO, int64_t N,
                     float* dqkv, cudaStream_t s) {
+  if (attn_tc_ok(ctx)) return attn_bwd_tc(ctx, qkv, A, dO, N, dqkv, s);  // bf16 ctx: tensor cores
   switch (ctx->cfg.hidden / ctx->cfg.attn_heads) {
     case 8: return launch_attn_bwd<8>(ctx, qkv, A, dO, N, dqkv, s);
     case 16: return launch_attn_bwd<16>(ctx, qkv, A, dO, N, dqkv, s);

@@ -185,6 +185,12 @@ tlp_status tc_gemm(tlp_ctx* ctx, bool ta, bool tb, int64_t M, int64_t N, int64_t
                    const float* A, int64_t lda, const float* B, int64_t ldb, float* C,
                    int64_t ldc, const EpiParams& e, int splits, int64_t kslice, cudaStream_t s);
 
+// k_attn_tc.cu: tf32 mma.sync attention core of bf16-context training (d_h = 32)
+bool attn_tc_ok(const tlp_ctx* ctx);
+tlp_status attn_fwd_tc(tlp_ctx* ctx, const float* qkv, int64_t N, float* O, float* A,
+                       const float* kvalid, cudaStream_t s);
+tlp_status attn_bwd_tc(tlp_ctx* ctx, const float* qkv, const float* A, const float* dO, int64_t N,
+                       float* dqkv, cudaStream_t s);
 // k_rank.cu: MSE (NEXT-3): present-label counts per task, then loss + dscores
 tlp_status mse_counts(tlp_ctx* ctx, const float* labels, int64_t B, double* d_counts, cudaStream_t s);
 tlp_status mse_loss_grad(tlp_ctx* ctx, const float* scores, const float* labels, int64_t B,

@@ -423,6 +423,39 @@ def test_grads_parity_pos_enc(tp, tokscale, precision, tol):
     assert not bad, bad
 
 
+@pytest.mark.parametrize("mask", [False, True])
+def test_grads_parity_bf16_paper_shape(tp, tokscale, mask):
+    """bf16 context at the paper shape (d_h = 32): the training attention core
+    runs on the tensor cores (tf32 mma.sync, k_attn_tc.cu), the dense layers on
+    tcgen05 (bf16x3); the whole gradient against the fp64 oracle at 1e-2."""
+    tokens, scale = tokscale
+    ocfg = oracle_cfg(n_attn=1)
+    ocfg.attn_mask = mask
+    X, y, off = train_inputs(tokens, scale, 1, sizes=(9, 16, 12, 16, 11, 7))
+    for seed in range(50, 90):  # within-group score gaps > 2e-4 (R26)
+        flat = flat_params(ocfg, seed=seed)
+        p = OM.unflatten(ocfg, flat)
+        s_ref, acts = OM.forward(ocfg, p, X, save=True)
+        if min_rel_gap(s_ref, off) > 2e-4:
+            break
+    loss_ref, g = OLR.mtl_lambdarank(s_ref, y.astype(np.float64), off)
+    grads_ref = OM.backward(ocfg, p, acts, g)
+    m = tp.TLP(product_cfg(ocfg, "bf16"))
+    m.set_params(flat.astype(np.float32))
+    loss = m.compute_grads(torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda(), off)
+    m.sync()
+    assert abs(float(loss.cpu()) - loss_ref) <= 1e-2 * abs(loss_ref)
+    got = OM.unflatten(ocfg, m.get_grads().astype(np.float64))
+    bad = {}
+    for name, _ in OM.param_shapes(ocfg):
+        if ZERO_GRAD.search(name) or CANCEL_GRAD.search(name):
+            continue
+        e = rel_err(got[name], grads_ref[name])
+        if e > 1e-2:
+            bad[name] = e
+    assert not bad, bad
+
+
 def test_finetune_from_checkpoint(tp, tokscale):
     """NEXT-3 fine-tuning (P:518 transfer): parameters saved from one ctx
     (tlp_get_params) and loaded into a fresh ctx (tlp_set_params) continue
