@@ -84,12 +84,22 @@ __device__ __forceinline__ void gemm32(const float* X, const float* Y, float (&c
   }
 }
 
-// stage rows [0, L) of a [*, ld] fp32 matrix slice (32 columns from col0), zero pad
+// stage rows [0, L) of a [*, ld] fp32 matrix slice (32 columns), zero pad:
+// 16-byte cp.async (all eight chunks of every row in flight at once; rows of
+// the QKV / dO buffers are 16-byte aligned), zero-fill for the pad rows
 __device__ __forceinline__ void stage(float* dst, const float* src, int64_t ld, int L, int lane) {
-  for (int e = lane; e < LP * DH; e += 32) {
-    const int m = e / DH, d = e % DH;
-    dst[m * LD + d] = m < L ? src[(int64_t)m * ld + d] : 0.f;
+#pragma unroll
+  for (int i = 0; i < LP * DH / 4 / 32; ++i) {
+    const int e = lane + 32 * i, m = e >> 3, c = (e & 7) * 4;
+    const float* g = src + (int64_t)(m < L ? m : 0) * ld + c;
+    const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(dst + m * LD + c));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(g), "r"(m < L ? 16 : 0)
+                 : "memory");
   }
+}
+__device__ __forceinline__ void stage_wait() {
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncwarp();
 }
 
 __global__ void __launch_bounds__(128) attn_fwd_tc_kernel(const float* __restrict__ QKV, int L, int H,
@@ -109,7 +119,7 @@ __global__ void __launch_bounds__(128) attn_fwd_tc_kernel(const float* __restric
   stage(Qs, QKV + row0 * ld + hd * DH, ld, L, lane);
   stage(Ks, QKV + row0 * ld + H + hd * DH, ld, L, lane);
   stage(Vs, QKV + row0 * ld + 2 * H + hd * DH, ld, L, lane);
-  __syncwarp();
+  stage_wait();
   float c[2][4][4];
   gemm32<false, true>(Qs, Ks, c, lane);  // S = Q K^T
   const int g = lane >> 2, t = lane & 3;
@@ -203,7 +213,7 @@ __global__ void __launch_bounds__(64) attn_bwd_tc_kernel(const float* __restrict
     const int l = e / LP, m = e % LP;
     As[l * LD + m] = (l < L && m < L) ? Ab[l * L + m] : 0.f;
   }
-  __syncwarp();
+  stage_wait();
   const int g = lane >> 2, t = lane & 3;
   float c[2][4][4];
   gemm32<false, true>(dOs, Vs, c, lane);  // dA = dO V^T
