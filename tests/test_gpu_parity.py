@@ -734,3 +734,53 @@ def test_search_round_errors(tp, tokscale):
     idx, _ = m.search_round(hb, off, 4)  # the ctx is still usable after the refusals
     m.sync()
     assert (idx.numpy()[:, :4] >= 0).all()
+
+
+# ---------------------------------------------------------------- edge cases
+def test_empty_and_single_candidate(tp, tokscale):
+    """N = 0 is a no-op for encode / score / top-k (segments empty -> padding);
+    N = 1 scores like the oracle on both paths (one ragged tile)."""
+    tokens, scale = tokscale
+    ocfg = oracle_cfg(n_attn=2)
+    flat = flat_params(ocfg, seed=61)
+    for prec, tol in (("fp32", 1e-5), ("bf16", 1e-2)):
+        m = tp.TLP(product_cfg(ocfg, prec))
+        m.set_token_table(sorted(tokens, key=tokens.get))
+        m.set_norm_scales(scale)
+        m.set_params(flat.astype(np.float32))
+        empty = torch.empty((0, 25, 22), device="cuda")
+        s0 = m.score(empty)
+        assert s0.shape == (0, 1)
+        idx, val = m.topk(s0, np.array([0, 0], np.int64), 4)
+        m.sync()
+        assert (idx.cpu().numpy() == -1).all() and np.isneginf(val.cpu().numpy()).all()
+        b, X = encoded_batch(62, 1, tokens, scale)
+        Xd = m.encode(tp.DeviceBatch.from_packed(b))
+        assert np.array_equal(Xd.cpu().numpy().view(np.uint32), X.view(np.uint32))
+        s1 = m.score(Xd)
+        m.sync()
+        assert rel_err(s1.cpu().numpy(), OM.forward(ocfg, OM.unflatten(ocfg, flat), X)) <= tol
+
+
+def test_crop_boundaries_bit_exact(tp, tokscale):
+    """Sequences of exactly 24 / 25 / 26 / 54 primitives and primitives with
+    exactly 10 / 11 / 12 arguments: the crop boundaries of R4 (rows >= 25 and
+    argument slots >= 11 are dropped) are bit-exact against the oracle."""
+    tokens, scale = tokscale
+    b = synth.generate(63, 400)
+    seqs = b.to_lists()
+    lens = np.array([len(sq) for sq in seqs])
+    picked = [int(np.flatnonzero(lens == k)[0]) for k in (24, 25, 26) if (lens == k).any()]
+    picked += [int(np.argmax(lens))]
+    nargs = [max(len(p[1]) for p in sq) for sq in seqs]
+    for k in (10, 11, 12):
+        hits = [i for i, a in enumerate(nargs) if a == k]
+        if hits:
+            picked.append(hits[0])
+    sub = [seqs[i] for i in picked]
+    assert max(lens[picked]) > 25 and any(nargs[i] > 11 for i in picked)
+    ref = oracle.encode(sub, tokens, scale)
+    m = make_encoder(tp, tokens, scale)
+    X = m.encode(tp.DeviceBatch.from_packed(synth.pack(sub)))
+    m.sync()
+    assert np.array_equal(X.cpu().numpy().view(np.uint32), ref.view(np.uint32))
