@@ -97,7 +97,78 @@ probe(const float* A, const float* B, float* D, int N, int mode) {
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256) : "memory");
 }
 
+// timing: the leader issues `iters` back-to-back MMAs (M = 256, N, K = 16 each)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
+rate(int N, int iters, long long* out, int a_tmem) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint32_t tptr;
+  __shared__ __align__(8) uint64_t bar;
+  const uint32_t rank = cta_rank();
+  const int warp = threadIdx.x >> 5;
+  const uint32_t sb = tc::smem_u32(smem);
+  for (int e = threadIdx.x; e < (128 * K * 2 + 128 * K * 2) / 16; e += 128)
+    reinterpret_cast<uint4*>(smem)[e] = make_uint4(0x3f803f80u, 0, 0x3f803f80u, 0);
+  if (threadIdx.x == 0) { tc::mbar_init(tc::smem_u32(&bar), 1); tc::fence_barrier_init(); }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tc::smem_u32(&tptr)), "r"(512) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc::fence_proxy_async_smem();
+  tc::tc_fence_before();
+  cluster_sync();
+  tc::tc_fence_after();
+  const uint32_t tmem = tptr;
+  if (rank == 0 && threadIdx.x == 0) {
+    const uint32_t idesc = tc::idesc_bf16(256, N);
+    const long long t0 = clock64();
+    for (int i = 0; i < iters; ++i) {
+      const int ks = i & 3;
+      const uint64_t bd = tc::smem_desc(sb + 128 * K * 2 + ks * 2 * 128, 128, K * 16);
+      if (a_tmem) {
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                     "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem + 256),
+                     "r"(tmem + 384 + ks * 8), "l"(bd), "r"(idesc), "r"((uint32_t)(i > 0)) : "memory");
+      } else {
+        const uint64_t ad = tc::smem_desc(sb + ks * 2 * 128, 128, K * 16);
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                     "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+                     "l"(ad), "l"(bd), "r"(idesc), "r"((uint32_t)(i > 0)) : "memory");
+      }
+    }
+    const uint16_t mask = 0x3;
+    asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+                 ::"r"(tc::smem_u32(&bar)), "h"(mask) : "memory");
+    tc::mbar_wait(tc::smem_u32(&bar), 0);
+    out[blockIdx.x / 2] = clock64() - t0;
+  } else {
+    tc::mbar_wait(tc::smem_u32(&bar), 0);
+  }
+  tc::tc_fence_before();
+  cluster_sync();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
+}
+
 int main() {
+  {
+    long long* out;
+    cudaMalloc(&out, 148 * sizeof(long long));
+    const int smem = 128 * K * 2 * 2;
+    cudaFuncSetAttribute(rate, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    for (int a_tmem : {0, 1})
+      for (int N : {96, 128, 192, 256}) {
+        const int iters = 4096;
+        rate<<<148, 128, smem>>>(N, iters, out, a_tmem);
+        rate<<<148, 128, smem>>>(N, iters, out, a_tmem);
+        cudaError_t e = cudaDeviceSynchronize();
+        long long h[74];
+        cudaMemcpy(h, out, sizeof(h), cudaMemcpyDeviceToHost);
+        long long mx = 0;
+        for (int i = 0; i < 74; ++i) mx = h[i] > mx ? h[i] : mx;
+        printf("cta_group::2 A=%s N=%3d: %.1f cycles per M=256 MMA (= %.1f per SM-tile of 128 rows) %s\n",
+               a_tmem ? "tmem" : "smem", N, (double)mx / iters, (double)mx / iters / 2, cudaGetErrorString(e));
+      }
+  }
   for (int mode : {0, 1})
     for (int N : {64, 128, 256}) {
       std::vector<float> hA(256 * K), hB(N * K), hD(256 * N, -1.f);
