@@ -67,7 +67,7 @@ constexpr uint32_t OFF_V = OFF_K + kKP * kRowB;     // V_j    [160][32]
 constexpr uint32_t OFF_O = OFF_V + kKP * kRowB;     // O_j    3 x [128 x 32] canonical (A of oproj), j % 3
 constexpr uint32_t OFF_DOT = OFF_O + 3 * 8192;      // 2 x 128 fp32 row dots
 constexpr uint32_t OFF_BAR = OFF_DOT + 1024;        // mbarriers (<= 32)
-constexpr uint32_t OFF_TPTR = OFF_BAR + 256;
+constexpr uint32_t OFF_TPTR = OFF_BAR + 512;
 constexpr uint32_t OFF_KV = OFF_TPTR + 128;         // R42: key-valid byte per tile row (attn_mask)
 constexpr uint32_t OFF_RING = OFF_KV + 128;         // kStages x 16 KB
 constexpr uint32_t OFF_VEC = OFF_RING + kStages * kStageBytes;  // epilogue vectors (fp32)
@@ -334,13 +334,76 @@ __device__ __forceinline__ void attn_unit_mma(uint8_t* smem, uint32_t sbase, uin
   }
 }
 
+// ---- cluster-pair (tcgen05 cta_group::2) helpers: two SMs run one M = 256 MMA
+// per instruction, each holding its own 128-row tile (A) and half of every
+// weight chunk (B split by N at the same SMEM offset); tools/umma2sm_probe.cu
+// verified the operand split and measured the issue rate (M = 256 at the cost
+// of M = 128).
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
+}
+// address of the same SMEM location in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t map_to(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\tWAITC_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAITC_%=;\n\t}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+template <bool PAIR>
+__device__ __forceinline__ void mma_ss(uint32_t d, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t en) {
+  if (PAIR)
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                 "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+                 "l"(ad), "l"(bd), "r"(idesc), "r"(en) : "memory");
+  else
+    tc::mma_bf16(d, ad, bd, idesc, en);
+}
+template <bool PAIR>
+__device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a_tmem, uint64_t bd, uint32_t idesc, uint32_t en) {
+  if (PAIR)
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                 "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+                 "r"(a_tmem), "l"(bd), "r"(idesc), "r"(en) : "memory");
+  else
+    tc::mma_bf16_ta(d, a_tmem, bd, idesc, en);
+}
+// commit: in pair mode the arrival is multicast to the same barrier in both CTAs
+template <bool PAIR>
+__device__ __forceinline__ void commit(uint32_t bar) {
+  if (PAIR)
+    asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+                 ::"r"(bar), "h"((uint16_t)3) : "memory");
+  else
+    tc::mma_commit(bar);
+}
+
+template <bool PAIR>
 __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t sbase = tc::smem_u32(smem);
-  const uint32_t bar_full = sbase + OFF_BAR;             // kStages
-  const uint32_t bar_empty = bar_full + 8 * kStages;     // kStages
-  const uint32_t bar_acc = bar_empty + 8 * kStages;      // generic GEMM done
+  // pair mode: every CTA holds half of each chunk, so the same 64 KB ring has
+  // twice the stages (more weight bytes in flight per MMA-time)
+  constexpr int NS = PAIR ? 2 * kStages : kStages;
+  constexpr uint32_t SB = PAIR ? kStageBytes / 2 : kStageBytes;
+  const uint32_t bar_full = sbase + OFF_BAR;             // [NS]
+  const uint32_t bar_empty = bar_full + 8 * NS;          // [NS]
+  const uint32_t bar_acc = bar_empty + 8 * NS;           // generic GEMM done
   // Attention-phase barriers, indexed so that phase n+1 of a barrier cannot
   // complete before every waiter has observed phase n (a parity wait can never
   // miss a phase): QKV_{j+2} is issued after conv_j is observed, O_{j+4} needs
@@ -349,6 +412,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
   const uint32_t bar_opnd = bar_qkv + 16;                // epilogue -> MMA (kEpi arrivals)
   const uint32_t bar_conv = bar_opnd + 8;                // [2] QKV_j read, TMEM buffer free (j % 2)
   const uint32_t bar_attn = bar_conv + 16;               // [4] O_j ready (j % 4)
+  const uint32_t bar_peer = bar_attn + 32;               // [NS] pair: the peer's half landed
+  const uint32_t rank = PAIR ? cluster_rank() : 0u;      // pair: 0 = leader (issues the MMAs)
+  const uint32_t E = PAIR ? 2u : 1u;                     // epilogue arrivals scale (both CTAs)
   uint32_t* tptr = reinterpret_cast<uint32_t*>(smem + OFF_TPTR);
   float* vs = reinterpret_cast<float*>(smem + OFF_VEC);
 
@@ -358,45 +424,89 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
   for (int i = threadIdx.x; i < a.vec_floats / 4; i += kThreads)
     reinterpret_cast<float4*>(vs)[i] = __ldg(reinterpret_cast<const float4*>(a.vec) + i);
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < NS; ++s) {
       tc::mbar_init(bar_full + 8 * s, 1);
       tc::mbar_init(bar_empty + 8 * s, 1);
     }
     tc::mbar_init(bar_acc, 1);
     tc::mbar_init(bar_qkv, 1);
     tc::mbar_init(bar_qkv + 8, 1);
-    tc::mbar_init(bar_opnd, kEpi);
-    for (int i = 0; i < 2; ++i) tc::mbar_init(bar_conv + 8 * i, kAttn);
-    for (int i = 0; i < 4; ++i) tc::mbar_init(bar_attn + 8 * i, kAttn);
+    tc::mbar_init(bar_opnd, E * kEpi);
+    for (int i = 0; i < 2; ++i) tc::mbar_init(bar_conv + 8 * i, E * kAttn);
+    for (int i = 0; i < 4; ++i) tc::mbar_init(bar_attn + 8 * i, E * kAttn);
+    for (int s = 0; s < NS; ++s) tc::mbar_init(bar_peer + 8 * s, 1);
     tc::fence_barrier_init();
   }
-  if (warp == 1) tc::tmem_alloc(tc::smem_u32(tptr), 512);
+  if (warp == 1) {
+    if (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tc::smem_u32(tptr)),
+                   "r"(512) : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      tc::tmem_alloc(tc::smem_u32(tptr), 512);
+    }
+  }
   tc::fence_proxy_async_smem();
   tc::tc_fence_before();
-  __syncthreads();
+  if (PAIR) cluster_sync_all(); else __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = *tptr;
   const int NA = a.n_attn, NR = a.n_res, NT = a.n_tasks;
+  // tile walk: single CTA -> tiles blockIdx.x + k gridDim.x; pair -> tile pairs
+  // (2 it, 2 it + 1), the CTA of rank r taking 2 it + r (past ntile: an empty tile)
+  const int64_t n_it = PAIR ? (a.ntile + 1) / 2 : a.ntile;
+  const int64_t it0 = PAIR ? blockIdx.x / 2 : blockIdx.x;
+  const int64_t it_step = PAIR ? gridDim.x / 2 : gridDim.x;
+  auto tile_of = [&](int64_t it) -> int64_t { return PAIR ? 2 * it + rank : it; };
+  // epilogue -> MMA arrivals go to the leader's barriers
+  // (warp-uniform call sites: after each lane's fences the warp arrives once
+  // with count 32 -- one remote operation per warp in pair mode)
+  auto arrive_mma = [&](uint32_t bar) {
+    __syncwarp();
+    if (lane == 0) {
+      if (PAIR && rank != 0)
+        asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0], 32;" ::"r"(map_to(bar, 0)) : "memory");
+      else
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], 32;" ::"r"(bar) : "memory");
+    }
+  };
 
   if (warp == 0) {
     // ------------------------------------------------ TMA producer
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int64_t tile = blockIdx.x; tile < a.ntile; tile += gridDim.x) {
+      for (int64_t it = it0; it < n_it; it += it_step) {
         for (int c = 0; c < a.nchunks; ++c) {
           tc::mbar_wait(bar_empty + 8 * stage, phase ^ 1);
           const ChunkRef ch = a.chunks[c];
-          tc::mbar_arrive_expect_tx(bar_full + 8 * stage, ch.bytes);
-          tc::bulk_g2s(sbase + OFF_RING + stage * kStageBytes, a.wstream + (size_t)ch.off16 * 16,
-                       ch.bytes, bar_full + 8 * stage);
-          if (++stage == kStages) { stage = 0; phase ^= 1; }
+          // pair: this CTA's half of the chunk = rows [rank N/2, (rank+1) N/2) of the
+          // canonical K-major B (8-row groups are contiguous: the first half of the bytes)
+          const uint32_t bytes = PAIR ? ch.bytes / 2 : ch.bytes;
+          tc::mbar_arrive_expect_tx(bar_full + 8 * stage, bytes);
+          tc::bulk_g2s(sbase + OFF_RING + stage * SB,
+                       a.wstream + (size_t)ch.off16 * 16 + (PAIR ? rank * bytes : 0u), bytes,
+                       bar_full + 8 * stage);
+          if (++stage == NS) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------ MMA issuer
-    if (lane == 0) {
+    // ------------------------------------------------ MMA issuer (the leader in pair mode)
+    if (PAIR && rank != 0 && lane == 0) {
+      // the peer's idle issuer warp relays: this CTA's half of a stage landed
+      int stage = 0;
+      uint32_t phase = 0;
+      const uint32_t peer_bar0 = map_to(bar_peer, 0);
+      for (int64_t it = it0; it < n_it; it += it_step) {
+        for (int c = 0; c < a.nchunks; ++c) {
+          tc::mbar_wait(bar_full + 8 * stage, phase);
+          mbar_arrive_remote(peer_bar0 + 8 * stage);
+          if (++stage == NS) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+    if (lane == 0 && rank == 0) {
       int stage = 0;
       uint32_t phase = 0, op_phase = 0, cv_phase[2] = {0, 0}, at_phase[4] = {0, 0, 0, 0};
       // diagnostics (a.trace, CTA 0): cycles the issuer spends waiting per tile on
@@ -405,7 +515,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
       long long wt[4] = {0, 0, 0, 0};
       auto timed_wait = [&](int k, uint32_t bar, uint32_t ph) {
         const long long t0 = trc ? clock64() : 0;
-        tc::mbar_wait(bar, ph);
+        if (PAIR) mbar_wait_cluster(bar, ph);  // arrivals include the peer CTA's
+        else tc::mbar_wait(bar, ph);
         if (trc) wt[k] += clock64() - t0;
       };
       auto wait_opnd = [&]() {
@@ -417,77 +528,78 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
       // layout with Kt = a_kt at byte offset a_off) or in TMEM (column a_off).
       auto gemm_w = [&](bool a_tmem, uint32_t a_off, uint32_t a_kt, uint32_t d_col, uint32_t N,
                         int K, int Kc, bool acc) {
-        const uint32_t idesc = tc::idesc_bf16(128, N);
+        const uint32_t idesc = tc::idesc_bf16(PAIR ? 256 : 128, N);
         for (int kc = 0; kc < K; kc += Kc) {
           timed_wait(0, bar_full + 8 * stage, phase);
+          if (PAIR) timed_wait(0, bar_peer + 8 * stage, phase);  // the peer's half
           tc::tc_fence_after();
-          const uint32_t b = sbase + OFF_RING + stage * kStageBytes;
+          const uint32_t b = sbase + OFF_RING + stage * SB;
 #pragma unroll 4
           for (int ks = 0; ks < Kc; ks += 16) {
             const uint64_t bd = tc::smem_desc(b + (ks >> 3) * 128, 128, Kc * 16);
             const uint32_t en = (acc || kc + ks > 0) ? 1u : 0u;
             if (a_tmem)
-              tc::mma_bf16_ta(tmem + d_col, tmem + a_off + ((kc + ks) >> 1), bd, idesc, en);
+              mma_ts<PAIR>(tmem + d_col, tmem + a_off + ((kc + ks) >> 1), bd, idesc, en);
             else
-              tc::mma_bf16(tmem + d_col,
+              mma_ss<PAIR>(tmem + d_col,
                            tc::smem_desc(sbase + a_off + ((kc + ks) >> 3) * 128, 128, a_kt * 16),
                            bd, idesc, en);
           }
-          tc::mma_commit(bar_empty + 8 * stage);
-          if (++stage == kStages) { stage = 0; phase ^= 1; }
+          commit<PAIR>(bar_empty + 8 * stage);
+          if (++stage == NS) { stage = 0; phase ^= 1; }
         }
       };
       int mt = 0;
-      for (int64_t tile = blockIdx.x; tile < a.ntile; tile += gridDim.x, ++mt) {
+      for (int64_t it = it0; it < n_it; it += it_step, ++mt) {
         if (trc && mt < 8) {
           for (int k = 0; k < 4; ++k) wt[k] = 0;
           a.trace[512 + mt * 8 + 4] = clock64();
         }
         wait_opnd();                                                      // E0: X
         gemm_w(false, OFF_X, kKX, T_B, 128, kKX, 32, false);              // up0 -> T_B
-        tc::mma_commit(bar_acc);
+        commit<PAIR>(bar_acc);
         wait_opnd();                                                      // E1: U1 -> T_AOP
         gemm_w(true, T_AOP, 0, T_A, kH, 128, 32, false);                  // up1 -> T_A
-        tc::mma_commit(bar_acc);
+        commit<PAIR>(bar_acc);
         wait_opnd();                                                      // E2: h
         for (int l = 0; l < NA; ++l) {
           gemm_w(false, OFF_H, kH, T_QKV, 96, kH, 64, false);             // QKV_0 -> buf 0
-          tc::mma_commit(bar_qkv);
+          commit<PAIR>(bar_qkv);
           gemm_w(false, OFF_H, kH, T_QKV + 96, 96, kH, 64, false);        // QKV_1 -> buf 1
-          tc::mma_commit(bar_qkv + 8);
+          commit<PAIR>(bar_qkv + 8);
           for (int j = 0; j < kHeads; ++j) {
             if (j + 2 < kHeads) {
               timed_wait(1, bar_conv + 8 * (j & 1), cv_phase[j & 1]);     // QKV_j read: buf j%2 free
               cv_phase[j & 1] ^= 1;
               tc::tc_fence_after();
               gemm_w(false, OFF_H, kH, T_QKV + 96 * (j & 1), 96, kH, 64, false);  // QKV_{j+2}
-              tc::mma_commit(bar_qkv + 8 * (j & 1));
+              commit<PAIR>(bar_qkv + 8 * (j & 1));
             }
             timed_wait(2, bar_attn + 8 * (j & 3), at_phase[j & 3]);       // O_j ready
             at_phase[j & 3] ^= 1;
             tc::tc_fence_after();
             gemm_w(false, OFF_O + 8192 * (j % 3), kDH, T_A, kH, kDH, 32, j > 0);  // acc += O_j Wo_j
           }
-          tc::mma_commit(bar_acc);
+          commit<PAIR>(bar_acc);
           wait_opnd();                                                    // E_resid
         }
         for (int r = 0; r < NR; ++r) {
           // G1 half 1 goes ahead of G2 part 0 so that the epilogue of r_h1 overlaps
           // G2 part 0 (the two r halves live in separate TMEM operand slots)
           gemm_w(false, OFF_H, kH, T_B, 128, kH, 64, false);              // G1 half 0
-          tc::mma_commit(bar_acc);
+          commit<PAIR>(bar_acc);
           wait_opnd();                                                    // r_h0 -> T_AOP0
           gemm_w(false, OFF_H, kH, T_B, 128, kH, 64, false);              // G1 half 1
-          tc::mma_commit(bar_acc);
+          commit<PAIR>(bar_acc);
           gemm_w(true, T_AOP0, 0, T_A, kH, 128, 32, false);               // G2 part 0
           wait_opnd();                                                    // r_h1 -> T_AOP
           gemm_w(true, T_AOP, 0, T_A, kH, 128, 32, true);                 // G2 part 1
-          tc::mma_commit(bar_acc);
+          commit<PAIR>(bar_acc);
           wait_opnd();                                                    // E_resid
         }
         for (int t = 0; t < NT; ++t) {
           gemm_w(false, OFF_H, kH, T_B, kHD, kH, 64, false);              // head t
-          tc::mma_commit(bar_acc);
+          commit<PAIR>(bar_acc);
           if (t < NT - 1) wait_opnd();
         }
         if (trc && mt < 8)
@@ -519,7 +631,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
     auto signal = [&]() {
       tc::fence_proxy_async_smem();
       tc::tc_fence_before();
-      tc::mbar_arrive(bar_opnd);
+      arrive_mma(bar_opnd);
       tr();
     };
     // column split between the quarter's two warps
@@ -530,7 +642,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
     const bool real = r < kCand * kL;
     const float sm_scale = 1.4426950408889634f / sqrtf((float)kDH);  // log2(e)/sqrt(d_h)
 
-    for (int64_t tile = blockIdx.x; tile < a.ntile; tile += gridDim.x, ++titer) {
+    for (int64_t it = it0; it < n_it; it += it_step, ++titer) {
+      const int64_t tile = tile_of(it);
       tev = 0;
       tr();
       const int64_t n = tile * kCand + slot;
@@ -604,7 +717,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
             }
           }
           tc::tc_fence_before();                          // QKV_j read: TMEM buffer j%2 free
-          if (j + 2 < kHeads) tc::mbar_arrive(bar_conv + 8 * (j & 1));
+          if (j + 2 < kHeads) arrive_mma(bar_conv + 8 * (j & 1));
           asm volatile("bar.sync 2, 320;" ::: "memory");  // Q/K/V of head j complete
           if (a.attn_mask) {  // R42: drop padding keys (an all-padding slot keeps every key)
             const uint32_t cand = unit >> 1;
@@ -616,7 +729,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
           }
           tc::fence_proxy_async_smem();                   // O_j ready
           tc::tc_fence_before();
-          tc::mbar_arrive(bar_attn + 8 * (j & 3));
+          arrive_mma(bar_attn + 8 * (j & 3));
           tr();
         }
         if (rowwise) {
@@ -666,10 +779,11 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
     }
   }
   tc::tc_fence_before();
-  __syncthreads();
+  if (PAIR) cluster_sync_all(); else __syncthreads();
   if (warp == 1) {
     tc::tc_fence_after();
-    tc::tmem_dealloc(tmem, 512);
+    if (PAIR) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
+    else tc::tmem_dealloc(tmem, 512);
   }
 }
 
@@ -817,7 +931,9 @@ tlp_status tc_prepare(tlp_ctx* ctx, cudaStream_t s) {
     TLP_CUDA_TRY(cudaMalloc(&w.pack, w.nchunks * sizeof(PackChunk)));
     TLP_CUDA_TRY(cudaMemcpy(w.chunks, refs.data(), w.nchunks * sizeof(ChunkRef), cudaMemcpyHostToDevice));
     TLP_CUDA_TRY(cudaMemcpy(w.pack, w.host.data(), w.nchunks * sizeof(PackChunk), cudaMemcpyHostToDevice));
-    TLP_CUDA_TRY(cudaFuncSetAttribute(tc_forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    TLP_CUDA_TRY(cudaFuncSetAttribute(tc_forward_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)kMaxSmem));
+    TLP_CUDA_TRY(cudaFuncSetAttribute(tc_forward_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)kMaxSmem));
   }
   TcWeights& w = *ctx->tc;
@@ -844,7 +960,15 @@ tlp_status tc_forward(tlp_ctx* ctx, const float* feats, int64_t N, float* scores
   a.pos = ctx->cfg.pos_enc ? w.pos : nullptr;
   a.n_attn = c.n_attn; a.n_res = c.n_res; a.n_tasks = c.n_tasks;
   a.attn_mask = c.attn_mask;
-  const int grid = (int)std::min<int64_t>(a.ntile, ctx->num_sms);
+  // Experimental (TLP_TC_PAIR=1): cluster pairs with tcgen05 cta_group::2 -- one
+  // M = 256 MMA stream per pair of SMs, each SM on its own tile.  Correct (the
+  // parity tests pass in this mode) but slower today: the two tiles advance in
+  // lockstep and the cross-CTA handshakes (peer half of every weight chunk,
+  // epilogue arrivals) leave the issuer waiting ~60% of the time.
+  static const char* pe = getenv("TLP_TC_PAIR");
+  const bool pair = pe && pe[0] == '1' && ctx->num_sms >= 2 && a.ntile >= 2;
+  const int grid = pair ? (int)std::min<int64_t>((a.ntile + 1) / 2, ctx->num_sms / 2) * 2
+                        : (int)std::min<int64_t>(a.ntile, ctx->num_sms);
   // Diagnostics: TLP_TC_TRACE=1 prints CTA 0's epilogue phase timeline (cycles
   // between successive waits/signals) for its first tiles to stderr.
   static const bool trace = getenv("TLP_TC_TRACE") != nullptr;
@@ -854,7 +978,21 @@ tlp_status tc_forward(tlp_ctx* ctx, const float* feats, int64_t N, float* scores
     TLP_CUDA_TRY(cudaMemset(d_trace, 0, 8 * 72 * sizeof(long long)));
   }
   a.trace = d_trace;
-  tc_forward_kernel<<<grid, kThreads, w.smem, s>>>(a);
+  if (pair) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = w.smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    TLP_CUDA_TRY(cudaLaunchKernelEx(&cfg, tc_forward_kernel<true>, a));
+  } else {
+    tc_forward_kernel<false><<<grid, kThreads, w.smem, s>>>(a);
+  }
   TLP_LAUNCH_CHECK();
   if (trace) {
     std::vector<long long> h(8 * 72);
