@@ -27,6 +27,10 @@ Pins (tests/test_oracle_*.py, ``-m "not gpu"``):
   dp         -- R-rank emulation equals the unsharded step.
   dataset    -- (NEXT-2) SPEC duplicate-rate / dedup / top-k-score examples,
                 brute-force pairwise classes, permutation invariance.
+  search     -- (NEXT-1) Philox4x64-10 == numpy's Philox; fitness-proportional
+                selection by enumeration; SPEC genetic-operator properties;
+                cheating model finds the brute-force optimum; constant model
+                == random search; tuner budget / monotonicity invariants.
 """
 from .tokenizer import build_token_table, extract_rows, fit_scales, encode  # noqa: F401
 from .model import Config, param_shapes, unflatten, flatten, forward, backward  # noqa: F401

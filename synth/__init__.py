@@ -303,3 +303,152 @@ def init_params(seed: int, shapes: Sequence[Tuple[str, Tuple[int, ...]]],
         v = rng.uniform(-b, b, shp)
         out.append(bf16_round(v) if bf16 else v)
     return out
+
+
+# ----------------------------------------------------------------------------
+# Search-space templates for the synthetic Ansor-style round driver (SURVEY
+# §8(f) NEXT-1; "SyntheticSubgraph" / "SyntheticOracle").
+# Plumbing only: a template is a fixed skeleton sequence (the "sketch" Ansor
+# derives for a subgraph by predefined rules) whose tunable arguments
+# ("knobs": split factors, annotation enums, pragma strings) each take one
+# value of a small domain.  A candidate is one domain index per knob (a gene
+# vector).  The latency function stands in for the target hardware (P:558
+# "measure the latency"); it is the SPEC's log-linear form with pairwise terms.
+# ----------------------------------------------------------------------------
+
+FACTOR_DOMAIN = tuple(float(2 ** i) for i in range(7))   # split factors 1..64
+ANNOT_DOMAIN = tuple(float(i) for i in range(6))          # annotation enum
+MAX_KNOBS = 64                                            # gene row width cap
+
+
+@dataclass
+class Template:
+    """One subgraph's search space.  ``prims`` is the skeleton in the abstract
+    form [(type, [num | name, ...])]; knob g replaces ``prims[knob_prim[g]]``'s
+    argument ``knob_arg[g]`` by ``domains[g][gene]``."""
+    prims: List[Prim]
+    knob_prim: List[int]
+    knob_arg: List[int]
+    domains: List[Tuple[Arg, ...]]
+
+    @property
+    def G(self) -> int:
+        return len(self.knob_prim)
+
+    def dom_sizes(self) -> np.ndarray:
+        return np.array([len(d) for d in self.domains], np.int64)
+
+    def knob_groups(self) -> np.ndarray:
+        """Ordinal of each knob's primitive among the knob-bearing primitives
+        (the crossover unit: whole primitives)."""
+        order = {p: i for i, p in enumerate(sorted(set(self.knob_prim)))}
+        return np.array([order[p] for p in self.knob_prim], np.int64)
+
+
+def make_template(seed: int, subgraph: int, min_len: int = 12, max_knobs: int = MAX_KNOBS) -> Template:
+    """A seeded TenSet-shaped skeleton whose SP split factors, AN annotations
+    and PR pragma strings are knobs."""
+    rng = np.random.default_rng([seed, subgraph])
+    L = int(np.clip(draw_lengths(rng, 1)[0], min_len, 54))
+    seq = generate(int(rng.integers(0, 2 ** 31)), 1, unseen_rate=0.0, lengths=[L]).to_lists()[0]
+    kp: List[int] = []
+    ka: List[int] = []
+    dom: List[Tuple[Arg, ...]] = []
+    for p, (t, args) in enumerate(seq):
+        slots: List[Tuple[int, Tuple[Arg, ...]]] = []
+        if t == SP:
+            slots = [(i, FACTOR_DOMAIN) for i in range(3, len(args) - 1)]
+        elif t == AN:
+            slots = [(2, ANNOT_DOMAIN)]
+        elif t == PR:
+            slots = [(2, PRAGMAS)]
+        for i, d in slots:
+            if len(kp) < max_knobs:
+                kp.append(p); ka.append(i); dom.append(d)
+    return Template(seq, kp, ka, dom)
+
+
+def small_template(domain_sizes: Sequence[int]) -> Template:
+    """A hand-built template with one SP factor knob per entry (domain = the
+    first ``d`` split factors), e.g. (4, 4, 4) = a 64-point search space."""
+    prims: List[Prim] = [(CHW, [0.0, "local"])]
+    kp, ka, dom = [], [], []
+    for d in domain_sizes:
+        assert 1 <= d <= len(FACTOR_DOMAIN)
+        kp.append(len(prims)); ka.append(3); dom.append(FACTOR_DOMAIN[:d])
+        prims.append((SP, [0.0, 1.0, 64.0, 1.0, 0.0]))
+    prims.append((AN, [0.0, 1.0, 2.0]))
+    return Template(prims, kp, ka, dom)
+
+
+def template_weights(seed: int, subgraph: int, G: int) -> Tuple[float, np.ndarray, np.ndarray]:
+    """(base, w [G], v [G,G] upper-triangular) of the synthetic latency."""
+    rng = np.random.default_rng([seed, subgraph, 7])
+    base = float(10.0 ** rng.uniform(-4, -2))
+    w = rng.normal(0.0, 1.0, G)
+    v = np.triu(rng.normal(0.0, 0.5 / np.sqrt(max(G, 1)), (G, G)), 1)
+    return base, w, v
+
+
+def template_latency(tmpl: Template, genes: np.ndarray, seed: int, subgraph: int) -> np.ndarray:
+    """Synthetic hardware: base * exp(w.g + sum_{j<l} v_jl g_j g_l)
+    with g = gene / (|domain| - 1) in [0, 1].  > 0, deterministic."""
+    genes = np.atleast_2d(np.asarray(genes, np.int64))
+    base, w, v = template_weights(seed, subgraph, tmpl.G)
+    D = tmpl.dom_sizes().astype(np.float64)
+    g = genes[:, :tmpl.G] / np.maximum(D - 1.0, 1.0)
+    return base * np.exp(g @ w + np.einsum("ni,ij,nj->n", g, v, g))
+
+
+@dataclass
+class PackedSpace:
+    """Device layout of ``tlp_ga_space`` (include/tlp.h): S skeletons packed
+    as one batch plus flat knob / domain tables.  Host numpy arrays."""
+    tmpl: PackedBatch
+    knob_off: np.ndarray   # int64 [S+1]
+    knob_arg: np.ndarray   # int64 [K]  global argument index into tmpl's args
+    knob_grp: np.ndarray   # int32 [K]  crossover group within the subgraph
+    dom_off: np.ndarray    # int64 [K+1]
+    dom_num: np.ndarray    # float64 [D]
+    dom_name: np.ndarray   # int32 [D]  string index, -1 for a number
+
+    @property
+    def S(self) -> int:
+        return len(self.knob_off) - 1
+
+    @property
+    def G(self) -> int:
+        return int(np.diff(self.knob_off).max()) if self.S else 0
+
+
+def pack_space(templates: Sequence[Template]) -> PackedSpace:
+    strings: List[str] = []
+    for t in templates:  # every domain string enters the batch string table
+        for d in t.domains:
+            for v in d:
+                if isinstance(v, str) and v not in strings:
+                    strings.append(v)
+    b = pack([t.prims for t in templates])
+    for s in b.strings:
+        if s not in strings:
+            strings.append(s)
+    remap = np.array([strings.index(s) for s in b.strings] or [0], np.int32)
+    arg_name = np.where(b.arg_name >= 0, remap[np.maximum(b.arg_name, 0)], -1).astype(np.int32)
+    b = PackedBatch(b.seq_off, b.prim_type, b.arg_off, b.arg_kind, b.arg_num, arg_name, strings)
+    knob_off = [0]; knob_arg = []; knob_grp = []; dom_off = [0]; dom_num = []; dom_name = []
+    for s, t in enumerate(templates):
+        grp = t.knob_groups()
+        for g in range(t.G):
+            p = int(b.seq_off[s]) + t.knob_prim[g]
+            knob_arg.append(int(b.arg_off[p]) + t.knob_arg[g])
+            knob_grp.append(int(grp[g]))
+            for v in t.domains[g]:
+                if isinstance(v, str):
+                    dom_num.append(0.0); dom_name.append(strings.index(v))
+                else:
+                    dom_num.append(float(v)); dom_name.append(-1)
+            dom_off.append(len(dom_num))
+        knob_off.append(len(knob_arg))
+    return PackedSpace(b, np.asarray(knob_off, np.int64), np.asarray(knob_arg, np.int64),
+                       np.asarray(knob_grp, np.int32), np.asarray(dom_off, np.int64),
+                       np.asarray(dom_num, np.float64), np.asarray(dom_name, np.int32))
