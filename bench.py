@@ -261,6 +261,7 @@ def run_ours(args):
     # --- NEXT-2 rows: duplicate scan of this round's features and
     # the §6.1 top-k score of its scores against synthetic latencies ---
     next_rows = next2_measure(scorer, feats, scores, task_off, args, stream, dev)
+    next_rows.update(next1_measure(scorer, args, stream, rank))
 
     K = args.steps
     cand_s = world * N_ROUND * K / (round_ms / 1e3)
@@ -313,6 +314,49 @@ def run_ours(args):
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+GA_S, GA_POP, GA_CHILD, GA_ITERS = 100, 512, 1920, 4
+
+
+def next1_measure(m, args, stream, rank):
+    """NEXT-1: one device-resident tuning round of 100 synthetic
+    subgraphs (tlp_ga_round): 512 + 1,920 initial programs, then 4 GA
+    iterations of 1,920 children per subgraph = 10,112 programs featurised and
+    scored per subgraph per round ("approximately 10,000 ... for each
+    subgraph in one round"), the paper-size 2-layer bf16 model.  Timed with CUDA
+    events over K rounds after W warm-up rounds; then 3 rounds of the host
+    tuner (round + survivors D2H + 10 synthetic measurements per subgraph,
+    P:558) timed by the host clock around synchronised rounds."""
+    import time
+    import torch
+    from paper_2211_03578_b200.search import Tuner
+    ts = [synth.make_template(2000 + rank, s) for s in range(GA_S)]
+    m.ga_set_space(synth.pack_space(ts))
+    per_round = GA_S * (GA_POP + GA_CHILD + GA_ITERS * GA_CHILD)
+    for r in range(args.warmup):
+        m.ga_round(GA_POP, GA_CHILD, GA_ITERS, 0.5, 0.2, seed=1, rnd=r, stream=stream)
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for r in range(args.steps):
+        m.ga_round(GA_POP, GA_CHILD, GA_ITERS, 0.5, 0.2, seed=1, rnd=100 + r, stream=stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    tuner = Tuner(m, GA_S, [t.G for t in ts], n_pop=GA_POP, n_child=GA_CHILD, iters=GA_ITERS, seed=2)
+    lat = lambda s, g: float(synth.template_latency(ts[s], g, 2000 + rank, s)[0])  # noqa: E731
+    tuner.run_round(0, lat)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for r in range(1, 4):
+        tuner.run_round(r, lat)
+    host_ms = (time.perf_counter() - t0) * 1e3 / 3
+    return {"tune_round": {"value": per_round / (ms / 1e3), "unit": "candidates/s", "ms_per_round": ms,
+                           "candidates_per_round": per_round,
+                           "config": "100 subgraphs x (512 + 1920 + 4 x 1920) programs, 2-layer bf16 model",
+                           "tuner_ms_per_round": host_ms,
+                           "tuner_measurements": tuner.total}}
 
 
 # ------------------------------------------------------------------ oracle arm

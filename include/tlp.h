@@ -281,6 +281,90 @@ tlp_status tlp_topk_score(tlp_ctx* ctx, const float* scores, int32_t score_strid
                           const float* latency, const int64_t* group_off, const double* weight,
                           int32_t G, int32_t k, double* out, void* stream);
 
+/* ---- NEXT-1: the synthetic Ansor-style tuning round --------
+ * P:558 (§6.3): "Ansor will first generate some initial tensor programs for a
+ * subgraph according to predefined rules.  Then use the cost model to pick out
+ * potential tensor programs.  Use these potential tensor programs to generate
+ * more tensor programs through the genetic algorithm and use the cost model
+ * again to prune the poor performers.  This step will iterate multiple times."
+ * "approximately 10,000 schedule primitive sequences ... for each
+ * subgraph in one round".  The genetic operators, the counter-based random
+ * numbers and the pruning follow DESIGN.md readings R44-R48.
+ *
+ * A search space holds S subgraphs.  Subgraph s is a skeleton sequence (one
+ * candidate of `tmpl`) whose tunable arguments ("knobs") take a value from a
+ * small domain; a candidate program is one domain index per knob (its "gene
+ * vector", uint8).  Gene arrays are row-major [rows, G] uint8 with
+ * G = tlp_ga_num_genes(ctx) (the largest knob count, <= 64; unused columns 0);
+ * rows are grouped by subgraph: row s * n + c is candidate c of subgraph s. */
+typedef struct {
+  tlp_seq_batch tmpl;       /* HOST arrays: S skeletons, one candidate per subgraph */
+  int32_t S;                /* subgraphs, >= 1 */
+  const int64_t* knob_off;  /* HOST [S+1]: knobs of subgraph s = [knob_off[s], knob_off[s+1]), <= 64 */
+  const int64_t* knob_arg;  /* HOST [K]: argument index (into tmpl's args) the knob sets, inside
+                               its subgraph's skeleton */
+  const int32_t* knob_grp;  /* HOST [K]: crossover group = ordinal of the knob's primitive among the
+                               subgraph's knob-bearing primitives (0, non-decreasing, steps of <= 1) */
+  const int64_t* dom_off;   /* HOST [K+1]: domain of knob k = entries [dom_off[k], dom_off[k+1]),
+                               1..255 values */
+  const double* dom_num;    /* HOST [D]: numeric value (knob on a Number argument) */
+  const int32_t* dom_name;  /* HOST [D]: string index into tmpl's string table (knob on a NameParam
+                               argument), -1 for numbers; must match the skeleton's arg_kind */
+} tlp_ga_space;
+
+/* Copy a search space into ctx-owned device memory (replaces any previous one).
+ * Validates every offset / index / kind (SHAPE or ARG on violation).  Sync. */
+tlp_status tlp_ga_set_space(tlp_ctx* ctx, const tlp_ga_space* host_space);
+/* Gene row width G of the ctx's space (0 if none set). */
+int32_t tlp_ga_num_genes(const tlp_ctx* ctx);
+/* Total primitives / arguments of n materialised candidates per subgraph
+ * (sizes of tlp_ga_materialize's outputs). */
+tlp_status tlp_ga_batch_size(tlp_ctx* ctx, int64_t n, int64_t* P_out, int64_t* A_out);
+
+/* R45: genes_out [S*n, G] device <- n uniform candidates per subgraph drawn
+ * with Philox4x64-10 (key (seed, 0x544C50), counter (c, s, round<<16, 1<<32|j/4)). */
+tlp_status tlp_ga_init(tlp_ctx* ctx, int32_t n, uint64_t seed, int32_t round, uint8_t* genes_out,
+                       void* stream);
+
+/* R46/R47: child_out [S*n_child, G] device <- children of the survivors
+ * pop [S*n_pop, G] (device, each subgraph's rows in rank order, best first);
+ * pop_scores [S*n_pop] fp32 device: parents come from the finite-score prefix
+ * of each subgraph's survivors.  0 <= p_cross, p_mut <= 1; iter >= 1. */
+tlp_status tlp_ga_evolve(tlp_ctx* ctx, const uint8_t* pop, const float* pop_scores, int32_t n_pop,
+                         int32_t n_child, double p_cross, double p_mut, uint64_t seed,
+                         int32_t round, int32_t iter, uint8_t* child_out, void* stream);
+
+/* The abstract primitive sequences of S*n gene rows (device, grouped by
+ * subgraph, n per subgraph): skeleton s with knob k's argument set to its
+ * domain value.  Outputs are caller-owned device arrays of the tlp_seq_batch
+ * layout sized by tlp_ga_batch_size: seq_off [S*n+1], prim_type [P],
+ * arg_off [P+1], arg_kind [A], arg_num [A], arg_name [A]; the string table is
+ * the space's (str_blob / str_off as passed to tlp_ga_set_space). */
+tlp_status tlp_ga_materialize(tlp_ctx* ctx, const uint8_t* genes, int64_t n, int64_t* seq_off,
+                              uint8_t* prim_type, int64_t* arg_off, uint8_t* arg_kind,
+                              double* arg_num, int32_t* arg_name, void* stream);
+
+/* R48 duplicate dropping: within each subgraph's n rows of genes [S*n, G]
+ * (device), every row equal to an earlier row of the same subgraph gets
+ * scores[row] = -inf (scores [S*n] fp32 device, updated in place). */
+tlp_status tlp_ga_drop_duplicates(tlp_ctx* ctx, const uint8_t* genes, int32_t n, float* scores,
+                                  void* stream);
+
+/* One tuning round of every subgraph entirely on the device (R48):
+ * n_pop + n_child initial candidates -> materialise -> tlp_encode -> tlp_score
+ * (column `head`) -> drop duplicates (-inf) -> keep the n_pop best (tlp_topk
+ * order); then `iters` times: n_child children -> materialise -> encode ->
+ * score -> pool = survivors + children -> drop duplicates -> keep n_pop best.
+ * genes_out [S*n_pop, G] uint8 device and scores_out [S*n_pop] fp32 device
+ * receive the final survivors in rank order (a -inf score marks a duplicate
+ * survivor when a pool has fewer than n_pop distinct programs).  Requires
+ * tlp_set_norm_scales and tlp_set_params; 1 <= n_pop <= 1024, n_child >= 1,
+ * n_pop + n_child <= 16384, iters >= 0.  Device workspaces are ctx-owned and
+ * grow to the largest round.  Asynchronous on `stream`. */
+tlp_status tlp_ga_round(tlp_ctx* ctx, int32_t n_pop, int32_t n_child, int32_t iters,
+                        double p_cross, double p_mut, uint64_t seed, int32_t round, int32_t head,
+                        uint8_t* genes_out, float* scores_out, void* stream);
+
 /* ---- training-data preparation, P:295-296 -------------------------------
  * label_i = min_{j in g} latency_j / latency_i per group g (fp64 quotient,
  * rounded to fp32).  latency [M] fp32 device > 0; group_off [G+1] HOST int64;

@@ -12,6 +12,11 @@ Paper (P:295 [§4.4], P:431 [§6.1.3], P:355 [§5.2]):
    rows of X, R7) are masked out of every softmax; queries are unchanged.
    NEXT-3 variant (cfg.pos_enc, R43): a learned positional table pos [L, H]
    is added to the upsampled rows before the first attention layer.
+  NEXT-4 variant (cfg.backbone = "lstm", R49): "we use the self-attention or
+   LSTM module, which we call the backbone basic module" -- n_attn layers of a
+   single-direction LSTM (hidden -> hidden, gates i, f, g, o, h_0 = c_0 = 0,
+   rows in sequence order, pads included) in place of the attention layers,
+   with the same identity residual h <- h + LSTM(h) (R10).
   "Then two residual blocks follow" -> R12: h + relu(h Wa + a) Wb + b.
   "Finally, multiple linear layers and a sum operation are used to obtain a
    prediction score" -> R13: per position relu(h W1 + c1) w2 + c2, summed over
@@ -19,7 +24,7 @@ Paper (P:295 [§4.4], P:431 [§6.1.3], P:355 [§5.2]):
   MTL-TLP: one such head per task on a shared backbone.
 
 Parameter order R24: upsample (W, b)...; per attention layer Wq, bq, Wk, bk,
-Wv, bv, Wo, bo; per residual block Wa, a, Wb, b; per task head W1, c1, w2, c2.
+Wv, bv, Wo, bo (or per LSTM layer Wih [H, 4H], bih, Whh [H, 4H], bhh); per residual block Wa, a, Wb, b; per task head W1, c1, w2, c2.
 W is [in, out].
 """
 from __future__ import annotations
@@ -44,11 +49,13 @@ class Config:
     n_tasks: int = 1
     attn_mask: bool = False  # NEXT-3 / R42: mask padding keys (the paper: no mask, R8)
     pos_enc: bool = False    # NEXT-3 / R43: learned positional table (the paper: none, R9)
+    backbone: str = "attn"   # NEXT-4 / R49: "attn" (the paper's choice) or "lstm"
 
     def __post_init__(self):
         self.up_dims = tuple(self.up_dims)
         assert self.up_dims[-1] == self.hidden
         assert self.hidden % self.attn_heads == 0
+        assert self.backbone in ("attn", "lstm")
 
     @property
     def d_h(self) -> int:
@@ -66,6 +73,10 @@ def param_shapes(cfg: Config) -> List[Tuple[str, Tuple[int, ...]]]:
     if cfg.pos_enc:
         out += [("pos", (cfg.L, H))]  # R43: right after the upsample (R24 order)
     for l in range(cfg.n_attn):
+        if cfg.backbone == "lstm":
+            out += [("lstm%d.Wih" % l, (H, 4 * H)), ("lstm%d.bih" % l, (4 * H,)),
+                    ("lstm%d.Whh" % l, (H, 4 * H)), ("lstm%d.bhh" % l, (4 * H,))]
+            continue
         for nm in ("q", "k", "v", "o"):
             out += [("attn%d.W%s" % (l, nm), (H, H)), ("attn%d.b%s" % (l, nm), (H,))]
     for r in range(cfg.n_res):
@@ -107,6 +118,60 @@ def softmax_rows(S):
     return e / e.sum(axis=-1, keepdims=True)
 
 
+def sigmoid(x):
+    return 0.5 * (1.0 + np.tanh(0.5 * x))
+
+
+def lstm_forward(p: Dict[str, np.ndarray], pre: str, h: np.ndarray):
+    """R49: one LSTM layer over the L rows of every candidate, in order.
+    z_t = h_t Wih + bih + hprev Whh + bhh; [i, f, g, o] = [sig, sig, tanh, sig](z_t);
+    c_t = f c_{t-1} + i g; hl_t = o tanh(c_t); returns the sequence hl and the
+    per-step values backward needs."""
+    N, L, H = h.shape
+    hp = np.zeros((N, H))
+    cp = np.zeros((N, H))
+    out = np.zeros((N, L, H))
+    steps = []
+    for t in range(L):
+        z = h[:, t] @ p[pre + "Wih"] + p[pre + "bih"] + hp @ p[pre + "Whh"] + p[pre + "bhh"]
+        i, f = sigmoid(z[:, :H]), sigmoid(z[:, H:2 * H])
+        g, o = np.tanh(z[:, 2 * H:3 * H]), sigmoid(z[:, 3 * H:])
+        c = f * cp + i * g
+        hl = o * np.tanh(c)
+        steps.append(dict(i=i, f=f, g=g, o=o, c=c, cp=cp, hp=hp))
+        out[:, t] = hl
+        hp, cp = hl, c
+    return out, steps
+
+
+def lstm_backward(p: Dict[str, np.ndarray], pre: str, h: np.ndarray, steps, dout: np.ndarray,
+                  grads: Dict[str, np.ndarray]) -> np.ndarray:
+    """Backpropagation through time of lstm_forward; returns d h (the input)."""
+    N, L, H = h.shape
+    dh_in = np.zeros_like(h)
+    dWih = np.zeros((H, 4 * H)); dWhh = np.zeros((H, 4 * H)); db = np.zeros(4 * H)
+    dhn = np.zeros((N, H))
+    dcn = np.zeros((N, H))
+    for t in reversed(range(L)):
+        st = steps[t]
+        dht = dout[:, t] + dhn
+        tc = np.tanh(st["c"])
+        do = dht * tc
+        dc = dcn + dht * st["o"] * (1.0 - tc * tc)
+        di, dg, df = dc * st["g"], dc * st["i"], dc * st["cp"]
+        dcn = dc * st["f"]
+        dz = np.concatenate([di * st["i"] * (1 - st["i"]), df * st["f"] * (1 - st["f"]),
+                             dg * (1 - st["g"] ** 2), do * st["o"] * (1 - st["o"])], axis=1)
+        dWih += h[:, t].T @ dz
+        dWhh += st["hp"].T @ dz
+        db += dz.sum(axis=0)
+        dhn = dz @ p[pre + "Whh"].T
+        dh_in[:, t] = dz @ p[pre + "Wih"].T
+    grads[pre + "Wih"], grads[pre + "Whh"] = dWih, dWhh
+    grads[pre + "bih"], grads[pre + "bhh"] = db, db.copy()
+    return dh_in
+
+
 def forward(cfg: Config, p: Dict[str, np.ndarray], X: np.ndarray, save: bool = False):
     """O2.  X [N, L, E] -> scores [N, n_tasks] (float64).  With ``save`` also
     returns the activations backward() needs."""
@@ -123,7 +188,11 @@ def forward(cfg: Config, p: Dict[str, np.ndarray], X: np.ndarray, save: bool = F
         h = relu(pre)
     if cfg.pos_enc:
         h = h + p["pos"][None, :L, :]                           # R43
-    for l in range(cfg.n_attn):
+    for l in range(cfg.n_attn if cfg.backbone == "lstm" else 0):
+        out, steps = lstm_forward(p, "lstm%d." % l, h)
+        acts["attn"].append(dict(h=h, steps=steps))
+        h = h + out                                            # R49 (as R10)
+    for l in range(cfg.n_attn if cfg.backbone == "attn" else 0):
         pre = "attn%d." % l
         Q = h @ p[pre + "Wq"] + p[pre + "bq"]
         K = h @ p[pre + "Wk"] + p[pre + "bk"]
@@ -187,7 +256,10 @@ def backward(cfg: Config, p: Dict[str, np.ndarray], acts, g: np.ndarray) -> Dict
         grads[pre + "Wa"] = np.einsum("nli,nlo->io", a["h"], dv)
         grads[pre + "a"] = dv.sum(axis=(0, 1))
         dh_ = dh_ + dv @ p[pre + "Wa"].T
-    for l in reversed(range(cfg.n_attn)):
+    for l in reversed(range(cfg.n_attn if cfg.backbone == "lstm" else 0)):
+        a = acts["attn"][l]
+        dh_ = dh_ + lstm_backward(p, "lstm%d." % l, a["h"], a["steps"], dh_, grads)
+    for l in reversed(range(cfg.n_attn if cfg.backbone == "attn" else 0)):
         pre = "attn%d." % l
         a = acts["attn"][l]
         grads[pre + "Wo"] = np.einsum("nli,nlo->io", a["O"], dh_)

@@ -377,3 +377,85 @@ class TLP:
         self._check(self.lib.tlp_normalize_labels(self.h, latency.data_ptr(), goff.ctypes.data,
                                                   len(goff) - 1, out.data_ptr(), _stream_ptr(stream)))
         return out
+
+    # ---------------------------------------------------------------- NEXT-1
+    def ga_set_space(self, space):
+        """tlp_ga_set_space from a host search space (any object with the
+        fields of synth.PackedSpace: tmpl (packed batch), knob_off, knob_arg,
+        knob_grp, dom_off, dom_num, dom_name)."""
+        arrs = DeviceBatch.host_arrays(space.tmpl)
+        keep = dict(arrs)
+        keep["knob_off"] = np.ascontiguousarray(space.knob_off, np.int64)
+        keep["knob_arg"] = np.ascontiguousarray(space.knob_arg, np.int64)
+        keep["knob_grp"] = np.ascontiguousarray(space.knob_grp, np.int32)
+        keep["dom_off"] = np.ascontiguousarray(space.dom_off, np.int64)
+        keep["dom_num"] = np.ascontiguousarray(space.dom_num, np.float64)
+        keep["dom_name"] = np.ascontiguousarray(space.dom_name, np.int32)
+        sp = _lib.tlp_ga_space()
+        t = sp.tmpl
+        t.seq_off, t.prim_type, t.arg_off = (keep[k].ctypes.data for k in ("seq_off", "prim_type", "arg_off"))
+        t.arg_kind, t.arg_num, t.arg_name = (keep[k].ctypes.data for k in ("arg_kind", "arg_num", "arg_name"))
+        t.str_blob, t.str_off = keep["str_blob"].ctypes.data, keep["str_off"].ctypes.data
+        t.P, t.A, t.U = len(arrs["prim_type"]), len(arrs["arg_kind"]), len(arrs["str_off"]) - 1
+        sp.S = len(keep["knob_off"]) - 1
+        for k in ("knob_off", "knob_arg", "knob_grp", "dom_off", "dom_num", "dom_name"):
+            setattr(sp, k, keep[k].ctypes.data)
+        self._check(self.lib.tlp_ga_set_space(self.h, C.byref(sp)))
+        self._ga_S = sp.S
+        self._ga_strings = (arrs["str_blob"], arrs["str_off"])
+        self.ga_G = int(self.lib.tlp_ga_num_genes(self.h))
+
+    def ga_init(self, n: int, seed: int, rnd: int, out=None, stream=None) -> torch.Tensor:
+        if out is None:
+            out = torch.empty((self._ga_S * n, self.ga_G), dtype=torch.uint8, device="cuda")
+        self._check(self.lib.tlp_ga_init(self.h, n, seed, rnd, out.data_ptr(), _stream_ptr(stream)))
+        return out
+
+    def ga_evolve(self, pop: torch.Tensor, pop_scores: torch.Tensor, n_pop: int, n_child: int,
+                  p_cross: float, p_mut: float, seed: int, rnd: int, it: int, out=None,
+                  stream=None) -> torch.Tensor:
+        if out is None:
+            out = torch.empty((self._ga_S * n_child, self.ga_G), dtype=torch.uint8, device="cuda")
+        self._check(self.lib.tlp_ga_evolve(self.h, pop.data_ptr(), pop_scores.data_ptr(), n_pop, n_child,
+                                           p_cross, p_mut, seed, rnd, it, out.data_ptr(),
+                                           _stream_ptr(stream)))
+        return out
+
+    def ga_materialize(self, genes: torch.Tensor, n: int, stream=None) -> DeviceBatch:
+        """The packed abstract primitives of S*n gene rows (a DeviceBatch
+        sharing the space's string table)."""
+        P, A = C.c_int64(0), C.c_int64(0)
+        self._check(self.lib.tlp_ga_batch_size(self.h, n, C.byref(P), C.byref(A)))
+        dev = genes.device
+        N = self._ga_S * n
+        e = lambda k, dt: torch.empty(max(k, 1), dtype=dt, device=dev)  # noqa: E731
+        b = DeviceBatch(e(N + 1, torch.int64), e(P.value, torch.uint8), e(P.value + 1, torch.int64),
+                        e(A.value, torch.uint8), e(A.value, torch.float64), e(A.value, torch.int32),
+                        torch.from_numpy(self._ga_strings[0]).to(dev),
+                        torch.from_numpy(self._ga_strings[1]).to(dev),
+                        N=N, P=P.value, A=A.value, U=len(self._ga_strings[1]) - 1)
+        self._check(self.lib.tlp_ga_materialize(self.h, genes.data_ptr(), n, b.seq_off.data_ptr(),
+                                                b.prim_type.data_ptr(), b.arg_off.data_ptr(),
+                                                b.arg_kind.data_ptr(), b.arg_num.data_ptr(),
+                                                b.arg_name.data_ptr(), _stream_ptr(stream)))
+        return b
+
+    def ga_drop_duplicates(self, genes: torch.Tensor, n: int, scores: torch.Tensor, stream=None):
+        self._check(self.lib.tlp_ga_drop_duplicates(self.h, genes.data_ptr(), n, scores.data_ptr(),
+                                                    _stream_ptr(stream)))
+        return scores
+
+    def ga_round(self, n_pop: int, n_child: int, iters: int, p_cross: float, p_mut: float,
+                 seed: int, rnd: int, head: int = 0, genes_out=None, scores_out=None, stream=None):
+        """tlp_ga_round: one device-resident tuning round of every subgraph.
+        Returns (genes [S*n_pop, G] uint8, scores [S*n_pop] fp32) on the device,
+        each subgraph's survivors in rank order."""
+        S = self._ga_S
+        if genes_out is None:
+            genes_out = torch.empty((S * n_pop, self.ga_G), dtype=torch.uint8, device="cuda")
+        if scores_out is None:
+            scores_out = torch.empty(S * n_pop, dtype=torch.float32, device="cuda")
+        self._check(self.lib.tlp_ga_round(self.h, n_pop, n_child, iters, p_cross, p_mut, seed, rnd, head,
+                                          genes_out.data_ptr(), scores_out.data_ptr(),
+                                          _stream_ptr(stream)))
+        return genes_out, scores_out

@@ -18,7 +18,8 @@ EXPORTS = ("tlp_create", "tlp_destroy", "tlp_last_error", "tlp_default_config",
            "tlp_get_params", "tlp_get_grads", "tlp_set_comm", "tlp_get_unique_id", "tlp_encode",
            "tlp_score", "tlp_train_step", "tlp_compute_grads", "tlp_lambdarank", "tlp_mse", "tlp_topk", "tlp_topk_merge",
            "tlp_search_round", "tlp_dedup", "tlp_topk_score", "tlp_normalize_labels", "tlp_sync", "tlp_launch_count", "tlp_debug_umma",
-           "tlp_debug_gemm")
+           "tlp_debug_gemm", "tlp_ga_set_space", "tlp_ga_num_genes", "tlp_ga_batch_size", "tlp_ga_init",
+           "tlp_ga_evolve", "tlp_ga_materialize", "tlp_ga_drop_duplicates", "tlp_ga_round")
 
 
 class tlp_config(C.Structure):
@@ -35,6 +36,12 @@ class tlp_seq_batch(C.Structure):
                 ("arg_kind", C.c_void_p), ("arg_num", C.c_void_p), ("arg_name", C.c_void_p),
                 ("str_blob", C.c_void_p), ("str_off", C.c_void_p), ("P", C.c_int64),
                 ("A", C.c_int64), ("U", C.c_int32)]
+
+
+class tlp_ga_space(C.Structure):
+    _fields_ = [("tmpl", tlp_seq_batch), ("S", C.c_int32), ("knob_off", C.c_void_p),
+                ("knob_arg", C.c_void_p), ("knob_grp", C.c_void_p), ("dom_off", C.c_void_p),
+                ("dom_num", C.c_void_p), ("dom_name", C.c_void_p)]
 
 
 _lib = None
@@ -80,6 +87,16 @@ def load() -> C.CDLL:
         "tlp_launch_count": (i64, [vp]),
         "tlp_debug_umma": (C.c_int, [vp, vp, vp, i32, i32, i32, vp]),
         "tlp_debug_gemm": (C.c_int, [vp, i32, i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, i32, vp]),
+        "tlp_ga_set_space": (C.c_int, [vp, C.POINTER(tlp_ga_space)]),
+        "tlp_ga_num_genes": (i32, [vp]),
+        "tlp_ga_batch_size": (C.c_int, [vp, i64, vp, vp]),
+        "tlp_ga_init": (C.c_int, [vp, i32, C.c_uint64, i32, vp, vp]),
+        "tlp_ga_evolve": (C.c_int, [vp, vp, vp, i32, i32, C.c_double, C.c_double, C.c_uint64, i32,
+                                    i32, vp, vp]),
+        "tlp_ga_materialize": (C.c_int, [vp, vp, i64, vp, vp, vp, vp, vp, vp, vp]),
+        "tlp_ga_drop_duplicates": (C.c_int, [vp, vp, i32, vp, vp]),
+        "tlp_ga_round": (C.c_int, [vp, i32, i32, i32, C.c_double, C.c_double, C.c_uint64, i32, i32,
+                                   vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)

@@ -146,6 +146,7 @@ void tlp_destroy(tlp_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->comm) ncclCommDestroy(reinterpret_cast<ncclComm_t>(ctx->comm));
   tc_free(ctx);
+  ga_free(ctx);
   cudaFree(ctx->d_params); cudaFree(ctx->d_grads); cudaFree(ctx->d_m); cudaFree(ctx->d_v);
   cudaFree(ctx->d_scale); cudaFree(ctx->d_err);
   cudaFree(ctx->d_hkeys); cudaFree(ctx->d_hval); cudaFree(ctx->d_hstr);

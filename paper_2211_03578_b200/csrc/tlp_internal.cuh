@@ -55,6 +55,7 @@ struct DevBuf {
 };
 
 struct TcWeights;  // bf16 tcgen05 weight images (k_tc_forward.cu)
+struct GaSpace;    // NEXT-1 search space + round workspaces (k_search.cu)
 
 struct tlp_ctx {
   tlp_config cfg;
@@ -103,6 +104,9 @@ struct tlp_ctx {
   int rank = 0, world = 1;
 
   int64_t launches = 0;
+
+  // NEXT-1 tuning-round search space (tlp_ga_set_space)
+  GaSpace* ga = nullptr;
 
   // training forward state kept for backward (k_simt.cu)
   int64_t train_N = -1;
@@ -214,3 +218,6 @@ void tc_free(tlp_ctx* ctx);
 
 // api.cu
 tlp_status dev_error_status(tlp_ctx* ctx);
+
+// k_search.cu
+void ga_free(tlp_ctx* ctx);

@@ -376,7 +376,7 @@ def small_template(domain_sizes: Sequence[int]) -> Template:
     for d in domain_sizes:
         assert 1 <= d <= len(FACTOR_DOMAIN)
         kp.append(len(prims)); ka.append(3); dom.append(FACTOR_DOMAIN[:d])
-        prims.append((SP, [0.0, 1.0, 64.0, 1.0, 0.0]))
+        prims.append((SP, [float(len(prims)), 1.0, 64.0, 1.0, 0.0]))  # distinct stages: rows differ
     prims.append((AN, [0.0, 1.0, 2.0]))
     return Template(prims, kp, ka, dom)
 
