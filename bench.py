@@ -262,6 +262,7 @@ def run_ours(args):
     # the §6.1 top-k score of its scores against synthetic latencies ---
     next_rows = next2_measure(scorer, feats, scores, task_off, args, stream, dev)
     next_rows.update(next1_measure(scorer, args, stream, rank))
+    next_rows.update(next4_measure(feats, tfeats, labels, goff, precision, names, scale, args, stream, local))
 
     K = args.steps
     cand_s = world * N_ROUND * K / (round_ms / 1e3)
@@ -317,6 +318,47 @@ def run_ours(args):
 
 
 GA_S, GA_POP, GA_CHILD, GA_ITERS = 100, 512, 1920, 4
+
+
+def next4_measure(feats, tfeats, labels, goff, precision, names, scale, args, stream, local):
+    """NEXT-4: the LSTM backbone (R49, 1 layer, paper widths) in
+    place of attention -- scoring the round's 409,600 encoded candidates and
+    one C3-shape LambdaRank train step (8,192 samples), CUDA events, W warm-up
+    + K timed calls.  Layer-by-layer path: bf16x3 tcgen05 GEMMs for the input
+    projection and each of the 25 recurrent steps, SIMT cells."""
+    import torch
+    import paper_2211_03578_b200 as tp
+    from oracle import model as OM
+    ocfg = OM.Config(n_attn=1, backbone="lstm")
+    flat = np.concatenate([v.ravel() for v in synth.init_params(9, OM.param_shapes(ocfg))]).astype(np.float32)
+    out = {}
+    m = tp.TLP(tp.TLPConfig(n_attn=1, precision=precision, backbone="lstm"), device=local)
+    m.set_params(flat)
+    sc = torch.empty((feats.shape[0], 1), dtype=torch.float32, device=feats.device)
+    loss = torch.empty(1, dtype=torch.float32, device=feats.device)
+
+    def timed(fn, steps):
+        for _ in range(args.warmup):
+            fn()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / steps
+
+    steps = max(1, min(args.steps, 3))
+    ms = timed(lambda: m.score(feats, out=sc, stream=stream), steps)
+    fl = 25 * (2 * (2 * 256 * 1024)) + (fwd_flops_per_cand(n_attn=0))  # LSTM GEMMs + the rest
+    out["lstm_score"] = {"value": feats.shape[0] / (ms / 1e3), "unit": "candidates/s", "ms_per_call": ms,
+                         "tflops": fl * feats.shape[0] / (ms / 1e3) / 1e12,
+                         "config": "409,600 candidates, 1 LSTM layer (hidden 256), %s" % precision}
+    ms = timed(lambda: m.train_step(tfeats, labels, goff, loss_out=loss, stream=stream), steps)
+    out["lstm_train"] = {"value": tfeats.shape[0] / (ms / 1e3), "unit": "samples/s", "ms_per_step": ms,
+                         "config": "8,192 samples (16 groups x 512), LambdaRank, 1 LSTM layer, %s" % precision}
+    return out
 
 
 def next1_measure(m, args, stream, rank):

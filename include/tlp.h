@@ -73,7 +73,8 @@ typedef enum {
  * its dense layers on the tensor cores for any shape; TLP_PREC_BF16 scoring
  * (the fused kernel) requires the paper shape (E=22, hidden=256,
  * up_dims={128,256}, attn_heads=8, head_dim=128, L=25) and otherwise
- * tlp_score returns TLP_ERR_UNSUPPORTED.
+ * tlp_score returns TLP_ERR_UNSUPPORTED (an LSTM backbone, NEXT-4, scores
+ * through the layer-by-layer tensor-core GEMMs instead).
  */
 typedef struct {
   int L, E, T;
@@ -94,6 +95,12 @@ typedef struct {
   int pos_enc;                /* NEXT-3 / R43: 1 = learned positional table pos [L, hidden] added
                                  after the upsample (R24: right after the upsample parameters);
                                  0 = none (the paper, R9) */
+  int backbone;               /* NEXT-4 / R49: 0 = n_attn self-attention layers (the paper's
+                                 choice); 1 = n_attn LSTM layers hidden -> hidden (gates
+                                 i, f, g, o; h0 = c0 = 0; identity residual), "the
+                                 self-attention or LSTM module".  LSTM contexts score through
+                                 the layer-by-layer path (fp32 SIMT, or bf16x3 tcgen05 GEMMs for
+                                 TLP_PREC_BF16) and require attn_mask = 0. */
 } tlp_config;
 
 typedef enum {

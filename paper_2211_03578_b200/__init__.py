@@ -50,6 +50,7 @@ class TLPConfig:
     loss: str = "lambdarank"  # "lambdarank" (R16, the paper's choice) | "mse" (NEXT-3)
     attn_mask: bool = False   # NEXT-3 / R42: mask padding keys (the paper: no mask, R8)
     pos_enc: bool = False     # NEXT-3 / R43: learned positional table (the paper: none, R9)
+    backbone: str = "attn"    # NEXT-4 / R49: "attn" (the paper's choice) | "lstm"
 
     def to_c(self) -> tlp_config:
         c = tlp_config()
@@ -64,6 +65,7 @@ class TLPConfig:
         c.loss = {"lambdarank": 0, "mse": 1}[self.loss]
         c.attn_mask = 1 if self.attn_mask else 0
         c.pos_enc = 1 if self.pos_enc else 0
+        c.backbone = {"attn": 0, "lstm": 1}[self.backbone]
         return c
 
 

@@ -28,7 +28,8 @@ class tlp_config(C.Structure):
                 ("n_attn", C.c_int), ("n_res", C.c_int), ("head_dim", C.c_int),
                 ("n_tasks", C.c_int), ("precision", C.c_int), ("lr", C.c_float),
                 ("beta1", C.c_float), ("beta2", C.c_float), ("eps", C.c_float),
-                ("seed", C.c_ulonglong), ("loss", C.c_int), ("attn_mask", C.c_int), ("pos_enc", C.c_int)]
+                ("seed", C.c_ulonglong), ("loss", C.c_int), ("attn_mask", C.c_int), ("pos_enc", C.c_int),
+                ("backbone", C.c_int)]
 
 
 class tlp_seq_batch(C.Structure):

@@ -39,6 +39,11 @@ ParamOffsets compute_offsets(const tlp_config& c) {
   o.pos = -1;
   if (c.pos_enc) { o.pos = p; p += (int64_t)c.L * H; }  // R43, right after the upsample (R24)
   for (int l = 0; l < c.n_attn; ++l) {
+    if (c.backbone == 1) {  // R49: Wih [H, 4H], bih, Whh [H, 4H], bhh
+      o.Wih[l] = p; p += 4 * H * H; o.bih[l] = p; p += 4 * H;
+      o.Whh[l] = p; p += 4 * H * H; o.bhh[l] = p; p += 4 * H;
+      continue;
+    }
     o.Wq[l] = p; p += H * H; o.bq[l] = p; p += H;
     o.Wk[l] = p; p += H * H; o.bk[l] = p; p += H;
     o.Wv[l] = p; p += H * H; o.bv[l] = p; p += H;
@@ -64,13 +69,15 @@ std::string check_config(const tlp_config& c) {
   if (c.loss != TLP_LOSS_LAMBDARANK && c.loss != TLP_LOSS_MSE) return "loss must be 0 (LambdaRank) or 1 (MSE)";
   if (c.attn_mask != 0 && c.attn_mask != 1) return "attn_mask must be 0 or 1";
   if (c.pos_enc != 0 && c.pos_enc != 1) return "pos_enc must be 0 or 1";
+  if (c.backbone != 0 && c.backbone != 1) return "backbone must be 0 (attention) or 1 (LSTM)";
+  if (c.backbone == 1 && c.attn_mask) return "attn_mask applies to the attention backbone only";
   if (c.hidden < 8 || c.hidden > 512) return "hidden must be in [8, 512]";
   if (c.up_dims[c.n_up - 1] != c.hidden) return "up_dims[n_up-1] must equal hidden";
   for (int i = 0; i < c.n_up; ++i)
     if (c.up_dims[i] < 1 || c.up_dims[i] > c.hidden) return "up_dims must be in [1, hidden]";
   if (c.attn_heads < 1 || c.hidden % c.attn_heads) return "hidden % attn_heads must be 0";
   const int dh = c.hidden / c.attn_heads;
-  if (c.n_attn > 0 && dh != 8 && dh != 16 && dh != 32 && dh != 64) return "hidden/attn_heads must be 8/16/32/64";
+  if (c.backbone == 0 && c.n_attn > 0 && dh != 8 && dh != 16 && dh != 32 && dh != 64) return "hidden/attn_heads must be 8/16/32/64";
   if (c.n_attn < 0 || c.n_attn > TLP_MAX_ATTN) return "n_attn must be in [0, 4]";
   if (c.n_res < 0 || c.n_res > TLP_MAX_RES) return "n_res must be in [0, 4]";
   if (c.head_dim < 1 || c.head_dim > c.hidden) return "head_dim must be in [1, hidden]";
@@ -263,7 +270,7 @@ tlp_status tlp_score(tlp_ctx* ctx, const float* feats, int64_t N, float* scores,
   CHECK_CTX();
   if (N < 0 || (N > 0 && (!feats || !scores))) return fail(ctx, TLP_ERR_ARG, "null buffer");
   if (!ctx->have_params) return fail(ctx, TLP_ERR_STATE, "tlp_set_params first");
-  if (ctx->cfg.precision == TLP_PREC_BF16 && !tc_supported(ctx->cfg))
+  if (!score_supported(ctx->cfg))
     return fail(ctx, TLP_ERR_UNSUPPORTED,
                 "bf16 tensor-core scoring needs the paper shape (E=22, L=25, hidden=256, "
                 "up_dims={128,256}, 8 heads, head_dim=128); use TLP_PREC_FP32");
@@ -275,7 +282,7 @@ tlp_status tlp_score(tlp_ctx* ctx, const float* feats, int64_t N, float* scores,
 }  // extern "C"
 
 tlp_status score_launch(tlp_ctx* ctx, const float* feats, int64_t N, float* scores, cudaStream_t s) {
-  if (ctx->cfg.precision == TLP_PREC_BF16) {
+  if (ctx->cfg.precision == TLP_PREC_BF16 && tc_supported(ctx->cfg)) {
     if (ctx->tc_dirty) {
       tlp_status st = tc_prepare(ctx, s);
       if (st != TLP_OK) return st;

@@ -579,7 +579,7 @@ tlp_status tlp_ga_round(tlp_ctx* ctx, int32_t n_pop, int32_t n_child, int32_t it
     return ga_fail(ctx, TLP_ERR_ARG, "tlp_ga_round: bad args");
   if (!ctx->have_scales) return ga_fail(ctx, TLP_ERR_STATE, "tlp_set_norm_scales first");
   if (!ctx->have_params) return ga_fail(ctx, TLP_ERR_STATE, "tlp_set_params first");
-  if (c.precision == TLP_PREC_BF16 && !tc_supported(c))
+  if (!score_supported(c))
     return ga_fail(ctx, TLP_ERR_UNSUPPORTED, "bf16 scoring needs the paper shape");
   cudaSetDevice(ctx->device);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);

@@ -427,6 +427,61 @@ __global__ void dc2_kernel(const float* __restrict__ g, int64_t N, int t, int nt
   if (threadIdx.x == 0) out[0] = (float)L * red[0];
 }
 
+// ---------------------------------------------------------------- R49 LSTM (NEXT-4)
+// Step t of a layer, thread per (candidate, unit j).  gates row (n, t) holds
+// the pre-activation z = h_t Wih + bih + h_{t-1} Whh + bhh (written by the step
+// GEMM); it is overwritten by the activated [i, f, g, o] that backward needs.
+// c_t -> C, h_t -> hprev row t+1 (the next step's GEMM operand and dWhh's
+// A operand), layer output hin + h_t -> hout (identity residual, R49).
+// Full-precision expf / tanhf (R29).
+__device__ __forceinline__ float sigmoid_f(float x) { return 1.0f / (1.0f + expf(-x)); }
+
+__global__ void lstm_cell_fwd(int64_t n, int L, int H, int t, float* __restrict__ gates,
+                              float* __restrict__ C, float* __restrict__ hprev,
+                              const float* __restrict__ hin, float* __restrict__ hout) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= n * H) return;
+  const int64_t cand = idx / H;
+  const int j = (int)(idx - cand * H);
+  const int64_t row = cand * L + t;
+  float* z = gates + row * 4 * H;
+  const float i = sigmoid_f(z[j]), f = sigmoid_f(z[H + j]);
+  const float g = tanhf(z[2 * H + j]), o = sigmoid_f(z[3 * H + j]);
+  const float cp = t > 0 ? C[(row - 1) * H + j] : 0.f;
+  const float c = f * cp + i * g;
+  const float hl = o * tanhf(c);
+  z[j] = i; z[H + j] = f; z[2 * H + j] = g; z[3 * H + j] = o;
+  C[row * H + j] = c;
+  if (t + 1 < L) hprev[(row + 1) * H + j] = hl;
+  hout[row * H + j] = hin[row * H + j] + hl;
+}
+
+// Backward of step t: dh_t = dout_t + dhr (= dz_{t+1} Whh^T), carried dc;
+// writes dz_t (pre-activation gradients) into dG.
+__global__ void lstm_cell_bwd(int64_t n, int L, int H, int t, const float* __restrict__ gates,
+                              const float* __restrict__ C, const float* __restrict__ dout,
+                              const float* __restrict__ dhr, float* __restrict__ dcar,
+                              float* __restrict__ dG) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= n * H) return;
+  const int64_t cand = idx / H;
+  const int j = (int)(idx - cand * H);
+  const int64_t row = cand * L + t;
+  const float* z = gates + row * 4 * H;
+  const float i = z[j], f = z[H + j], g = z[2 * H + j], o = z[3 * H + j];
+  const float c = C[row * H + j];
+  const float cp = t > 0 ? C[(row - 1) * H + j] : 0.f;
+  const float dht = dout[row * H + j] + (t + 1 < L ? dhr[cand * H + j] : 0.f);
+  const float tc = tanhf(c);
+  const float dc = (t + 1 < L ? dcar[cand * H + j] : 0.f) + dht * o * (1.f - tc * tc);
+  dcar[cand * H + j] = dc * f;
+  float* d = dG + row * 4 * H;
+  d[j] = dc * g * i * (1.f - i);
+  d[H + j] = dc * cp * f * (1.f - f);
+  d[2 * H + j] = dc * i * (1.f - g * g);
+  d[3 * H + j] = dht * tc * o * (1.f - o);
+}
+
 __global__ void relu_mask_inplace(float* __restrict__ d, const float* __restrict__ act,
                                   int64_t n) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -438,6 +493,10 @@ __global__ void relu_mask_inplace(float* __restrict__ d, const float* __restrict
 struct ActLayout {
   int64_t up[TLP_MAX_UP];
   int64_t qkv[TLP_MAX_ATTN], A[TLP_MAX_ATTN], O[TLP_MAX_ATTN], hattn[TLP_MAX_ATTN];
+  // R49 LSTM layers: input projection, gates (pre-activation -> activated),
+  // cell states, shifted hidden states (row t holds h_{t-1}, row 0 zero)
+  int64_t xg[TLP_MAX_ATTN], gates[TLP_MAX_ATTN], cst[TLP_MAX_ATTN], hprev[TLP_MAX_ATTN];
+  int64_t dG, dcar, dhr;  // LSTM backward scratch
   int64_t r[TLP_MAX_RES], hres[TLP_MAX_RES];
   int64_t U[TLP_MAX_TASKS], pooled[TLP_MAX_TASKS];
   int64_t kvalid;  // R42 key-validity flags (attn_mask)
@@ -454,9 +513,16 @@ ActLayout act_layout(const tlp_config& c, int64_t N) {
   auto take = [&](int64_t n) { int64_t r = o; o += (n + 63) / 64 * 64; return r; };
   for (int i = 0; i < c.n_up; ++i) a.up[i] = take(M * c.up_dims[i]);
   for (int l = 0; l < c.n_attn; ++l) {
-    a.qkv[l] = take(M * 3 * H);
-    a.A[l] = take(N * c.attn_heads * (int64_t)c.L * c.L);
-    a.O[l] = take(M * H);
+    if (c.backbone == 1) {
+      a.xg[l] = take(M * 4 * H);
+      a.gates[l] = take(M * 4 * H);
+      a.cst[l] = take(M * H);
+      a.hprev[l] = take(M * H);
+    } else {
+      a.qkv[l] = take(M * 3 * H);
+      a.A[l] = take(N * c.attn_heads * (int64_t)c.L * c.L);
+      a.O[l] = take(M * H);
+    }
     a.hattn[l] = take(M * H);
   }
   for (int r = 0; r < c.n_res; ++r) { a.r[r] = take(M * H); a.hres[r] = take(M * H); }
@@ -468,6 +534,11 @@ ActLayout act_layout(const tlp_config& c, int64_t N) {
   a.dtmp = take(M * std::max<int64_t>(H, c.up_dims[0]));
   a.dqkv = take(M * 3 * H);
   a.dU = take(M * c.head_dim);
+  if (c.backbone == 1 && c.n_attn > 0) {
+    a.dG = take(M * 4 * H);
+    a.dcar = take(N * H);
+    a.dhr = take(N * H);
+  }
   a.total = o;
   return a;
 }
@@ -606,7 +677,8 @@ tlp_status simt_forward(tlp_ctx* ctx, const float* X, int64_t N, float* scores, 
   const float* P = ctx->d_params;
   const int64_t H = c.hidden;
   // inference processes bounded chunks; training keeps the whole batch
-  const int64_t chunk = save ? N : std::min<int64_t>(N, 8192);
+  // (LSTM: larger chunks, so each of the L sequential step GEMMs has more rows)
+  const int64_t chunk = save ? N : std::min<int64_t>(N, c.backbone == 1 ? 65536 : 8192);
   ActLayout lay = act_layout(c, chunk);
   TLP_CUDA_TRY(ctx->ws_act.ensure((size_t)(save ? lay.total : lay.total_fwd) * sizeof(float)));
   float* W = ctx->ws_act.as<float>();
@@ -633,7 +705,26 @@ tlp_status simt_forward(tlp_ctx* ctx, const float* X, int64_t N, float* scores, 
       TLP_LAUNCH_CHECK();
       h = W + lay.hpos;
     }
-    for (int l = 0; l < c.n_attn; ++l) {
+    for (int l = 0; l < c.n_attn && c.backbone == 1; ++l) {  // R49
+      const int64_t H4 = 4 * H;
+      float* xg = W + lay.xg[l];
+      float* gt = W + lay.gates[l];
+      float* hp = W + lay.hprev[l];
+      EpiParams ex; ex.bias = P + o.bih[l];
+      TRY(sgemm(ctx, false, false, M, H4, H, h, H, P + o.Wih[l], H4, xg, H4, ex, s));
+      TLP_CUDA_TRY(cudaMemset2DAsync(hp, (size_t)c.L * H * sizeof(float), 0, (size_t)H * sizeof(float),
+                                     (size_t)n, s));  // h_{-1} = 0
+      for (int t = 0; t < c.L; ++t) {
+        EpiParams eh; eh.bias = P + o.bhh[l]; eh.resid = xg + t * H4; eh.ldr = c.L * H4;
+        TRY(sgemm(ctx, false, false, n, H4, H, hp + t * H, c.L * H, P + o.Whh[l], H4, gt + t * H4,
+                  c.L * H4, eh, s));
+        lstm_cell_fwd<<<(unsigned)cdiv(n * H, 256), 256, 0, s>>>(n, c.L, (int)H, t, gt, W + lay.cst[l], hp,
+                                                                 h, W + lay.hattn[l]);
+        TLP_LAUNCH_CHECK();
+      }
+      h = W + lay.hattn[l];
+    }
+    for (int l = 0; l < c.n_attn && c.backbone == 0; ++l) {
       float* qkv = W + lay.qkv[l];
       const int64_t wq[3] = {o.Wq[l], o.Wk[l], o.Wv[l]}, bq[3] = {o.bq[l], o.bk[l], o.bv[l]};
       for (int j = 0; j < 3; ++j) {
@@ -711,8 +802,30 @@ tlp_status simt_backward(tlp_ctx* ctx, int64_t N, const float* g, cudaStream_t s
     EpiParams ea; ea.accumulate = true;
     TRY(sgemm(ctx, false, true, M, H, H, dtmp, H, P + o.Wa[r], H, dh, H, ea, s));
   }
+  // R49 LSTM layers: backpropagation through time, then the batched weight gradients
+  for (int l = c.n_attn - 1; l >= 0 && c.backbone == 1; --l) {
+    const float* hin = l > 0 ? W + lay.hattn[l - 1] : (c.pos_enc ? W + lay.hpos : W + lay.up[c.n_up - 1]);
+    const int64_t H4 = 4 * H;
+    float* dG = W + lay.dG;
+    for (int t = c.L - 1; t >= 0; --t) {
+      lstm_cell_bwd<<<(unsigned)cdiv(N * H, 256), 256, 0, s>>>(N, c.L, (int)H, t, W + lay.gates[l],
+                                                               W + lay.cst[l], dh, W + lay.dhr,
+                                                               W + lay.dcar, dG);
+      TLP_LAUNCH_CHECK();
+      if (t > 0) {
+        EpiParams e0;
+        TRY(sgemm(ctx, false, true, N, H, H4, dG + t * H4, c.L * H4, P + o.Whh[l], H4, W + lay.dhr, H, e0, s));
+      }
+    }
+    TRY(sgemm_wgrad(ctx, M, H, H4, hin, H, dG, H4, G + o.Wih[l], s));
+    TRY(sgemm_wgrad(ctx, M, H, H4, W + lay.hprev[l], H, dG, H4, G + o.Whh[l], s));
+    TRY(colsum(ctx, M, H4, dG, H4, G + o.bih[l], s));
+    TLP_CUDA_TRY(cudaMemcpyAsync(G + o.bhh[l], G + o.bih[l], H4 * sizeof(float), cudaMemcpyDeviceToDevice, s));
+    EpiParams ea; ea.accumulate = true;
+    TRY(sgemm(ctx, false, true, M, H, H4, dG, H4, P + o.Wih[l], H4, dh, H, ea, s));
+  }
   // attention layers
-  for (int l = c.n_attn - 1; l >= 0; --l) {
+  for (int l = c.n_attn - 1; l >= 0 && c.backbone == 0; --l) {
     const float* hin = l > 0 ? W + lay.hattn[l - 1] : (c.pos_enc ? W + lay.hpos : W + lay.up[c.n_up - 1]);
     TRY(sgemm_wgrad(ctx, M, H, H, W + lay.O[l], H, dh, H, G + o.Wo[l], s));
     TRY(colsum(ctx, M, H, dh, H, G + o.bo[l], s));

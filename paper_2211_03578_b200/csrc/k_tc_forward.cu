@@ -834,7 +834,7 @@ struct TcWeights {
 };
 
 bool tc_supported(const tlp_config& c) {
-  return c.L == kL && c.E == kE && c.T == 11 && c.hidden == kH && c.n_up == 2 &&
+  return c.backbone == 0 && c.L == kL && c.E == kE && c.T == 11 && c.hidden == kH && c.n_up == 2 &&
          c.up_dims[0] == 128 && c.up_dims[1] == kH && c.attn_heads == kHeads &&
          c.head_dim == kHD && c.n_tasks <= TLP_MAX_TASKS;
 }

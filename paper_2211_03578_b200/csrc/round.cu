@@ -63,7 +63,7 @@ tlp_status tlp_search_round(tlp_ctx* ctx, const tlp_seq_batch* h, int64_t N,
   if (head < 0 || head >= c.n_tasks) return round_fail(ctx, TLP_ERR_ARG, "tlp_search_round: bad head");
   if (!ctx->have_scales) return round_fail(ctx, TLP_ERR_STATE, "tlp_set_norm_scales first");
   if (!ctx->have_params) return round_fail(ctx, TLP_ERR_STATE, "tlp_set_params first");
-  if (c.precision == TLP_PREC_BF16 && !tc_supported(c))
+  if (!score_supported(c))
     return round_fail(ctx, TLP_ERR_UNSUPPORTED, "bf16 scoring needs the paper shape");
   if (task_off[0] < 0 || task_off[T] > N)
     return round_fail(ctx, TLP_ERR_SHAPE, "tlp_search_round: task_off outside [0, N]");

@@ -33,6 +33,8 @@ struct ParamOffsets {
   int64_t Wv[TLP_MAX_ATTN], bv[TLP_MAX_ATTN], Wo[TLP_MAX_ATTN], bo[TLP_MAX_ATTN];
   int64_t Wa[TLP_MAX_RES], a[TLP_MAX_RES], Wb[TLP_MAX_RES], b[TLP_MAX_RES];
   int64_t W1[TLP_MAX_TASKS], c1[TLP_MAX_TASKS], w2[TLP_MAX_TASKS], c2[TLP_MAX_TASKS];
+  // R49 LSTM layers (backbone == 1) in place of the attention layers
+  int64_t Wih[TLP_MAX_ATTN], bih[TLP_MAX_ATTN], Whh[TLP_MAX_ATTN], bhh[TLP_MAX_ATTN];
   int64_t total;
 };
 
@@ -212,6 +214,11 @@ tlp_status adam_launch(tlp_ctx* ctx, cudaStream_t s);
 
 // k_tc_forward.cu : bf16 tcgen05 fused forward
 bool tc_supported(const tlp_config& c);
+// scoring is available: fp32, the fused bf16 kernel, or (LSTM, NEXT-4) the
+// layer-by-layer bf16x3 GEMM path
+inline bool score_supported(const tlp_config& c) {
+  return c.precision != TLP_PREC_BF16 || c.backbone == 1 || tc_supported(c);
+}
 tlp_status tc_prepare(tlp_ctx* ctx, cudaStream_t s);
 tlp_status tc_forward(tlp_ctx* ctx, const float* feats, int64_t N, float* scores, cudaStream_t s);
 void tc_free(tlp_ctx* ctx);

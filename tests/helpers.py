@@ -22,7 +22,7 @@ def product_cfg(ocfg: OM.Config, precision="fp32"):
     return TLPConfig(L=ocfg.L, E=ocfg.E, T=ocfg.T, hidden=ocfg.hidden, up_dims=tuple(ocfg.up_dims),
                      attn_heads=ocfg.attn_heads, n_attn=ocfg.n_attn, n_res=ocfg.n_res,
                      head_dim=ocfg.head_dim, n_tasks=ocfg.n_tasks, precision=precision,
-                     attn_mask=ocfg.attn_mask, pos_enc=ocfg.pos_enc)
+                     attn_mask=ocfg.attn_mask, pos_enc=ocfg.pos_enc, backbone=ocfg.backbone)
 
 
 def flat_params(ocfg: OM.Config, seed: int, scale: float = 1.0, bf16: bool = True) -> np.ndarray:
