@@ -24,7 +24,7 @@ PR = os.path.join(ROOT, "profiles")
 
 
 def short(name: str) -> str:
-    m = re.search(r"(\w+_kernel\w*|\w+_partial\w*|reduce_partials|label_kernel|finalize_\w+|sum_counts|resolve_tokens|pack_kernel)", name)
+    m = re.search(r"(\w+_kernel\w*|\w+_partial\w*|reduce_partials|label_kernel|finalize_\w+|sum_counts|resolve_tokens|pack_kernel|lstm_cell_\w+)", name)
     k = m.group(1) if m else name.split("(")[0][:40]
     t = re.search(r"<([^>]*)>", name)
     if t and ("gemm" in k or "attn" in k or "encode" in k):
@@ -57,6 +57,32 @@ def launches(tag: str):
     for k, v in sorted(agg.items(), key=lambda kv: -kv[1]):
         w.writerow([k, cnt[k], "%.4f" % (v / 1e6), "%.4f" % (v / tot)])
     return out.getvalue(), tot
+
+
+def tune_round_launches(tag: str):
+    """Launch list of one NEXT-1 device tuning round (tlp_ga_round): the
+    launches between the last two ga_init_kernel launches of the bench."""
+    path = os.path.join(GO, tag + "_launches.csv")
+    rows = list(csv.reader(open(path)))
+    start = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
+    hdr = rows[start]
+    ik, iv = hdr.index("Kernel Name"), hdr.index("Metric Value")
+    data = rows[start + 1:]
+    inits = [i for i, r in enumerate(data) if "ga_init_kernel" in r[ik]]
+    if len(inits) < 2:
+        return None
+    agg, cnt = collections.OrderedDict(), collections.Counter()
+    for r in data[inits[-2]:inits[-1]]:
+        k = short(r[ik])
+        agg[k] = agg.get(k, 0.0) + float(r[iv].replace(",", ""))
+        cnt[k] += 1
+    tot = sum(agg.values())
+    out = io.StringIO()
+    w = csv.writer(out)
+    w.writerow(["kernel", "launches", "total_ms", "share_of_round"])
+    for k, v in sorted(agg.items(), key=lambda kv: -kv[1]):
+        w.writerow([k, cnt[k], "%.4f" % (v / 1e6), "%.4f" % (v / tot)])
+    return out.getvalue()
 
 
 def raw_metrics(rep: str):
@@ -105,6 +131,10 @@ def main():
     os.makedirs(PR, exist_ok=True)
     csv_txt, tot = launches(tag)
     open(os.path.join(PR, tag + "_launches.csv"), "w").write(csv_txt)
+    tr = tune_round_launches(tag)
+    if tr:
+        open(os.path.join(PR, tag + "_tune_round_launches.csv"), "w").write(tr)
+        print(tr)
     md, traffic = kernels(tag)
     open(os.path.join(PR, tag + "_kernels.md"), "w").write(md)
     json.dump(traffic, open(os.path.join(PR, tag + "_traffic.json"), "w"), indent=1)
