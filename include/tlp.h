@@ -317,6 +317,9 @@ typedef struct {
   const double* dom_num;    /* HOST [D]: numeric value (knob on a Number argument) */
   const int32_t* dom_name;  /* HOST [D]: string index into tmpl's string table (knob on a NameParam
                                argument), -1 for numbers; must match the skeleton's arg_kind */
+  int32_t id_base;          /* global id of subgraph 0: every random-number counter uses
+                               id_base + s (R44), so a space sharded across ranks in contiguous
+                               blocks draws exactly what the unsharded space draws */
 } tlp_ga_space;
 
 /* Copy a search space into ctx-owned device memory (replaces any previous one).

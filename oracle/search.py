@@ -205,11 +205,13 @@ def search_round(tmpl, s: int, cost_model: CostModel, seed: int, rnd: int, n_pop
 
 def tune(templates, cost_model: CostModel, latency: Callable[[int, np.ndarray], float],
          rounds: int, measure: int, seed: int, n_pop: int, n_child: int, iters: int,
-         p_cross: float, p_mut: float) -> Dict[str, list]:
+         p_cross: float, p_mut: float, ids: Sequence[int] | None = None) -> Dict[str, list]:
     """Round-robin over the subgraphs: every round every subgraph
     runs search_round and measures its first `measure` never-measured
     survivors.  Returns the trajectory: per round the measurements spent and
-    the best measured latency per subgraph so far."""
+    the best measured latency per subgraph so far.  ``ids`` are the subgraphs'
+    global ids (the random-number counters and the callables' first argument;
+    default 0..S-1)."""
     S = len(templates)
     seen: List[Dict[Tuple[int, ...], float]] = [dict() for _ in range(S)]
     best = [float("inf")] * S
@@ -218,7 +220,8 @@ def tune(templates, cost_model: CostModel, latency: Callable[[int, np.ndarray], 
     for rnd in range(rounds):
         picked = []
         for s in range(S):
-            pop, ps = search_round(templates[s], s, cost_model, seed, rnd, n_pop, n_child, iters,
+            sid = s if ids is None else int(ids[s])
+            pop, ps = search_round(templates[s], sid, cost_model, seed, rnd, n_pop, n_child, iters,
                                    p_cross, p_mut)
             got = 0
             for row, sc in zip(pop, ps):
@@ -229,10 +232,10 @@ def tune(templates, cost_model: CostModel, latency: Callable[[int, np.ndarray], 
                 key = tuple(int(v) for v in row)
                 if key in seen[s]:
                     continue
-                lat = float(latency(s, row))
+                lat = float(latency(sid, row))
                 seen[s][key] = lat
                 best[s] = min(best[s], lat)
-                picked.append((s, key, lat))
+                picked.append((sid, key, lat))
                 got += 1
                 total += 1
         traj["measurements"].append(total)

@@ -381,10 +381,11 @@ class TLP:
         return out
 
     # ---------------------------------------------------------------- NEXT-1
-    def ga_set_space(self, space):
+    def ga_set_space(self, space, id_base: int = 0):
         """tlp_ga_set_space from a host search space (any object with the
         fields of synth.PackedSpace: tmpl (packed batch), knob_off, knob_arg,
-        knob_grp, dom_off, dom_num, dom_name)."""
+        knob_grp, dom_off, dom_num, dom_name); id_base = global id of its
+        first subgraph (sharded tuning, dist.shard_subgraphs)."""
         arrs = DeviceBatch.host_arrays(space.tmpl)
         keep = dict(arrs)
         keep["knob_off"] = np.ascontiguousarray(space.knob_off, np.int64)
@@ -400,6 +401,7 @@ class TLP:
         t.str_blob, t.str_off = keep["str_blob"].ctypes.data, keep["str_off"].ctypes.data
         t.P, t.A, t.U = len(arrs["prim_type"]), len(arrs["arg_kind"]), len(arrs["str_off"]) - 1
         sp.S = len(keep["knob_off"]) - 1
+        sp.id_base = id_base
         for k in ("knob_off", "knob_arg", "knob_grp", "dom_off", "dom_num", "dom_name"):
             setattr(sp, k, keep[k].ctypes.data)
         self._check(self.lib.tlp_ga_set_space(self.h, C.byref(sp)))

@@ -42,7 +42,7 @@ class tlp_seq_batch(C.Structure):
 class tlp_ga_space(C.Structure):
     _fields_ = [("tmpl", tlp_seq_batch), ("S", C.c_int32), ("knob_off", C.c_void_p),
                 ("knob_arg", C.c_void_p), ("knob_grp", C.c_void_p), ("dom_off", C.c_void_p),
-                ("dom_num", C.c_void_p), ("dom_name", C.c_void_p)]
+                ("dom_num", C.c_void_p), ("dom_name", C.c_void_p), ("id_base", C.c_int32)]
 
 
 _lib = None

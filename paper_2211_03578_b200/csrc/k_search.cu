@@ -66,7 +66,8 @@ __device__ __forceinline__ Philox4 ga_block(uint64_t seed, int64_t c, int s, int
 __device__ __forceinline__ uint64_t uniform_index(uint64_t w, uint64_t n) { return __umul64hi(w, n); }
 
 __global__ void ga_init_kernel(const int64_t* __restrict__ knob_off, const int64_t* __restrict__ dom_off,
-                               int S, int n, int G, uint64_t seed, int rnd, uint8_t* __restrict__ genes) {
+                               int S, int n, int G, int id_base, uint64_t seed, int rnd,
+                               uint8_t* __restrict__ genes) {
   const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (row >= (int64_t)S * n) return;
   const int s = (int)(row / n);
@@ -76,7 +77,7 @@ __global__ void ga_init_kernel(const int64_t* __restrict__ knob_off, const int64
   uint8_t* out = genes + row * G;
   for (int b = 0; b * 4 < G; ++b) {
     Philox4 r{};
-    if (b * 4 < K) r = ga_block(seed, c, s, rnd, 0, kStreamInit, b);
+    if (b * 4 < K) r = ga_block(seed, c, id_base + s, rnd, 0, kStreamInit, b);
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int j = b * 4 + q;
@@ -101,7 +102,7 @@ __device__ __forceinline__ int select_rank(uint64_t u, int64_t n) {
 }
 
 __global__ void ga_evolve_kernel(const int64_t* __restrict__ knob_off, const int64_t* __restrict__ dom_off,
-                                 const int32_t* __restrict__ knob_grp, int S, int G,
+                                 const int32_t* __restrict__ knob_grp, int S, int G, int id_base,
                                  const uint8_t* __restrict__ pop, const float* __restrict__ pop_scores,
                                  int n_pop, int n_child, uint64_t th_cross, uint64_t th_mut,
                                  uint64_t seed, int rnd, int it, uint8_t* __restrict__ child) {
@@ -120,7 +121,7 @@ __global__ void ga_evolve_kernel(const int64_t* __restrict__ knob_off, const int
   }
   const int64_t n_eff = lo > 0 ? lo : 1;
   const uint64_t F = (uint64_t)(n_eff * (n_eff + 1) / 2);
-  const Philox4 sel = ga_block(seed, c, s, rnd, it, kStreamSel, 0);
+  const Philox4 sel = ga_block(seed, c, id_base + s, rnd, it, kStreamSel, 0);
   const int ra = select_rank(uniform_index(sel.w[0], F), n_eff);
   const int rb = select_rank(uniform_index(sel.w[1], F), n_eff);
   const uint8_t* A = pop + ((int64_t)s * n_pop + ra) * G;
@@ -136,7 +137,7 @@ __global__ void ga_evolve_kernel(const int64_t* __restrict__ knob_off, const int
   }
   if (th_mut > 0) {
     for (int b = 0; b * 4 < K; ++b) {
-      const Philox4 m = ga_block(seed, c, s, rnd, it, kStreamMut, b);
+      const Philox4 m = ga_block(seed, c, id_base + s, rnd, it, kStreamMut, b);
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int j = b * 4 + q;
@@ -324,7 +325,7 @@ size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 // ctx-owned device copy of the search space (tlp_ga_set_space)
 struct GaSpace {
-  int S = 0, G = 0, U = 0;
+  int S = 0, G = 0, U = 0, id_base = 0;
   int64_t Ptot = 0, Atot = 0;  // skeleton primitives / arguments over all subgraphs
   DevBuf mem;
   TmplView t{};
@@ -399,7 +400,7 @@ tlp_status evolve_launch(tlp_ctx* ctx, const uint8_t* pop, const float* pop_scor
   const int64_t N = (int64_t)g.S * n_child;
   if (N == 0) return TLP_OK;
   ga_evolve_kernel<<<(unsigned)cdiv(N, 128), 128, 0, s>>>(
-      g.knob_off, g.dom_off, g.knob_grp, g.S, g.G, pop, pop_scores, n_pop, n_child,
+      g.knob_off, g.dom_off, g.knob_grp, g.S, g.G, g.id_base, pop, pop_scores, n_pop, n_child,
       threshold53(p_cross), threshold53(p_mut), seed, rnd, it, child);
   TLP_LAUNCH_CHECK();
   return TLP_OK;
@@ -409,8 +410,8 @@ tlp_status init_launch(tlp_ctx* ctx, int n, uint64_t seed, int rnd, uint8_t* gen
   GaSpace& g = *ctx->ga;
   const int64_t N = (int64_t)g.S * n;
   if (N == 0 || g.G == 0) return TLP_OK;
-  ga_init_kernel<<<(unsigned)cdiv(N, 128), 128, 0, s>>>(g.knob_off, g.dom_off, g.S, n, g.G, seed,
-                                                         rnd, genes);
+  ga_init_kernel<<<(unsigned)cdiv(N, 128), 128, 0, s>>>(g.knob_off, g.dom_off, g.S, n, g.G, g.id_base,
+                                                         seed, rnd, genes);
   TLP_LAUNCH_CHECK();
   return TLP_OK;
 }
@@ -421,7 +422,7 @@ extern "C" {
 
 tlp_status tlp_ga_set_space(tlp_ctx* ctx, const tlp_ga_space* h) {
   if (!ctx) return TLP_ERR_ARG;
-  if (!h || h->S < 1 || !h->knob_off || !h->tmpl.seq_off || !h->tmpl.arg_off)
+  if (!h || h->S < 1 || h->id_base < 0 || !h->knob_off || !h->tmpl.seq_off || !h->tmpl.arg_off)
     return ga_fail(ctx, TLP_ERR_ARG, "tlp_ga_set_space: null pointer or S < 1");
   const tlp_seq_batch& t = h->tmpl;
   const int S = h->S;
@@ -495,7 +496,7 @@ tlp_status tlp_ga_set_space(tlp_ctx* ctx, const tlp_ga_space* h) {
     TLP_CUDA_TRY(put(o_so, t.str_off, 8 * (t.U + 1)));
     TLP_CUDA_TRY(put(o_sb, t.str_blob, blob));
   }
-  g.S = S; g.G = G; g.U = t.U; g.Ptot = t.P; g.Atot = t.A;
+  g.S = S; g.G = G; g.U = t.U; g.Ptot = t.P; g.Atot = t.A; g.id_base = h->id_base;
   g.t = TmplView{reinterpret_cast<const int64_t*>(b + o_seq), b + o_pt,
                  reinterpret_cast<const int64_t*>(b + o_ao), b + o_ak,
                  reinterpret_cast<const double*>(b + o_an), reinterpret_cast<const int32_t*>(b + o_am)};

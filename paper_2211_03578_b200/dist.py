@@ -29,6 +29,14 @@ def shard_range(n: int, world: int, rank: int, align: int = TILE) -> Tuple[int, 
     return min(n, lo_u * align), min(n, hi_u * align)
 
 
+def shard_subgraphs(n_subgraphs: int, world: int, rank: int) -> Tuple[int, int]:
+    """[lo, hi) of rank's contiguous block of subgraphs for the sharded tuning
+    round (NEXT-1): a rank sets its block with id_base = lo, so every random
+    draw (counter = global subgraph id, R44) and hence every survivor equals
+    the unsharded run's; no collective on the data path."""
+    return shard_range(n_subgraphs, world, rank, align=1)
+
+
 def local_task_off(task_off: Sequence[int], lo: int, hi: int) -> np.ndarray:
     """Task segment offsets restricted to the shard [lo, hi), rebased to 0."""
     t = np.asarray(task_off, np.int64)

@@ -115,3 +115,55 @@ def test_assign_groups_partitions_all_groups():
     assert np.array_equal(allg, np.arange(37))
     loads = [int(np.diff(goff)[p].sum()) for p in parts]
     assert max(loads) - min(loads) <= 4000
+
+
+# ---------------------------------------------------------------- NEXT-1 sharded tuning
+def _tune_worker(rank, world, port, q):
+    """Each rank tunes its contiguous block of subgraphs (dist.shard_subgraphs)
+    with global ids; Tuner-style gather of the per-subgraph bests over gloo."""
+    import synth
+    from oracle import search as OS
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        S = 5
+        ts = [synth.make_template(41, s) for s in range(S)]
+        lo, hi = D.shard_subgraphs(S, world, rank)
+        lat = lambda s, g: float(synth.template_latency(ts[s], g, 41, s)[0])  # noqa: E731
+        cost = lambda s, g: -np.log(synth.template_latency(ts[s], g, 41, s)) + 0.2 * np.cos(g.sum(1))  # noqa: E731
+        traj = OS.tune(ts[lo:hi], cost, lat, rounds=2, measure=3, seed=4, n_pop=8, n_child=16, iters=2,
+                       p_cross=0.5, p_mut=0.3, ids=list(range(lo, hi)))
+        parts = [None] * world
+        dist.all_gather_object(parts, (lo, traj["best"][-1], [m for r in traj["measured"] for m in r]))
+        q.put((rank, sorted(parts, key=lambda x: x[0])))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_tuning_equals_unsharded():
+    import synth
+    from oracle import search as OS
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_tune_worker, args=(r, WORLD, port, q)) for r in range(WORLD)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    S = 5
+    ts = [synth.make_template(41, s) for s in range(S)]
+    lat = lambda s, g: float(synth.template_latency(ts[s], g, 41, s)[0])  # noqa: E731
+    cost = lambda s, g: -np.log(synth.template_latency(ts[s], g, 41, s)) + 0.2 * np.cos(g.sum(1))  # noqa: E731
+    full = OS.tune(ts, cost, lat, rounds=2, measure=3, seed=4, n_pop=8, n_child=16, iters=2,
+                   p_cross=0.5, p_mut=0.3)
+    for rank in range(WORLD):
+        parts = res[rank]
+        best = [b for _, bs, _ in parts for b in bs]
+        assert best == full["best"][-1]
+        measured = sorted(m for _, _, ms in parts for m in ms)
+        assert measured == sorted(m for r in full["measured"] for m in r)
+    assert [D.shard_subgraphs(S, WORLD, r) for r in range(WORLD)] == [(0, 3), (3, 5)]

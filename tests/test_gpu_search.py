@@ -243,3 +243,27 @@ def test_paper_shape_bf16_round(tp):
         assert (np.diff(v) <= 0).all()
         ref = OM.forward(ocfg, params, oracle.encode(OS.materialize(ts[s], rows[s]), tokens, scale))[:, 0]
         assert rel_err(v, ref) <= 1e-2
+
+
+def test_sharded_device_rounds_equal_the_full_round(env, tp):
+    """Multi-GPU protocol on one GPU: two contexts, each with a contiguous
+    block of the subgraphs (dist.shard_subgraphs, id_base = its first global
+    id), produce exactly the full space's survivors (no exchange step)."""
+    from paper_2211_03578_b200 import dist as D
+    m = env["m"]
+    S, n_pop = 5, 16
+    ts = [synth.make_template(43, s) for s in range(S)]
+    m.ga_set_space(synth.pack_space(ts))
+    g_full, s_full = m.ga_round(n_pop, 48, 2, 0.5, 0.2, seed=3, rnd=1)
+    g_full = g_full.cpu().numpy().reshape(S, n_pop, -1)
+    s_full = s_full.cpu().numpy().reshape(S, n_pop)
+    for rank in range(2):
+        lo, hi = D.shard_subgraphs(S, 2, rank)
+        m.ga_set_space(synth.pack_space(ts[lo:hi]), id_base=lo)
+        g, sc = m.ga_round(n_pop, 48, 2, 0.5, 0.2, seed=3, rnd=1)
+        g = g.cpu().numpy().reshape(hi - lo, n_pop, -1)
+        sc = sc.cpu().numpy().reshape(hi - lo, n_pop)
+        for j, s in enumerate(range(lo, hi)):
+            K = ts[s].G
+            assert np.array_equal(g[j][:, :K], g_full[s][:, :K])
+            assert np.array_equal(sc[j].view(np.uint32), s_full[s].view(np.uint32))
