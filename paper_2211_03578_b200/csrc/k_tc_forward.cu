@@ -774,6 +774,11 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
             a.scores[nn * NT + t] = s2 + (float)kL * vs[a.c2[t]];
           }
         }
+        // rowdot is rewritten by the next task / tile: order the fixed-order
+        // sums above before any later write with a CTA barrier (the epilogue ->
+        // MMA -> epilogue mbarrier chain already orders them, through the
+        // warp-aggregated arrivals, but racecheck cannot follow that chain)
+        asm volatile("bar.sync 1, 256;" ::: "memory");
         if (t < NT - 1) signal();
       }
     }

@@ -2,7 +2,8 @@
 racecheck / synccheck): encode -> score (fp32 + bf16 fused, with and without the
 padding mask / positional table) -> top-k -> labels -> train steps (LambdaRank
 and MSE; fp32 and bf16 contexts, incl. the B-image and wgrad GEMMs) -> top-k
-merge -> tlp_search_round -> tlp_dedup -> tlp_topk_score."""
+merge -> tlp_search_round -> tlp_dedup -> tlp_topk_score; NEXT-1 device tuning
+rounds (fp32 and bf16 scoring) and NEXT-4 LSTM contexts (score + train)."""
 import os
 import sys
 
@@ -49,4 +50,25 @@ Xb = torch.rand((64, 25, 22), device="cuda")
 yb = torch.rand((64, 1), device="cuda") + 0.01
 big.train_step(Xb, yb, np.array([0, 32, 64], np.int64))
 big.sync()
+# NEXT-1: device tuning rounds (GA kernels + dedup + materialise -> encode -> score -> top-k)
+ts = [synth.make_template(5, s) for s in range(3)] + [synth.small_template((2, 3))]
+for prec, cfg in (("fp32", OM.Config(hidden=64, up_dims=(32, 64), head_dim=32)), ("bf16", OM.Config(n_attn=2))):
+    m = tp.TLP(tp.TLPConfig(hidden=cfg.hidden, up_dims=cfg.up_dims, head_dim=cfg.head_dim,
+                            n_attn=cfg.n_attn, precision=prec))
+    m.set_token_table(names)
+    m.set_norm_scales(np.full(22, 8.0, np.float32))
+    m.set_params(np.concatenate([v.ravel() for v in synth.init_params(3, OM.param_shapes(cfg))]).astype(np.float32))
+    m.ga_set_space(synth.pack_space(ts), id_base=2)
+    m.ga_round(8, 24, 2, 0.5, 0.3, seed=1, rnd=0)
+    m.sync()
+# NEXT-4: LSTM contexts
+for prec in ("fp32", "bf16"):
+    cfg = OM.Config(hidden=64, up_dims=(32, 64), head_dim=32, n_attn=2, backbone="lstm")
+    m = tp.TLP(tp.TLPConfig(hidden=64, up_dims=(32, 64), head_dim=32, n_attn=2, precision=prec,
+                            backbone="lstm"))
+    m.set_params(np.concatenate([v.ravel() for v in synth.init_params(4, OM.param_shapes(cfg))]).astype(np.float32))
+    Xl = torch.rand((23, 25, 22), device="cuda")
+    m.score(Xl)
+    m.train_step(Xl, torch.rand((23, 1), device="cuda") + 0.01, off)
+    m.sync()
 print("sanitize smoke ok")
