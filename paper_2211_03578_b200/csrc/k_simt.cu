@@ -655,6 +655,27 @@ tlp_status sgemm_wgrad(tlp_ctx* ctx, int64_t M, int64_t K, int64_t N, const floa
   return TLP_OK;
 }
 
+tlp_status sgemm_wgrad_bias(tlp_ctx* ctx, int64_t M, int64_t K, int64_t N, const float* A, int64_t lda,
+                            const float* dY, int64_t lddy, float* dW, float* db, cudaStream_t s) {
+  const int64_t slice = 2048;
+  const int Z = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(M, slice), 256));
+  const int64_t kslice = cdiv(cdiv(M, Z), BK) * BK;
+  if (ctx->cfg.precision == TLP_PREC_BF16 && db == dW + K * N && Z > 1) {
+    TLP_CUDA_TRY(ctx->ws_partial.ensure((size_t)Z * (K + 1) * N * sizeof(float)));
+    float* part = ctx->ws_partial.as<float>();
+    tlp_status st = TLP_OK;
+    if (tc_wgrad_bias(ctx, K, N, M, A, lda, dY, lddy, part, Z, kslice, s, &st)) {
+      if (st != TLP_OK) return st;
+      reduce_partials<<<(unsigned)cdiv((K + 1) * N, 256), 256, 0, s>>>(part, (K + 1) * N, Z, dW);
+      TLP_LAUNCH_CHECK();
+      return TLP_OK;
+    }
+  }
+  tlp_status st = sgemm_wgrad(ctx, M, K, N, A, lda, dY, lddy, dW, s);
+  if (st != TLP_OK) return st;
+  return colsum(ctx, M, N, dY, lddy, db, s);
+}
+
 tlp_status colsum(tlp_ctx* ctx, int64_t M, int64_t N, const float* X, int64_t ldx, float* out,
                   cudaStream_t s) {
   const int64_t rows = 256;
@@ -780,8 +801,7 @@ tlp_status simt_backward(tlp_ctx* ctx, int64_t N, const float* g, cudaStream_t s
     head_bwd_kernel<<<(unsigned)cdiv(M * hd, 256), 256, 0, s>>>(W + lay.U[t], c.L, hd, N,
                                                                 P + o.w2[t], g, t, c.n_tasks, dU);
     TLP_LAUNCH_CHECK();
-    TRY(sgemm_wgrad(ctx, M, H, hd, hfin, H, dU, hd, G + o.W1[t], s));
-    TRY(colsum(ctx, M, hd, dU, hd, G + o.c1[t], s));
+    TRY(sgemm_wgrad_bias(ctx, M, H, hd, hfin, H, dU, hd, G + o.W1[t], G + o.c1[t], s));
     TRY(sgemm_wgrad(ctx, N, hd, 1, W + lay.pooled[t], hd, g + t, c.n_tasks, G + o.w2[t], s));
     dc2_kernel<<<1, 256, 0, s>>>(g, N, t, c.n_tasks, c.L, G + o.c2[t]);
     TLP_LAUNCH_CHECK();
@@ -793,12 +813,10 @@ tlp_status simt_backward(tlp_ctx* ctx, int64_t N, const float* g, cudaStream_t s
     const float* hin = r > 0 ? W + lay.hres[r - 1]
                      : (c.n_attn ? W + lay.hattn[c.n_attn - 1] : (c.pos_enc ? W + lay.hpos : W + lay.up[c.n_up - 1]));
     const float* rr = W + lay.r[r];
-    TRY(sgemm_wgrad(ctx, M, H, H, rr, H, dh, H, G + o.Wb[r], s));
-    TRY(colsum(ctx, M, H, dh, H, G + o.b[r], s));
+    TRY(sgemm_wgrad_bias(ctx, M, H, H, rr, H, dh, H, G + o.Wb[r], G + o.b[r], s));
     EpiParams em; em.mask = rr; em.ldm = H;
     TRY(sgemm(ctx, false, true, M, H, H, dh, H, P + o.Wb[r], H, dtmp, H, em, s));
-    TRY(sgemm_wgrad(ctx, M, H, H, hin, H, dtmp, H, G + o.Wa[r], s));
-    TRY(colsum(ctx, M, H, dtmp, H, G + o.a[r], s));
+    TRY(sgemm_wgrad_bias(ctx, M, H, H, hin, H, dtmp, H, G + o.Wa[r], G + o.a[r], s));
     EpiParams ea; ea.accumulate = true;
     TRY(sgemm(ctx, false, true, M, H, H, dtmp, H, P + o.Wa[r], H, dh, H, ea, s));
   }
@@ -827,15 +845,13 @@ tlp_status simt_backward(tlp_ctx* ctx, int64_t N, const float* g, cudaStream_t s
   // attention layers
   for (int l = c.n_attn - 1; l >= 0 && c.backbone == 0; --l) {
     const float* hin = l > 0 ? W + lay.hattn[l - 1] : (c.pos_enc ? W + lay.hpos : W + lay.up[c.n_up - 1]);
-    TRY(sgemm_wgrad(ctx, M, H, H, W + lay.O[l], H, dh, H, G + o.Wo[l], s));
-    TRY(colsum(ctx, M, H, dh, H, G + o.bo[l], s));
+    TRY(sgemm_wgrad_bias(ctx, M, H, H, W + lay.O[l], H, dh, H, G + o.Wo[l], G + o.bo[l], s));
     EpiParams e0;
     TRY(sgemm(ctx, false, true, M, H, H, dh, H, P + o.Wo[l], H, dtmp, H, e0, s));  // dO
     TRY(attn_bwd(ctx, W + lay.qkv[l], W + lay.A[l], dtmp, N, dqkv, s));
     const int64_t wq[3] = {o.Wq[l], o.Wk[l], o.Wv[l]}, bq[3] = {o.bq[l], o.bk[l], o.bv[l]};
     for (int j = 0; j < 3; ++j) {
-      TRY(sgemm_wgrad(ctx, M, H, H, hin, H, dqkv + j * H, 3 * H, G + wq[j], s));
-      TRY(colsum(ctx, M, H, dqkv + j * H, 3 * H, G + bq[j], s));
+      TRY(sgemm_wgrad_bias(ctx, M, H, H, hin, H, dqkv + j * H, 3 * H, G + wq[j], G + bq[j], s));
       EpiParams ea; ea.accumulate = true;
       TRY(sgemm(ctx, false, true, M, H, H, dqkv + j * H, 3 * H, P + wq[j], H, dh, H, ea, s));
     }
@@ -853,8 +869,7 @@ tlp_status simt_backward(tlp_ctx* ctx, int64_t N, const float* g, cudaStream_t s
     relu_mask_inplace<<<(unsigned)cdiv(M * w, 256), 256, 0, s>>>(cur, W + lay.up[i], M * w);
     TLP_LAUNCH_CHECK();
     const float* xin = i > 0 ? W + lay.up[i - 1] : ctx->train_X;
-    TRY(sgemm_wgrad(ctx, M, din, w, xin, din, cur, w, G + o.up_W[i], s));
-    TRY(colsum(ctx, M, w, cur, w, G + o.up_b[i], s));
+    TRY(sgemm_wgrad_bias(ctx, M, din, w, xin, din, cur, w, G + o.up_W[i], G + o.up_b[i], s));
     if (i > 0) {
       float* nxt = (cur == dh) ? dtmp : dh;
       EpiParams e0;

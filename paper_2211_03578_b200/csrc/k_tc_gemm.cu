@@ -473,7 +473,8 @@ __global__ void __launch_bounds__(THREADS, 1) tc_wgrad_kernel(int64_t M, int64_t
                                                                const float* __restrict__ A, int64_t lda,
                                                                const float* __restrict__ B, int64_t ldb,
                                                                float* __restrict__ part, int64_t ldc,
-                                                               int64_t kslice, int avec, int bvec) {
+                                                               int64_t kslice, int avec, int bvec,
+                                                               int colsum) {
   extern __shared__ __align__(128) uint8_t smem[];
   const uint32_t sb = tc::smem_u32(smem);
   const uint32_t bar = sb + STAGES * WSTAGE;
@@ -496,9 +497,24 @@ __global__ void __launch_bounds__(THREADS, 1) tc_wgrad_kernel(int64_t M, int64_t
   const Src sa{A, lda, M, 0, avec != 0};
   const Src sbb{B, ldb, N, 0, bvec != 0};
   float4 ra[WCH], rb[WCH];
+  // colsum: the bias gradient 1^T B of this slice rides along -- every thread
+  // always moves the same columns (chunk_rk), so it sums its chunks over the
+  // K tiles in order, then a fixed-order reduction over the 32 tile rows
+  float4 cs[WCH];
+#pragma unroll
+  for (int i = 0; i < WCH; ++i) cs[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  auto col_acc = [&]() {
+    if (colsum) {
+#pragma unroll
+      for (int i = 0; i < WCH; ++i) {
+        cs[i].x += rb[i].x; cs[i].y += rb[i].y; cs[i].z += rb[i].z; cs[i].w += rb[i].w;
+      }
+    }
+  };
   if (nk > 0) {
     load_regs<false, WROWS>(sa, kb, ke, ra);
     load_regs<false, WROWS>(sbb, kb, ke, rb);
+    col_acc();
     store_smem<false, WROWS>(smem, smem + WT, ra);
     store_smem<false, WROWS>(smem + 2 * WT, smem + 3 * WT, rb);
     if (nk > 1) {
@@ -535,6 +551,7 @@ __global__ void __launch_bounds__(THREADS, 1) tc_wgrad_kernel(int64_t M, int64_t
       const int ns = (it + 1) % STAGES;
       if (it + 1 >= STAGES) tc::mbar_wait(bar + 8 * ns, (uint32_t)(((it + 1 - STAGES) / STAGES) & 1));
       uint8_t* st = smem + ns * WSTAGE;
+      col_acc();
       store_smem<false, WROWS>(st, st + WT, ra);
       store_smem<false, WROWS>(st + 2 * WT, st + 3 * WT, rb);
       if (it + 2 < nk) {
@@ -550,7 +567,8 @@ __global__ void __launch_bounds__(THREADS, 1) tc_wgrad_kernel(int64_t M, int64_t
   tc::tc_fence_after();
   __syncthreads();
   // epilogue: raw partial sums, TMEM -> smem transpose -> coalesced rows of part[z]
-  float* Pz = part + (int64_t)blockIdx.z * M * ldc;
+  // (with colsum, part[z] has M + 1 rows: row M is the slice's column sum)
+  float* Pz = part + (int64_t)blockIdx.z * (M + (colsum ? 1 : 0)) * ldc;
   float* stage = reinterpret_cast<float*>(smem);
   constexpr int EPI_COLS = 64, EPI_LD = 68;
   const int q = warp & 3, hh = warp >> 2;
@@ -576,6 +594,21 @@ __global__ void __launch_bounds__(THREADS, 1) tc_wgrad_kernel(int64_t M, int64_t
       __syncthreads();
       epi_store_slab(stage, EPI_LD, mh * BM, M, p * EPI_COLS, N, Pz, ldc, none, true);
       __syncthreads();
+    }
+  }
+  if (colsum) {
+    float* red = reinterpret_cast<float*>(smem);  // [32 tile rows][WROWS columns]
+#pragma unroll
+    for (int i = 0; i < WCH; ++i) {
+      int r, k;
+      chunk_rk<false, WROWS>(i, r, k);
+      *reinterpret_cast<float4*>(red + k * WROWS + r) = cs[i];
+    }
+    __syncthreads();
+    for (int c = tid; c < N; c += THREADS) {
+      float sum = 0.f;
+      for (int k = 0; k < BK; ++k) sum += red[k * WROWS + c];  // fixed order
+      Pz[M * ldc + c] = sum;
     }
   }
   tc::tc_fence_before();
@@ -612,7 +645,7 @@ tlp_status tc_gemm(tlp_ctx* ctx, bool ta, bool tb, int64_t M, int64_t N, int64_t
     }
     const int av = aligned16(A) && lda % 4 == 0, bv = aligned16(B) && ldb % 4 == 0;
     tc_wgrad_kernel<<<dim3(1, 1, (unsigned)splits), THREADS, WSMEM, s>>>(M, N, K, A, lda, B, ldb, C,
-                                                                         ldc, kslice, av, bv);
+                                                                         ldc, kslice, av, bv, 0);
     TLP_LAUNCH_CHECK();
     return TLP_OK;
   }
@@ -642,6 +675,33 @@ tlp_status tc_gemm(tlp_ctx* ctx, bool ta, bool tb, int64_t M, int64_t N, int64_t
   else tc_gemm_kernel<true, true><<<grid, THREADS, SMEM_BYTES, s>>>(M, N, K, A, lda, B, ldb, C, ldc, ep, kslice, av, bv);
   TLP_LAUNCH_CHECK();
   return TLP_OK;
+}
+
+// dW partials + bias-gradient partials in one pass (the fused path of
+// sgemm_wgrad_bias): part [splits][M + 1][N], row M = column sums of B's
+// slice.  Returns false (nothing launched) if the shape is not the wgrad
+// kernel's.
+bool tc_wgrad_bias(tlp_ctx* ctx, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,
+                   const float* B, int64_t ldb, float* part, int splits, int64_t kslice,
+                   cudaStream_t s, tlp_status* st) {
+  if (!(splits > 1 && M > BM && M <= WROWS && N > BN && N <= WROWS)) return false;
+  static bool wattr = false;
+  if (!wattr) {
+    cudaFuncSetAttribute(tc_wgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, WSMEM);
+    wattr = true;
+  }
+  const int av = aligned16(A) && lda % 4 == 0, bv = aligned16(B) && ldb % 4 == 0;
+  tc_wgrad_kernel<<<dim3(1, 1, (unsigned)splits), THREADS, WSMEM, s>>>(M, N, K, A, lda, B, ldb, part, N,
+                                                                       kslice, av, bv, 1);
+  ctx->launches++;
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    ctx->last_error = std::string("CUDA launch: ") + cudaGetErrorString(e);
+    *st = TLP_ERR_CUDA;
+  } else {
+    *st = TLP_OK;
+  }
+  return true;
 }
 
 // ---------------------------------------------------------------- test hook

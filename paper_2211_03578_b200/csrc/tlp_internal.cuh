@@ -181,6 +181,13 @@ tlp_status sgemm_wgrad(tlp_ctx* ctx, int64_t M, int64_t K, int64_t N, const floa
                        const float* dY, int64_t lddy, float* dW, cudaStream_t s);
 tlp_status colsum(tlp_ctx* ctx, int64_t M, int64_t N, const float* X, int64_t ldx, float* out,
                   cudaStream_t s);
+// dW = A^T dY and db = colsum(dY) (db must be dW + K*N, the R24 layout): one
+// fused tcgen05 pass on bf16 contexts where the shape allows, else the two calls.
+tlp_status sgemm_wgrad_bias(tlp_ctx* ctx, int64_t M, int64_t K, int64_t N, const float* A, int64_t lda,
+                            const float* dY, int64_t lddy, float* dW, float* db, cudaStream_t s);
+bool tc_wgrad_bias(tlp_ctx* ctx, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,
+                   const float* B, int64_t ldb, float* part, int splits, int64_t kslice,
+                   cudaStream_t s, tlp_status* st);
 tlp_status simt_forward(tlp_ctx* ctx, const float* feats, int64_t N, float* scores, bool save,
                         cudaStream_t s);
 tlp_status simt_backward(tlp_ctx* ctx, int64_t N, const float* dscores, cudaStream_t s);
