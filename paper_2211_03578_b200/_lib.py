@@ -5,7 +5,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtlp.so")
+LIB_PATH = os.environ.get("TLP_LIB_PATH") or os.path.join(_HERE, "libtlp.so")  # override: A/B timing of builds
 
 TLP_STATUS = {0: "OK", -1: "ERR_ARG", -2: "ERR_SHAPE", -3: "ERR_EMPTY_SEQ",
               -4: "ERR_UNKNOWN_TYPE", -5: "ERR_NONFINITE", -6: "ERR_NAN_LOSS",

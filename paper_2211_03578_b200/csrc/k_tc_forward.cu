@@ -66,7 +66,7 @@ constexpr uint32_t OFF_K = OFF_Q + kKP * kRowB;     // K_j    [160][32] (padded 
 constexpr uint32_t OFF_V = OFF_K + kKP * kRowB;     // V_j    [160][32]
 constexpr uint32_t OFF_O = OFF_V + kKP * kRowB;     // O_j    3 x [128 x 32] canonical (A of oproj), j % 3
 constexpr uint32_t OFF_DOT = OFF_O + 3 * 8192;      // 2 x 128 fp32 row dots
-constexpr uint32_t OFF_BAR = OFF_DOT + 1024;        // mbarriers (<= 32)
+constexpr uint32_t OFF_BAR = OFF_DOT + 1024;        // mbarriers (<= 64)
 constexpr uint32_t OFF_TPTR = OFF_BAR + 512;
 constexpr uint32_t OFF_KV = OFF_TPTR + 128;         // R42: key-valid byte per tile row (attn_mask)
 constexpr uint32_t OFF_RING = OFF_KV + 128;         // kStages x 16 KB
@@ -80,6 +80,19 @@ constexpr uint32_t T_B = 256;    // 128: up0, residual-block first GEMM halves, 
 constexpr uint32_t T_QKV = 256;  // 2 x 96: QKV_j double buffer (attention phase only)
 constexpr uint32_t T_AOP = 448;  // 64:  bf16 A operand (U1, residual-block second half)
 constexpr uint32_t T_AOP0 = 384; // 64:  bf16 A operand (residual-block first half; res phase only)
+
+// diagnostics (TLP_TC_TRACE=1): kTrEv epilogue timestamps per tile for 8 tiles
+// of CTA 0, then 8 words of MMA-issuer wait totals per tile
+// Compiled in only with -DTLP_TRACE (tools/abl_build.sh): even a never-taken
+// timestamp branch per head cost ~13% of the kernel (clock reads pin the
+// scheduling of the surrounding code).
+constexpr int kTrEv = 160, kTrW = 8 * kTrEv;
+#ifdef TLP_TRACE
+constexpr bool kTrace = true;
+#else
+constexpr bool kTrace = false;
+#endif
+
 
 struct ChunkRef {
   uint32_t off16;  // byte offset / 16 into the weight stream
@@ -158,6 +171,20 @@ __device__ __forceinline__ void epi_relu_to_tmem(uint32_t tl, uint32_t src, int 
     tc::tmem_st16(tl + dst + c / 2, pk);
     relu_pack32(v1, bias + c + 32, pk);
     tc::tmem_st16(tl + dst + c / 2 + 16, pk);
+  }
+  tc::tmem_wait_st();
+}
+
+// same, 32 columns per tcgen05.ld (ranges that are multiples of 32)
+__device__ __forceinline__ void epi_relu_to_tmem32(uint32_t tl, uint32_t src, int c0, int c1,
+                                                   const float* bias, uint32_t dst) {
+  for (int c = c0; c < c1; c += 32) {
+    float v0[32];
+    uint32_t pk[16];
+    tc::tmem_ld32(tl + src + c, v0);
+    tc::tmem_wait_ld();
+    relu_pack32(v0, bias + c, pk);
+    tc::tmem_st16(tl + dst + c / 2, pk);
   }
   tc::tmem_wait_st();
 }
@@ -413,6 +440,10 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
   const uint32_t bar_conv = bar_opnd + 8;                // [2] QKV_j read, TMEM buffer free (j % 2)
   const uint32_t bar_attn = bar_conv + 16;               // [4] O_j ready (j % 4)
   const uint32_t bar_peer = bar_attn + 32;               // [NS] pair: the peer's half landed
+  // second half of a K-split operand (h columns [128, 256), U1 columns [64, 128)):
+  // the GEMM that follows starts on the first K half while the epilogue still
+  // writes the second
+  const uint32_t bar_opnd2 = bar_peer + 8 * NS;
   const uint32_t rank = PAIR ? cluster_rank() : 0u;      // pair: 0 = leader (issues the MMAs)
   const uint32_t E = PAIR ? 2u : 1u;                     // epilogue arrivals scale (both CTAs)
   uint32_t* tptr = reinterpret_cast<uint32_t*>(smem + OFF_TPTR);
@@ -432,6 +463,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
     tc::mbar_init(bar_qkv, 1);
     tc::mbar_init(bar_qkv + 8, 1);
     tc::mbar_init(bar_opnd, E * kEpi);
+    tc::mbar_init(bar_opnd2, E * kEpi);
     for (int i = 0; i < 2; ++i) tc::mbar_init(bar_conv + 8 * i, E * kAttn);
     for (int i = 0; i < 4; ++i) tc::mbar_init(bar_attn + 8 * i, E * kAttn);
     for (int s = 0; s < NS; ++s) tc::mbar_init(bar_peer + 8 * s, 1);
@@ -508,10 +540,11 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
     }
     if (lane == 0 && rank == 0) {
       int stage = 0;
-      uint32_t phase = 0, op_phase = 0, cv_phase[2] = {0, 0}, at_phase[4] = {0, 0, 0, 0};
+      uint32_t phase = 0, op_phase = 0, op2_phase = 0, cv_phase[2] = {0, 0}, at_phase[4] = {0, 0, 0, 0};
+      bool split = false;  // the next GEMM's second K half waits on bar_opnd2
       // diagnostics (a.trace, CTA 0): cycles the issuer spends waiting per tile on
       // weight chunks / QKV reads / O_j / other epilogue operands
-      const bool trc = a.trace != nullptr && blockIdx.x == 0;
+      const bool trc = kTrace && a.trace != nullptr && blockIdx.x == 0;
       long long wt[4] = {0, 0, 0, 0};
       auto timed_wait = [&](int k, uint32_t bar, uint32_t ph) {
         const long long t0 = trc ? clock64() : 0;
@@ -530,6 +563,12 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
                         int K, int Kc, bool acc) {
         const uint32_t idesc = tc::idesc_bf16(PAIR ? 256 : 128, N);
         for (int kc = 0; kc < K; kc += Kc) {
+          if (split && kc == K / 2) {  // K-split operand: second half written
+            timed_wait(3, bar_opnd2, op2_phase);
+            op2_phase ^= 1;
+            tc::tc_fence_after();
+            split = false;
+          }
           timed_wait(0, bar_full + 8 * stage, phase);
           if (PAIR) timed_wait(0, bar_peer + 8 * stage, phase);  // the peer's half
           tc::tc_fence_after();
@@ -553,15 +592,17 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
       for (int64_t it = it0; it < n_it; it += it_step, ++mt) {
         if (trc && mt < 8) {
           for (int k = 0; k < 4; ++k) wt[k] = 0;
-          a.trace[512 + mt * 8 + 4] = clock64();
+          a.trace[kTrW + mt * 8 + 4] = clock64();
         }
         wait_opnd();                                                      // E0: X
         gemm_w(false, OFF_X, kKX, T_B, 128, kKX, 32, false);              // up0 -> T_B
         commit<PAIR>(bar_acc);
-        wait_opnd();                                                      // E1: U1 -> T_AOP
+        wait_opnd();                                                      // E1: U1[:, :64] -> T_AOP
+        split = true;                                                     //     U1[:, 64:]
         gemm_w(true, T_AOP, 0, T_A, kH, 128, 32, false);                  // up1 -> T_A
         commit<PAIR>(bar_acc);
-        wait_opnd();                                                      // E2: h
+        wait_opnd();                                                      // E2: h[:, :128]
+        split = true;                                                     //     h[:, 128:]
         for (int l = 0; l < NA; ++l) {
           gemm_w(false, OFF_H, kH, T_QKV, 96, kH, 64, false);             // QKV_0 -> buf 0
           commit<PAIR>(bar_qkv);
@@ -581,7 +622,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
             gemm_w(false, OFF_O + 8192 * (j % 3), kDH, T_A, kH, kDH, 32, j > 0);  // acc += O_j Wo_j
           }
           commit<PAIR>(bar_acc);
-          wait_opnd();                                                    // E_resid
+          wait_opnd();                                                    // E_resid h[:, :128]
+          split = true;                                                   //         h[:, 128:]
         }
         for (int r = 0; r < NR; ++r) {
           // G1 half 1 goes ahead of G2 part 0 so that the epilogue of r_h1 overlaps
@@ -595,7 +637,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
           wait_opnd();                                                    // r_h1 -> T_AOP
           gemm_w(true, T_AOP, 0, T_A, kH, 128, 32, true);                 // G2 part 1
           commit<PAIR>(bar_acc);
-          wait_opnd();                                                    // E_resid
+          wait_opnd();                                                    // E_resid h[:, :128]
+          split = true;                                                   //         h[:, 128:]
         }
         for (int t = 0; t < NT; ++t) {
           gemm_w(false, OFF_H, kH, T_B, kHD, kH, 64, false);              // head t
@@ -603,7 +646,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
           if (t < NT - 1) wait_opnd();
         }
         if (trc && mt < 8)
-          for (int k = 0; k < 4; ++k) a.trace[512 + mt * 8 + k] = wt[k];
+          for (int k = 0; k < 4; ++k) a.trace[kTrW + mt * 8 + k] = wt[k];
       }
     }
   } else {
@@ -618,8 +661,8 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
     uint32_t ph_acc = 0, ph_qkv[2] = {0, 0};
     int titer = 0, tev = 0;
     auto tr = [&]() {  // diagnostics only (a.trace == nullptr in production)
-      if (a.trace && blockIdx.x == 0 && threadIdx.x == 64 && titer < 8 && tev < 64)
-        a.trace[titer * 64 + tev] = clock64();
+      if (kTrace && a.trace && blockIdx.x == 0 && threadIdx.x == 64 && titer < 8 && tev < kTrEv)
+        a.trace[titer * kTrEv + tev] = clock64();
       ++tev;
     };
     auto wait_on = [&](uint32_t bar, uint32_t& ph) {
@@ -634,9 +677,30 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
       arrive_mma(bar_opnd);
       tr();
     };
-    // column split between the quarter's two warps
+    auto signal2 = [&]() {  // second half of a K-split operand
+      tc::fence_proxy_async_smem();
+      tc::tc_fence_before();
+      arrive_mma(bar_opnd2);
+    };
+    // K-split operands: the quarter's two warps first write columns
+    // [0, n/2) (n/4 each), signal, then [n/2, n)
     auto lo_of = [&](int n) { return (int)hh * (n / 2); };
     auto hi_of = [&](int n) { return ((int)hh + 1) * (n / 2); };
+    auto kA = [&](int n) { return (int)hh * (n / 4); };
+    auto kB = [&](int n) { return n / 2 + (int)hh * (n / 4); };
+    auto signal_part = [&](int part) {
+      if (part == 0) signal(); else signal2();
+    };
+    // h = h + acc + bias in two K halves (residual of an attention layer or a residual block)
+    auto resid_split = [&](const float* bias) {
+#pragma unroll 1
+      for (int part = 0; part < 2; ++part) {
+        const int c0 = part ? kB(kH) : kA(kH);
+        epi_residual(smem, tl, bias, r, c0, c0 + 64);
+        signal_part(part);
+      }
+    };
+    // column split between the quarter's two warps
     const uint32_t slot = r / kL;                      // candidate slot (5 = pad rows)
     const uint32_t kk = r - slot * kL;
     const bool real = r < kCand * kL;
@@ -667,17 +731,26 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
         }
         signal();
         wait_on(bar_acc, ph_acc);
-        epi_relu_to_tmem(tl, T_B, lo_of(128), hi_of(128), vs + a.up_b0, T_AOP);   // U1 -> TMEM
-        signal();
+#pragma unroll 1
+        for (int part = 0; part < 2; ++part) {  // U1 -> TMEM (K halves; one copy of the code)
+          const int c0 = part ? kB(128) : kA(128);
+          epi_relu_to_tmem32(tl, T_B, c0, c0 + 32, vs + a.up_b0, T_AOP);
+          signal_part(part);
+        }
         wait_on(bar_acc, ph_acc);
-        epi_relu_to_smem(smem, tl, T_A, lo_of(kH), hi_of(kH), vs + a.up_b1, OFF_H, kH, r,
-                         a.pos ? a.pos + kk * kH : nullptr);  // h (+ pos, R43)
-        signal();
+        const float* pos_row = a.pos ? a.pos + kk * kH : nullptr;  // h (+ pos, R43)
+#pragma unroll 1
+        for (int part = 0; part < 2; ++part) {
+          const int c0 = part ? kB(kH) : kA(kH);
+          epi_relu_to_smem(smem, tl, T_A, c0, c0 + 64, vs + a.up_b1, OFF_H, kH, r, pos_row);
+          signal_part(part);
+        }
       }
       for (int l = 0; l < NA; ++l) {
         for (int j = 0; j < kHeads; ++j) {
           wait_on(bar_qkv + 8 * (j & 1), ph_qkv[j & 1]);
           asm volatile("bar.sync 2, 320;" ::: "memory");  // all warps done reading head j-1
+          tr();
           {  // QKV_j (TMEM) + bias -> Q, K, V tiles at padded positions 32 slot + kk
             const uint32_t tq = tl + T_QKV + 96 * (j & 1);
             const uint32_t pos = (32 * slot + kk) * kRowB;
@@ -718,14 +791,20 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
           }
           tc::tc_fence_before();                          // QKV_j read: TMEM buffer j%2 free
           if (j + 2 < kHeads) arrive_mma(bar_conv + 8 * (j & 1));
+          tr();
           asm volatile("bar.sync 2, 320;" ::: "memory");  // Q/K/V of head j complete
-          if (a.attn_mask) {  // R42: drop padding keys (an all-padding slot keeps every key)
+          tr();
+          {  // R42 key mask: drop padding keys (an all-padding slot keeps every key)
             const uint32_t cand = unit >> 1;
-            uint32_t kmask = __ballot_sync(0xffffffffu, lane < (uint32_t)kL && smem[OFF_KV + kL * cand + lane]);
-            if (!kmask) kmask = (1u << kL) - 1u;
-            attn_unit_mma<true>(smem, sbase, cand, unit & 1, lane, sm_scale, OFF_O + 8192 * (j % 3), kmask);
-          } else {
-            attn_unit_mma<false>(smem, sbase, unit >> 1, unit & 1, lane, sm_scale, OFF_O + 8192 * (j % 3), 0u);
+            uint32_t kmask = (1u << kL) - 1u;
+            if (a.attn_mask) {
+              kmask = __ballot_sync(0xffffffffu, lane < (uint32_t)kL && smem[OFF_KV + kL * cand + lane]);
+              if (!kmask) kmask = (1u << kL) - 1u;
+            }
+            // two instantiations: the unmasked core tests key positions against
+            // a constant (a runtime mask there measured 5% slower overall)
+            if (a.attn_mask) attn_unit_mma<true>(smem, sbase, cand, unit & 1, lane, sm_scale, OFF_O + 8192 * (j % 3), kmask);
+            else attn_unit_mma<false>(smem, sbase, cand, unit & 1, lane, sm_scale, OFF_O + 8192 * (j % 3), kmask);
           }
           tc::fence_proxy_async_smem();                   // O_j ready
           tc::tc_fence_before();
@@ -734,8 +813,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
         }
         if (rowwise) {
           wait_on(bar_acc, ph_acc);
-          epi_residual(smem, tl, vs + a.bo[l], r, lo_of(kH), hi_of(kH));
-          signal();
+          resid_split(vs + a.bo[l]);
         }
       }
       if (!rowwise) continue;
@@ -747,8 +825,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
         epi_relu_to_tmem(tl, T_B, lo_of(128), hi_of(128), vs + a.ra[rb] + 128, T_AOP);
         signal();
         wait_on(bar_acc, ph_acc);
-        epi_residual(smem, tl, vs + a.rb[rb], r, lo_of(kH), hi_of(kH));
-        signal();
+        resid_split(vs + a.rb[rb]);
       }
       for (int t = 0; t < NT; ++t) {
         wait_on(bar_acc, ph_acc);
@@ -976,11 +1053,12 @@ tlp_status tc_forward(tlp_ctx* ctx, const float* feats, int64_t N, float* scores
                         : (int)std::min<int64_t>(a.ntile, ctx->num_sms);
   // Diagnostics: TLP_TC_TRACE=1 prints CTA 0's epilogue phase timeline (cycles
   // between successive waits/signals) for its first tiles to stderr.
-  static const bool trace = getenv("TLP_TC_TRACE") != nullptr;
+  // (needs a -DTLP_TRACE build, tools/abl_build.sh NAME -DTLP_TRACE)
+  static const bool trace = kTrace && getenv("TLP_TC_TRACE") != nullptr;
   long long* d_trace = nullptr;
   if (trace) {
-    TLP_CUDA_TRY(cudaMalloc(&d_trace, 8 * 72 * sizeof(long long)));
-    TLP_CUDA_TRY(cudaMemset(d_trace, 0, 8 * 72 * sizeof(long long)));
+    TLP_CUDA_TRY(cudaMalloc(&d_trace, (kTrW + 64) * sizeof(long long)));
+    TLP_CUDA_TRY(cudaMemset(d_trace, 0, (kTrW + 64) * sizeof(long long)));
   }
   a.trace = d_trace;
   if (pair) {
@@ -1000,15 +1078,15 @@ tlp_status tc_forward(tlp_ctx* ctx, const float* feats, int64_t N, float* scores
   }
   TLP_LAUNCH_CHECK();
   if (trace) {
-    std::vector<long long> h(8 * 72);
+    std::vector<long long> h(kTrW + 64);
     TLP_CUDA_TRY(cudaStreamSynchronize(s));
     TLP_CUDA_TRY(cudaMemcpy(h.data(), d_trace, h.size() * sizeof(long long), cudaMemcpyDeviceToHost));
     cudaFree(d_trace);
     for (int t = 1; t < 4; ++t) {
       fprintf(stderr, "tile %d:", t);
-      for (int e = 1; e < 64 && h[t * 64 + e]; ++e) fprintf(stderr, " %lld", h[t * 64 + e] - h[t * 64 + e - 1]);
-      fprintf(stderr, " | total %lld\n", h[(t + 1) * 64] ? h[(t + 1) * 64] - h[t * 64] : 0LL);
-      const long long* m = &h[512 + t * 8];
+      for (int e = 1; e < kTrEv && h[t * kTrEv + e]; ++e) fprintf(stderr, " %lld", h[t * kTrEv + e] - h[t * kTrEv + e - 1]);
+      fprintf(stderr, " | total %lld\n", h[(t + 1) * kTrEv] ? h[(t + 1) * kTrEv] - h[t * kTrEv] : 0LL);
+      const long long* m = &h[kTrW + t * 8];
       fprintf(stderr, "  mma issuer waits: chunks %lld, qkv-read %lld, O_j %lld, operands %lld (tile %lld)\n",
               m[0], m[1], m[2], m[3], m[12] ? m[12] - m[4] : 0LL);
     }
