@@ -850,11 +850,17 @@ tlp_status simt_backward(tlp_ctx* ctx, int64_t N, const float* g, cudaStream_t s
     TRY(sgemm(ctx, false, true, M, H, H, dh, H, P + o.Wo[l], H, dtmp, H, e0, s));  // dO
     TRY(attn_bwd(ctx, W + lay.qkv[l], W + lay.A[l], dtmp, N, dqkv, s));
     const int64_t wq[3] = {o.Wq[l], o.Wk[l], o.Wv[l]}, bq[3] = {o.bq[l], o.bk[l], o.bv[l]};
-    for (int j = 0; j < 3; ++j) {
+    for (int j = 0; j < 3; ++j)
       TRY(sgemm_wgrad_bias(ctx, M, H, H, hin, H, dqkv + j * H, 3 * H, G + wq[j], G + bq[j], s));
-      EpiParams ea; ea.accumulate = true;
-      TRY(sgemm(ctx, false, true, M, H, H, dqkv + j * H, 3 * H, P + wq[j], H, dh, H, ea, s));
-    }
+    // dh += [dQ | dK | dV] [Wq | Wk | Wv]^T as ONE K = 3H GEMM (dqkv read once,
+    // dh read and written once instead of three times); Wcat[i][jH + k] = W_j[i][k]
+    TLP_CUDA_TRY(ctx->ws_wcat.ensure((size_t)H * 3 * H * sizeof(float)));
+    float* wcat = ctx->ws_wcat.as<float>();
+    for (int j = 0; j < 3; ++j)
+      TLP_CUDA_TRY(cudaMemcpy2DAsync(wcat + j * H, 3 * H * sizeof(float), P + wq[j], H * sizeof(float),
+                                     H * sizeof(float), H, cudaMemcpyDeviceToDevice, s));
+    EpiParams ea; ea.accumulate = true;
+    TRY(sgemm(ctx, false, true, M, H, 3 * H, dqkv, 3 * H, wcat, 3 * H, dh, H, ea, s));
   }
   // R43: dpos = sum over candidates; d(up_out) = d(up_out + pos) unchanged
   if (c.pos_enc) {

@@ -90,6 +90,7 @@ struct tlp_ctx {
   // workspaces
   DevBuf ws_tokens, ws_act, ws_train, ws_rank, ws_topk, ws_misc, ws_partial, ws_merge;
   DevBuf ws_bimg;  // bf16 hi/lo image of a training GEMM's weight operand (k_tc_gemm.cu)
+  DevBuf ws_wcat;  // [Wq | Wk | Wv] rows side by side: the fused Q/K/V dgrad operand (k_simt.cu)
 
   // bf16 tensor-core path
   TcWeights* tc = nullptr;
