@@ -68,6 +68,7 @@ struct EpiDev {
   int64_t ldm;
   int relu;
   int accumulate;
+  int mask_after;
 };
 
 // C[M,N] = epi(op(A)[M,K] op(B)[K,N]).  blockIdx.z selects a K slice of
@@ -134,8 +135,9 @@ __global__ void __launch_bounds__(256) sgemm_kernel(int64_t M, int64_t N, int64_
         if (ep.bias) v += ep.bias[gj];
         if (ep.resid) v += ep.resid[gi * ep.ldr + gj];
         if (ep.relu) v = fmaxf(v, 0.f);
-        if (ep.mask) v = ep.mask[gi * ep.ldm + gj] > 0.f ? v : 0.f;
+        if (ep.mask && !ep.mask_after) v = ep.mask[gi * ep.ldm + gj] > 0.f ? v : 0.f;
         if (ep.accumulate) v += Cz[gi * ldc + gj];
+        if (ep.mask && ep.mask_after) v = ep.mask[gi * ep.ldm + gj] > 0.f ? v : 0.f;
       }
       Cz[gi * ldc + gj] = v;
     }
@@ -610,7 +612,7 @@ tlp_status sgemm(tlp_ctx* ctx, bool ta, bool tb, int64_t M, int64_t N, int64_t K
   // operands allow 16-byte async copies; the fp32 context stays on FFMA (1e-5).
   if (ctx->cfg.precision == TLP_PREC_BF16 && tc_gemm_ok(A, lda, B, ldb))
     return tc_gemm(ctx, ta, tb, M, N, K, A, lda, B, ldb, C, ldc, e, 1, K, s);
-  EpiDev ed{e.bias, e.resid, e.ldr, e.mask, e.ldm, e.relu ? 1 : 0, e.accumulate ? 1 : 0};
+  EpiDev ed{e.bias, e.resid, e.ldr, e.mask, e.ldm, e.relu ? 1 : 0, e.accumulate ? 1 : 0, e.mask_after ? 1 : 0};
   dim3 grid((unsigned)cdiv(N, BN), (unsigned)cdiv(M, BM), 1);
   const int64_t ks = K > 0 ? K : 1;
   if (!ta && !tb) sgemm_kernel<false, false><<<grid, 256, 0, s>>>(M, N, K, A, lda, B, ldb, C, ldc, ed, ks);
@@ -843,6 +845,7 @@ tlp_status simt_backward(tlp_ctx* ctx, int64_t N, const float* g, cudaStream_t s
     TRY(sgemm(ctx, false, true, M, H, H4, dG, H4, P + o.Wih[l], H4, dh, H, ea, s));
   }
   // attention layers
+  int up_masked = -1;  // upsample layer whose ReLU' a GEMM epilogue already applied to `cur`
   for (int l = c.n_attn - 1; l >= 0 && c.backbone == 0; --l) {
     const float* hin = l > 0 ? W + lay.hattn[l - 1] : (c.pos_enc ? W + lay.hpos : W + lay.up[c.n_up - 1]);
     TRY(sgemm_wgrad_bias(ctx, M, H, H, W + lay.O[l], H, dh, H, G + o.Wo[l], G + o.bo[l], s));
@@ -860,6 +863,10 @@ tlp_status simt_backward(tlp_ctx* ctx, int64_t N, const float* g, cudaStream_t s
       TLP_CUDA_TRY(cudaMemcpy2DAsync(wcat + j * H, 3 * H * sizeof(float), P + wq[j], H * sizeof(float),
                                      H * sizeof(float), H, cudaMemcpyDeviceToDevice, s));
     EpiParams ea; ea.accumulate = true;
+    if (l == 0 && !c.pos_enc) {  // dh is final here: fold the upsample ReLU' (relu_mask) in
+      ea.mask = W + lay.up[c.n_up - 1]; ea.ldm = H; ea.mask_after = true;
+      up_masked = c.n_up - 1;
+    }
     TRY(sgemm(ctx, false, true, M, H, 3 * H, dqkv, 3 * H, wcat, 3 * H, dh, H, ea, s));
   }
   // R43: dpos = sum over candidates; d(up_out) = d(up_out + pos) unchanged
@@ -872,13 +879,17 @@ tlp_status simt_backward(tlp_ctx* ctx, int64_t N, const float* g, cudaStream_t s
   for (int i = c.n_up - 1; i >= 0; --i) {
     const int64_t w = c.up_dims[i];
     const int64_t din = i > 0 ? c.up_dims[i - 1] : c.E;
-    relu_mask_inplace<<<(unsigned)cdiv(M * w, 256), 256, 0, s>>>(cur, W + lay.up[i], M * w);
-    TLP_LAUNCH_CHECK();
+    if (up_masked != i) {
+      relu_mask_inplace<<<(unsigned)cdiv(M * w, 256), 256, 0, s>>>(cur, W + lay.up[i], M * w);
+      TLP_LAUNCH_CHECK();
+    }
     const float* xin = i > 0 ? W + lay.up[i - 1] : ctx->train_X;
     TRY(sgemm_wgrad_bias(ctx, M, din, w, xin, din, cur, w, G + o.up_W[i], G + o.up_b[i], s));
     if (i > 0) {
       float* nxt = (cur == dh) ? dtmp : dh;
-      EpiParams e0;
+      EpiParams e0;  // the next layer's ReLU' rides in this dgrad's epilogue
+      e0.mask = W + lay.up[i - 1]; e0.ldm = din;
+      up_masked = i - 1;
       TRY(sgemm(ctx, false, true, M, din, w, cur, w, P + o.up_W[i], w, nxt, din, e0, s));
       cur = nxt;
     }

@@ -43,6 +43,7 @@ struct Epi {
   int64_t ldm;
   int relu;
   int accumulate;
+  int mask_after;  // mask the accumulated value (C + result) instead of the result
 };
 
 struct Src {
@@ -188,8 +189,9 @@ __device__ __forceinline__ void epi_store_slab(const float* stage, int ld, int64
         y.x += b.x; y.y += b.y;
         y.x += rv[u].x; y.y += rv[u].y;
         if (ep.relu) { y.x = fmaxf(y.x, 0.f); y.y = fmaxf(y.y, 0.f); }
-        if (mask) { y.x = mv[u].x > 0.f ? y.x : 0.f; y.y = mv[u].y > 0.f ? y.y : 0.f; }
+        if (mask && !ep.mask_after) { y.x = mv[u].x > 0.f ? y.x : 0.f; y.y = mv[u].y > 0.f ? y.y : 0.f; }
         y.x += cv[u].x; y.y += cv[u].y;
+        if (mask && ep.mask_after) { y.x = mv[u].x > 0.f ? y.x : 0.f; y.y = mv[u].y > 0.f ? y.y : 0.f; }
       }
       if (vec) *reinterpret_cast<float2*>(Cz + gi * ldc + gj) = y;
       else {
@@ -636,7 +638,7 @@ tlp_status tc_gemm(tlp_ctx* ctx, bool ta, bool tb, int64_t M, int64_t N, int64_t
     cudaFuncSetAttribute(tc_gemm_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     attr = true;
   }
-  Epi ep{e.bias, e.resid, e.ldr, e.mask, e.ldm, e.relu ? 1 : 0, e.accumulate ? 1 : 0};
+  Epi ep{e.bias, e.resid, e.ldr, e.mask, e.ldm, e.relu ? 1 : 0, e.accumulate ? 1 : 0, e.mask_after ? 1 : 0};
   if (ta && !tb && splits > 1 && M > BM && M <= WROWS && N > BN && N <= WROWS) {
     static bool wattr = false;
     if (!wattr) {

@@ -173,6 +173,7 @@ struct EpiParams {
   int64_t ldm = 0;
   bool relu = false;
   bool accumulate = false;       // C += result (C read before write)
+  bool mask_after = false;       // apply `mask` to the accumulated value (C + result)
 };
 tlp_status sgemm(tlp_ctx* ctx, bool ta, bool tb, int64_t M, int64_t N, int64_t K, const float* A,
                  int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc,
