@@ -678,6 +678,36 @@ tlp_status sgemm_wgrad_bias(tlp_ctx* ctx, int64_t M, int64_t K, int64_t N, const
   return colsum(ctx, M, N, dY, lddy, db, s);
 }
 
+// J weight + bias gradients that share the activation A (the Q/K/V projections):
+// dY_j = dY + j * jcol (columns of one [M, J*N] array), dW_j / db_j = dW[j] / dW[j] + K*N.
+// bf16 contexts: one wgrad launch (A read from HBM once per slice); else J calls.
+tlp_status sgemm_wgrad_bias_shared(tlp_ctx* ctx, int J, int64_t M, int64_t K, int64_t N, const float* A,
+                                   int64_t lda, const float* dY, int64_t lddy, int64_t jcol,
+                                   float* const* dW, cudaStream_t s) {
+  const int64_t slice = 2048;
+  const int Z = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(M, slice), 256));
+  const int64_t kslice = cdiv(cdiv(M, Z), BK) * BK;
+  if (ctx->cfg.precision == TLP_PREC_BF16 && Z > 1) {
+    const int64_t pj = (int64_t)Z * (K + 1) * N;
+    TLP_CUDA_TRY(ctx->ws_partial.ensure((size_t)J * pj * sizeof(float)));
+    float* part = ctx->ws_partial.as<float>();
+    tlp_status st = TLP_OK;
+    if (tc_wgrad_bias(ctx, K, N, M, A, lda, dY, lddy, part, Z, kslice, s, &st, J, jcol, pj)) {
+      if (st != TLP_OK) return st;
+      for (int j = 0; j < J; ++j) {
+        reduce_partials<<<(unsigned)cdiv((K + 1) * N, 256), 256, 0, s>>>(part + j * pj, (K + 1) * N, Z, dW[j]);
+        TLP_LAUNCH_CHECK();
+      }
+      return TLP_OK;
+    }
+  }
+  for (int j = 0; j < J; ++j) {
+    tlp_status st = sgemm_wgrad_bias(ctx, M, K, N, A, lda, dY + j * jcol, lddy, dW[j], dW[j] + K * N, s);
+    if (st != TLP_OK) return st;
+  }
+  return TLP_OK;
+}
+
 tlp_status colsum(tlp_ctx* ctx, int64_t M, int64_t N, const float* X, int64_t ldx, float* out,
                   cudaStream_t s) {
   const int64_t rows = 256;
@@ -853,8 +883,15 @@ tlp_status simt_backward(tlp_ctx* ctx, int64_t N, const float* g, cudaStream_t s
     TRY(sgemm(ctx, false, true, M, H, H, dh, H, P + o.Wo[l], H, dtmp, H, e0, s));  // dO
     TRY(attn_bwd(ctx, W + lay.qkv[l], W + lay.A[l], dtmp, N, dqkv, s));
     const int64_t wq[3] = {o.Wq[l], o.Wk[l], o.Wv[l]}, bq[3] = {o.bq[l], o.bk[l], o.bv[l]};
-    for (int j = 0; j < 3; ++j)
-      TRY(sgemm_wgrad_bias(ctx, M, H, H, hin, H, dqkv + j * H, 3 * H, G + wq[j], G + bq[j], s));
+    bool contiguous = true;  // R24: each bias right after its weight
+    for (int j = 0; j < 3; ++j) contiguous &= bq[j] == wq[j] + H * H;
+    if (contiguous) {
+      float* const dws[3] = {G + wq[0], G + wq[1], G + wq[2]};
+      TRY(sgemm_wgrad_bias_shared(ctx, 3, M, H, H, hin, H, dqkv, 3 * H, H, dws, s));
+    } else {
+      for (int j = 0; j < 3; ++j)
+        TRY(sgemm_wgrad_bias(ctx, M, H, H, hin, H, dqkv + j * H, 3 * H, G + wq[j], G + bq[j], s));
+    }
     // dh += [dQ | dK | dV] [Wq | Wk | Wv]^T as ONE K = 3H GEMM (dqkv read once,
     // dh read and written once instead of three times); Wcat[i][jH + k] = W_j[i][k]
     TLP_CUDA_TRY(ctx->ws_wcat.ensure((size_t)H * 3 * H * sizeof(float)));

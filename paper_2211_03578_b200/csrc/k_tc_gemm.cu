@@ -476,8 +476,13 @@ __global__ void __launch_bounds__(THREADS, 1) tc_wgrad_kernel(int64_t M, int64_t
                                                                const float* __restrict__ B, int64_t ldb,
                                                                float* __restrict__ part, int64_t ldc,
                                                                int64_t kslice, int avec, int bvec,
-                                                               int colsum) {
+                                                               int colsum, int64_t bjs, int64_t pjs) {
   extern __shared__ __align__(128) uint8_t smem[];
+  // blockIdx.y = j of J products sharing A (B_j = B + j bjs, partials + j pjs):
+  // the J CTAs of one slice are adjacent in launch order, so A's slice comes
+  // from HBM once and from L2 for the other J - 1
+  B += blockIdx.y * bjs;
+  part += blockIdx.y * pjs;
   const uint32_t sb = tc::smem_u32(smem);
   const uint32_t bar = sb + STAGES * WSTAGE;
   uint32_t* tptr = reinterpret_cast<uint32_t*>(smem + STAGES * WSTAGE + 64);
@@ -647,7 +652,7 @@ tlp_status tc_gemm(tlp_ctx* ctx, bool ta, bool tb, int64_t M, int64_t N, int64_t
     }
     const int av = aligned16(A) && lda % 4 == 0, bv = aligned16(B) && ldb % 4 == 0;
     tc_wgrad_kernel<<<dim3(1, 1, (unsigned)splits), THREADS, WSMEM, s>>>(M, N, K, A, lda, B, ldb, C,
-                                                                         ldc, kslice, av, bv, 0);
+                                                                         ldc, kslice, av, bv, 0, 0, 0);
     TLP_LAUNCH_CHECK();
     return TLP_OK;
   }
@@ -685,16 +690,18 @@ tlp_status tc_gemm(tlp_ctx* ctx, bool ta, bool tb, int64_t M, int64_t N, int64_t
 // kernel's.
 bool tc_wgrad_bias(tlp_ctx* ctx, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,
                    const float* B, int64_t ldb, float* part, int splits, int64_t kslice,
-                   cudaStream_t s, tlp_status* st) {
+                   cudaStream_t s, tlp_status* st, int J, int64_t bjs, int64_t pjs) {
   if (!(splits > 1 && M > BM && M <= WROWS && N > BN && N <= WROWS)) return false;
+  if (J > 1 && (bjs % 4 != 0)) return false;
   static bool wattr = false;
   if (!wattr) {
     cudaFuncSetAttribute(tc_wgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, WSMEM);
     wattr = true;
   }
   const int av = aligned16(A) && lda % 4 == 0, bv = aligned16(B) && ldb % 4 == 0;
-  tc_wgrad_kernel<<<dim3(1, 1, (unsigned)splits), THREADS, WSMEM, s>>>(M, N, K, A, lda, B, ldb, part, N,
-                                                                       kslice, av, bv, 1);
+  tc_wgrad_kernel<<<dim3(1, (unsigned)J, (unsigned)splits), THREADS, WSMEM, s>>>(M, N, K, A, lda, B, ldb,
+                                                                                part, N, kslice, av, bv, 1,
+                                                                                bjs, pjs);
   ctx->launches++;
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {

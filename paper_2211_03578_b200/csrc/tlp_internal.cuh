@@ -189,7 +189,7 @@ tlp_status sgemm_wgrad_bias(tlp_ctx* ctx, int64_t M, int64_t K, int64_t N, const
                             const float* dY, int64_t lddy, float* dW, float* db, cudaStream_t s);
 bool tc_wgrad_bias(tlp_ctx* ctx, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,
                    const float* B, int64_t ldb, float* part, int splits, int64_t kslice,
-                   cudaStream_t s, tlp_status* st);
+                   cudaStream_t s, tlp_status* st, int J = 1, int64_t bjs = 0, int64_t pjs = 0);
 tlp_status simt_forward(tlp_ctx* ctx, const float* feats, int64_t N, float* scores, bool save,
                         cudaStream_t s);
 tlp_status simt_backward(tlp_ctx* ctx, int64_t N, const float* dscores, cudaStream_t s);
