@@ -287,6 +287,15 @@ __device__ __forceinline__ void attn_unit_mma(uint8_t* smem, uint32_t sbase, uin
 #pragma unroll
   for (int ks = 0; ks < 2; ++ks)
     tc::ldsm_x4(sbase + OFF_Q + (q0 + (lane & 15)) * kRowB + (16 * ks + 8 * (lane >> 4)) * 2, qa[ks]);
+  uint32_t vbe[2][2][4];  // V B-fragments, loaded before S so their latency hides under it
+#pragma unroll
+  for (int kbk = 0; kbk < 2; ++kbk)
+#pragma unroll
+    for (int dp = 0; dp < 2; ++dp) {
+      const uint32_t krow = k0 + 16 * kbk + (lane & 7) + 8 * ((lane >> 3) & 1);
+      const uint32_t dcol = 8 * (2 * dp + (lane >> 4));
+      tc::ldsm_x4_t(sbase + OFF_V + krow * kRowB + dcol * 2, vbe[kbk][dp]);
+    }
   float s[4][4];
 #pragma unroll
   for (int nt = 0; nt < 4; ++nt) {
@@ -322,7 +331,9 @@ __device__ __forceinline__ void attn_unit_mma(uint8_t* smem, uint32_t sbase, uin
       }
     sum += __shfl_xor_sync(0xffffffffu, sum, 1);
     sum += __shfl_xor_sync(0xffffffffu, sum, 2);
-    inv[half] = 1.0f / sum;
+    // R29: approximate reciprocal on the bf16 path (sum >= 1: the row max term is
+    // exp2(0)); the IEEE division's slow-path call cost 3.4% of the kernel
+    inv[half] = __fdividef(1.0f, sum);
   }
   uint32_t pa[2][4];  // P as A fragments per 16-key block
 #pragma unroll
@@ -341,10 +352,7 @@ __device__ __forceinline__ void attn_unit_mma(uint8_t* smem, uint32_t sbase, uin
   for (int kbk = 0; kbk < 2; ++kbk)
 #pragma unroll
     for (int dp = 0; dp < 2; ++dp) {  // pairs of d n-tiles
-      uint32_t vb[4];                 // (dn=2dp: b0,b1) (dn=2dp+1: b0,b1)
-      const uint32_t krow = k0 + 16 * kbk + (lane & 7) + 8 * ((lane >> 3) & 1);
-      const uint32_t dcol = 8 * (2 * dp + (lane >> 4));
-      tc::ldsm_x4_t(sbase + OFF_V + krow * kRowB + dcol * 2, vb);
+      const uint32_t (&vb)[4] = vbe[kbk][dp];  // (dn=2dp: b0,b1) (dn=2dp+1: b0,b1)
       tc::mma16816(o[2 * dp], pa[kbk], vb[0], vb[1]);
       tc::mma16816(o[2 * dp + 1], pa[kbk], vb[2], vb[3]);
     }
