@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(128) attn_fwd_tc_kernel(const float* __restric
         }
       sum += __shfl_xor_sync(0xffffffffu, sum, 1);
       sum += __shfl_xor_sync(0xffffffffu, sum, 2);
-      const float inv = 1.0f / sum;
+      const float inv = __frcp_rn(sum);  // == 1.0f / sum bitwise (correctly rounded)
 #pragma unroll
       for (int nt = 0; nt < 4; ++nt)
 #pragma unroll

@@ -24,6 +24,7 @@ namespace {
 
 constexpr int kThreads = 512;
 constexpr float kLn2 = 0.693147180559945309f;
+constexpr float kInvLn2 = 1.44269504088896341f;  // 1 / ln 2
 
 __device__ __forceinline__ float block_sum(float v, float* red) {
   for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -151,16 +152,18 @@ __global__ void __launch_bounds__(kThreads) rank_kernel(const float* __restrict_
       // z = s_hi - s_lo of the ordered pair
       const float z = (yi > yj) ? (si - s[j]) : (s[j] - si);
       const float e = expf(-fabsf(z));
-      const float sig = (z >= 0.f) ? e / (1.0f + e) : 1.0f / (1.0f + e);  // sigmoid(-z)
+      const float r = __frcp_rn(1.0f + e);                  // one correctly rounded reciprocal
+      const float sig = (z >= 0.f) ? e * r : r;             // sigmoid(-z), sign-stable (R30)
       if (yi > yj) {
-        li += w * (fmaxf(-z, 0.f) + log1pf(e)) / kLn2;
-        gi -= w * sig / kLn2;
+        li += w * (fmaxf(-z, 0.f) + log1pf(e));
+        gi -= w * sig;
       } else {
-        gi += w * sig / kLn2;
+        gi += w * sig;
       }
     }
-    dscores[(lo + idx[i]) * nt + t] = gi;
-    lsum += li;
+    // the 1/ln 2 of log2 and of d/ds log2(1 + e^{-z}) applied once per item
+    dscores[(lo + idx[i]) * nt + t] = gi * kInvLn2;
+    lsum += li * kInvLn2;
   }
   const float L = block_sum(lsum, red);
   if (threadIdx.x == 0) loss_part[(int64_t)t * gridDim.x + g] = L;
