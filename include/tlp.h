@@ -149,7 +149,9 @@ tlp_status tlp_get_params(tlp_ctx* ctx, float* flat, int64_t n);
 tlp_status tlp_get_grads(tlp_ctx* ctx, float* flat, int64_t n);
 /* Data-parallel communicator: `nccl_id` points to the 128-byte
  * ncclUniqueId created by rank 0 and broadcast by the caller; blocks until all
- * `world` ranks have joined.  world == 1 is accepted and disables collectives. */
+ * `world` ranks have joined.  world == 1 with nccl_id == NULL disables
+ * collectives; world == 1 with an id builds a 1-rank communicator (the
+ * collective code paths then run on one GPU, as the tests use it). */
 tlp_status tlp_set_comm(tlp_ctx* ctx, const void* nccl_id, int rank, int world);
 /* Fill a 128-byte buffer with a fresh ncclUniqueId (rank 0 only). */
 tlp_status tlp_get_unique_id(void* nccl_id_out);

@@ -243,7 +243,10 @@ tlp_status tlp_set_comm(tlp_ctx* ctx, const void* nccl_id, int rank, int world) 
   }
   ctx->rank = rank;
   ctx->world = world;
-  if (world == 1) return TLP_OK;
+  // world 1 without an id: no communicator (the single-GPU path).  World 1 WITH
+  // an id builds a 1-rank communicator, so the collective code paths (count and
+  // gradient allreduce, top-k allgather + merge) run on one GPU (tests).
+  if (world == 1 && !nccl_id) return TLP_OK;
   if (!nccl_id) return fail(ctx, TLP_ERR_ARG, "null nccl id");
   ncclUniqueId id;
   std::memcpy(&id, nccl_id, sizeof(id));
