@@ -11,6 +11,7 @@
 #include "tlp_internal.cuh"
 
 #include <algorithm>
+#include <vector>
 
 namespace {
 
@@ -78,9 +79,17 @@ tlp_status tlp_search_round(tlp_ctx* ctx, const tlp_seq_batch* h, int64_t N,
   if (blob < 0 || (h->U > 0 && h->str_off[0] != 0))
     return round_fail(ctx, TLP_ERR_SHAPE, "tlp_search_round: bad str_off");
 
-  // chunk boundaries (multiples of 5 candidates = one tensor-core tile)
+  // chunk boundaries (multiples of 5 candidates = one tensor-core tile).  The
+  // first two chunks are a quarter and a half of the others, so the kernels
+  // start after a short copy (pipeline fill); only while the event array allows.
   const int64_t cs = std::max<int64_t>(5, cdiv(cdiv(std::max<int64_t>(N, 1), chunks), 5) * 5);
-  const int nch = N > 0 ? (int)cdiv(N, cs) : 0;
+  std::vector<int64_t> bnd(1, 0);
+  {
+    const bool ramp = chunks + 2 <= TLP_MAX_ROUND_CHUNKS && cs >= 20;
+    const int64_t first[2] = {ramp ? cdiv(cs / 4, 5) * 5 : cs, ramp ? cdiv(cs / 2, 5) * 5 : cs};
+    for (int i = 0; bnd.back() < N; ++i) bnd.push_back(std::min<int64_t>(N, bnd.back() + (i < 2 ? first[i] : cs)));
+  }
+  const int nch = (int)bnd.size() - 1;
   // validate the host offsets the chunk copies rely on: seq_off in full
   // (non-decreasing within [0, P]), arg_off at the chunk boundaries
   if (N > 0) {
@@ -91,7 +100,7 @@ tlp_status tlp_search_round(tlp_ctx* ctx, const tlp_seq_batch* h, int64_t N,
         return round_fail(ctx, TLP_ERR_SHAPE, "tlp_search_round: seq_off must be non-decreasing");
     int64_t prev = 0;
     for (int ci = 0; ci <= nch; ++ci) {
-      const int64_t a = h->arg_off[h->seq_off[std::min<int64_t>(N, (int64_t)ci * cs)]];
+      const int64_t a = h->arg_off[h->seq_off[bnd[ci]]];
       if (a < prev || a > h->A)
         return round_fail(ctx, TLP_ERR_SHAPE, "tlp_search_round: arg_off outside [0, A]");
       prev = a;
@@ -139,7 +148,7 @@ tlp_status tlp_search_round(tlp_ctx* ctx, const tlp_seq_batch* h, int64_t N,
     TLP_CUDA_TRY(copy_range(dev, L.str_blob, h->str_blob, 0, blob, cs_));
   }
   for (int ci = 0; ci < nch; ++ci) {
-    const int64_t c0 = (int64_t)ci * cs, c1 = std::min<int64_t>(N, c0 + cs);
+    const int64_t c0 = bnd[ci], c1 = bnd[ci + 1];
     const int64_t p0 = h->seq_off[c0], p1 = h->seq_off[c1];
     const int64_t a0 = h->arg_off[p0], a1 = h->arg_off[p1];
     TLP_CUDA_TRY(copy_range(dev, L.seq_off, h->seq_off, c0, c1 + 1, cs_));
@@ -157,7 +166,7 @@ tlp_status tlp_search_round(tlp_ctx* ctx, const tlp_seq_batch* h, int64_t N,
 
   tlp_status st = TLP_OK;
   for (int ci = 0; ci < nch && st == TLP_OK; ++ci) {
-    const int64_t c0 = (int64_t)ci * cs, c1 = std::min<int64_t>(N, c0 + cs);
+    const int64_t c0 = bnd[ci], c1 = bnd[ci + 1];
     TLP_CUDA_TRY(cudaStreamWaitEvent(s, ctx->round_ev[ci], 0));
     if (ci == 0) st = encode_resolve(ctx, &d, s);
     if (st != TLP_OK) break;
