@@ -263,6 +263,7 @@ def run_ours(args):
     next_rows = next2_measure(scorer, feats, scores, task_off, args, stream, dev)
     next_rows.update(next1_measure(scorer, args, stream, rank))
     next_rows.update(next4_measure(feats, tfeats, labels, goff, precision, names, scale, args, stream, local))
+    next_rows.update(c5_measure(scorer, feats, args, stream, world))
 
     K = args.steps
     cand_s = world * N_ROUND * K / (round_ms / 1e3)
@@ -359,6 +360,48 @@ def next4_measure(feats, tfeats, labels, goff, precision, names, scale, args, st
     out["lstm_train"] = {"value": tfeats.shape[0] / (ms / 1e3), "unit": "samples/s", "ms_per_step": ms,
                          "config": "8,192 samples (16 groups x 512), LambdaRank, 1 LSTM layer, %s" % precision}
     return out
+
+
+def c5_measure(m, feats, args, stream, world):
+    """C5 (BASELINE configs[4]): candidates per round swept over
+    10^4 .. 10^7 on each GPU -- tlp_score + per-task top-16 over 100 tasks
+    (with the NCCL allgather merge when N > 1 GPUs: world x N candidates per
+    round) on device-resident encoded features; beyond the C2 round's 409,600
+    rows the features repeat.  Encode is excluded here (the main line times it:
+    0.64 ms per 409,600).  Shows the small-N regime, where a round is one
+    partial wave of the 148-SM persistent forward plus launch latency."""
+    import torch
+    points = []
+    steps = max(1, min(args.steps, 3))
+    for n in (10_000, 100_000, 1_000_000, 10_000_000):
+        if n <= feats.shape[0]:
+            x = feats[:n]
+        else:
+            x = feats.repeat((n + feats.shape[0] - 1) // feats.shape[0], 1, 1)[:n].contiguous()
+        sc = torch.empty((n, 1), dtype=torch.float32, device=feats.device)
+        off = np.linspace(0, n, T_TASKS + 1).astype(np.int64)
+        ti = torch.empty((T_TASKS, TOPK), dtype=torch.int64, device=feats.device)
+        tv = torch.empty((T_TASKS, TOPK), dtype=torch.float32, device=feats.device)
+
+        def call():
+            m.score(x, out=sc, stream=stream)
+            m.topk(sc, off, TOPK, idx_out=ti, val_out=tv, stream=stream)
+        for _ in range(args.warmup):
+            call()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            call()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        points.append({"N_per_gpu": n, "value": world * n / (ms / 1e3), "ms_per_round": ms})
+        del x, sc
+    torch.cuda.empty_cache()
+    return {"c5_sweep": {"unit": "candidates/s", "points": points,
+                         "config": "score + top-16 per task over 100 tasks, 2-layer bf16 model, "
+                                   "device-resident features, %d GPU(s)" % world}}
 
 
 def next1_measure(m, args, stream, rank):
