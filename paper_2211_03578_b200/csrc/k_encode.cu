@@ -63,6 +63,15 @@ __global__ void resolve_tokens(const uint8_t* __restrict__ blob, const int64_t* 
 // candidate's L*E floats to HBM with coalesced 8-byte stores (a candidate
 // block is 2,200 B, 8-byte aligned).
 constexpr int kEncWarps = 8;
+
+// R3's IEEE division x / s.  A zero numerator over a positive scale is
+// answered directly (the quotient is x itself, sign included); otherwise the
+// correctly rounded __fdiv_rn.  Most of a row's 22 entries are zeros (the
+// one-hot's other columns, absent arguments), and a zero numerator sends
+// __fdiv_rn down its slow path (FCHK), which dominated the kernel.
+__device__ __forceinline__ float div_rn(float x, float s) {
+  return (x == 0.f && s > 0.f) ? x : __fdiv_rn(x, s);
+}
 constexpr int kEncMaxElems = 32 * 64;  // L <= 32, E <= 64
 
 template <int E_, int T_>
@@ -100,7 +109,7 @@ __global__ void __launch_bounds__(32 * kEncWarps) encode_warp_kernel(
         }
       }
 #pragma unroll
-      for (int c = 0; c < Tr; ++c) row[c] = __fdiv_rn((tau >= 0 && c == tau) ? 1.f : 0.f, s_scale[c]);
+      for (int c = 0; c < Tr; ++c) row[c] = div_rn((tau >= 0 && c == tau) ? 1.f : 0.f, s_scale[c]);
       for (int a = 0; a < Er - Tr; ++a) {
         float v = 0.f;
         if (tau >= 0 && a < na) {
@@ -113,7 +122,7 @@ __global__ void __launch_bounds__(32 * kEncWarps) encode_warp_kernel(
             if (!isfinite(d) || !isfinite(v)) atomicOr(err, DERR_NONFINITE);
           }
         }
-        row[Tr + a] = __fdiv_rn(v, s_scale[Tr + a]);  // R3: IEEE round-to-nearest division
+        row[Tr + a] = div_rn(v, s_scale[Tr + a]);  // R3: IEEE round-to-nearest division
       }
     }
     __syncwarp();
