@@ -239,8 +239,10 @@ tlp_status tlp_topk_merge(tlp_ctx* ctx, const float* vals, const int64_t* idx, i
  *   task_off     HOST int64 [T+1], candidate segments per task (as tlp_topk).
  *   head         score column ranked (0 <= head < n_tasks).
  *   shard_base   global index of candidate 0 (sharded rounds, as tlp_topk).
- *   chunks       1..64: the candidates are cut into `chunks` ranges (multiples
- *                of 5 candidates); chunk c+1's host->device copy runs on an
+ *   chunks       1..64: the candidates are cut into about `chunks` ranges
+ *                (multiples of 5 candidates; with chunks <= 62 the first two
+ *                are a quarter and a half of the rest, a shorter pipeline
+ *                fill); chunk c+1's host->device copy runs on an
  *                internal copy stream while chunk c is encoded and scored on
  *                `stream`.  The result does not depend on `chunks` (batch
  *                invariance, R34).
