@@ -103,6 +103,26 @@ tlp_status dev_error_status(tlp_ctx* ctx) {
   return fail(ctx, TLP_ERR_STATE, "unknown device error");
 }
 
+// C-1 gradient bucket (declared in tlp_internal.cuh; called from simt_backward)
+tlp_status grad_bucket_ready(tlp_ctx* ctx, int64_t lo, int64_t hi, cudaStream_t s) {
+  static const char* env = getenv("TLP_GRAD_BUCKETS");
+  static const bool on = !(env && env[0] == '0');
+  ncclComm_t comm = reinterpret_cast<ncclComm_t>(ctx->comm);
+  if (!comm || !on || hi <= lo) return TLP_OK;
+  if (!ctx->comm_stream) {
+    TLP_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking));
+    for (cudaEvent_t& e : ctx->bucket_ev) TLP_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  cudaEvent_t ev = ctx->bucket_ev[ctx->buckets_issued % 4];
+  TLP_CUDA_TRY(cudaEventRecord(ev, s));
+  TLP_CUDA_TRY(cudaStreamWaitEvent(ctx->comm_stream, ev, 0));
+  if (ncclAllReduce(ctx->d_grads + lo, ctx->d_grads + lo, (size_t)(hi - lo), ncclFloat32, ncclSum, comm,
+                    ctx->comm_stream) != ncclSuccess)
+    return fail(ctx, TLP_ERR_NCCL, "gradient bucket allreduce failed");
+  ++ctx->buckets_issued;
+  return TLP_OK;
+}
+
 extern "C" {
 
 void tlp_default_config(tlp_config* c) {
@@ -165,6 +185,9 @@ void tlp_destroy(tlp_ctx* ctx) {
   for (cudaEvent_t& e : ctx->round_ev)
     if (e) cudaEventDestroy(e);
   if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+  if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);
+  for (cudaEvent_t e : ctx->bucket_ev)
+    if (e) cudaEventDestroy(e);
   delete ctx;
 }
 
@@ -366,12 +389,17 @@ tlp_status grads_impl(tlp_ctx* ctx, const float* feats, const float* labels,
            : rank_loss_grad(ctx, w.scores, labels, w.goff, G, B, max_group, w.counts, loss_out,
                             w.dscores, s);
   if (st != TLP_OK) return st;
+  ctx->buckets_issued = 0;
   if ((st = simt_backward(ctx, B, w.dscores, s)) != TLP_OK) return st;
   if (comm) {
     // C-1: gradient allreduce (sum); every rank then applies the same Adam step.
-    if (ncclAllReduce(ctx->d_grads, ctx->d_grads, ctx->off.total, ncclFloat32, ncclSum, comm, s) !=
-        ncclSuccess)
+    if (ctx->buckets_issued) {  // the buckets went out during the backward: join them
+      TLP_CUDA_TRY(cudaEventRecord(ctx->bucket_ev[4], ctx->comm_stream));
+      TLP_CUDA_TRY(cudaStreamWaitEvent(s, ctx->bucket_ev[4], 0));
+    } else if (ncclAllReduce(ctx->d_grads, ctx->d_grads, ctx->off.total, ncclFloat32, ncclSum, comm, s) !=
+               ncclSuccess) {
       return fail(ctx, TLP_ERR_NCCL, "gradient allreduce failed");
+    }
     if (ncclAllReduce(loss_out, loss_out, 1, ncclFloat32, ncclSum, comm, s) != ncclSuccess)
       return fail(ctx, TLP_ERR_NCCL, "loss allreduce failed");
   }

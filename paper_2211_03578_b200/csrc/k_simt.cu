@@ -840,6 +840,12 @@ tlp_status simt_backward(tlp_ctx* ctx, int64_t N, const float* g, cudaStream_t s
     EpiParams e; e.accumulate = t > 0;
     TRY(sgemm(ctx, false, true, M, H, hd, dU, hd, P + o.W1[t], hd, dh, H, e, s));
   }
+  // C-1 buckets in reverse R24 order: heads | residual blocks | attention (or
+  // LSTM) layers | upsample + positional table
+  const int64_t b_heads = o.W1[0];
+  const int64_t b_res = c.n_res ? o.Wa[0] : b_heads;
+  const int64_t b_mid = c.n_attn ? (c.backbone == 1 ? o.Wih[0] : o.Wq[0]) : b_res;
+  TRY(grad_bucket_ready(ctx, b_heads, o.total, s));
   // residual blocks
   for (int r = c.n_res - 1; r >= 0; --r) {
     const float* hin = r > 0 ? W + lay.hres[r - 1]
@@ -852,6 +858,7 @@ tlp_status simt_backward(tlp_ctx* ctx, int64_t N, const float* g, cudaStream_t s
     EpiParams ea; ea.accumulate = true;
     TRY(sgemm(ctx, false, true, M, H, H, dtmp, H, P + o.Wa[r], H, dh, H, ea, s));
   }
+  TRY(grad_bucket_ready(ctx, b_res, b_heads, s));
   // R49 LSTM layers: backpropagation through time, then the batched weight gradients
   for (int l = c.n_attn - 1; l >= 0 && c.backbone == 1; --l) {
     const float* hin = l > 0 ? W + lay.hattn[l - 1] : (c.pos_enc ? W + lay.hpos : W + lay.up[c.n_up - 1]);
@@ -906,6 +913,7 @@ tlp_status simt_backward(tlp_ctx* ctx, int64_t N, const float* g, cudaStream_t s
     }
     TRY(sgemm(ctx, false, true, M, H, 3 * H, dqkv, 3 * H, wcat, 3 * H, dh, H, ea, s));
   }
+  TRY(grad_bucket_ready(ctx, b_mid, b_res, s));
   // R43: dpos = sum over candidates; d(up_out) = d(up_out + pos) unchanged
   if (c.pos_enc) {
     pos_grad_kernel<<<(unsigned)cdiv((int64_t)c.L * H, 256), 256, 0, s>>>(dh, N, c.L, (int)H, G + o.pos);
@@ -931,5 +939,6 @@ tlp_status simt_backward(tlp_ctx* ctx, int64_t N, const float* g, cudaStream_t s
       cur = nxt;
     }
   }
+  TRY(grad_bucket_ready(ctx, 0, b_mid, s));
   return TLP_OK;
 }

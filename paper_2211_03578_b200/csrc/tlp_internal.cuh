@@ -104,6 +104,12 @@ struct tlp_ctx {
 
   // NCCL
   void* comm = nullptr;  // ncclComm_t
+  // C-1 gradient buckets: each finished parameter range is
+  // allreduced on comm_stream while the backward continues (TLP_GRAD_BUCKETS=0:
+  // one allreduce after the backward, the no-overlap variant)
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t bucket_ev[5] = {};
+  int buckets_issued = 0;
   int rank = 0, world = 1;
 
   int64_t launches = 0;
@@ -192,6 +198,9 @@ bool tc_wgrad_bias(tlp_ctx* ctx, int64_t M, int64_t N, int64_t K, const float* A
                    cudaStream_t s, tlp_status* st, int J = 1, int64_t bjs = 0, int64_t pjs = 0);
 tlp_status simt_forward(tlp_ctx* ctx, const float* feats, int64_t N, float* scores, bool save,
                         cudaStream_t s);
+// C-1 bucket: gradients [lo, hi) are final on stream s -> allreduce them on the
+// comm stream (no-op without a communicator or with TLP_GRAD_BUCKETS=0)
+tlp_status grad_bucket_ready(tlp_ctx* ctx, int64_t lo, int64_t hi, cudaStream_t s);
 tlp_status simt_backward(tlp_ctx* ctx, int64_t N, const float* dscores, cudaStream_t s);
 
 // k_tc_gemm.cu : tf32 tcgen05 GEMM used by the training path of bf16 contexts
