@@ -258,6 +258,27 @@ def run_ours(args):
         dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
     e2e_ms = float(e2e_ms.item())
 
+    # --- host side, reported separately: the H2D copy of one packed
+    # round from pinned memory alone, and host packing of candidate sequences
+    # (synth.pack, pure Python) on a bounded sample; neither is in `value` ---
+    import time
+    hb = hbatch.nbytes()
+    src_h = torch.empty(hb, dtype=torch.uint8).pin_memory()
+    dst_d = torch.empty(hb, dtype=torch.uint8, device=dev)
+    dst_d.copy_(src_h, non_blocking=True)
+    torch.cuda.synchronize()
+    h0 = torch.cuda.Event(enable_timing=True); h1 = torch.cuda.Event(enable_timing=True)
+    h0.record(); dst_d.copy_(src_h, non_blocking=True); h1.record(); h1.synchronize()
+    h2d_ms = h0.elapsed_time(h1)
+    del src_h, dst_d
+    sample = packed.to_lists()[:20000]
+    t0 = time.perf_counter()
+    synth.pack(sample)
+    pack_s = time.perf_counter() - t0
+    host_side = {"h2d_ms_per_round": h2d_ms, "h2d_GBps": hb / (h2d_ms / 1e3) / 1e9,
+                 "pack_us_per_candidate": pack_s / len(sample) * 1e6,
+                 "pack_sample": "synth.pack of %d candidates (Python, one core)" % len(sample)}
+
     # --- NEXT-2 rows: duplicate scan of this round's features and
     # the §6.1 top-k score of its scores against synthetic latencies ---
     next_rows = next2_measure(scorer, feats, scores, task_off, args, stream, dev)
@@ -302,6 +323,8 @@ def run_ours(args):
         "train_samples_per_s": train_s,
         "phase_ms_per_step": {"encode": enc_ms / K, "score": score_ms / K, "topk": topk_ms / K,
                               "train": train_ms / K},
+        "score_only": {"value": world * N_ROUND * K / (score_ms / 1e3), "unit": "candidates/s"},
+        "host_side": host_side,
         "roofline": roof,
         "e2e": {"value": world * N_ROUND * K / (e2e_ms / 1e3), "unit": "candidates/s",
                 "h2d_bytes_per_step": hbatch.nbytes(), "d2h_bytes_per_step": T_TASKS * TOPK * 12,
