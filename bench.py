@@ -285,6 +285,7 @@ def run_ours(args):
     next_rows.update(next1_measure(scorer, args, stream, rank))
     next_rows.update(next4_measure(feats, tfeats, labels, goff, precision, names, scale, args, stream, local))
     next_rows.update(c5_measure(scorer, feats, args, stream, world))
+    next_rows.update(k9_measure(trainer, labels, goff, args, stream))
 
     K = args.steps
     cand_s = world * N_ROUND * K / (round_ms / 1e3)
@@ -383,6 +384,37 @@ def next4_measure(feats, tfeats, labels, goff, precision, names, scale, args, st
     out["lstm_train"] = {"value": tfeats.shape[0] / (ms / 1e3), "unit": "samples/s", "ms_per_step": ms,
                          "config": "8,192 samples (16 groups x 512), LambdaRank, 1 LSTM layer, %s" % precision}
     return out
+
+
+def k9_measure(m, labels, goff, args, stream):
+    """K9: the LambdaRank loss + dL/ds kernel alone on the
+    training batch (16 groups x 512, seeded scores), CUDA events over K calls.
+    Work = ordered pairs evaluated (sum over groups of n^2), ~30 FLOP + 2 SFU per
+    pair; roofline: the FP32 SIMT peak SMs x 128 x 2 x clock."""
+    import torch
+    g = torch.Generator(device=labels.device).manual_seed(5)
+    sc = torch.randn(labels.shape, generator=g, device=labels.device, dtype=torch.float32)
+    steps = max(1, args.steps)
+    for _ in range(args.warmup):
+        m.lambdarank(sc, labels, goff, stream=stream)
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        m.lambdarank(sc, labels, goff, stream=stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    sizes = np.diff(np.asarray(goff, np.int64))
+    pairs = float((sizes.astype(np.float64) ** 2).sum())
+    props = torch.cuda.get_device_properties(labels.device)
+    peak = props.multi_processor_count * 128 * 2 * 1.965e9 / 1e12
+    ach = 30.0 * pairs / (ms / 1e3) / 1e12
+    return {"k9_lambdarank": {"value": pairs / (ms / 1e3), "unit": "ordered pairs/s", "ms_per_call": ms,
+                              "roofline": {"bound": "alu", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
+                                           "frac": ach / peak,
+                                           "peak_kind": "derived: SMs x 128 FP32 lanes x 2 x 1965 MHz"},
+                              "note": "one call incl. the host group offsets; 16 groups x 512"}}
 
 
 def c5_measure(m, feats, args, stream, world):
