@@ -109,7 +109,9 @@ __global__ void sum_counts(const double* __restrict__ part, int G, int nt,
   counts[t] = s;
 }
 
-__global__ void __launch_bounds__(kThreads) rank_kernel(const float* __restrict__ scores,
+constexpr int kRankThreads = 1024;  // two threads per item of a 512-item group
+
+__global__ void __launch_bounds__(kRankThreads) rank_kernel(const float* __restrict__ scores,
                                                         const float* __restrict__ labels,
                                                         const int64_t* __restrict__ goff, int nt,
                                                         float* __restrict__ loss_part,
@@ -125,45 +127,66 @@ __global__ void __launch_bounds__(kThreads) rank_kernel(const float* __restrict_
   float* iD = Gs + cap;
   int* idx = reinterpret_cast<int*>(iD + cap);
   const int n = gather_present(scores, labels, lo, hi, t, nt, s, y, idx);
+  // Two threads per item (kRankThreads = 1024: item i = pair tid / 2, each half
+  // of the pair scans half of the j range; the halves are combined with one
+  // shuffle).  Every thread runs every round so the shuffles see full warps.
+  const int half = threadIdx.x & 1, nth = blockDim.x >> 1;
+  const int jm = n / 2, j0 = half ? jm : 0, j1 = half ? n : jm;
   // ranks (R17) and ideal ranks -> maxDCG
   float dcg = 0.f;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const float si = s[i], yi = y[i];
-    int rs = 1, ry = 1;
-    for (int j = 0; j < n; ++j) {
-      const float sj = s[j], yj = y[j];
-      rs += (sj > si) || (sj == si && j < i);
-      ry += (yj > yi) || (yj == yi && j < i);
+  for (int base = 0; base < n; base += nth) {
+    const int i = base + (threadIdx.x >> 1);
+    const bool act = i < n;
+    const float si = act ? s[i] : 0.f, yi = act ? y[i] : 0.f;
+    int rs = 0, ry = 0;
+    if (act) {
+      for (int j = j0; j < j1; ++j) {
+        const float sj = s[j], yj = y[j];
+        rs += (sj > si) || (sj == si && j < i);
+        ry += (yj > yi) || (yj == yi && j < i);
+      }
     }
-    iD[i] = 1.0f / log2f(1.0f + (float)rs);
-    dcg += expm1f(yi * kLn2) / log2f(1.0f + (float)ry);
+    rs += __shfl_xor_sync(0xffffffffu, rs, 1);
+    ry += __shfl_xor_sync(0xffffffffu, ry, 1);
+    if (act && half == 0) {
+      iD[i] = 1.0f / log2f(2.0f + (float)rs);               // rank = 1 + rs
+      dcg += expm1f(yi * kLn2) / log2f(2.0f + (float)ry);
+    }
   }
   const float maxdcg = fmaxf(block_sum(dcg, red), 1e-10f);
   for (int i = threadIdx.x; i < n; i += blockDim.x) Gs[i] = expm1f(y[i] * kLn2) / maxdcg;
   __syncthreads();
   float lsum = 0.f;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const float si = s[i], yi = y[i], Gi = Gs[i], iDi = iD[i];
+  for (int base = 0; base < n; base += nth) {
+    const int i = base + (threadIdx.x >> 1);
+    const bool act = i < n;
     float gi = 0.f, li = 0.f;
-    for (int j = 0; j < n; ++j) {
-      const float yj = y[j];
-      if (yi == yj) continue;
-      const float w = fabsf(Gi - Gs[j]) * fabsf(iDi - iD[j]);
-      // z = s_hi - s_lo of the ordered pair
-      const float z = (yi > yj) ? (si - s[j]) : (s[j] - si);
-      const float e = expf(-fabsf(z));
-      const float r = __frcp_rn(1.0f + e);                  // one correctly rounded reciprocal
-      const float sig = (z >= 0.f) ? e * r : r;             // sigmoid(-z), sign-stable (R30)
-      if (yi > yj) {
-        li += w * (fmaxf(-z, 0.f) + log1pf(e));
-        gi -= w * sig;
-      } else {
-        gi += w * sig;
+    if (act) {
+      const float si = s[i], yi = y[i], Gi = Gs[i], iDi = iD[i];
+      for (int j = j0; j < j1; ++j) {
+        const float yj = y[j];
+        if (yi == yj) continue;
+        const float w = fabsf(Gi - Gs[j]) * fabsf(iDi - iD[j]);
+        // z = s_hi - s_lo of the ordered pair
+        const float z = (yi > yj) ? (si - s[j]) : (s[j] - si);
+        const float e = expf(-fabsf(z));
+        const float r = __frcp_rn(1.0f + e);                  // one correctly rounded reciprocal
+        const float sig = (z >= 0.f) ? e * r : r;             // sigmoid(-z), sign-stable (R30)
+        if (yi > yj) {
+          li += w * (fmaxf(-z, 0.f) + log1pf(e));
+          gi -= w * sig;
+        } else {
+          gi += w * sig;
+        }
       }
     }
-    // the 1/ln 2 of log2 and of d/ds log2(1 + e^{-z}) applied once per item
-    dscores[(lo + idx[i]) * nt + t] = gi * kInvLn2;
-    lsum += li * kInvLn2;
+    gi += __shfl_xor_sync(0xffffffffu, gi, 1);
+    li += __shfl_xor_sync(0xffffffffu, li, 1);
+    if (act && half == 0) {
+      // the 1/ln 2 of log2 and of d/ds log2(1 + e^{-z}) applied once per item
+      dscores[(lo + idx[i]) * nt + t] = gi * kInvLn2;
+      lsum += li * kInvLn2;
+    }
   }
   const float L = block_sum(lsum, red);
   if (threadIdx.x == 0) loss_part[(int64_t)t * gridDim.x + g] = L;
@@ -309,7 +332,7 @@ tlp_status rank_loss_grad(tlp_ctx* ctx, const float* scores, const float* labels
   TLP_CUDA_TRY(cudaMemsetAsync(dscores, 0, (size_t)B * nt * sizeof(float), s));
   const size_t smem = (size_t)max_group * (4 * sizeof(float) + sizeof(int));
   cudaFuncSetAttribute(rank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  rank_kernel<<<dim3(G, nt), kThreads, smem, s>>>(scores, labels, d_goff, nt, loss_part, dscores);
+  rank_kernel<<<dim3(G, nt), kRankThreads, smem, s>>>(scores, labels, d_goff, nt, loss_part, dscores);
   TLP_LAUNCH_CHECK();
   finalize_rank<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv((int64_t)B * nt, 256), 1024)), 256, 0, s>>>(
       loss_part, G, nt, d_counts, dscores, B, loss_out, ctx->d_err);
