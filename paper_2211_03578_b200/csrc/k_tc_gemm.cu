@@ -691,7 +691,10 @@ tlp_status tc_gemm(tlp_ctx* ctx, bool ta, bool tb, int64_t M, int64_t N, int64_t
 bool tc_wgrad_bias(tlp_ctx* ctx, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,
                    const float* B, int64_t ldb, float* part, int splits, int64_t kslice,
                    cudaStream_t s, tlp_status* st, int J, int64_t bjs, int64_t pjs) {
-  if (!(splits > 1 && M > BM && M <= WROWS && N > BN && N <= WROWS)) return false;
+  // 64 < M, N <= 256: also the head (256 x 128) and second upsample (128 x 256)
+  // layers, whose bias sums then ride along instead of a separate colsum pass
+  // (the unused part of the 256 x 256 tile computes zeros)
+  if (!(splits > 1 && M > 64 && M <= WROWS && N > 64 && N <= WROWS)) return false;
   if (J > 1 && (bjs % 4 != 0)) return false;
   static bool wattr = false;
   if (!wattr) {
