@@ -128,12 +128,20 @@ def fwd_flops_per_cand(L=25, E=22, H=256, up=(128, 256), heads=8, n_attn=2, n_re
     return f
 
 
+def train_flops_per_sample(n_attn=1, n_tasks=1, **kw):
+    """Algorithmic forward + backward FLOPs per training sample: every dense
+    layer costs its forward GEMM plus the dgrad and wgrad GEMMs (2x), except
+    the first upsample layer, whose input is data (no dgrad); the attention
+    core QK^T / PV likewise 3x (90.68 M at 1 layer)."""
+    L, E, up = kw.get("L", 25), kw.get("E", 22), kw.get("up", (128, 256))
+    return 3 * fwd_flops_per_cand(n_attn=n_attn, n_tasks=n_tasks, **kw) - 2 * L * E * up[0]
+
+
 # ------------------------------------------------------------------ our arm
 def run_ours(args):
     import torch
     import torch.distributed as dist
     import paper_2211_03578_b200 as tp
-    import oracle  # only for cpu_baseline (allowed) and token-table/scale fitting of inputs
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -143,36 +151,33 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     precision = args.precision
-    # --- inputs (host, seeded per rank: each rank scores its own shard) ---
-    tokens = oracle.build_token_table(synth.training_stream())
-    names = sorted(tokens, key=tokens.get)
-    train_raw = synth.generate(99, 2000, unseen_rate=0.0)
-    raw = np.stack([oracle.extract_rows(s, tokens, 25, 22, 11) for s in train_raw.to_lists()])
-    scale = oracle.fit_scales(raw)
+    dev = torch.device("cuda", local)
+    # --- model state through the library only (no oracle code on this arm):
+    # rank 0 fits the token table (R1) and the normalisation scales (R3) on a
+    # seeded training split and initialises the weights; tlp_broadcast_state
+    # (C-3) hands the state to the other ranks ---
     packed = synth.generate(1000 + rank, N_ROUND)
     task_off = synth.uniform_task_off(T_TASKS, PER_TASK)
 
+    def init_flat(cfg, seed):
+        return np.concatenate([v.ravel() for v in synth.init_params(seed, cfg.param_shapes())]).astype(np.float32)
+
+    def make(cfg, seed):
+        m = tp.TLP(cfg, device=local)
+        if rank == 0:
+            m.fit_token_table(synth.generate(12345, 2000, unseen_rate=0.0))
+            m.fit_norm_scales(tp.DeviceBatch.from_packed(synth.generate(99, 2000, unseen_rate=0.0), device=dev))
+            m.set_params(init_flat(cfg, seed))
+        if world > 1:
+            m.init_comm()
+            m.broadcast_state(root=0)
+        return m
+
     cfg2 = tp.TLPConfig(n_attn=2, precision=precision)
-    scorer = tp.TLP(cfg2, device=local)
-    scorer.set_token_table(names)
-    scorer.set_norm_scales(scale)
-    from oracle import model as OM
-    ocfg2 = OM.Config(n_attn=2)
-    flat2 = np.concatenate([v.ravel() for v in synth.init_params(7, OM.param_shapes(ocfg2))]).astype(np.float32)
-    scorer.set_params(flat2)
-
+    scorer = make(cfg2, 7)
     cfg1 = tp.TLPConfig(n_attn=1, precision=precision)
-    trainer = tp.TLP(cfg1, device=local)
-    ocfg1 = OM.Config(n_attn=1)
-    flat1 = np.concatenate([v.ravel() for v in synth.init_params(8, OM.param_shapes(ocfg1))]).astype(np.float32)
-    trainer.set_params(flat1)
-    trainer.set_norm_scales(scale)
-    trainer.set_token_table(names)
-    if world > 1:
-        scorer.init_comm()
-        trainer.init_comm()
+    trainer = make(cfg1, 8)
 
-    dev = torch.device("cuda", local)
     dbatch = tp.DeviceBatch.from_packed(packed, device=dev)
     feats = torch.empty((N_ROUND, 25, 22), dtype=torch.float32, device=dev)
     scores = torch.empty((N_ROUND, 1), dtype=torch.float32, device=dev)
@@ -283,7 +288,7 @@ def run_ours(args):
     # the §6.1 top-k score of its scores against synthetic latencies ---
     next_rows = next2_measure(scorer, feats, scores, task_off, args, stream, dev)
     next_rows.update(next1_measure(scorer, args, stream, rank))
-    next_rows.update(next4_measure(feats, tfeats, labels, goff, precision, names, scale, args, stream, local))
+    next_rows.update(next4_measure(feats, tfeats, labels, goff, precision, args, stream, local))
     next_rows.update(c5_measure(scorer, feats, args, stream, world))
     next_rows.update(k9_measure(trainer, labels, goff, args, stream))
 
@@ -293,12 +298,21 @@ def run_ours(args):
     peaks, peaks_kind = load_peaks()
     fl = fwd_flops_per_cand()
     score_launch_ms = score_ms / K
+    clocks = clk.summary()
+    # burst peak for a kernel that ran at (near) the maximum clock -- the
+    # sustained figure was measured at a lower median clock (MEASURED_PEAKS.json
+    # clocks_under_load); both fractions are reported
+    at_max = bool(clocks.get("sm_mhz") and clocks.get("sm_max_mhz") and
+                  clocks["sm_mhz"] >= 0.95 * clocks["sm_max_mhz"])
+    burst, sust = peaks["bf16_tflops"], peaks["bf16_tflops_sustained"]
+    peak_used, kind_used = (burst, "bf16 burst") if at_max else (sust, "bf16 sustained")
     if precision == "bf16":
         achieved = fl * N_ROUND / (score_launch_ms / 1e3) / 1e12
-        peak = peaks["bf16_tflops_sustained"]
         roof = {"bound": "tensor", "kernel": "tc_forward_kernel (tlp_score, 1 launch/round)",
-                "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                "traffic": _traffic("tc_forward_kernel"), "peak_kind": peaks_kind + " bf16 sustained",
+                "achieved": achieved, "peak": peak_used, "unit": "TFLOP/s", "frac": achieved / peak_used,
+                "frac_burst": achieved / burst, "frac_sustained": achieved / sust,
+                "traffic": _traffic("tc_forward_kernel"), "peak_kind": peaks_kind + " " + kind_used +
+                " (burst when the timed region's median SM clock >= 95% of max)",
                 "flops_per_launch": fl * N_ROUND,
                 "traffic_note": "dram__bytes_read+write per launch from profiles/*_traffic.json "
                                 "(ncu --set full of the same command); algorithmic input 2,200 B/cand"}
@@ -332,10 +346,25 @@ def run_ours(args):
                 "call": "tlp_search_round, %d chunks" % args.chunks},
         "gpu_launches": launches,
         "next_rows": next_rows,
-        "clocks": clk.summary(),
+        "clocks": clocks,
     }
+    tfl = train_flops_per_sample(n_attn=1)
+    t_ach = tfl * B_TRAIN / (train_ms / K / 1e3) / 1e12
+    out["roofline_train"] = {
+        "bound": "tensor", "scope": "whole C3 train step (label normalisation, forward, LambdaRank, "
+                                    "backward, allreduce, Adam; all kernels)",
+        "achieved": t_ach, "peak": peak_used, "unit": "TFLOP/s", "frac": t_ach / peak_used,
+        "frac_burst": t_ach / burst, "flops_per_step": tfl * B_TRAIN,
+        "flops_note": "algorithmic fwd + bwd (bwd = dgrad + wgrad) per sample %.2f M x %d samples; "
+                      "the bf16 context executes the dense layers as bf16x3 (3 MMAs per product, R37)"
+                      % (tfl / 1e6, B_TRAIN)}
+    out["c4_mtl"] = c4_measure(scorer, feats, args, stream, local, dev, world)
+    out["c1_tiny"] = c1_measure(args, local, dev)
+    if world > 1:
+        out["allreduce"] = allreduce_measure(trainer, dev)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        out["cpu_baseline"] = cpu_baseline(seconds_hint=15.0)
+        out["cpu_baseline"] = cpu_baseline(seconds_hint=12.0)
+        out["cpu_baseline_1core"] = cpu_baseline(seconds_hint=8.0, threads=1)
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:
@@ -345,7 +374,136 @@ def run_ours(args):
 GA_S, GA_POP, GA_CHILD, GA_ITERS = 100, 512, 1920, 4
 
 
-def next4_measure(feats, tfeats, labels, goff, precision, names, scale, args, stream, local):
+def c4_measure(enc, feats, args, stream, local, dev, world):
+    """C4 (BASELINE configs[3]): MTL-TLP, a shared 1-layer encoder and 4
+    hardware heads, the target head's labels on a seeded 7%
+    Bernoulli subset, tasks 1..3 fully labelled.  Training: the C3-shape
+    step (16 groups x 512) through tlp_train_step; scoring: tlp_score (4 scores
+    per candidate, fused bf16 kernel) over the round's 409,600 encoded
+    candidates.  CUDA events, W warm-up + K timed calls; model state as the
+    main line (library-initialised weights, device-side labels)."""
+    import torch
+    import paper_2211_03578_b200 as tp
+    cfg = tp.TLPConfig(n_attn=1, n_tasks=4, precision=args.precision)
+    m = tp.TLP(cfg, device=local)
+    m.set_params(np.concatenate([v.ravel() for v in synth.init_params(10, cfg.param_shapes())]).astype(np.float32))
+    if world > 1:
+        m.init_comm()
+    rank = int(os.environ.get("RANK", "0"))
+    tp_b = synth.generate(3000 + rank, B_TRAIN)
+    goff = np.arange(TRAIN_GROUPS + 1, dtype=np.int64) * TRAIN_PER_GROUP
+    lab = np.stack([synth.latencies(tp_b, goff, 40 + rank, task_noise=0.3 * (t > 0)) for t in range(4)], 1)
+    lab_d = torch.from_numpy(lab.astype(np.float32)).to(dev)
+    y = torch.empty((B_TRAIN, 4), dtype=torch.float32, device=dev)
+    for t in range(4):
+        col = m.normalize_labels(lab_d[:, t].contiguous(), goff, stream=stream)
+        y[:, t] = col
+    keep = torch.from_numpy(np.random.default_rng(41 + rank).random(B_TRAIN) < 0.07).to(dev)
+    y[:, 0] = torch.where(keep, y[:, 0], torch.full_like(y[:, 0], float("nan")))
+    y = y.contiguous()
+    X = enc.encode(tp.DeviceBatch.from_packed(tp_b, device=dev), stream=stream)
+    loss = torch.empty(1, dtype=torch.float32, device=dev)
+    sc = torch.empty((feats.shape[0], 4), dtype=torch.float32, device=dev)
+
+    def timed(fn, steps):
+        for _ in range(args.warmup):
+            fn()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / steps
+
+    steps = max(1, args.steps)
+    t_ms = timed(lambda: m.train_step(X, y, goff, loss_out=loss, stream=stream), steps)
+    s_ms = timed(lambda: m.score(feats, out=sc, stream=stream), max(1, min(steps, 5)))
+    m.sync()
+    fl_t, fl_s = train_flops_per_sample(n_attn=1, n_tasks=4), fwd_flops_per_cand(n_attn=1, n_tasks=4)
+    return {"train": {"value": world * B_TRAIN / (t_ms / 1e3), "unit": "samples/s", "ms_per_step": t_ms,
+                      "tflops": fl_t * B_TRAIN / (t_ms / 1e3) / 1e12},
+            "score": {"value": world * feats.shape[0] / (s_ms / 1e3), "unit": "candidates/s",
+                      "ms_per_call": s_ms, "tflops": fl_s * feats.shape[0] / (s_ms / 1e3) / 1e12},
+            "target_label_frac": float(keep.float().mean().item()),
+            "config": "MTL-TLP 4 heads, 1 attention layer, hidden 256, %s; train 16 groups x 512 "
+                      "(target head on 7%% of samples); score 409,600 candidates" % args.precision}
+
+
+def c1_measure(args, local, dev):
+    """C1 (BASELINE configs[0]): the tiny model (hidden 64, 1 layer, 1 task) on
+    256 synthetic candidates: tlp_encode -> tlp_score -> LambdaRank (loss +
+    dL/ds) -> top-16, the fp32 SIMT context (the bf16 tensor-core kernels need
+    the paper shape).  Launch-latency bound: reported as wall time per call
+    (host clock around the synchronised sequence, median of K) and as device
+    time (CUDA events)."""
+    import time
+    import torch
+    import paper_2211_03578_b200 as tp
+    cfg = tp.tiny_config()
+    m = tp.TLP(cfg, device=local)
+    m.fit_token_table(synth.generate(12345, 500, unseen_rate=0.0))
+    b = tp.DeviceBatch.from_packed(synth.generate(77, 256), device=dev)
+    m.fit_norm_scales(b)
+    m.set_params(np.concatenate([v.ravel() for v in synth.init_params(11, cfg.param_shapes())]).astype(np.float32))
+    goff = np.array([0, 256], np.int64)
+    lat = torch.from_numpy(synth.latencies(synth.generate(77, 256), goff, 3).astype(np.float32)).to(dev)
+    y = m.normalize_labels(lat, goff).view(256, 1).contiguous()
+    stream = torch.cuda.current_stream(dev)
+
+    def call():
+        X = m.encode(b, stream=stream)
+        s = m.score(X, stream=stream)
+        m.lambdarank(s, y, goff, stream=stream)
+        m.topk(s, goff, TOPK, stream=stream)
+    for _ in range(args.warmup):
+        call()
+    torch.cuda.synchronize()
+    walls = []
+    for _ in range(max(5, args.steps)):
+        t0 = time.perf_counter()
+        call()
+        torch.cuda.synchronize()
+        walls.append((time.perf_counter() - t0) * 1e3)
+    e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(max(5, args.steps)):
+        call()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return {"wall_ms_per_call": statistics.median(walls),
+            "device_ms_per_call": e0.elapsed_time(e1) / max(5, args.steps),
+            "config": "256 candidates, hidden 64, 1 attention layer, fp32: encode + score + LambdaRank + top-16"}
+
+
+def allreduce_measure(m, dev):
+    """The C-1 gradient allreduce alone: ncclAllReduce (sum, fp32) of the
+    trainer's gradient vector through torch.distributed (the same NCCL, same
+    size as the library's in-step allreduce), CUDA events, max over ranks."""
+    import torch
+    import torch.distributed as dist
+    n = m.num_params
+    buf = torch.zeros(n, dtype=torch.float32, device=dev)
+    for _ in range(5):
+        dist.all_reduce(buf)
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+    reps = 20
+    e0.record()
+    for _ in range(reps):
+        dist.all_reduce(buf)
+    e1.record()
+    torch.cuda.synchronize()
+    us = torch.tensor([e0.elapsed_time(e1) * 1e3 / reps], dtype=torch.float64, device=dev)
+    dist.all_reduce(us, op=dist.ReduceOp.MAX)
+    return {"us_per_allreduce": float(us.item()), "bytes": 4 * n,
+            "nccl_debug_file": os.environ.get("NCCL_DEBUG_FILE"),
+            "note": "torch.distributed NCCL allreduce of the same fp32 gradient size; NCCL_DEBUG=INFO "
+                    "log (algorithm / protocol / NVLS selection) written to nccl_debug_file"}
+
+
+def next4_measure(feats, tfeats, labels, goff, precision, args, stream, local):
     """NEXT-4: the LSTM backbone (R49, 1 layer, paper widths) in
     place of attention -- scoring the round's 409,600 encoded candidates and
     one C3-shape LambdaRank train step (8,192 samples), CUDA events, W warm-up
@@ -353,11 +511,10 @@ def next4_measure(feats, tfeats, labels, goff, precision, names, scale, args, st
     projection and each of the 25 recurrent steps, SIMT cells."""
     import torch
     import paper_2211_03578_b200 as tp
-    from oracle import model as OM
-    ocfg = OM.Config(n_attn=1, backbone="lstm")
-    flat = np.concatenate([v.ravel() for v in synth.init_params(9, OM.param_shapes(ocfg))]).astype(np.float32)
+    cfg = tp.TLPConfig(n_attn=1, precision=precision, backbone="lstm")
+    flat = np.concatenate([v.ravel() for v in synth.init_params(9, cfg.param_shapes())]).astype(np.float32)
     out = {}
-    m = tp.TLP(tp.TLPConfig(n_attn=1, precision=precision, backbone="lstm"), device=local)
+    m = tp.TLP(cfg, device=local)
     m.set_params(flat)
     sc = torch.empty((feats.shape[0], 1), dtype=torch.float32, device=feats.device)
     loss = torch.empty(1, dtype=torch.float32, device=feats.device)
@@ -578,15 +735,26 @@ def oracle_sample(n_cand: int, seed: int = 0):
     return time.perf_counter() - t0
 
 
-def cpu_baseline(seconds_hint=15.0):
-    n = 256
-    dt = oracle_sample(n)
-    # scale the sample to ~seconds_hint of CPU work
-    n2 = int(min(16384, max(256, n * seconds_hint / max(dt, 1e-3))))
-    dt2 = oracle_sample(n2, seed=1)
-    return {"value": n2 / dt2, "unit": "candidates/s", "cores": _oracle_threads(), "kind": "oracle",
+def cpu_baseline(seconds_hint=15.0, threads=None):
+    """The oracle as it stands on the host cores: all BLAS threads (threads=None)
+    or limited with threadpoolctl (threads=1: one core, SURVEY §8(d) "time it
+    twice")."""
+    import contextlib
+    ctx = contextlib.nullcontext()
+    if threads is not None:
+        from threadpoolctl import threadpool_limits
+        ctx = threadpool_limits(limits=threads)
+    with ctx:
+        cores = _oracle_threads()
+        n = 128
+        dt = oracle_sample(n)
+        # scale the sample to ~seconds_hint of CPU work
+        n2 = int(min(16384, max(128, n * seconds_hint / max(dt, 1e-3))))
+        dt2 = oracle_sample(n2, seed=1)
+    return {"value": n2 / dt2, "unit": "candidates/s", "cores": cores, "kind": "oracle",
+            "host_cpus": os.cpu_count(), "affinity": len(os.sched_getaffinity(0)),
             "sample": "%d candidates of the C2 round (1 task): oracle encode + fp64 forward (2 attention "
-                      "layers, hidden 256) + top-16, %.1f s" % (n2, dt2)}
+                      "layers, hidden 256) + top-16, %.1f s, %d BLAS thread(s)" % (n2, dt2, cores)}
 
 
 def run_reference(args):
@@ -613,6 +781,26 @@ def run_reference(args):
     print(json.dumps(out), flush=True)
 
 
+def spawn(n: int) -> int:
+    """`python bench.py --gpus N` without torchrun: re-launch this command under
+    torch.distributed.run with N local ranks (one per GPU, 127.0.0.1
+    rendezvous), the way the driver launches it; rank 0 prints the line."""
+    import socket
+    import subprocess
+    import torch
+    have = torch.cuda.device_count()
+    if have < n:
+        print(json.dumps({"metric": METRIC, "error": "--gpus %d but only %d visible GPU(s)" % (n, have)}),
+              flush=True)
+        return 2
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(n),
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -626,6 +814,18 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(spawn(args.gpus))
+    if "WORLD_SIZE" in os.environ and int(os.environ["WORLD_SIZE"]) != args.gpus:
+        print("bench.py: --gpus %d but WORLD_SIZE=%s; measuring WORLD_SIZE ranks"
+              % (args.gpus, os.environ["WORLD_SIZE"]), file=sys.stderr)
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        # NCCL's algorithm / protocol choice (NVLS, ring, tree) for the scaling record
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT,TUNING")
+        logdir = os.path.join(ROOT, "gpurun_out")
+        os.environ.setdefault("NCCL_DEBUG_FILE", os.path.join(
+            logdir if os.path.isdir(logdir) else "/tmp", "nccl_bench.%h.%p.log"))
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -21,7 +21,7 @@
  *     workspaces and the NCCL communicator.
  *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
  *     Calls are stream-ordered; none synchronises the device except
- *     tlp_sync / tlp_get_params / tlp_get_grads.
+ *     tlp_sync / tlp_get_params / tlp_get_grads / tlp_get_train_scores.
  *   - Host-detectable errors (NULL pointers, bad sizes, config mismatch) return
  *     immediately with a negative status and leave all outputs untouched.
  *     Device-detected data errors (empty sequence, type id >= T, non-finite
@@ -139,6 +139,20 @@ tlp_status tlp_set_token_table(tlp_ctx* ctx, const uint8_t* blob, const int64_t*
 /* Post-processing normalisation scales ("normalization"; R3): [E] host
  * floats, all > 0.  Output column c is divided by scale[c] (IEEE fp32). */
 tlp_status tlp_set_norm_scales(tlp_ctx* ctx, const float* scale);
+/* R1 / R3 fitted by the library from a training split (the paper's
+ * post-processing "normalization", fitted instead of supplied):
+ * tlp_fit_token_table: token i + 2 for the i-th distinct name argument in
+ *   first-occurrence order over the packed batch `in` (HOST memory; candidates,
+ *   primitives, arguments in order; all arguments, cropped or not).  Replaces
+ *   the ctx table.  TLP_ERR_ARG on a name index outside the string table.
+ * tlp_fit_norm_scales: scale[c] = max over the kept data (crop R4) of |x[n,r,c]|
+ *   of the un-normalised rows tlp_encode would build (one-hot 1, RN_f32 number,
+ *   token of the ctx table), 1.0 for an all-zero column; `in` in DEVICE memory.
+ *   Stream-ordered; sets the ctx scales and, if scale_out != NULL, copies the
+ *   [E] floats there (host or device).  Device errors as tlp_encode. */
+tlp_status tlp_fit_token_table(tlp_ctx* ctx, const tlp_seq_batch* in, int64_t N);
+tlp_status tlp_fit_norm_scales(tlp_ctx* ctx, const tlp_seq_batch* in, int64_t N, float* scale_out,
+                               void* stream);
 /* Number of fp32 parameters in the R24 flat order. */
 int64_t tlp_num_params(const tlp_ctx* ctx);
 /* Flat fp32 parameters in R24 order (W stored [in,out] row-major).  `flat` may
@@ -147,12 +161,25 @@ tlp_status tlp_set_params(tlp_ctx* ctx, const float* flat, int64_t n);
 tlp_status tlp_get_params(tlp_ctx* ctx, float* flat, int64_t n);
 /* Gradient of the last tlp_compute_grads / tlp_train_step (after allreduce). */
 tlp_status tlp_get_grads(tlp_ctx* ctx, float* flat, int64_t n);
+/* Test hook (R26): the scores [B, n_tasks] fp32 of the forward pass of the last
+ * tlp_compute_grads / tlp_train_step -- the scores its LambdaRank ranked --
+ * copied to `out` (host or device, n = B * n_tasks).  Synchronises the device.
+ * TLP_ERR_STATE before the first training call, TLP_ERR_SHAPE on a count
+ * mismatch. */
+tlp_status tlp_get_train_scores(tlp_ctx* ctx, float* out, int64_t n);
 /* Data-parallel communicator: `nccl_id` points to the 128-byte
  * ncclUniqueId created by rank 0 and broadcast by the caller; blocks until all
  * `world` ranks have joined.  world == 1 with nccl_id == NULL disables
  * collectives; world == 1 with an id builds a 1-rank communicator (the
  * collective code paths then run on one GPU, as the tests use it). */
 tlp_status tlp_set_comm(tlp_ctx* ctx, const void* nccl_id, int rank, int world);
+/* C-3: make every rank's model state rank `root`'s -- the
+ * parameters and Adam moments / step count (if the root has parameters), the
+ * normalisation scales (if set) and the token table -- by ncclBroadcast over
+ * the ctx communicator.  Collective: every rank of the communicator calls it
+ * with the same root.  Synchronises `stream` once (the sizes in a small header
+ * decide the receivers' allocations).  TLP_ERR_STATE without a communicator. */
+tlp_status tlp_broadcast_state(tlp_ctx* ctx, int root, void* stream);
 /* Fill a 128-byte buffer with a fresh ncclUniqueId (rank 0 only). */
 tlp_status tlp_get_unique_id(void* nccl_id_out);
 
@@ -386,7 +413,13 @@ tlp_status tlp_ga_round(tlp_ctx* ctx, int32_t n_pop, int32_t n_child, int32_t it
 tlp_status tlp_normalize_labels(tlp_ctx* ctx, const float* latency, const int64_t* group_off,
                                 int32_t G, float* label_out, void* stream);
 
-/* Synchronise the device and return (then clear) the sticky device error. */
+/* Synchronise the device and return (then clear) the sticky device error.
+ * With a communicator, first waits for the last collective the ctx enqueued,
+ * at most TLP_NCCL_TIMEOUT_S seconds (default 300) while polling
+ * ncclCommGetAsyncError; on a timeout or an asynchronous NCCL error the
+ * communicator is aborted (ncclCommAbort, the ctx continues without one) and
+ * TLP_ERR_NCCL is returned.  A training step that fails after entering its
+ * collectives aborts the communicator the same way. */
 tlp_status tlp_sync(tlp_ctx* ctx);
 /* Number of kernels this ctx launched since creation (bench evidence). */
 int64_t tlp_launch_count(const tlp_ctx* ctx);
@@ -399,7 +432,8 @@ int64_t tlp_launch_count(const tlp_ctx* ctx);
 tlp_status tlp_debug_umma(const float* A, const float* B, float* D, int32_t N, int32_t K,
                           int32_t a_in_tmem, void* stream);
 
-/* Test hook for the tf32 tcgen05 GEMM of the bf16-context training path:
+/* Test hook for the bf16x3 tcgen05 GEMM of the bf16-context training path (R37:
+ * fp32 operands split hi + lo, three bf16 MMAs per product, fp32 accumulation):
  * C = op(A) op(B) (op = transpose when ta / tb), fp32 device row-major with the
  * given leading dimensions (multiples of 4, 16-byte aligned pointers).  With
  * splits > 1, C receives `splits` partial products [splits, M, ldc] (fixed K

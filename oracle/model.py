@@ -30,7 +30,7 @@ W is [in, out].
 from __future__ import annotations
 
 from dataclasses import dataclass, field
-from typing import Dict, List, Tuple
+from typing import Dict, List, Optional, Tuple
 
 import numpy as np
 
@@ -145,11 +145,13 @@ def lstm_forward(p: Dict[str, np.ndarray], pre: str, h: np.ndarray):
 
 
 def lstm_backward(p: Dict[str, np.ndarray], pre: str, h: np.ndarray, steps, dout: np.ndarray,
-                  grads: Dict[str, np.ndarray]) -> np.ndarray:
-    """Backpropagation through time of lstm_forward; returns d h (the input)."""
+                  grads: Dict[str, np.ndarray], rms: Optional[Dict[str, np.ndarray]] = None) -> np.ndarray:
+    """Backpropagation through time of lstm_forward; returns d h (the input).
+    ``rms``: as in backward() (R50)."""
     N, L, H = h.shape
     dh_in = np.zeros_like(h)
     dWih = np.zeros((H, 4 * H)); dWhh = np.zeros((H, 4 * H)); db = np.zeros(4 * H)
+    sWih = np.zeros((H, 4 * H)); sWhh = np.zeros((H, 4 * H)); sb = np.zeros(4 * H)
     dhn = np.zeros((N, H))
     dcn = np.zeros((N, H))
     for t in reversed(range(L)):
@@ -165,10 +167,17 @@ def lstm_backward(p: Dict[str, np.ndarray], pre: str, h: np.ndarray, steps, dout
         dWih += h[:, t].T @ dz
         dWhh += st["hp"].T @ dz
         db += dz.sum(axis=0)
+        if rms is not None:
+            sWih += (h[:, t] ** 2).T @ dz ** 2
+            sWhh += (st["hp"] ** 2).T @ dz ** 2
+            sb += (dz ** 2).sum(axis=0)
         dhn = dz @ p[pre + "Whh"].T
         dh_in[:, t] = dz @ p[pre + "Wih"].T
     grads[pre + "Wih"], grads[pre + "Whh"] = dWih, dWhh
     grads[pre + "bih"], grads[pre + "bhh"] = db, db.copy()
+    if rms is not None:
+        rms[pre + "Wih"], rms[pre + "Whh"] = np.sqrt(sWih), np.sqrt(sWhh)
+        rms[pre + "bih"], rms[pre + "bhh"] = np.sqrt(sb), np.sqrt(sb)
     return dh_in
 
 
@@ -228,10 +237,29 @@ def forward(cfg: Config, p: Dict[str, np.ndarray], X: np.ndarray, save: bool = F
     return (scores, acts) if save else scores
 
 
-def backward(cfg: Config, p: Dict[str, np.ndarray], acts, g: np.ndarray) -> Dict[str, np.ndarray]:
+def _w_rms(x, d):
+    """sqrt(sum_rows x_r^2 (x) d_r^2): RMS scale of the per-row terms x_r^T d_r of
+    a weight gradient sum_r x_r^T d_r (R50)."""
+    return np.sqrt(np.einsum("nli,nlo->io", x * x, d * d))
+
+
+def _b_rms(d):
+    return np.sqrt((d * d).sum(axis=(0, 1)))
+
+
+def backward(cfg: Config, p: Dict[str, np.ndarray], acts, g: np.ndarray,
+             rms: Optional[Dict[str, np.ndarray]] = None) -> Dict[str, np.ndarray]:
     """O3.  g = dLoss/dscores [N, n_tasks] -> gradient for every parameter.
-    relu'(0) := 0.  Sums over l run over all L rows, pads included."""
+    relu'(0) := 0.  Sums over l run over all L rows, pads included.
+
+    Every parameter gradient is a sum over the N*L rows of per-row terms.  If a
+    dict is passed as ``rms``, it also receives, per parameter, the root of the
+    sum of the squared terms (elementwise) -- the scale at which independent
+    per-term rounding errors accumulate, used by the tests to state fp32 error
+    bounds for cancelling sums (R50).  The gradients are unaffected."""
     g = np.asarray(g, np.float64)
+    R = rms if rms is not None else {}
+    track = rms is not None
     nh, dh, H = cfg.attn_heads, cfg.d_h, cfg.hidden
     N, L = acts["h"].shape[0], acts["h"].shape[1]
     grads: Dict[str, np.ndarray] = {}
@@ -246,6 +274,10 @@ def backward(cfg: Config, p: Dict[str, np.ndarray], acts, g: np.ndarray) -> Dict
         du = gt * p[pre + "w2"][:, 0][None, None, :] * (u > 0)
         grads[pre + "W1"] = np.einsum("nli,nlo->io", h, du)
         grads[pre + "c1"] = du.sum(axis=(0, 1))
+        if track:
+            R[pre + "w2"] = np.sqrt(np.einsum("nlk,n->k", z * z, g[:, t] ** 2))[:, None]
+            R[pre + "c2"] = np.array([np.sqrt(L * (g[:, t] ** 2).sum())])
+            R[pre + "W1"], R[pre + "c1"] = _w_rms(h, du), _b_rms(du)
         dh_ += du @ p[pre + "W1"].T
     for r in reversed(range(cfg.n_res)):
         pre = "res%d." % r
@@ -255,15 +287,21 @@ def backward(cfg: Config, p: Dict[str, np.ndarray], acts, g: np.ndarray) -> Dict
         dv = (dh_ @ p[pre + "Wb"].T) * (a["v"] > 0)
         grads[pre + "Wa"] = np.einsum("nli,nlo->io", a["h"], dv)
         grads[pre + "a"] = dv.sum(axis=(0, 1))
+        if track:
+            R[pre + "Wb"], R[pre + "b"] = _w_rms(a["r"], dh_), _b_rms(dh_)
+            R[pre + "Wa"], R[pre + "a"] = _w_rms(a["h"], dv), _b_rms(dv)
         dh_ = dh_ + dv @ p[pre + "Wa"].T
     for l in reversed(range(cfg.n_attn if cfg.backbone == "lstm" else 0)):
         a = acts["attn"][l]
-        dh_ = dh_ + lstm_backward(p, "lstm%d." % l, a["h"], a["steps"], dh_, grads)
+        dh_ = dh_ + lstm_backward(p, "lstm%d." % l, a["h"], a["steps"], dh_, grads,
+                                  R if track else None)
     for l in reversed(range(cfg.n_attn if cfg.backbone == "attn" else 0)):
         pre = "attn%d." % l
         a = acts["attn"][l]
         grads[pre + "Wo"] = np.einsum("nli,nlo->io", a["O"], dh_)
         grads[pre + "bo"] = dh_.sum(axis=(0, 1))
+        if track:
+            R[pre + "Wo"], R[pre + "bo"] = _w_rms(a["O"], dh_), _b_rms(dh_)
         dO = dh_ @ p[pre + "Wo"].T
         dOh = dO.reshape(N, L, nh, dh).transpose(0, 2, 1, 3)
         A, Qh, Kh, Vh = a["A"], a["Qh"], a["Kh"], a["Vh"]
@@ -279,14 +317,20 @@ def backward(cfg: Config, p: Dict[str, np.ndarray], acts, g: np.ndarray) -> Dict
         for nm, d in (("q", dQ), ("k", dK), ("v", dV)):
             grads[pre + "W" + nm] = np.einsum("nli,nlo->io", hin, d)
             grads[pre + "b" + nm] = d.sum(axis=(0, 1))
+            if track:
+                R[pre + "W" + nm], R[pre + "b" + nm] = _w_rms(hin, d), _b_rms(d)
         dh_ = dh_ + dQ @ p[pre + "Wq"].T + dK @ p[pre + "Wk"].T + dV @ p[pre + "Wv"].T
     if cfg.pos_enc:
         grads["pos"] = dh_.sum(axis=0)                         # R43: d h / d pos = identity per row
+        if track:
+            R["pos"] = np.sqrt((dh_ * dh_).sum(axis=0))
     for i in reversed(range(len(cfg.up_dims))):
         pre_ = "up%d." % i
         dpre = dh_ * (acts["up_pre"][i] > 0)
         grads[pre_ + "W"] = np.einsum("nli,nlo->io", acts["up_in"][i], dpre)
         grads[pre_ + "b"] = dpre.sum(axis=(0, 1))
+        if track:
+            R[pre_ + "W"], R[pre_ + "b"] = _w_rms(acts["up_in"][i], dpre), _b_rms(dpre)
         if i > 0:
             dh_ = dpre @ p[pre_ + "W"].T
     return grads

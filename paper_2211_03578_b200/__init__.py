@@ -52,6 +52,32 @@ class TLPConfig:
     pos_enc: bool = False     # NEXT-3 / R43: learned positional table (the paper: none, R9)
     backbone: str = "attn"    # NEXT-4 / R49: "attn" (the paper's choice) | "lstm"
 
+    def param_shapes(self):
+        """[(name, shape)] of the flat parameter vector in the library's R24 order
+        (include/tlp.h tlp_set_params): upsample (W [in, out], b)...; the R43
+        table; per attention layer Wq bq Wk bk Wv bv Wo bo (per LSTM layer Wih
+        bih Whh bhh); per residual block Wa a Wb b; per task W1 c1 w2 c2."""
+        out, d_in, H = [], self.E, self.hidden
+        for i, d in enumerate(self.up_dims):
+            out += [("up%d.W" % i, (d_in, d)), ("up%d.b" % i, (d,))]
+            d_in = d
+        if self.pos_enc:
+            out.append(("pos", (self.L, H)))
+        for l in range(self.n_attn):
+            if self.backbone == "lstm":
+                out += [("lstm%d.Wih" % l, (H, 4 * H)), ("lstm%d.bih" % l, (4 * H,)),
+                        ("lstm%d.Whh" % l, (H, 4 * H)), ("lstm%d.bhh" % l, (4 * H,))]
+            else:
+                for nm in "qkvo":
+                    out += [("attn%d.W%s" % (l, nm), (H, H)), ("attn%d.b%s" % (l, nm), (H,))]
+        for r in range(self.n_res):
+            out += [("res%d.Wa" % r, (H, H)), ("res%d.a" % r, (H,)), ("res%d.Wb" % r, (H, H)),
+                    ("res%d.b" % r, (H,))]
+        for t in range(self.n_tasks):
+            out += [("head%d.W1" % t, (H, self.head_dim)), ("head%d.c1" % t, (self.head_dim,)),
+                    ("head%d.w2" % t, (self.head_dim, 1)), ("head%d.c2" % t, (1,))]
+        return out
+
     def to_c(self) -> tlp_config:
         c = tlp_config()
         c.L, c.E, c.T, c.hidden = self.L, self.E, self.T, self.hidden
@@ -84,9 +110,11 @@ def _ptr(t: Optional[torch.Tensor]) -> Optional[int]:
     return None if t is None else t.data_ptr()
 
 
-def _stream_ptr(stream) -> Optional[int]:
+def _stream_ptr(stream, device: Optional[int] = None) -> Optional[int]:
+    """The cudaStream_t of `stream`; None = the current stream OF `device` (the
+    ctx's GPU), not of whatever device happens to be current."""
     if stream is None:
-        stream = torch.cuda.current_stream()
+        stream = torch.cuda.current_stream(device)
     return stream.cuda_stream
 
 
@@ -196,6 +224,23 @@ class TLP:
         assert s.shape == (self.cfg.E,)
         self._check(self.lib.tlp_set_norm_scales(self.h, s.ctypes.data))
 
+    def fit_token_table(self, packed):
+        """tlp_fit_token_table (R1) from a host packed batch (anything
+        DeviceBatch.host_arrays accepts, or a host DeviceBatch)."""
+        hb = packed if isinstance(packed, DeviceBatch) else DeviceBatch.from_packed(packed, device="cpu")
+        assert not hb.seq_off.is_cuda
+        b = hb.c_struct()
+        self._check(self.lib.tlp_fit_token_table(self.h, C.byref(b), hb.N))
+
+    def fit_norm_scales(self, batch: "DeviceBatch", stream=None) -> np.ndarray:
+        """tlp_fit_norm_scales (R3) from a device batch; returns the [E] scales."""
+        out = np.zeros(self.cfg.E, np.float32)
+        b = batch.c_struct()
+        self._check(self.lib.tlp_fit_norm_scales(self.h, C.byref(b), batch.N, out.ctypes.data,
+                                                 _stream_ptr(stream, self.device)))
+        torch.cuda.synchronize(self.device)
+        return out
+
     def set_params(self, flat):
         if isinstance(flat, torch.Tensor):
             t = flat.detach().to(torch.float32).contiguous()
@@ -212,6 +257,12 @@ class TLP:
     def get_grads(self) -> np.ndarray:
         a = np.zeros(self.num_params, np.float32)
         self._check(self.lib.tlp_get_grads(self.h, a.ctypes.data, a.size))
+        return a
+
+    def get_train_scores(self, B: int) -> np.ndarray:
+        """Scores [B, n_tasks] of the last training forward (test hook, R26)."""
+        a = np.zeros((B, self.cfg.n_tasks), np.float32)
+        self._check(self.lib.tlp_get_train_scores(self.h, a.ctypes.data, a.size))
         return a
 
     def init_comm(self, group=None):
@@ -231,6 +282,11 @@ class TLP:
         with torch.cuda.device(self.device):
             self._check(self.lib.tlp_set_comm(self.h, buf, rank, world))
 
+    def broadcast_state(self, root: int = 0, stream=None):
+        """tlp_broadcast_state (C-3): parameters + Adam state, scales and token
+        table from rank `root` to every rank of the communicator."""
+        self._check(self.lib.tlp_broadcast_state(self.h, root, _stream_ptr(stream, self.device)))
+
     def sync(self):
         self._check(self.lib.tlp_sync(self.h))
 
@@ -244,7 +300,7 @@ class TLP:
         if out is None:
             out = torch.empty((batch.N, c.L, c.E), dtype=torch.float32, device="cuda:%d" % self.device)
         b = batch.c_struct()
-        self._check(self.lib.tlp_encode(self.h, C.byref(b), batch.N, out.data_ptr(), _stream_ptr(stream)))
+        self._check(self.lib.tlp_encode(self.h, C.byref(b), batch.N, out.data_ptr(), _stream_ptr(stream, self.device)))
         return out
 
     def score(self, feats: torch.Tensor, out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
@@ -252,7 +308,7 @@ class TLP:
         N = feats.shape[0]
         if out is None:
             out = torch.empty((N, self.cfg.n_tasks), dtype=torch.float32, device=feats.device)
-        self._check(self.lib.tlp_score(self.h, feats.data_ptr(), N, out.data_ptr(), _stream_ptr(stream)))
+        self._check(self.lib.tlp_score(self.h, feats.data_ptr(), N, out.data_ptr(), _stream_ptr(stream, self.device)))
         return out
 
     def _train(self, fn, feats, labels, group_off, loss_out, stream):
@@ -262,7 +318,7 @@ class TLP:
         if loss_out is None:
             loss_out = torch.empty(1, dtype=torch.float32, device=feats.device)
         self._check(fn(self.h, feats.data_ptr(), labels.data_ptr(), goff.ctypes.data, B,
-                       len(goff) - 1, loss_out.data_ptr(), _stream_ptr(stream)))
+                       len(goff) - 1, loss_out.data_ptr(), _stream_ptr(stream, self.device)))
         return loss_out
 
     def train_step(self, feats, labels, group_off, loss_out=None, stream=None) -> torch.Tensor:
@@ -278,7 +334,7 @@ class TLP:
         ds = torch.empty_like(scores)
         self._check(self.lib.tlp_lambdarank(self.h, scores.data_ptr(), labels.data_ptr(),
                                             goff.ctypes.data, B, len(goff) - 1, loss.data_ptr(),
-                                            ds.data_ptr(), _stream_ptr(stream)))
+                                            ds.data_ptr(), _stream_ptr(stream, self.device)))
         return loss, ds
 
     def mse(self, scores, labels, stream=None):
@@ -287,7 +343,7 @@ class TLP:
         loss = torch.empty(1, dtype=torch.float32, device=scores.device)
         ds = torch.empty_like(scores)
         self._check(self.lib.tlp_mse(self.h, scores.data_ptr(), labels.data_ptr(), B, loss.data_ptr(),
-                                     ds.data_ptr(), _stream_ptr(stream)))
+                                     ds.data_ptr(), _stream_ptr(stream, self.device)))
         return loss, ds
 
     def topk(self, scores: torch.Tensor, task_off, k: int, head: int = 0, shard_base: int = 0,
@@ -301,7 +357,7 @@ class TLP:
             val_out = torch.empty((T, k), dtype=torch.float32, device=scores.device)
         self._check(self.lib.tlp_topk(self.h, scores.data_ptr(), stride, head, toff.ctypes.data, T, k,
                                       shard_base, idx_out.data_ptr(), val_out.data_ptr(),
-                                      _stream_ptr(stream)))
+                                      _stream_ptr(stream, self.device)))
         return idx_out, val_out
 
     def search_round(self, host_batch: DeviceBatch, task_off, k: int, head: int = 0,
@@ -320,7 +376,7 @@ class TLP:
         cs = host_batch.c_struct()
         self._check(self.lib.tlp_search_round(self.h, C.byref(cs), host_batch.N, toff.ctypes.data, T, k,
                                               head, shard_base, chunks, idx_out.data_ptr(),
-                                              val_out.data_ptr(), _stream_ptr(stream)))
+                                              val_out.data_ptr(), _stream_ptr(stream, self.device)))
         return idx_out, val_out
 
     def dedup(self, feats: torch.Tensor, group_off, labels: Optional[torch.Tensor] = None,
@@ -343,7 +399,7 @@ class TLP:
                                        labels.data_ptr() if labels is not None else None,
                                        keep.data_ptr() if N else None,
                                        lab.data_ptr() if lab is not None else None,
-                                       C.byref(n), _stream_ptr(stream)))
+                                       C.byref(n), _stream_ptr(stream, self.device)))
         return keep, lab, int(n.value)
 
     def topk_score(self, scores: torch.Tensor, latency: torch.Tensor, group_off, weight, k: int,
@@ -355,7 +411,7 @@ class TLP:
         out = C.c_double(0.0)
         self._check(self.lib.tlp_topk_score(self.h, scores.data_ptr(), stride, head, latency.data_ptr(),
                                             goff.ctypes.data, w.ctypes.data, len(goff) - 1, k,
-                                            C.byref(out), _stream_ptr(stream)))
+                                            C.byref(out), _stream_ptr(stream, self.device)))
         return float(out.value)
 
     def topk_merge(self, vals: torch.Tensor, idx: torch.Tensor, idx_out=None, val_out=None,
@@ -369,7 +425,7 @@ class TLP:
             val_out = torch.empty((T, k), dtype=torch.float32, device=vals.device)
         self._check(self.lib.tlp_topk_merge(self.h, vals.data_ptr(), idx.data_ptr(), W, T, k,
                                             idx_out.data_ptr(), val_out.data_ptr(),
-                                            _stream_ptr(stream)))
+                                            _stream_ptr(stream, self.device)))
         return idx_out, val_out
 
     def normalize_labels(self, latency: torch.Tensor, group_off, out=None, stream=None):
@@ -377,7 +433,7 @@ class TLP:
         if out is None:
             out = torch.empty_like(latency)
         self._check(self.lib.tlp_normalize_labels(self.h, latency.data_ptr(), goff.ctypes.data,
-                                                  len(goff) - 1, out.data_ptr(), _stream_ptr(stream)))
+                                                  len(goff) - 1, out.data_ptr(), _stream_ptr(stream, self.device)))
         return out
 
     # ---------------------------------------------------------------- NEXT-1
@@ -412,7 +468,7 @@ class TLP:
     def ga_init(self, n: int, seed: int, rnd: int, out=None, stream=None) -> torch.Tensor:
         if out is None:
             out = torch.empty((self._ga_S * n, self.ga_G), dtype=torch.uint8, device="cuda")
-        self._check(self.lib.tlp_ga_init(self.h, n, seed, rnd, out.data_ptr(), _stream_ptr(stream)))
+        self._check(self.lib.tlp_ga_init(self.h, n, seed, rnd, out.data_ptr(), _stream_ptr(stream, self.device)))
         return out
 
     def ga_evolve(self, pop: torch.Tensor, pop_scores: torch.Tensor, n_pop: int, n_child: int,
@@ -422,7 +478,7 @@ class TLP:
             out = torch.empty((self._ga_S * n_child, self.ga_G), dtype=torch.uint8, device="cuda")
         self._check(self.lib.tlp_ga_evolve(self.h, pop.data_ptr(), pop_scores.data_ptr(), n_pop, n_child,
                                            p_cross, p_mut, seed, rnd, it, out.data_ptr(),
-                                           _stream_ptr(stream)))
+                                           _stream_ptr(stream, self.device)))
         return out
 
     def ga_materialize(self, genes: torch.Tensor, n: int, stream=None) -> DeviceBatch:
@@ -441,12 +497,12 @@ class TLP:
         self._check(self.lib.tlp_ga_materialize(self.h, genes.data_ptr(), n, b.seq_off.data_ptr(),
                                                 b.prim_type.data_ptr(), b.arg_off.data_ptr(),
                                                 b.arg_kind.data_ptr(), b.arg_num.data_ptr(),
-                                                b.arg_name.data_ptr(), _stream_ptr(stream)))
+                                                b.arg_name.data_ptr(), _stream_ptr(stream, self.device)))
         return b
 
     def ga_drop_duplicates(self, genes: torch.Tensor, n: int, scores: torch.Tensor, stream=None):
         self._check(self.lib.tlp_ga_drop_duplicates(self.h, genes.data_ptr(), n, scores.data_ptr(),
-                                                    _stream_ptr(stream)))
+                                                    _stream_ptr(stream, self.device)))
         return scores
 
     def ga_round(self, n_pop: int, n_child: int, iters: int, p_cross: float, p_mut: float,
@@ -461,5 +517,5 @@ class TLP:
             scores_out = torch.empty(S * n_pop, dtype=torch.float32, device="cuda")
         self._check(self.lib.tlp_ga_round(self.h, n_pop, n_child, iters, p_cross, p_mut, seed, rnd, head,
                                           genes_out.data_ptr(), scores_out.data_ptr(),
-                                          _stream_ptr(stream)))
+                                          _stream_ptr(stream, self.device)))
         return genes_out, scores_out

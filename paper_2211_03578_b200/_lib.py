@@ -14,8 +14,8 @@ TLP_STATUS = {0: "OK", -1: "ERR_ARG", -2: "ERR_SHAPE", -3: "ERR_EMPTY_SEQ",
 
 # Every symbol include/tlp.h declares (checked by tests/test_boundary.py).
 EXPORTS = ("tlp_create", "tlp_destroy", "tlp_last_error", "tlp_default_config",
-           "tlp_set_token_table", "tlp_set_norm_scales", "tlp_num_params", "tlp_set_params",
-           "tlp_get_params", "tlp_get_grads", "tlp_set_comm", "tlp_get_unique_id", "tlp_encode",
+           "tlp_set_token_table", "tlp_set_norm_scales", "tlp_fit_token_table", "tlp_fit_norm_scales", "tlp_num_params", "tlp_set_params",
+           "tlp_get_params", "tlp_get_grads", "tlp_get_train_scores", "tlp_set_comm", "tlp_broadcast_state", "tlp_get_unique_id", "tlp_encode",
            "tlp_score", "tlp_train_step", "tlp_compute_grads", "tlp_lambdarank", "tlp_mse", "tlp_topk", "tlp_topk_merge",
            "tlp_search_round", "tlp_dedup", "tlp_topk_score", "tlp_normalize_labels", "tlp_sync", "tlp_launch_count", "tlp_debug_umma",
            "tlp_debug_gemm", "tlp_ga_set_space", "tlp_ga_num_genes", "tlp_ga_batch_size", "tlp_ga_init",
@@ -65,12 +65,16 @@ def load() -> C.CDLL:
         "tlp_default_config": (None, [C.POINTER(tlp_config)]),
         "tlp_set_token_table": (C.c_int, [vp, vp, vp, i32]),
         "tlp_set_norm_scales": (C.c_int, [vp, vp]),
+        "tlp_fit_token_table": (C.c_int, [vp, C.POINTER(tlp_seq_batch), i64]),
+        "tlp_fit_norm_scales": (C.c_int, [vp, C.POINTER(tlp_seq_batch), i64, vp, vp]),
         "tlp_num_params": (i64, [vp]),
         "tlp_set_params": (C.c_int, [vp, vp, i64]),
         "tlp_get_params": (C.c_int, [vp, vp, i64]),
         "tlp_get_grads": (C.c_int, [vp, vp, i64]),
+        "tlp_get_train_scores": (C.c_int, [vp, vp, i64]),
         "tlp_set_comm": (C.c_int, [vp, vp, C.c_int, C.c_int]),
         "tlp_get_unique_id": (C.c_int, [vp]),
+        "tlp_broadcast_state": (C.c_int, [vp, C.c_int, vp]),
         "tlp_encode": (C.c_int, [vp, C.POINTER(tlp_seq_batch), i64, vp, vp]),
         "tlp_score": (C.c_int, [vp, vp, i64, vp, vp]),
         "tlp_train_step": (C.c_int, [vp, vp, vp, vp, i32, i32, vp, vp]),

@@ -9,8 +9,11 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
+#include <thread>
 #include <cmath>
 #include <cstring>
+#include <vector>
 
 tlp_status topk_merge_launch(tlp_ctx* ctx, const float* cand_s, const int64_t* cand_i, int T,
                              int64_t per_seg, int k, int64_t* idx_out, float* val_out,
@@ -24,6 +27,29 @@ tlp_status fail(tlp_ctx* ctx, tlp_status st, const std::string& msg) {
   if (ctx) ctx->last_error = msg;
   else g_tls_error = msg;
   return st;
+}
+
+// after a call enqueued collectives on stream s: tlp_sync's bounded wait
+tlp_status note_collective(tlp_ctx* ctx, cudaStream_t s) {
+  if (!ctx->coll_ev) TLP_CUDA_TRY(cudaEventCreateWithFlags(&ctx->coll_ev, cudaEventDisableTiming));
+  TLP_CUDA_TRY(cudaEventRecord(ctx->coll_ev, s));
+  return TLP_OK;
+}
+
+// tear the communicator down after a timeout or an asynchronous NCCL error
+// (SURVEY §5 failure detection): ncclCommAbort unblocks any kernels still
+// waiting on peers; the ctx then runs without collectives until tlp_set_comm
+tlp_status abort_comm(tlp_ctx* ctx, const std::string& why) {
+  ncclCommAbort(reinterpret_cast<ncclComm_t>(ctx->comm));
+  ctx->comm = nullptr;
+  ctx->world = 1;
+  return fail(ctx, TLP_ERR_NCCL, why + " (communicator aborted)");
+}
+
+double nccl_timeout_s() {
+  const char* e = getenv("TLP_NCCL_TIMEOUT_S");
+  const double v = e ? atof(e) : 300.0;
+  return v > 0 ? v : 300.0;
 }
 
 ParamOffsets compute_offsets(const tlp_config& c) {
@@ -214,6 +240,53 @@ tlp_status tlp_set_norm_scales(tlp_ctx* ctx, const float* scale) {
   return TLP_OK;
 }
 
+tlp_status tlp_fit_token_table(tlp_ctx* ctx, const tlp_seq_batch* in, int64_t N) {
+  CHECK_CTX();
+  if (!in || N < 0 || (N > 0 && (!in->seq_off || !in->arg_off))) return fail(ctx, TLP_ERR_ARG, "null input");
+  if (in->A > 0 && (!in->arg_kind || !in->arg_name)) return fail(ctx, TLP_ERR_ARG, "null argument arrays");
+  if (in->U > 0 && (!in->str_blob || !in->str_off)) return fail(ctx, TLP_ERR_ARG, "null string table");
+  // R1: tokens from 2 in first-occurrence order of the name arguments of the
+  // training stream (candidates, primitives, arguments in order)
+  const int64_t a_end = N > 0 ? in->arg_off[in->seq_off[N]] : 0;
+  const int64_t a_beg = N > 0 ? in->arg_off[in->seq_off[0]] : 0;
+  std::vector<uint8_t> seen(in->U > 0 ? in->U : 1, 0);
+  std::vector<int64_t> off(1, 0);
+  std::vector<uint8_t> blob;
+  for (int64_t a = a_beg; a < a_end; ++a) {
+    if (!in->arg_kind[a]) continue;
+    const int32_t u = in->arg_name[a];
+    if (u < 0 || u >= in->U) return fail(ctx, TLP_ERR_ARG, "name index outside the string table");
+    if (seen[u]) continue;
+    seen[u] = 1;
+    const uint8_t* b = reinterpret_cast<const uint8_t*>(in->str_blob) + in->str_off[u];
+    blob.insert(blob.end(), b, b + (in->str_off[u + 1] - in->str_off[u]));
+    off.push_back((int64_t)blob.size());
+  }
+  // equal strings under different string-table indices keep the first token
+  // (build_token_table skips later duplicates)
+  const int32_t n = (int32_t)(off.size() - 1);
+  if (n >= (1 << 24) - 2) return fail(ctx, TLP_ERR_ARG, "token table exceeds 2^24 entries");
+  cudaSetDevice(ctx->device);
+  return build_token_table(ctx, blob.data(), off.data(), n);
+}
+
+tlp_status tlp_fit_norm_scales(tlp_ctx* ctx, const tlp_seq_batch* in, int64_t N, float* scale_out,
+                               void* stream) {
+  CHECK_CTX();
+  if (!in || N < 0 || (N > 0 && (!in->seq_off || !in->prim_type || !in->arg_off)))
+    return fail(ctx, TLP_ERR_ARG, "null input");
+  if (in->A > 0 && (!in->arg_kind || !in->arg_num || !in->arg_name))
+    return fail(ctx, TLP_ERR_ARG, "null argument arrays");
+  if (in->U > 0 && (!in->str_blob || !in->str_off)) return fail(ctx, TLP_ERR_ARG, "null string table");
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  tlp_status st = fit_scales_launch(ctx, in, N, s);
+  if (st != TLP_OK) return st;
+  if (scale_out)
+    TLP_CUDA_TRY(cudaMemcpyAsync(scale_out, ctx->d_scale, ctx->cfg.E * sizeof(float), cudaMemcpyDefault, s));
+  return TLP_OK;
+}
+
 int64_t tlp_num_params(const tlp_ctx* ctx) { return ctx ? ctx->off.total : -1; }
 
 tlp_status tlp_set_params(tlp_ctx* ctx, const float* flat, int64_t n) {
@@ -248,6 +321,16 @@ tlp_status tlp_get_grads(tlp_ctx* ctx, float* flat, int64_t n) {
   return TLP_OK;
 }
 
+tlp_status tlp_get_train_scores(tlp_ctx* ctx, float* out, int64_t n) {
+  CHECK_CTX();
+  if (!ctx->train_scores || ctx->train_N < 0) return fail(ctx, TLP_ERR_STATE, "no training step yet");
+  if (!out || n != ctx->train_N * ctx->cfg.n_tasks) return fail(ctx, TLP_ERR_SHAPE, "score count mismatch");
+  cudaSetDevice(ctx->device);
+  TLP_CUDA_TRY(cudaDeviceSynchronize());
+  TLP_CUDA_TRY(cudaMemcpy(out, ctx->train_scores, (size_t)n * sizeof(float), cudaMemcpyDefault));
+  return TLP_OK;
+}
+
 tlp_status tlp_get_unique_id(void* out) {
   if (!out) return fail(nullptr, TLP_ERR_ARG, "null id buffer");
   ncclUniqueId id;
@@ -277,6 +360,67 @@ tlp_status tlp_set_comm(tlp_ctx* ctx, const void* nccl_id, int rank, int world) 
   ncclResult_t r = ncclCommInitRank(&comm, world, id, rank);
   if (r != ncclSuccess) return fail(ctx, TLP_ERR_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
   ctx->comm = comm;
+  return TLP_OK;
+}
+
+tlp_status tlp_broadcast_state(tlp_ctx* ctx, int root, void* stream) {
+  CHECK_CTX();
+  ncclComm_t comm = reinterpret_cast<ncclComm_t>(ctx->comm);
+  if (!comm) return fail(ctx, TLP_ERR_STATE, "tlp_set_comm first");
+  if (root < 0 || root >= ctx->world) return fail(ctx, TLP_ERR_ARG, "bad root rank");
+  cudaSetDevice(ctx->device);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  // header: what the root holds (sizes the receivers must allocate)
+  int64_t hdr[6] = {ctx->have_params ? 1 : 0, ctx->have_scales ? 1 : 0, (int64_t)ctx->hcap,
+                    (int64_t)ctx->tok_n, ctx->tok_bytes, ctx->adam_t};
+  TLP_CUDA_TRY(ctx->ws_misc.ensure(64));
+  int64_t* d_hdr = ctx->ws_misc.as<int64_t>();
+  TLP_CUDA_TRY(cudaMemcpyAsync(d_hdr, hdr, sizeof(hdr), cudaMemcpyHostToDevice, s));
+  auto bc = [&](void* buf, size_t count, ncclDataType_t t) {
+    return count == 0 || ncclBroadcast(buf, buf, count, t, root, comm, s) == ncclSuccess;
+  };
+  if (!bc(d_hdr, 6, ncclInt64)) return fail(ctx, TLP_ERR_NCCL, "state header broadcast failed");
+  TLP_CUDA_TRY(cudaMemcpyAsync(hdr, d_hdr, sizeof(hdr), cudaMemcpyDeviceToHost, s));
+  TLP_CUDA_TRY(cudaStreamSynchronize(s));
+  const bool params = hdr[0] != 0, scales = hdr[1] != 0;
+  const uint32_t cap = (uint32_t)hdr[2];
+  const int32_t n = (int32_t)hdr[3];
+  const int64_t nbytes = hdr[4];
+  // receivers: token-table arrays of the root's size (contents arrive below)
+  if (ctx->rank != root) {
+    cudaFree(ctx->d_hkeys); cudaFree(ctx->d_hval); cudaFree(ctx->d_hstr);
+    cudaFree(ctx->d_tblob); cudaFree(ctx->d_toff);
+    ctx->d_hkeys = nullptr; ctx->d_hval = nullptr; ctx->d_hstr = nullptr;
+    ctx->d_tblob = nullptr; ctx->d_toff = nullptr;
+    if (cap) {
+      TLP_CUDA_TRY(cudaMalloc(&ctx->d_hkeys, cap * sizeof(uint64_t)));
+      TLP_CUDA_TRY(cudaMalloc(&ctx->d_hval, cap * sizeof(int32_t)));
+      TLP_CUDA_TRY(cudaMalloc(&ctx->d_hstr, cap * sizeof(int32_t)));
+      TLP_CUDA_TRY(cudaMalloc(&ctx->d_tblob, nbytes > 0 ? nbytes : 1));
+      TLP_CUDA_TRY(cudaMalloc(&ctx->d_toff, ((size_t)n + 1) * sizeof(int64_t)));
+    }
+    ctx->hcap = cap;
+    ctx->tok_n = n;
+    ctx->tok_bytes = nbytes;
+  }
+  const size_t np = (size_t)ctx->off.total;
+  bool ok = ncclGroupStart() == ncclSuccess;
+  if (params) ok = ok && bc(ctx->d_params, np, ncclFloat32) && bc(ctx->d_m, np, ncclFloat32) &&
+                   bc(ctx->d_v, np, ncclFloat32);
+  if (scales) ok = ok && bc(ctx->d_scale, ctx->cfg.E, ncclFloat32);
+  if (cap) ok = ok && bc(ctx->d_hkeys, cap, ncclUint64) && bc(ctx->d_hval, cap, ncclInt32) &&
+                bc(ctx->d_hstr, cap, ncclInt32) && bc(ctx->d_tblob, (size_t)nbytes, ncclUint8) &&
+                bc(ctx->d_toff, (size_t)n + 1, ncclInt64);
+  ok = (ncclGroupEnd() == ncclSuccess) && ok;
+  if (!ok) return fail(ctx, TLP_ERR_NCCL, "state broadcast failed");
+  tlp_status st = note_collective(ctx, s);
+  if (st != TLP_OK) return st;
+  if (params) {
+    ctx->have_params = true;
+    ctx->adam_t = hdr[5];
+    ctx->tc_dirty = true;  // the bf16 weight images are re-packed from the new parameters
+  }
+  if (scales) ctx->have_scales = true;
   return TLP_OK;
 }
 
@@ -384,13 +528,31 @@ tlp_status grads_impl(tlp_ctx* ctx, const float* feats, const float* labels,
     if (ncclAllReduce(w.counts, w.counts, nt, ncclFloat64, ncclSum, comm, s) != ncclSuccess)
       return fail(ctx, TLP_ERR_NCCL, "loss-count allreduce failed");
   }
-  if ((st = simt_forward(ctx, feats, B, w.scores, true, s)) != TLP_OK) return st;
+  // From here on this rank has entered the step's collectives (C-0 above, the
+  // gradient buckets during the backward): a failure must not leave its peers
+  // waiting for collectives it will never issue.  Join any buckets in flight
+  // (the next step's backward must not race their in-place allreduce) and
+  // abort the communicator.
+  auto bail = [&](tlp_status e) {
+    if (comm) {
+      if (ctx->buckets_issued && ctx->comm_stream) {
+        cudaEventRecord(ctx->bucket_ev[4], ctx->comm_stream);
+        cudaStreamWaitEvent(s, ctx->bucket_ev[4], 0);
+      }
+      const std::string why = ctx->last_error;
+      abort_comm(ctx, why);
+      ctx->last_error = why + " (communicator aborted: this rank left the step)";
+    }
+    return e;
+  };
+  ctx->buckets_issued = 0;
+  if ((st = simt_forward(ctx, feats, B, w.scores, true, s)) != TLP_OK) return bail(st);
+  ctx->train_scores = w.scores;
   st = mse ? mse_loss_grad(ctx, w.scores, labels, B, w.counts, loss_out, w.dscores, s)
            : rank_loss_grad(ctx, w.scores, labels, w.goff, G, B, max_group, w.counts, loss_out,
                             w.dscores, s);
-  if (st != TLP_OK) return st;
-  ctx->buckets_issued = 0;
-  if ((st = simt_backward(ctx, B, w.dscores, s)) != TLP_OK) return st;
+  if (st != TLP_OK) return bail(st);
+  if ((st = simt_backward(ctx, B, w.dscores, s)) != TLP_OK) return bail(st);
   if (comm) {
     // C-1: gradient allreduce (sum); every rank then applies the same Adam step.
     if (ctx->buckets_issued) {  // the buckets went out during the backward: join them
@@ -402,6 +564,7 @@ tlp_status grads_impl(tlp_ctx* ctx, const float* feats, const float* labels,
     }
     if (ncclAllReduce(loss_out, loss_out, 1, ncclFloat32, ncclSum, comm, s) != ncclSuccess)
       return fail(ctx, TLP_ERR_NCCL, "loss allreduce failed");
+    if ((st = note_collective(ctx, s)) != TLP_OK) return st;
   }
   return TLP_OK;
 }
@@ -510,6 +673,7 @@ tlp_status tlp_topk(tlp_ctx* ctx, const float* scores, int32_t score_stride, int
       ncclAllGather(li, gi, loc, ncclInt64, comm, s) != ncclSuccess ||
       ncclGroupEnd() != ncclSuccess)
     return fail(ctx, TLP_ERR_NCCL, "top-k allgather failed");
+  if ((st = note_collective(ctx, s)) != TLP_OK) return st;
   return merge_gathered(ctx, gs, gi, ts, ti, W, T, k, idx_out, val_out, s);
 }
 
@@ -541,6 +705,27 @@ tlp_status tlp_normalize_labels(tlp_ctx* ctx, const float* latency, const int64_
 tlp_status tlp_sync(tlp_ctx* ctx) {
   CHECK_CTX();
   cudaSetDevice(ctx->device);
+  if (ctx->comm && ctx->coll_ev) {
+    // bounded wait on the last enqueued collective: a peer that never joins
+    // would otherwise hang cudaDeviceSynchronize forever
+    ncclComm_t comm = reinterpret_cast<ncclComm_t>(ctx->comm);
+    const auto t0 = std::chrono::steady_clock::now();
+    const double limit = nccl_timeout_s();
+    for (;;) {
+      const cudaError_t q = cudaEventQuery(ctx->coll_ev);
+      if (q == cudaSuccess) break;
+      if (q != cudaErrorNotReady) TLP_CUDA_TRY(q);
+      ncclResult_t ar = ncclSuccess;
+      ncclCommGetAsyncError(comm, &ar);
+      if (ar != ncclSuccess && ar != ncclInProgress)
+        return abort_comm(ctx, std::string("NCCL: ") + ncclGetErrorString(ar));
+      const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      if (el > limit)
+        return abort_comm(ctx, "NCCL collective not complete after " + std::to_string((int)limit) +
+                                   " s (TLP_NCCL_TIMEOUT_S)");
+      std::this_thread::sleep_for(std::chrono::microseconds(200));
+    }
+  }
   TLP_CUDA_TRY(cudaDeviceSynchronize());
   if (ctx->comm) {
     ncclResult_t ar = ncclSuccess;

@@ -281,11 +281,7 @@ tlp_status attn_fwd_tc(tlp_ctx* ctx, const float* qkv, int64_t N, float* O, floa
   const int64_t pairs = N * c.attn_heads;
   const int warps = 4;
   const size_t smem = (size_t)warps * 3 * MAT * sizeof(float);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(attn_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  TLP_SMEM_ATTR(attn_fwd_tc_kernel, smem);
   attn_fwd_tc_kernel<<<(unsigned)cdiv(pairs, warps), warps * 32, smem, s>>>(qkv, c.L, c.hidden,
                                                                            c.attn_heads, pairs, O, A, kvalid);
   TLP_LAUNCH_CHECK();
@@ -298,11 +294,7 @@ tlp_status attn_bwd_tc(tlp_ctx* ctx, const float* qkv, const float* A, const flo
   const int64_t pairs = N * c.attn_heads;
   const int warps = 2;
   const size_t smem = (size_t)warps * 6 * MAT * sizeof(float);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(attn_bwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  TLP_SMEM_ATTR(attn_bwd_tc_kernel, smem);
   attn_bwd_tc_kernel<<<(unsigned)cdiv(pairs, warps), warps * 32, smem, s>>>(qkv, A, dO, c.L, c.hidden,
                                                                            c.attn_heads, pairs, dqkv);
   TLP_LAUNCH_CHECK();

@@ -8,13 +8,16 @@
 //   this file must NOT be compiled with --use_fast_math / -prec-div=false).
 //
 // Two launches per batch:
-//   resolve_tokens: batch string table (U strings) -> token via the ctx hash
-//                   table (FNV-1a 64, linear probing, byte-exact verification).
-//   encode_kernel:  one thread per output element (n, r, c) so that the
-//                   2,200-byte fp32 rows are written fully coalesced; the
-//                   gathers of seq_off / prim_type / arg_off hit L1/L2.
+//   resolve_tokens:     batch string table (U strings) -> token via the ctx hash
+//                       table (FNV-1a 64, linear probing, byte-exact verification).
+//   encode_warp_kernel: one warp per candidate; lane r builds row r in shared
+//                       memory, then the warp streams the candidate's 2,200-byte
+//                       fp32 block to HBM with coalesced 8-byte stores.
+// tlp_fit_scales (R3's "normalization" fitted on the device): fit_scales_kernel
+// computes the same un-normalised rows and reduces max |x| per column.
 #include "tlp_internal.cuh"
 
+#include <algorithm>
 #include <cstring>
 
 namespace {
@@ -137,6 +140,69 @@ __global__ void __launch_bounds__(32 * kEncWarps) encode_warp_kernel(
   }
 }
 
+// R3 on the device: max over the kept data of |x[n, r, c]| of the un-normalised
+// rows (one-hot / RN_f32(number) / token), one thread per (candidate, row);
+// per-block maxima in shared memory, then one atomicMax per column on the IEEE
+// bits (non-negative floats order like their bit patterns, so the result does
+// not depend on the reduction order).  Validation as in encode (kept data only).
+__global__ void fit_scales_kernel(int64_t N, const int64_t* __restrict__ seq_off,
+                                  const uint8_t* __restrict__ prim_type,
+                                  const int64_t* __restrict__ arg_off,
+                                  const uint8_t* __restrict__ arg_kind,
+                                  const double* __restrict__ arg_num,
+                                  const int32_t* __restrict__ arg_name,
+                                  const int32_t* __restrict__ tokens, uint32_t* __restrict__ colmax,
+                                  uint32_t* __restrict__ err, int L, int E, int T) {
+  __shared__ uint32_t smax[64];
+  if (threadIdx.x < 64) smax[threadIdx.x] = 0u;
+  __syncthreads();
+  const int64_t total = N * L;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t n = i / L;
+    const int r = (int)(i - n * L);
+    const int64_t s0 = seq_off[n];
+    const int64_t len = seq_off[n + 1] - s0;
+    if (len <= 0) {
+      if (r == 0) atomicOr(err, DERR_EMPTY_SEQ);
+      continue;
+    }
+    if (r >= len) continue;  // padding row: zeros
+    const int64_t p = s0 + r;
+    const int tau = prim_type[p];
+    if (tau >= T) {
+      atomicOr(err, DERR_UNKNOWN_TYPE);
+      continue;
+    }
+    atomicMax(&smax[tau], __float_as_uint(1.f));
+    const int64_t a0 = arg_off[p];
+    const int na = (int)(arg_off[p + 1] - a0);
+    for (int a = 0; a < E - T && a < na; ++a) {
+      const int64_t ai = a0 + a;
+      float v;
+      if (arg_kind[ai]) {
+        v = (float)tokens[arg_name[ai]];
+      } else {
+        const double d = arg_num[ai];
+        v = __double2float_rn(d);
+        if (!isfinite(d) || !isfinite(v)) {
+          atomicOr(err, DERR_NONFINITE);
+          continue;
+        }
+      }
+      atomicMax(&smax[T + a], __float_as_uint(fabsf(v)));
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < E && smax[threadIdx.x]) atomicMax(&colmax[threadIdx.x], smax[threadIdx.x]);
+}
+
+// scale[c] = max, or 1.0 where the column is all zero (R3)
+__global__ void fit_scales_finish(const uint32_t* __restrict__ colmax, float* __restrict__ scale, int E) {
+  const int c = threadIdx.x;
+  if (c < E) scale[c] = colmax[c] ? __uint_as_float(colmax[c]) : 1.f;
+}
+
 }  // namespace
 
 tlp_status build_token_table(tlp_ctx* ctx, const uint8_t* blob, const int64_t* off, int32_t n) {
@@ -174,6 +240,7 @@ tlp_status build_token_table(tlp_ctx* ctx, const uint8_t* blob, const int64_t* o
   cudaFree(ctx->d_tblob); cudaFree(ctx->d_toff);
   ctx->d_hkeys = nullptr; ctx->d_hval = nullptr; ctx->d_hstr = nullptr;
   ctx->d_tblob = nullptr; ctx->d_toff = nullptr; ctx->hcap = 0;
+  ctx->tok_n = 0; ctx->tok_bytes = 0;
   if (cap == 0) return TLP_OK;
   TLP_CUDA_TRY(cudaMalloc(&ctx->d_hkeys, cap * sizeof(uint64_t)));
   TLP_CUDA_TRY(cudaMalloc(&ctx->d_hval, cap * sizeof(int32_t)));
@@ -186,6 +253,8 @@ tlp_status build_token_table(tlp_ctx* ctx, const uint8_t* blob, const int64_t* o
   if (nbytes > 0) TLP_CUDA_TRY(cudaMemcpy(ctx->d_tblob, blob, nbytes, cudaMemcpyHostToDevice));
   TLP_CUDA_TRY(cudaMemcpy(ctx->d_toff, off, (n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice));
   ctx->hcap = cap;
+  ctx->tok_n = n;
+  ctx->tok_bytes = nbytes;
   return TLP_OK;
 }
 
@@ -224,5 +293,27 @@ tlp_status encode_rows(tlp_ctx* ctx, const tlp_seq_batch* in, int64_t N, float* 
         tokens, ctx->d_scale, feats, ctx->d_err, c.L, c.E, c.T);
   }
   TLP_LAUNCH_CHECK();
+  return TLP_OK;
+}
+
+tlp_status fit_scales_launch(tlp_ctx* ctx, const tlp_seq_batch* in, int64_t N, cudaStream_t s) {
+  const tlp_config& c = ctx->cfg;
+  tlp_status st = encode_resolve(ctx, in, s);
+  if (st != TLP_OK) return st;
+  const int32_t* tokens = in->U > 0 ? ctx->ws_tokens.as<int32_t>() : nullptr;
+  TLP_CUDA_TRY(ctx->ws_misc.ensure(64 * sizeof(uint32_t)));
+  uint32_t* colmax = ctx->ws_misc.as<uint32_t>();
+  TLP_CUDA_TRY(cudaMemsetAsync(colmax, 0, 64 * sizeof(uint32_t), s));
+  if (N > 0) {
+    const int64_t want = cdiv(N * c.L, 256);
+    const unsigned grid = (unsigned)std::min<int64_t>(want, (int64_t)ctx->num_sms * 8);
+    fit_scales_kernel<<<grid, 256, 0, s>>>(N, in->seq_off, in->prim_type, in->arg_off, in->arg_kind,
+                                           in->arg_num, in->arg_name, tokens, colmax, ctx->d_err,
+                                           c.L, c.E, c.T);
+    TLP_LAUNCH_CHECK();
+  }
+  fit_scales_finish<<<1, 64, 0, s>>>(colmax, ctx->d_scale, c.E);
+  TLP_LAUNCH_CHECK();
+  ctx->have_scales = true;
   return TLP_OK;
 }

@@ -1,5 +1,7 @@
-// fp32 SIMT network: the 1e-5-relative path (TLP_PREC_FP32) and, for this
-// round, the training forward/backward of both precisions.
+// The layer-by-layer network: the fp32 SIMT kernels of the 1e-5-relative path
+// (TLP_PREC_FP32), and the training forward/backward orchestration of both
+// precisions -- a bf16 context routes every dense layer, dgrad and wgrad to the
+// bf16x3 tcgen05 GEMMs of k_tc_gemm.cu and the attention core to k_attn_tc.cu.
 //
 // Forward (readings R8-R14 in DESIGN.md):
 //   h = relu(relu(X W1 + b1) W2 + b2)                    upsample (R11)
@@ -565,12 +567,7 @@ tlp_status launch_attn_bwd(tlp_ctx* ctx, const float* qkv, const float* A, const
   const int64_t pairs = N * c.attn_heads;
   const int warps = 2;
   const size_t smem = (size_t)warps * (4 * 32 * DH + 2 * 32 * 33) * sizeof(float);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(attn_bwd_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    attr_set = true;
-  }
+  TLP_SMEM_ATTR(attn_bwd_kernel<DH>, smem);
   attn_bwd_kernel<DH><<<(unsigned)cdiv(pairs, warps), warps * 32, smem, s>>>(
       qkv, A, dO, c.L, c.hidden, c.attn_heads, pairs, dqkv);
   TLP_LAUNCH_CHECK();
@@ -610,7 +607,7 @@ tlp_status sgemm(tlp_ctx* ctx, bool ta, bool tb, int64_t M, int64_t N, int64_t K
   if (M == 0 || N == 0) return TLP_OK;
   // TLP_PREC_BF16 contexts train on the tensor cores (tf32 tcgen05) whenever the
   // operands allow 16-byte async copies; the fp32 context stays on FFMA (1e-5).
-  if (ctx->cfg.precision == TLP_PREC_BF16 && tc_gemm_ok(A, lda, B, ldb))
+  if (ctx->cfg.precision == TLP_PREC_BF16)
     return tc_gemm(ctx, ta, tb, M, N, K, A, lda, B, ldb, C, ldc, e, 1, K, s);
   EpiDev ed{e.bias, e.resid, e.ldr, e.mask, e.ldm, e.relu ? 1 : 0, e.accumulate ? 1 : 0, e.mask_after ? 1 : 0};
   dim3 grid((unsigned)cdiv(N, BN), (unsigned)cdiv(M, BM), 1);
@@ -632,7 +629,7 @@ tlp_status sgemm_wgrad(tlp_ctx* ctx, int64_t M, int64_t K, int64_t N, const floa
   const int64_t kslice = cdiv(cdiv(M, Z), BK) * BK;
   EpiDev ed{nullptr, nullptr, 0, nullptr, 0, 0, 0};
   dim3 grid((unsigned)cdiv(N, BN), (unsigned)cdiv(K, BM), (unsigned)Z);
-  if (ctx->cfg.precision == TLP_PREC_BF16 && tc_gemm_ok(A, lda, dY, lddy)) {
+  if (ctx->cfg.precision == TLP_PREC_BF16) {
     EpiParams none;
     if (Z == 1) return tc_gemm(ctx, true, false, K, N, M, A, lda, dY, lddy, dW, N, none, 1, M, s);
     TLP_CUDA_TRY(ctx->ws_partial.ensure((size_t)Z * K * N * sizeof(float)));

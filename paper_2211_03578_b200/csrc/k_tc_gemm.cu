@@ -630,26 +630,16 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 
 
 }  // namespace
 
-bool tc_gemm_ok(const float*, int64_t, const float*, int64_t) { return true; }
-
 tlp_status tc_gemm(tlp_ctx* ctx, bool ta, bool tb, int64_t M, int64_t N, int64_t K,
                    const float* A, int64_t lda, const float* B, int64_t ldb, float* C,
                    int64_t ldc, const EpiParams& e, int splits, int64_t kslice, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(tc_gemm_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    cudaFuncSetAttribute(tc_gemm_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    cudaFuncSetAttribute(tc_gemm_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    cudaFuncSetAttribute(tc_gemm_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    attr = true;
-  }
+  TLP_SMEM_ATTR((tc_gemm_kernel<false, false>), SMEM_BYTES);
+  TLP_SMEM_ATTR((tc_gemm_kernel<false, true>), SMEM_BYTES);
+  TLP_SMEM_ATTR((tc_gemm_kernel<true, false>), SMEM_BYTES);
+  TLP_SMEM_ATTR((tc_gemm_kernel<true, true>), SMEM_BYTES);
   Epi ep{e.bias, e.resid, e.ldr, e.mask, e.ldm, e.relu ? 1 : 0, e.accumulate ? 1 : 0, e.mask_after ? 1 : 0};
   if (ta && !tb && splits > 1 && M > BM && M <= WROWS && N > BN && N <= WROWS) {
-    static bool wattr = false;
-    if (!wattr) {
-      cudaFuncSetAttribute(tc_wgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, WSMEM);
-      wattr = true;
-    }
+    TLP_SMEM_ATTR(tc_wgrad_kernel, WSMEM);
     const int av = aligned16(A) && lda % 4 == 0, bv = aligned16(B) && ldb % 4 == 0;
     tc_wgrad_kernel<<<dim3(1, 1, (unsigned)splits), THREADS, WSMEM, s>>>(M, N, K, A, lda, B, ldb, C,
                                                                          ldc, kslice, av, bv, 0, 0, 0);
@@ -657,11 +647,7 @@ tlp_status tc_gemm(tlp_ctx* ctx, bool ta, bool tb, int64_t M, int64_t N, int64_t
     return TLP_OK;
   }
   if (!ta && splits == 1 && N > BN && N <= BNI && K > 0) {
-    static bool iattr = false;
-    if (!iattr) {
-      cudaFuncSetAttribute(tc_gemm_bimg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, ISMEM);
-      iattr = true;
-    }
+    TLP_SMEM_ATTR(tc_gemm_bimg_kernel, ISMEM);
     const int64_t nkb = cdiv(K, BK);
     TLP_CUDA_TRY(ctx->ws_bimg.ensure((size_t)nkb * 2 * IMG_HALF));
     uint8_t* img = ctx->ws_bimg.as<uint8_t>();
@@ -696,11 +682,7 @@ bool tc_wgrad_bias(tlp_ctx* ctx, int64_t M, int64_t N, int64_t K, const float* A
   // (the unused part of the 256 x 256 tile computes zeros)
   if (!(splits > 1 && M > 64 && M <= WROWS && N > 64 && N <= WROWS)) return false;
   if (J > 1 && (bjs % 4 != 0)) return false;
-  static bool wattr = false;
-  if (!wattr) {
-    cudaFuncSetAttribute(tc_wgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, WSMEM);
-    wattr = true;
-  }
+  TLP_SMEM_ATTR(tc_wgrad_kernel, WSMEM);
   const int av = aligned16(A) && lda % 4 == 0, bv = aligned16(B) && ldb % 4 == 0;
   tc_wgrad_kernel<<<dim3(1, (unsigned)J, (unsigned)splits), THREADS, WSMEM, s>>>(M, N, K, A, lda, B, ldb,
                                                                                 part, N, kslice, av, bv, 1,

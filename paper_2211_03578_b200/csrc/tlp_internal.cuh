@@ -8,6 +8,7 @@
 #include <string>
 #include <vector>
 #include <mutex>
+#include <atomic>
 
 #include "../../include/tlp.h"
 
@@ -111,6 +112,13 @@ struct tlp_ctx {
   cudaEvent_t bucket_ev[5] = {};
   int buckets_issued = 0;
   int rank = 0, world = 1;
+  // recorded after the last collective a call enqueued: tlp_sync waits on it
+  // with a bound (TLP_NCCL_TIMEOUT_S) and aborts the communicator on timeout
+  // or an asynchronous NCCL error
+  cudaEvent_t coll_ev = nullptr;
+  // size of the token table (tlp_broadcast_state)
+  int32_t tok_n = 0;
+  int64_t tok_bytes = 0;
 
   int64_t launches = 0;
 
@@ -120,6 +128,8 @@ struct tlp_ctx {
   // training forward state kept for backward (k_simt.cu)
   int64_t train_N = -1;
   const float* train_X = nullptr;
+  // scores [train_N, n_tasks] of the last training forward (tlp_get_train_scores)
+  const float* train_scores = nullptr;
 };
 
 // ---------------------------------------------------------------------------
@@ -148,6 +158,21 @@ struct tlp_ctx {
 
 static inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is per device: remember per
+// call site which devices already have it (bit = device ordinal), so a process
+// with contexts on several GPUs sets it on each of them.
+#define TLP_SMEM_ATTR(func, bytes)                                                       \
+  do {                                                                                 \
+    static std::atomic<uint64_t> _tlp_attr_mask{0};                                    \
+    int _tlp_dev = 0;                                                                  \
+    cudaGetDevice(&_tlp_dev);                                                          \
+    const uint64_t _tlp_bit = 1ull << (_tlp_dev & 63);                                 \
+    if (!(_tlp_attr_mask.load(std::memory_order_acquire) & _tlp_bit)) {                \
+      cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(bytes)); \
+      _tlp_attr_mask.fetch_or(_tlp_bit, std::memory_order_acq_rel);                    \
+    }                                                                                  \
+  } while (0)
+
 // ---------------------------------------------------------------------------
 // kernels / launchers implemented in the .cu files
 
@@ -159,6 +184,8 @@ tlp_status encode_launch(tlp_ctx* ctx, const tlp_seq_batch* in, int64_t N, float
 tlp_status encode_resolve(tlp_ctx* ctx, const tlp_seq_batch* in, cudaStream_t s);
 tlp_status encode_rows(tlp_ctx* ctx, const tlp_seq_batch* in, int64_t N, float* feats,
                        cudaStream_t s);
+// R3 scales fitted on the device from a packed training batch -> ctx->d_scale
+tlp_status fit_scales_launch(tlp_ctx* ctx, const tlp_seq_batch* in, int64_t N, cudaStream_t s);
 // api.cu: the bf16 / fp32 scoring dispatch behind tlp_score (no argument checks)
 tlp_status score_launch(tlp_ctx* ctx, const float* feats, int64_t N, float* scores, cudaStream_t s);
 tlp_status build_token_table(tlp_ctx* ctx, const uint8_t* blob, const int64_t* off, int32_t n);
@@ -203,8 +230,7 @@ tlp_status simt_forward(tlp_ctx* ctx, const float* feats, int64_t N, float* scor
 tlp_status grad_bucket_ready(tlp_ctx* ctx, int64_t lo, int64_t hi, cudaStream_t s);
 tlp_status simt_backward(tlp_ctx* ctx, int64_t N, const float* dscores, cudaStream_t s);
 
-// k_tc_gemm.cu : tf32 tcgen05 GEMM used by the training path of bf16 contexts
-bool tc_gemm_ok(const float* A, int64_t lda, const float* B, int64_t ldb);
+// k_tc_gemm.cu : bf16x3 tcgen05 GEMMs of the training path of bf16 contexts
 tlp_status tc_gemm(tlp_ctx* ctx, bool ta, bool tb, int64_t M, int64_t N, int64_t K,
                    const float* A, int64_t lda, const float* B, int64_t ldb, float* C,
                    int64_t ldc, const EpiParams& e, int splits, int64_t kslice, cudaStream_t s);

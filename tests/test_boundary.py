@@ -76,3 +76,15 @@ def test_null_arguments_rejected(lib):
     assert lib.tlp_create(None, 0, None) == -1
     assert lib.tlp_sync(None) == -1
     assert lib.tlp_num_params(None) == -1
+
+
+@pytest.mark.parametrize("kw", [dict(), dict(n_attn=2, n_tasks=4), dict(pos_enc=True, n_attn=2),
+                                dict(backbone="lstm", n_attn=1, hidden=64, up_dims=(32, 64), head_dim=32)])
+def test_product_param_layout_matches_r24(kw):
+    """The binding's parameter layout (used to initialise weights without the
+    oracle) equals the oracle's R24 order, names and shapes."""
+    from paper_2211_03578_b200 import TLPConfig
+    from oracle import model as OM
+    pc = TLPConfig(**kw)
+    oc = OM.Config(**{k: v for k, v in kw.items()})
+    assert pc.param_shapes() == [(n, tuple(s)) for n, s in OM.param_shapes(oc)]

@@ -13,8 +13,9 @@ from oracle import model as OM
 from oracle import rank_loss as OLR
 from oracle.optim import AdamState, adam_step
 
-from helpers import encoded_batch, fit_scales, flat_params, oracle_cfg, product_cfg, rel_err, token_table
-from test_gpu_parity import CANCEL_GRAD, ZERO_GRAD, min_rel_gap, train_inputs
+from helpers import (encoded_batch, fit_scales, flat_params, grad_mismatches, oracle_cfg, product_cfg, rel_err,
+                     token_table)
+from test_gpu_parity import min_rel_gap, train_inputs
 
 pytestmark = pytest.mark.gpu
 
@@ -93,13 +94,7 @@ def test_lstm_grads_parity(tp, tokscale, precision, tol):
     m.sync()
     assert abs(float(loss.cpu()) - loss_ref) <= tol * abs(loss_ref)
     got = OM.unflatten(ocfg, m.get_grads().astype(np.float64))
-    bad = {}
-    for name, _ in OM.param_shapes(ocfg):
-        if ZERO_GRAD.search(name) or CANCEL_GRAD.search(name):
-            continue  # R32
-        e = rel_err(got[name], grads_ref[name])
-        if e > tol:
-            bad[name] = e
+    bad = grad_mismatches(ocfg, p, acts, g, got, grads_ref, tol)
     assert not bad, bad
 
 
@@ -120,8 +115,7 @@ def test_lstm_grads_parity_two_layers_mtl(tp, tokscale):
     m.compute_grads(torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda(), off)
     m.sync()
     got = OM.unflatten(ocfg, m.get_grads().astype(np.float64))
-    bad = {n: rel_err(got[n], grads_ref[n]) for n, _ in OM.param_shapes(ocfg)
-           if not (ZERO_GRAD.search(n) or CANCEL_GRAD.search(n)) and rel_err(got[n], grads_ref[n]) > 1e-5}
+    bad = grad_mismatches(ocfg, p, acts, g, got, grads_ref, 1e-5)
     assert not bad, bad
 
 

@@ -15,8 +15,8 @@ from oracle import model as OM
 from oracle import rank_loss as OLR
 from oracle.optim import AdamState, adam_step
 
-from helpers import (encoded_batch, fit_scales, flat_params, oracle_cfg, product_cfg, rel_err,
-                     token_table)
+from helpers import (encoded_batch, fit_scales, flat_params, grad_mismatches, oracle_cfg, product_cfg,
+                     rel_err, token_table)
 
 pytestmark = pytest.mark.gpu
 HERE = os.path.dirname(__file__)
@@ -249,23 +249,7 @@ def test_grads_parity(tp, tokscale, n_tasks, n_attn, seed, sizes, precision, tol
     m.sync()
     assert abs(float(loss.cpu()) - loss_ref) <= tol * abs(loss_ref)
     got = OM.unflatten(ocfg, m.get_grads().astype(np.float64))
-    bad = {}
-    for name, _ in OM.param_shapes(ocfg):
-        if ZERO_GRAD.search(name):
-            ref_w = name.replace(".bk", ".Wk").replace(".c2", ".w2")
-            assert np.abs(got[name]).max() <= tol * np.abs(grads_ref[ref_w]).max() * ocfg.L, name
-            continue
-        mc = CANCEL_GRAD.search(name)
-        if mc:
-            t = int(mc.group(1))
-            u = acts["heads"][t]["u"]
-            terms = np.abs(g[:, t])[:, None, None] * np.abs(p["head%d.w2" % t][:, 0]) * (u > 0)
-            mag = terms.sum(axis=(0, 1))
-            assert np.all(np.abs(got[name] - grads_ref[name]) <= tol * mag.max()), name
-            continue
-        e = rel_err(got[name], grads_ref[name])
-        if e > tol:
-            bad[name] = e
+    bad = grad_mismatches(ocfg, p, acts, g, got, grads_ref, tol)
     assert not bad, bad
 
 
@@ -306,14 +290,7 @@ def test_grads_parity_mse(tp, tokscale, precision, tol):
     m.sync()
     assert abs(float(loss.cpu()) - loss_ref) <= tol * abs(loss_ref)
     got = OM.unflatten(ocfg, m.get_grads().astype(np.float64))
-    bad = {}
-    for name, _ in OM.param_shapes(ocfg):
-        if re.search(r"attn\d+\.bk$", name):
-            assert np.abs(got[name]).max() <= tol * np.abs(grads_ref[name.replace(".bk", ".Wk")]).max() * ocfg.L
-            continue
-        e = rel_err(got[name], grads_ref[name])
-        if e > tol:
-            bad[name] = e
+    bad = grad_mismatches(ocfg, p, acts, g, got, grads_ref, tol, lambdarank=False)
     assert not bad, bad
 
 
@@ -365,13 +342,7 @@ def test_grads_parity_attn_mask(tp, tokscale, precision, tol):
     m.sync()
     assert abs(float(loss.cpu()) - loss_ref) <= tol * abs(loss_ref)
     got = OM.unflatten(ocfg, m.get_grads().astype(np.float64))
-    bad = {}
-    for name, _ in OM.param_shapes(ocfg):
-        if ZERO_GRAD.search(name) or CANCEL_GRAD.search(name):
-            continue  # as in test_grads_parity (R32)
-        e = rel_err(got[name], grads_ref[name])
-        if e > tol:
-            bad[name] = e
+    bad = grad_mismatches(ocfg, p, acts, g, got, grads_ref, tol)
     assert not bad, bad
 
 
@@ -413,13 +384,7 @@ def test_grads_parity_pos_enc(tp, tokscale, precision, tol):
     m.sync()
     assert abs(float(loss.cpu()) - loss_ref) <= tol * abs(loss_ref)
     got = OM.unflatten(ocfg, m.get_grads().astype(np.float64))
-    bad = {}
-    for name, _ in OM.param_shapes(ocfg):
-        if ZERO_GRAD.search(name) or CANCEL_GRAD.search(name):
-            continue
-        e = rel_err(got[name], grads_ref[name])
-        if e > tol:
-            bad[name] = e
+    bad = grad_mismatches(ocfg, p, acts, g, got, grads_ref, tol)
     assert not bad, bad
 
 
@@ -446,13 +411,7 @@ def test_grads_parity_bf16_paper_shape(tp, tokscale, mask):
     m.sync()
     assert abs(float(loss.cpu()) - loss_ref) <= 1e-2 * abs(loss_ref)
     got = OM.unflatten(ocfg, m.get_grads().astype(np.float64))
-    bad = {}
-    for name, _ in OM.param_shapes(ocfg):
-        if ZERO_GRAD.search(name) or CANCEL_GRAD.search(name):
-            continue
-        e = rel_err(got[name], grads_ref[name])
-        if e > 1e-2:
-            bad[name] = e
+    bad = grad_mismatches(ocfg, p, acts, g, got, grads_ref, 1e-2)
     assert not bad, bad
 
 
@@ -784,3 +743,40 @@ def test_crop_boundaries_bit_exact(tp, tokscale):
     X = m.encode(tp.DeviceBatch.from_packed(synth.pack(sub)))
     m.sync()
     assert np.array_equal(X.cpu().numpy().view(np.uint32), ref.view(np.uint32))
+
+
+# ---------------------------------------------------------------- R1 / R3 fitted by the library
+def test_fit_token_table_and_scales_bit_exact(tp):
+    """tlp_fit_token_table (R1: first occurrence over the training stream's name
+    arguments) and tlp_fit_norm_scales (R3: per-column max |x| over the kept,
+    un-normalised rows, 1.0 for all-zero columns) against oracle.build_token_table
+    / oracle.fit_scales on the same seeded training split; then tlp_encode with
+    the fitted state equals oracle.encode bit for bit."""
+    train = synth.generate(12345, 2000, unseen_rate=0.0)
+    tokens = oracle.build_token_table(synth.training_stream(12345, 2000))
+    raw = np.stack([oracle.extract_rows(s, tokens, 25, 22, 11) for s in train.to_lists()])
+    scale_ref = oracle.fit_scales(raw)
+    assert (np.diff(train.seq_off) > 25).any() and (np.diff(train.arg_off) > 11).any()  # crops exercised
+    m = tp.TLP(tp.TLPConfig(precision="fp32"))
+    m.fit_token_table(train)
+    scale = m.fit_norm_scales(tp.DeviceBatch.from_packed(train))
+    m.sync()
+    assert np.array_equal(scale.view(np.uint32), scale_ref.view(np.uint32)), (scale, scale_ref)
+    b = synth.generate(5, 777)  # includes 1% unseen names -> token 1
+    X = m.encode(tp.DeviceBatch.from_packed(b))
+    m.sync()
+    X_ref = oracle.encode(b.to_lists(), tokens, scale_ref)
+    assert np.array_equal(X.cpu().numpy().view(np.uint32), X_ref.view(np.uint32))
+
+
+def test_fit_scales_errors_and_empty(tp):
+    """Device errors of the fit follow tlp_encode's (kept data only); an empty
+    batch gives scale 1.0 everywhere."""
+    m = tp.TLP(tp.TLPConfig(precision="fp32"))
+    empty = synth.pack([])
+    assert np.array_equal(m.fit_norm_scales(tp.DeviceBatch.from_packed(empty)), np.ones(22, np.float32))
+    bad = synth.pack([[(3, [1.0, float("inf")])]])
+    m.fit_norm_scales(tp.DeviceBatch.from_packed(bad))
+    with pytest.raises(tp.TLPError) as e:
+        m.sync()
+    assert e.value.code == "ERR_NONFINITE"

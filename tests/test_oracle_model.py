@@ -318,3 +318,45 @@ def test_posenc_breaks_permutation_invariance_and_zero_table_is_identity():
     assert np.allclose(M.forward(plain, q, X), M.forward(plain, q, X[:, perm]), rtol=0, atol=1e-12)
     p0 = dict(p, pos=np.zeros_like(p["pos"]))
     assert np.array_equal(M.forward(cfg, p0, X), M.forward(plain, q, X))
+
+
+# ---------------------------------------------------------------- R50: per-term RMS of each gradient
+@pytest.mark.parametrize("backbone", ["attn", "lstm"])
+def test_term_rms_brute_force_single_row(backbone):
+    """With L = 1 every candidate contributes exactly one row term to each
+    parameter gradient, so backward(..., rms=) must equal the root of the sum of
+    the squared per-candidate gradients, each computed alone by brute force;
+    and passing ``rms`` leaves the gradients bitwise unchanged."""
+    cfg = M.Config(L=1, E=8, T=3, hidden=16, up_dims=(12, 16), attn_heads=4, n_attn=1,
+                   n_res=2, head_dim=8, n_tasks=2, backbone=backbone, pos_enc=True)
+    p = rand_params(cfg, 3)
+    X = rand_X(cfg, 7, 4)
+    g = np.random.default_rng(5).normal(size=(7, 2))
+    s, acts = M.forward(cfg, p, X, save=True)
+    plain = M.backward(cfg, p, acts, g)
+    rms = {}
+    grads = M.backward(cfg, p, acts, g, rms=rms)
+    assert set(rms) == set(grads)
+    for k in grads:
+        assert np.array_equal(grads[k], plain[k]), k
+    sq = {k: np.zeros_like(v) for k, v in grads.items()}
+    for n in range(7):
+        _, a_n = M.forward(cfg, p, X[n:n + 1], save=True)
+        for k, v in M.backward(cfg, p, a_n, g[n:n + 1]).items():
+            sq[k] += v * v
+    for k in grads:
+        np.testing.assert_allclose(rms[k], np.sqrt(sq[k]), rtol=1e-12, atol=1e-300, err_msg=k)
+
+
+def test_term_rms_cauchy_schwarz():
+    """|grad| <= sqrt(#terms) * rms elementwise (N*L row terms), rms >= 0."""
+    p = rand_params(SMALL, 6)
+    X = rand_X(SMALL, 5, 7, n_real=4)
+    g = np.random.default_rng(8).normal(size=(5, 2))
+    _, acts = M.forward(SMALL, p, X, save=True)
+    rms = {}
+    grads = M.backward(SMALL, p, acts, g, rms=rms)
+    nt = 5 * SMALL.L
+    for k in grads:
+        assert np.all(rms[k] >= 0)
+        assert np.all(np.abs(grads[k]) <= np.sqrt(nt) * rms[k] * (1 + 1e-12) + 1e-300), k

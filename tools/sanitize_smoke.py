@@ -2,8 +2,10 @@
 racecheck / synccheck): encode -> score (fp32 + bf16 fused, with and without the
 padding mask / positional table) -> top-k -> labels -> train steps (LambdaRank
 and MSE; fp32 and bf16 contexts, incl. the B-image and wgrad GEMMs) -> top-k
-merge -> tlp_search_round -> tlp_dedup -> tlp_topk_score; NEXT-1 device tuning
-rounds (fp32 and bf16 scoring) and NEXT-4 LSTM contexts (score + train)."""
+merge -> tlp_search_round -> tlp_dedup -> tlp_topk_score; a 2,500-row bf16
+train step (fused wgrad + bias kernels, 1 and 4 heads); token-table / scale
+fitting; NEXT-1 device tuning rounds (fp32 and bf16 scoring) and NEXT-4 LSTM
+contexts (score + train)."""
 import os
 import sys
 
@@ -43,13 +45,24 @@ for prec, cfg, extra in cases:
     m.dedup(X, off, y[:, 0].contiguous())
     m.topk_score(s, lat, off, [1.0, 2.0, 1.0], 2)
     m.sync()
-# the training GEMM variants at their real shapes (N = 256 tiles, 256 x 256 wgrad)
-big = tp.TLP(tp.TLPConfig(n_attn=1))
-big.set_params(np.concatenate([v.ravel() for v in synth.init_params(2, OM.param_shapes(OM.Config()))]).astype(np.float32))
-Xb = torch.rand((64, 25, 22), device="cuda")
-yb = torch.rand((64, 1), device="cuda") + 0.01
-big.train_step(Xb, yb, np.array([0, 32, 64], np.int64))
-big.sync()
+# the training GEMM variants at their real shapes (N = 256 tiles, 256 x 256
+# wgrad): 100 samples = 2,500 rows > one 2,048-row slice, so the fused
+# wgrad + bias-sum kernel (J = 1 and the J = 3 Q/K/V launch) and the slice
+# reduction run, as in the benched step; MTL-4 heads
+for nt in (1, 4):
+    bcfg = OM.Config(n_tasks=nt)
+    big = tp.TLP(tp.TLPConfig(n_attn=1, n_tasks=nt))
+    big.set_params(np.concatenate([v.ravel() for v in synth.init_params(2, OM.param_shapes(bcfg))]).astype(np.float32))
+    Xb = torch.rand((100, 25, 22), device="cuda")
+    yb = torch.rand((100, nt), device="cuda") + 0.01
+    big.train_step(Xb, yb, np.array([0, 50, 100], np.int64))
+    big.sync()
+# R1 / R3 fitted on the device
+fit = tp.TLP(tp.TLPConfig(precision="fp32"))
+tb = synth.generate(9, 50, unseen_rate=0.0)
+fit.fit_token_table(tb)
+fit.fit_norm_scales(tp.DeviceBatch.from_packed(tb))
+fit.sync()
 # NEXT-1: device tuning rounds (GA kernels + dedup + materialise -> encode -> score -> top-k)
 ts = [synth.make_template(5, s) for s in range(3)] + [synth.small_template((2, 3))]
 for prec, cfg in (("fp32", OM.Config(hidden=64, up_dims=(32, 64), head_dim=32)), ("bf16", OM.Config(n_attn=2))):
