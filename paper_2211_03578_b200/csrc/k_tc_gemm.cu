@@ -653,6 +653,9 @@ tlp_status tc_gemm(tlp_ctx* ctx, bool ta, bool tb, int64_t M, int64_t N, int64_t
     uint8_t* img = ctx->ws_bimg.as<uint8_t>();
     bimg_kernel<<<(unsigned)nkb, 256, 0, s>>>(B, ldb, tb ? 1 : 0, N, K, img);
     TLP_LAUNCH_CHECK();
+    // the TMA-fed persistent kernel (k_tc_tma.cu) when the operands allow it
+    const tlp_status ts = tc_gemm_tma(ctx, M, N, K, A, lda, img, C, ldc, e, s);
+    if (ts != TLP_ERR_UNSUPPORTED) return ts;
     const int av = aligned16(A) && lda % 4 == 0;
     tc_gemm_bimg_kernel<<<dim3(1, (unsigned)cdiv(M, BM), 1), THREADS, ISMEM, s>>>(M, N, K, A, lda, img, C,
                                                                                 ldc, ep, av);

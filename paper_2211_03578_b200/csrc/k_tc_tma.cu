@@ -1,0 +1,444 @@
+// TMA-fed, warp-specialised, persistent tcgen05 GEMM for the dense layers of
+// bf16-context training ("the loss is back-propagated to update the
+// weights"): every forward layer and every dgrad whose output is 128 < N <= 256
+// wide and whose activation operand A is row-major fp32 (the layers bench.py's
+// C3 step spends most of its time in).
+//
+//   C[M, N] = epi( A[M, K] . B[K, N] ),  epi = + bias, + resid, ReLU, ReLU' mask,
+//                                               accumulate (C += .), as EpiParams
+//
+// Precision is the training path's bf16x3 (R37): A = Ah + Al (hi = truncated
+// bf16, lo = RN_bf16(A - hi)), B likewise (the per-call weight image of
+// bimg_kernel), A.B ~= Ah.Bh + Ah.Bl + Al.Bh with fp32 accumulation in TMEM.
+//
+// Why this kernel: the register-staged GEMM it replaces (tc_gemm_bimg_kernel)
+// moved 373 MB per 204,800 x 256 launch at 2.2 TB/s -- its loader threads
+// could keep only one 16 KB k-block in flight per CTA.  Here every byte of HBM
+// traffic is a tensor-memory-accelerator copy issued ahead of use:
+//   warp 0      TMA producer: A tiles [128 rows x 32 k] fp32 (128B swizzle)
+//               into a 3-deep ring;
+//   warps 2-5   converters: fp32 tile -> bf16 hi / lo in the K-major canonical
+//               UMMA layout (the k-block's 32 KB weight image arrives by a 1-D
+//               bulk copy the producer issues with the A tile, 3 deep);
+//   warp 1      MMA issuer: 6 x tcgen05.mma (M=128, N=256, K=16) per k-block
+//               into one of two TMEM accumulators (512 columns), so the
+//               epilogue of tile i overlaps the main loop of tile i+1;
+//   warps 6-13  epilogue, two per TMEM lane quarter, each independent of the
+//               others: thread = tile row = TMEM lane; per 16-column chunk the
+//               residual / mask / old-C input arrives by TMA (a 3-deep ring
+//               per warp, 64B swizzle, [32 rows x 16 cols] boxes), the result
+//               replaces it in the same stage and leaves by TMA store.
+// Measured by skipping parts (TLP_TMA_DEBUG): a first epilogue with two
+// 128-thread barriers per chunk ran 4-5x longer than the main loop; storing
+// rows straight from registers (32 rows, 16 B each per warp instruction) made
+// the stores half of the kernel; per-warp TMA boxes fix both.
+// Tiles (128 rows) are walked persistently, one CTA per SM.
+#include "tlp_internal.cuh"
+#include "tc_ptx.cuh"
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdlib>
+
+namespace {
+
+constexpr int TM = 128, TN = 256, TK = 32;
+constexpr int SA = 3;                        // fp32 A ring (TMA)
+constexpr int SB = 3;                        // B image ring (bulk copies, issued with A)
+constexpr int SC = 2;                        // converted A hi/lo ring (MMA operands)
+constexpr int SE = 3;                        // epilogue input ring per warp (16-column chunks)
+constexpr int EC = 16;                       // epilogue chunk columns
+constexpr uint32_t A_BYTES = TM * TK * 4;    // 16 KB fp32 tile
+constexpr uint32_t AH_BYTES = TM * TK * 2;   // 8 KB bf16
+constexpr uint32_t B_BYTES = 2 * TN * TK * 2;  // 32 KB hi | lo image block
+constexpr uint32_t C_STAGE = 2 * AH_BYTES;   // 16 KB hi | lo
+constexpr int EW = 8;                        // epilogue warps
+constexpr uint32_t E_BYTES = 32 * EC * 4;    // 2 KB: one warp's 32 rows x 16 columns of the input
+constexpr uint32_t OFF_A = 0;
+constexpr uint32_t OFF_B = OFF_A + SA * A_BYTES;
+constexpr uint32_t OFF_C = OFF_B + SB * B_BYTES;
+constexpr uint32_t OFF_E = OFF_C + SC * C_STAGE;
+constexpr uint32_t OFF_BAR = OFF_E + EW * SE * E_BYTES;
+constexpr uint32_t SMEM_USED = OFF_BAR + 512;
+constexpr uint32_t SMEM_ALLOC = SMEM_USED + 1024;  // manual 1 KB alignment of the base
+constexpr int THREADS = 448;  // warp 0 TMA, 1 MMA, 2-5 converters, 6-13 epilogue
+static_assert(SMEM_ALLOC <= 232448, "shared memory budget");
+static_assert(SE >= 3, "the two-input epilogue uses stages 0-1 (inputs) and 2 (output)");
+
+struct TmaArgs {
+  int64_t M, N, K;
+  int ntiles;
+  const uint8_t* img;    // bf16 hi/lo weight image, [K/32][hi 16 KB | lo 16 KB]
+  float* C;              // [M, ldc] output (and the old values when accumulating)
+  int64_t ldc;
+  const float* bias;     // [N] or null
+  int n_in;              // epilogue inputs by TMA: 0, 1 or 2
+  int in_kind[2];        // 0 = residual (added before ReLU), 1 = mask, 2 = old C (accumulate)
+  int relu, mask_after, accumulate, has_mask;
+  int dbg;  // timing experiments only (TLP_TMA_DEBUG): 1 = no epilogue work, 2 = no conversion,
+            // 3 = no epilogue stores, 4 = no TMEM loads
+};
+
+__device__ __forceinline__ void named_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+template <int NIN>  // epilogue inputs (a.n_in), specialised: the epilogue bounds the kernel
+__global__ void __launch_bounds__(THREADS, 1) tma_gemm_kernel(const __grid_constant__ CUtensorMap mA,
+                                                              const __grid_constant__ CUtensorMap mIn0,
+                                                              const __grid_constant__ CUtensorMap mIn1,
+                                                              const __grid_constant__ CUtensorMap mOut,
+                                                              const TmaArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t sraw = tc::smem_u32(smem_raw);
+  const uint32_t sb = (sraw + 1023u) & ~1023u;  // 1 KB aligned (128B-swizzle atoms)
+  uint8_t* smem = smem_raw + (sb - sraw);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t bar = sb + OFF_BAR;
+  const uint32_t a_full = bar, a_empty = a_full + 8 * SA;
+  const uint32_t b_full = a_empty + 8 * SA, b_empty = b_full + 8 * SB;
+  const uint32_t c_empty = b_empty + 8 * SB, conv_full = c_empty + 8 * SC;
+  const uint32_t acc_full = conv_full + 8 * SC, acc_empty = acc_full + 16, e_full = acc_empty + 16;
+  uint32_t* tptr = reinterpret_cast<uint32_t*>(smem + OFF_BAR + 480);
+  const int nk = (int)((a.K + TK - 1) / TK);
+  const int nch = (int)((a.N + EC - 1) / EC);
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < SA; ++i) { tc::mbar_init(a_full + 8 * i, 1); tc::mbar_init(a_empty + 8 * i, 4); }
+    for (int i = 0; i < SB; ++i) { tc::mbar_init(b_full + 8 * i, 1); tc::mbar_init(b_empty + 8 * i, 1); }
+    for (int i = 0; i < SC; ++i) { tc::mbar_init(c_empty + 8 * i, 1); tc::mbar_init(conv_full + 8 * i, 4); }
+    for (int i = 0; i < 2; ++i) { tc::mbar_init(acc_full + 8 * i, 1); tc::mbar_init(acc_empty + 8 * i, EW); }
+    for (int i = 0; i < EW * SE; ++i) tc::mbar_init(e_full + 8 * i, 1);
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) tc::tmem_alloc(tc::smem_u32(tptr), 512);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tptr;
+
+  if (warp == 0) {
+    // ------------------------------------------------ TMA producer: A tiles + weight image blocks
+    if (lane == 0) {
+      int s = 0, t = 0;
+      uint32_t ph = 0, pb = 0;
+      for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
+        for (int kb = 0; kb < nk; ++kb) {
+          tc::mbar_wait(a_empty + 8 * s, ph ^ 1);
+          tc::mbar_arrive_expect_tx(a_full + 8 * s, A_BYTES);
+          tc::tma_load_2d(sb + OFF_A + s * A_BYTES, &mA, kb * TK, tile * TM, a_full + 8 * s);
+          if (++s == SA) { s = 0; ph ^= 1; }
+          tc::mbar_wait(b_empty + 8 * t, pb ^ 1);
+          tc::mbar_arrive_expect_tx(b_full + 8 * t, B_BYTES);
+          tc::bulk_g2s(sb + OFF_B + t * B_BYTES, a.img + (size_t)kb * B_BYTES, B_BYTES, b_full + 8 * t);
+          if (++t == SB) { t = 0; pb ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      const uint32_t idesc = tc::idesc_bf16(TM, TN);
+      int s = 0, t = 0, sbk = 0;
+      uint32_t ph = 0, pb = 0;
+      for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++t) {
+        const int buf = t & 1;
+        tc::mbar_wait(acc_empty + 8 * buf, ((t >> 1) & 1) ^ 1);
+        tc::tc_fence_after();
+        const uint32_t d = tmem + (uint32_t)(buf * TN);
+        for (int kb = 0; kb < nk; ++kb) {
+          tc::mbar_wait(conv_full + 8 * s, ph);
+          tc::mbar_wait(b_full + 8 * sbk, pb);
+          tc::tc_fence_after();
+          const uint32_t ah = sb + OFF_C + s * C_STAGE, al = ah + AH_BYTES;
+          const uint32_t bh = sb + OFF_B + sbk * B_BYTES, bl = bh + B_BYTES / 2;
+#pragma unroll
+          for (int ks = 0; ks < TK / 16; ++ks) {
+            const uint64_t dah = tc::smem_desc(ah + ks * 256, 128, 512), dal = tc::smem_desc(al + ks * 256, 128, 512);
+            const uint64_t dbh = tc::smem_desc(bh + ks * 256, 128, 512), dbl = tc::smem_desc(bl + ks * 256, 128, 512);
+            tc::mma_bf16(d, dal, dbh, idesc, (kb > 0 || ks > 0) ? 1u : 0u);  // Al.Bh
+            tc::mma_bf16(d, dah, dbl, idesc, 1u);                          // Ah.Bl
+            tc::mma_bf16(d, dah, dbh, idesc, 1u);                          // Ah.Bh
+          }
+          tc::mma_commit(c_empty + 8 * s);
+          tc::mma_commit(b_empty + 8 * sbk);
+          if (++s == SC) { s = 0; ph ^= 1; }
+          if (++sbk == SB) { sbk = 0; pb ^= 1; }
+        }
+        tc::mma_commit(acc_full + 8 * buf);
+      }
+    }
+  } else if (warp < 6) {
+    // ------------------------------------------------ converters (128 threads)
+    const int cw = warp - 2;
+    int sa = 0, sc = 0;
+    uint32_t pa = 0, pc = 0;
+    for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
+      for (int kb = 0; kb < nk; ++kb) {
+        tc::mbar_wait(a_full + 8 * sa, pa);
+        tc::mbar_wait(c_empty + 8 * sc, pc ^ 1);  // the MMAs of this stage's last use are done
+        const uint32_t cst = OFF_C + sc * C_STAGE;
+        const uint8_t* src = smem + OFF_A + sa * A_BYTES;
+        uint8_t* hi = smem + cst;
+        uint8_t* lo = hi + AH_BYTES;
+#pragma unroll
+        for (int it = 0; it < (a.dbg == 2 ? 0 : 8); ++it) {
+          // 8 rows x 4 16-byte chunks per warp instruction: conflict-free reads of
+          // the 128B-swizzled tile (chunk j of row r at j ^ (r & 7)) and
+          // conflict-free 8-byte stores into the canonical layout
+          const int task = it * 4 + cw;
+          const int rg = task >> 1, jb = (task & 1) * 4;
+          const int r = rg * 8 + (lane & 7), j = jb + (lane >> 3);
+          const float4 v = *reinterpret_cast<const float4*>(src + r * 128 + ((j ^ (r & 7)) << 4));
+          const uint32_t x0 = __float_as_uint(v.x), x1 = __float_as_uint(v.y);
+          const uint32_t x2 = __float_as_uint(v.z), x3 = __float_as_uint(v.w);
+          const uint32_t h0 = __byte_perm(x0, x1, 0x7632), h1 = __byte_perm(x2, x3, 0x7632);
+          const uint32_t l0 = tc::pack_bf16(v.x - __uint_as_float(x0 & 0xffff0000u),
+                                            v.y - __uint_as_float(x1 & 0xffff0000u));
+          const uint32_t l1 = tc::pack_bf16(v.z - __uint_as_float(x2 & 0xffff0000u),
+                                            v.w - __uint_as_float(x3 & 0xffff0000u));
+          const uint32_t off = rg * 512 + (j >> 1) * 128 + (r & 7) * 16 + (j & 1) * 8;
+          *reinterpret_cast<uint2*>(hi + off) = make_uint2(h0, h1);
+          *reinterpret_cast<uint2*>(lo + off) = make_uint2(l0, l1);
+        }
+        tc::fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tc::mbar_arrive(a_empty + 8 * sa);
+          tc::mbar_arrive(conv_full + 8 * sc);
+        }
+        if (++sa == SA) { sa = 0; pa ^= 1; }
+        if (++sc == SC) { sc = 0; pc ^= 1; }
+      }
+    }
+  } else {
+    // ------------------------------------------------ epilogue (8 warps, 2 per TMEM lane quarter)
+    // Warp (q, hh) owns rows 32q..32q+31 (thread = row = TMEM lane) and the
+    // 16-column chunks c = hh, hh + 2, ...  It needs no other warp: its input
+    // boxes [32 rows x 16 cols] arrive by TMA on its own mbarriers (SE deep,
+    // issued ahead), and it stores its results straight from registers
+    // (64 contiguous bytes per row and chunk; L2 merges the sectors).
+    const int ew = warp - 6;
+    const int q = warp & 3, hh = ew >> 2;
+    const int r = 32 * q + lane;
+    const uint32_t tl = tmem + ((uint32_t)(32 * q) << 16);
+    const uint32_t my_e = e_full + 8 * SE * ew;
+    const uint32_t my_buf = sb + OFF_E + (uint32_t)ew * SE * E_BYTES;
+    const int nmine = (nch - hh + 1) / 2;  // chunks per tile for this warp
+    const long long tiles_mine = a.ntiles > (int)blockIdx.x ? (a.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const long long total = tiles_mine * nmine;
+    // One input (n_in <= 1): stage g % SE holds chunk g's input, then its result
+    // for the TMA store; the input of chunk g + SE - 1 is loaded into stage
+    // (g - 1) % SE once the store of chunk g - 1 has finished reading it.
+    // Two inputs (old C + ReLU' mask): stages 0-1 hold both inputs of one chunk
+    // (re-armed for chunk g + 1 as soon as they are in registers), stage 2 is
+    // the output staging buffer.
+    constexpr bool two = NIN == 2;
+    auto issue_in = [&](long long g) {  // this warp's g-th chunk overall
+      if (NIN == 0 || g >= total) return;
+      const int tile = blockIdx.x + (int)(g / nmine) * gridDim.x;
+      const int c = hh + 2 * (int)(g % nmine);
+      const int se = two ? 0 : (int)(g % SE);
+      tc::mbar_arrive_expect_tx(my_e + 8 * se, (uint32_t)NIN * E_BYTES);
+      tc::tma_load_2d(my_buf + se * E_BYTES, &mIn0, c * EC, tile * TM + 32 * q, my_e + 8 * se);
+      if (two) tc::tma_load_2d(my_buf + E_BYTES, &mIn1, c * EC, tile * TM + 32 * q, my_e);
+    };
+    if (lane == 0)
+      for (long long g = 0; g < (two ? 1 : SE - 1); ++g) issue_in(g);
+    long long g = 0;
+    int t = 0;
+    const int sw = (lane >> 1) & 3;  // 64B swizzle of box row `lane`: chunk j at j ^ ((lane >> 1) & 3)
+    for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++t) {
+      const int buf = t & 1;
+      tc::mbar_wait(acc_full + 8 * buf, (t >> 1) & 1);
+      tc::tc_fence_after();
+      for (int c = hh; c < (a.dbg == 1 ? 0 : nch); c += 2, ++g) {
+        float v[16];
+        if (a.dbg != 4) tc::tmem_ld16(tl + (uint32_t)(buf * TN + c * EC), v);
+        else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] = 0.f;
+        }
+        float b[16];
+        if (a.bias) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const float4 x = __ldg(reinterpret_cast<const float4*>(a.bias + c * EC) + i);
+            b[4 * i] = x.x; b[4 * i + 1] = x.y; b[4 * i + 2] = x.z; b[4 * i + 3] = x.w;
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) b[i] = 0.f;
+        }
+        const int se = two ? 0 : (int)(g % SE);
+        const int so = two ? 2 : se;  // output staging stage
+        uint8_t* stage = smem + (my_buf - sb) + se * E_BYTES + lane * 64;
+        uint8_t* ostage = smem + (my_buf - sb) + so * E_BYTES + lane * 64;
+        float in[NIN > 0 ? NIN : 1][16];
+        if (NIN > 0) {
+          tc::mbar_wait(my_e + 8 * se, (uint32_t)((two ? g : g / SE) & 1));
+#pragma unroll
+          for (int s2 = 0; s2 < NIN; ++s2) {
+            {
+#pragma unroll
+              for (int jj = 0; jj < 4; ++jj) {
+                const float4 x = *reinterpret_cast<const float4*>(stage + s2 * E_BYTES + ((jj ^ sw) << 4));
+                in[s2][4 * jj] = x.x; in[s2][4 * jj + 1] = x.y; in[s2][4 * jj + 2] = x.z; in[s2][4 * jj + 3] = x.w;
+              }
+            }
+          }
+          if (two) {
+            __syncwarp();
+            if (lane == 0) {
+              issue_in(g + 1);          // both input slots are in registers: prefetch the next chunk
+              tc::bulk_wait_read<0>();  // the output stage's previous store has read it
+            }
+            __syncwarp();
+          }
+        }
+        tc::tmem_wait_ld();
+        float y[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          float resid = 0.f, mask = 1.f, old = 0.f;
+#pragma unroll
+          for (int s2 = 0; s2 < NIN; ++s2) {
+            {
+              if (a.in_kind[s2] == 0) resid = in[s2][i];
+              else if (a.in_kind[s2] == 1) mask = in[s2][i];
+              else old = in[s2][i];
+            }
+          }
+          float x = v[i] + b[i] + resid;
+          if (a.relu) x = fmaxf(x, 0.f);
+          if (a.has_mask && !a.mask_after) x = mask > 0.f ? x : 0.f;
+          x += old;
+          if (a.has_mask && a.mask_after) x = mask > 0.f ? x : 0.f;
+          y[i] = x;
+        }
+        // one input: the result replaces the input in the same (swizzled)
+        // stage -- the last store from it (chunk g - SE) finished reading
+        // before the input of chunk g was loaded into it
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj)
+          *reinterpret_cast<float4*>(ostage + ((jj ^ sw) << 4)) =
+              make_float4(y[4 * jj], y[4 * jj + 1], y[4 * jj + 2], y[4 * jj + 3]);
+        tc::fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          if (a.dbg != 3) {
+            tc::tma_store_2d(&mOut, c * EC, tile * TM + 32 * q, my_buf + so * E_BYTES);
+            tc::bulk_commit();
+          }
+          if (!two) {
+            tc::bulk_wait_read<1>();  // chunk g - 1's store has read its stage
+            issue_in(g + SE - 1);     // -> that stage takes the input of chunk g + SE - 1
+          }
+        }
+        __syncwarp();
+      }
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(acc_empty + 8 * buf);
+    }
+    if (lane == 0) tc::bulk_wait_all();
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc::tc_fence_after();
+    tc::tmem_dealloc(tmem, 512);
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// fp32 [rows][ld] matrix, box [box_rows][box_cols]
+bool make_map(CUtensorMap* m, const float* base, int64_t cols, int64_t rows, int64_t ld, uint32_t box_cols,
+              uint32_t box_rows, CUtensorMapSwizzle sw) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(float)};
+  const cuuint32_t box[2] = {box_cols, box_rows};
+  const cuuint32_t es[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool tma_ok(const void* p, int64_t ld) {
+  return p && (reinterpret_cast<uintptr_t>(p) & 15) == 0 && ld % 4 == 0;
+}
+
+}  // namespace
+
+// Returns TLP_ERR_UNSUPPORTED (nothing launched) when the call does not fit the
+// kernel; the caller then uses the register-staged path.
+tlp_status tc_gemm_tma(tlp_ctx* ctx, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,
+                       const uint8_t* img, float* C, int64_t ldc, const EpiParams& e, cudaStream_t s) {
+  static const char* env = getenv("TLP_TMA_GEMM");
+  if (env && env[0] == '0') return TLP_ERR_UNSUPPORTED;
+  if (!(N > 128 && N <= TN && N % EC == 0 && K > 0 && M > 0 && M <= (int64_t)INT32_MAX - TM))
+    return TLP_ERR_UNSUPPORTED;
+  if (!tma_ok(A, lda) || !tma_ok(C, ldc)) return TLP_ERR_UNSUPPORTED;
+  TmaArgs a{};
+  a.M = M; a.N = N; a.K = K;
+  a.ntiles = (int)cdiv(M, TM);
+  a.img = img;
+  a.bias = e.bias;
+  a.relu = e.relu ? 1 : 0;
+  a.mask_after = e.mask_after ? 1 : 0;
+  a.accumulate = e.accumulate ? 1 : 0;
+  a.has_mask = e.mask ? 1 : 0;
+  static const char* dbg = getenv("TLP_TMA_DEBUG");
+  a.dbg = dbg ? atoi(dbg) : 0;
+  a.C = C;
+  a.ldc = ldc;
+  const float* ins[2] = {nullptr, nullptr};
+  int64_t lds[2] = {0, 0};
+  auto add_in = [&](const float* p, int64_t ld, int kind) {
+    if (a.n_in == 2) return false;
+    ins[a.n_in] = p; lds[a.n_in] = ld; a.in_kind[a.n_in] = kind; ++a.n_in;
+    return tma_ok(p, ld);
+  };
+  if (e.resid && !add_in(e.resid, e.ldr, 0)) return TLP_ERR_UNSUPPORTED;
+  if (e.accumulate && !add_in(C, ldc, 2)) return TLP_ERR_UNSUPPORTED;
+  if (e.mask && !add_in(e.mask, e.ldm, 1)) return TLP_ERR_UNSUPPORTED;
+  if (e.bias && (reinterpret_cast<uintptr_t>(e.bias) & 15)) return TLP_ERR_UNSUPPORTED;
+  CUtensorMap mA, mI0, mI1, mO;
+  if (!make_map(&mA, A, K, M, lda, TK, TM, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !make_map(&mO, C, N, M, ldc, EC, 32, CU_TENSOR_MAP_SWIZZLE_64B))
+    return TLP_ERR_UNSUPPORTED;
+  mI0 = mO;
+  mI1 = mO;
+  if (a.n_in > 0 && !make_map(&mI0, ins[0], N, M, lds[0], EC, 32, CU_TENSOR_MAP_SWIZZLE_64B))
+    return TLP_ERR_UNSUPPORTED;
+  if (a.n_in > 1 && !make_map(&mI1, ins[1], N, M, lds[1], EC, 32, CU_TENSOR_MAP_SWIZZLE_64B))
+    return TLP_ERR_UNSUPPORTED;
+  const int grid = (int)std::min<int64_t>(a.ntiles, ctx->num_sms);
+  if (a.n_in == 0) {
+    TLP_SMEM_ATTR(tma_gemm_kernel<0>, SMEM_ALLOC);
+    tma_gemm_kernel<0><<<grid, THREADS, SMEM_ALLOC, s>>>(mA, mI0, mI1, mO, a);
+  } else if (a.n_in == 1) {
+    TLP_SMEM_ATTR(tma_gemm_kernel<1>, SMEM_ALLOC);
+    tma_gemm_kernel<1><<<grid, THREADS, SMEM_ALLOC, s>>>(mA, mI0, mI1, mO, a);
+  } else {
+    TLP_SMEM_ATTR(tma_gemm_kernel<2>, SMEM_ALLOC);
+    tma_gemm_kernel<2><<<grid, THREADS, SMEM_ALLOC, s>>>(mA, mI0, mI1, mO, a);
+  }
+  TLP_LAUNCH_CHECK();
+  return TLP_OK;
+}

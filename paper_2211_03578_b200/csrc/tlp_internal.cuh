@@ -231,6 +231,10 @@ tlp_status grad_bucket_ready(tlp_ctx* ctx, int64_t lo, int64_t hi, cudaStream_t 
 tlp_status simt_backward(tlp_ctx* ctx, int64_t N, const float* dscores, cudaStream_t s);
 
 // k_tc_gemm.cu : bf16x3 tcgen05 GEMMs of the training path of bf16 contexts
+// k_tc_tma.cu: the TMA-fed persistent variant for 128 < N <= 256, row-major A
+// (img = bimg_kernel's weight image); TLP_ERR_UNSUPPORTED = not applicable
+tlp_status tc_gemm_tma(tlp_ctx* ctx, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,
+                       const uint8_t* img, float* C, int64_t ldc, const EpiParams& e, cudaStream_t s);
 tlp_status tc_gemm(tlp_ctx* ctx, bool ta, bool tb, int64_t M, int64_t N, int64_t K,
                    const float* A, int64_t lda, const float* B, int64_t ldb, float* C,
                    int64_t ldc, const EpiParams& e, int splits, int64_t kslice, cudaStream_t s);

@@ -567,7 +567,10 @@ def test_bf16_full_size_sampled(tp, tokscale):
 @pytest.mark.parametrize("ta,tb", [(0, 0), (0, 1), (1, 0), (1, 1)])
 @pytest.mark.parametrize("M,N,K,splits", [(300, 200, 72, 1), (128, 128, 32, 1), (1000, 96, 516, 3),
                                           (64, 256, 4096, 8), (37, 22, 22, 1), (130, 30, 50, 2),
-                                          (256, 256, 3000, 5), (200, 136, 777, 3)])
+                                          (256, 256, 3000, 5), (200, 136, 777, 3),
+                                          # ta = 0, splits = 1, 128 < N <= 256, N % 16 == 0: the
+                                          # TMA-fed persistent kernel (k_tc_tma.cu), ragged M / K
+                                          (300, 256, 72, 1), (1000, 144, 256, 1), (40000, 256, 768, 1)])
 def test_train_gemm_building_block(tp, ta, tb, M, N, K, splits):
     rng = np.random.default_rng(M + N + K + 10 * ta + tb)
     A = rng.normal(size=(K, M) if ta else (M, K)).astype(np.float32)
