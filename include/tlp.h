@@ -442,6 +442,15 @@ tlp_status tlp_debug_gemm(tlp_ctx* ctx, int32_t ta, int32_t tb, int64_t M, int64
                           const float* A, int64_t lda, const float* B, int64_t ldb, float* C,
                           int64_t ldc, int32_t splits, void* stream);
 
+/* Test hook for the weight + bias gradient of one dense layer of the training
+ * path: dWdb[0 : K*N] = X^T dY ([K, N] row-major, X [M][ldx] with K columns,
+ * dY [M][ldy] with N columns, fp32 device) and dWdb[K*N : K*N + N] = the column
+ * sums of dY -- the R24 (W, b) layout.  A bf16 ctx takes the kernels of its
+ * training step (for 32 <= K, N <= 256 multiples of 32: TMA-fed kind::tf32
+ * tiles per row slice + fixed-order slice reduction, R52). */
+tlp_status tlp_debug_wgrad(tlp_ctx* ctx, int64_t M, int64_t K, int64_t N, const float* X, int64_t ldx,
+                           const float* dY, int64_t ldy, float* dWdb, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -18,7 +18,7 @@ EXPORTS = ("tlp_create", "tlp_destroy", "tlp_last_error", "tlp_default_config",
            "tlp_get_params", "tlp_get_grads", "tlp_get_train_scores", "tlp_set_comm", "tlp_broadcast_state", "tlp_get_unique_id", "tlp_encode",
            "tlp_score", "tlp_train_step", "tlp_compute_grads", "tlp_lambdarank", "tlp_mse", "tlp_topk", "tlp_topk_merge",
            "tlp_search_round", "tlp_dedup", "tlp_topk_score", "tlp_normalize_labels", "tlp_sync", "tlp_launch_count", "tlp_debug_umma",
-           "tlp_debug_gemm", "tlp_ga_set_space", "tlp_ga_num_genes", "tlp_ga_batch_size", "tlp_ga_init",
+           "tlp_debug_gemm", "tlp_debug_wgrad", "tlp_ga_set_space", "tlp_ga_num_genes", "tlp_ga_batch_size", "tlp_ga_init",
            "tlp_ga_evolve", "tlp_ga_materialize", "tlp_ga_drop_duplicates", "tlp_ga_round")
 
 
@@ -92,6 +92,7 @@ def load() -> C.CDLL:
         "tlp_launch_count": (i64, [vp]),
         "tlp_debug_umma": (C.c_int, [vp, vp, vp, i32, i32, i32, vp]),
         "tlp_debug_gemm": (C.c_int, [vp, i32, i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, i32, vp]),
+        "tlp_debug_wgrad": (C.c_int, [vp, i64, i64, i64, vp, i64, vp, i64, vp, vp]),
         "tlp_ga_set_space": (C.c_int, [vp, C.POINTER(tlp_ga_space)]),
         "tlp_ga_num_genes": (i32, [vp]),
         "tlp_ga_batch_size": (C.c_int, [vp, i64, vp, vp]),

@@ -654,8 +654,38 @@ tlp_status sgemm_wgrad(tlp_ctx* ctx, int64_t M, int64_t K, int64_t N, const floa
   return TLP_OK;
 }
 
+// R52: the TMA-fed kind::tf32 weight-gradient kernel (k_tc_tma.cu) on bf16
+// contexts: one row slice per SM (J products share them), partials
+// [J][Z][K + 1][N] reduced in a fixed order.  Returns TLP_ERR_UNSUPPORTED if the
+// shapes do not fit it (nothing launched).
+static tlp_status wgrad_bias_tma(tlp_ctx* ctx, int J, int64_t M, int64_t K, int64_t N, const float* A,
+                                 int64_t lda, const float* dY, int64_t lddy, int64_t jcol,
+                                 float* const* dW, cudaStream_t s) {
+  if (ctx->cfg.precision != TLP_PREC_BF16) return TLP_ERR_UNSUPPORTED;
+  for (int j = 0; j < J; ++j)
+    if (dW[j] == nullptr) return TLP_ERR_UNSUPPORTED;
+  int Z = std::max(1, ctx->num_sms / J);
+  const int64_t kslice = cdiv(cdiv(M, Z), 32) * 32;
+  Z = (int)cdiv(M, kslice);
+  const int64_t pj = (int64_t)Z * (K + 1) * N;
+  TLP_CUDA_TRY(ctx->ws_partial.ensure((size_t)J * pj * sizeof(float)));
+  float* part = ctx->ws_partial.as<float>();
+  tlp_status st = tc_wgrad_tma(ctx, M, K, N, A, lda, dY, lddy, part, Z, kslice, true, J, jcol, s);
+  if (st != TLP_OK) return st;
+  for (int j = 0; j < J; ++j) {
+    reduce_partials<<<(unsigned)cdiv((K + 1) * N, 256), 256, 0, s>>>(part + j * pj, (K + 1) * N, Z, dW[j]);
+    TLP_LAUNCH_CHECK();
+  }
+  return TLP_OK;
+}
+
 tlp_status sgemm_wgrad_bias(tlp_ctx* ctx, int64_t M, int64_t K, int64_t N, const float* A, int64_t lda,
                             const float* dY, int64_t lddy, float* dW, float* db, cudaStream_t s) {
+  if (db == dW + K * N) {
+    float* const dws[1] = {dW};
+    const tlp_status ts = wgrad_bias_tma(ctx, 1, M, K, N, A, lda, dY, lddy, 0, dws, s);
+    if (ts != TLP_ERR_UNSUPPORTED) return ts;
+  }
   const int64_t slice = 2048;
   const int Z = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(M, slice), 256));
   const int64_t kslice = cdiv(cdiv(M, Z), BK) * BK;
@@ -681,6 +711,10 @@ tlp_status sgemm_wgrad_bias(tlp_ctx* ctx, int64_t M, int64_t K, int64_t N, const
 tlp_status sgemm_wgrad_bias_shared(tlp_ctx* ctx, int J, int64_t M, int64_t K, int64_t N, const float* A,
                                    int64_t lda, const float* dY, int64_t lddy, int64_t jcol,
                                    float* const* dW, cudaStream_t s) {
+  {
+    const tlp_status ts = wgrad_bias_tma(ctx, J, M, K, N, A, lda, dY, lddy, jcol, dW, s);
+    if (ts != TLP_ERR_UNSUPPORTED) return ts;
+  }
   const int64_t slice = 2048;
   const int Z = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(M, slice), 256));
   const int64_t kslice = cdiv(cdiv(M, Z), BK) * BK;
@@ -938,4 +972,13 @@ tlp_status simt_backward(tlp_ctx* ctx, int64_t N, const float* g, cudaStream_t s
   }
   TRY(grad_bucket_ready(ctx, 0, b_mid, s));
   return TLP_OK;
+}
+
+// ---------------------------------------------------------------- test hook
+extern "C" tlp_status tlp_debug_wgrad(tlp_ctx* ctx, int64_t M, int64_t K, int64_t N, const float* X,
+                                      int64_t ldx, const float* dY, int64_t ldy, float* dWdb,
+                                      void* stream) {
+  if (!ctx || !X || !dY || !dWdb || M < 1 || K < 1 || N < 1) return TLP_ERR_ARG;
+  return sgemm_wgrad_bias(ctx, M, K, N, X, ldx, dY, ldy, dWdb, dWdb + K * N,
+                          reinterpret_cast<cudaStream_t>(stream));
 }

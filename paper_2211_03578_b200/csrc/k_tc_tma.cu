@@ -353,6 +353,195 @@ __global__ void __launch_bounds__(THREADS, 1) tma_gemm_kernel(const __grid_const
   }
 }
 
+// ---------------------------------------------------------------- weight gradients
+// dW[Mf, Nf] (+ db = 1^T dY as row Mf) of one row slice, Mf, Nf <= 256:
+//   A = X^T (X [rows][Mf], MN-major), B = dY (dY [rows][Nf], MN-major),
+// both arriving by TMA as [32 rows x 32 cols] fp32 boxes with the 128B/32B-atom
+// swizzle -- exactly the MN-major SWIZZLE_128B_BASE32B UMMA operand layout, the
+// one kind::tf32 accepts for MN-major operands -- and consumed as
+// kind::tf32 (the tensor core reads the fp32 bits and drops the low 13
+// mantissa bits: no conversion pass, no second copy; R52).  One CTA per row
+// slice owns the whole 256 x 256 fp32 accumulator (two M = 128 halves, 512
+// TMEM columns), so X and dY are read from HBM exactly once; the bias
+// gradient is summed in fp32 on the CUDA cores from the same staged dY tiles.
+// Partials [slice][Mf + 1][Nf] leave by TMA store and are reduced in a fixed
+// order by the caller (deterministic).
+constexpr int WK = 32;                       // rows per k-block (4 tf32 k-steps)
+constexpr int WS = 3;                        // stages
+constexpr uint32_t WBOX = 32 * 32 * 4;       // one [32 x 32] fp32 box, 4 KB
+constexpr uint32_t WSTAGE = 16 * WBOX;       // X 8 boxes | dY 8 boxes = 64 KB
+constexpr uint32_t W_OFF_BAR = WS * WSTAGE;
+constexpr uint32_t W_SMEM = W_OFF_BAR + 256 + 1024;
+constexpr int W_THREADS = 192;               // warp 0 TMA, 1 MMA, 2-5 column sums + epilogue
+static_assert(W_SMEM <= 232448, "wgrad shared memory budget");
+
+struct WgradArgs {
+  int64_t R, kslice;
+  int Mf, Nf, Z;
+  int64_t cy0;                               // dY column of product j = blockIdx.x: cy0 * j
+  float* part;                               // [J][Z][Mf + 1][Nf]
+  int dbg;                                   // TLP_TMA_WGRAD_DEBUG (diagnostics)
+};
+
+template <bool COLSUM>
+__global__ void __launch_bounds__(W_THREADS, 1) tma_wgrad_kernel(const __grid_constant__ CUtensorMap mX,
+                                                                 const __grid_constant__ CUtensorMap mY,
+                                                                 const __grid_constant__ CUtensorMap mP,
+                                                                 const WgradArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t sraw = tc::smem_u32(smem_raw);
+  const uint32_t sb = (sraw + 1023u) & ~1023u;
+  uint8_t* smem = smem_raw + (sb - sraw);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int j = blockIdx.x, z = blockIdx.y;
+  const uint32_t full = sb + W_OFF_BAR, empty = full + 8 * WS, done = empty + 8 * WS;
+  uint32_t* tptr = reinterpret_cast<uint32_t*>(smem + W_OFF_BAR + 128);
+  const int64_t r0 = (int64_t)z * a.kslice;
+  const int64_t rows = std::max<int64_t>(0, std::min<int64_t>(a.kslice, a.R - r0));
+  const int nkb = (int)((rows + WK - 1) / WK);
+  const int nbx = a.Mf / 32, nby = a.Nf / 32, nmh = (a.Mf + 127) / 128;
+  const int cy = (int)(a.cy0 * j);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < WS; ++i) {
+      tc::mbar_init(full + 8 * i, 1);
+      tc::mbar_init(empty + 8 * i, COLSUM ? 5 : 1);
+    }
+    tc::mbar_init(done, 1);
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) tc::tmem_alloc(tc::smem_u32(tptr), 512);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tptr;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      for (int kb = 0; kb < nkb; ++kb) {
+        tc::mbar_wait(empty + 8 * s, ph ^ 1);
+        tc::mbar_arrive_expect_tx(full + 8 * s, (uint32_t)(nbx + nby) * WBOX);
+        const int row = (int)(r0 + (int64_t)kb * WK);
+        const uint32_t st = sb + s * WSTAGE;
+        for (int i = 0; i < nbx; ++i) tc::tma_load_2d(st + i * WBOX, &mX, 32 * i, row, full + 8 * s);
+        for (int i = 0; i < nby; ++i) tc::tma_load_2d(st + (8 + i) * WBOX, &mY, cy + 32 * i, row, full + 8 * s);
+        if (++s == WS) { s = 0; ph ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc = tc::idesc_tf32(128, (uint32_t)a.Nf, 1u, 1u);
+      int s = 0;
+      uint32_t ph = 0;
+      for (int kb = 0; kb < nkb; ++kb) {
+        tc::mbar_wait(full + 8 * s, ph);
+        tc::tc_fence_after();
+        const uint32_t st = sb + s * WSTAGE;
+#pragma unroll
+        for (int ks = 0; ks < WK / 8; ++ks) {
+          // MN-major SWIZZLE_128B_BASE32B: LBO = next 32-element MN block (next
+          // box), SBO = next 4 K rows (the 32B atom's K extent); a k-step = 8 rows
+          const uint64_t bd = tc::smem_desc_sw128_32b(st + 8 * WBOX + ks * 1024, WBOX, 512);
+          for (int mh = 0; mh < nmh; ++mh) {
+            const uint64_t ad = tc::smem_desc_sw128_32b(st + mh * 4 * WBOX + ks * 1024, WBOX, 512);
+            tc::mma_tf32(tmem + 256u * mh, ad, bd, idesc, (kb > 0 || ks > 0) ? 1u : 0u);
+          }
+        }
+        tc::mma_commit(empty + 8 * s);
+        if (++s == WS) { s = 0; ph ^= 1; }
+      }
+      tc::mma_commit(done);
+    }
+  } else {
+    // ---- warps 2..5: fp32 column sums of dY while the tiles stream, then the epilogue
+    const int et = threadIdx.x - 64;
+    float cs[2] = {0.f, 0.f};
+    if (COLSUM) {
+      int s = 0;
+      uint32_t ph = 0;
+      for (int kb = 0; kb < nkb; ++kb) {
+        tc::mbar_wait(full + 8 * s, ph);
+        const uint8_t* yb = smem + s * WSTAGE + 8 * WBOX;
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int n = et + 128 * i;
+          if (n < a.Nf) {
+            const uint8_t* box = yb + (n >> 5) * WBOX;
+            const int ch = (n & 31) >> 3, el = (n & 7) * 4;  // 32-byte chunk, byte in it
+            float acc = cs[i];
+#pragma unroll 8
+            for (int r = 0; r < WK; ++r)  // fixed order
+              acc += *reinterpret_cast<const float*>(box + r * 128 + ((ch ^ (r & 3)) << 5) + el);
+            cs[i] = acc;
+          }
+        }
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(empty + 8 * s);
+        if (++s == WS) { s = 0; ph ^= 1; }
+      }
+    }
+    const int q = warp & 3;
+    const int prow = (j * a.Z + z) * (a.Mf + 1);  // first partial row of (j, z)
+    if (nkb > 0) {
+      tc::mbar_wait(done, 0);
+      tc::tc_fence_after();
+    }
+    // staging: two 4 KB boxes per warp in the (now idle) stage 0
+    const uint32_t stg = sb + (uint32_t)(warp - 2) * 2 * WBOX;
+    uint8_t* stg_p = smem + (stg - sb);
+    int nb = 0;
+    for (int mh = 0; mh < nmh; ++mh) {
+      if (mh * 128 + 32 * q >= a.Mf) break;
+      for (int cb = 0; cb < nby; ++cb, ++nb) {
+        float v[32];
+        if (nkb > 0) {
+          tc::tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + 256u * mh + 32u * cb, v);
+          tc::tmem_wait_ld();
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = 0.f;
+        }
+        if (a.dbg == 1) {  // diagnostics: direct stores of the accumulator rows
+          float* d = a.part + (int64_t)(prow + mh * 128 + 32 * q + lane) * a.Nf + 32 * cb;
+          for (int i = 0; i < 32; ++i) d[i] = v[i];
+          continue;
+        }
+        if (a.dbg == 2) {  // diagnostics: accumulator lane / column pattern
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = (float)(1000 * (32 * q + lane) + 32 * cb + i);
+        }
+        if (lane == 0) tc::bulk_wait_read<1>();  // this staging box's previous store has read it
+        __syncwarp();
+        uint8_t* row = stg_p + (nb & 1) * WBOX + lane * 128;
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          *reinterpret_cast<float4*>(row + ((c ^ (lane & 7)) << 4)) =
+              make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+        tc::fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tc::tma_store_2d(&mP, 32 * cb, prow + mh * 128 + 32 * q, stg + (nb & 1) * WBOX);
+          tc::bulk_commit();
+        }
+      }
+    }
+    if (COLSUM) {
+      float* dst = a.part + (int64_t)(prow + a.Mf) * a.Nf;
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+        if (et + 128 * i < a.Nf) dst[et + 128 * i] = cs[i];
+    }
+    if (lane == 0) tc::bulk_wait_all();
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc::tc_fence_after();
+    tc::tmem_dealloc(tmem, 512);
+  }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -438,6 +627,40 @@ tlp_status tc_gemm_tma(tlp_ctx* ctx, int64_t M, int64_t N, int64_t K, const floa
   } else {
     TLP_SMEM_ATTR(tma_gemm_kernel<2>, SMEM_ALLOC);
     tma_gemm_kernel<2><<<grid, THREADS, SMEM_ALLOC, s>>>(mA, mI0, mI1, mO, a);
+  }
+  TLP_LAUNCH_CHECK();
+  return TLP_OK;
+}
+
+// Weight (+ bias) gradient partials of J products sharing X (dY_j = columns
+// [j cy0, j cy0 + Nf) of dY): part[j][z][Mf + colsum][Nf] for row slices of
+// kslice rows.  TLP_ERR_UNSUPPORTED (nothing launched) when the shapes or
+// alignments do not fit; the caller then uses the bf16x3 register-staged kernel.
+tlp_status tc_wgrad_tma(tlp_ctx* ctx, int64_t R, int64_t Mf, int64_t Nf, const float* X, int64_t ldx,
+                        const float* dY, int64_t ldy, float* part, int Z, int64_t kslice, bool colsum,
+                        int J, int64_t cy0, cudaStream_t s) {
+  static const char* env = getenv("TLP_TMA_WGRAD");
+  if (env && env[0] == '0') return TLP_ERR_UNSUPPORTED;
+  if (!(Mf % 32 == 0 && Mf >= 32 && Mf <= 256 && Nf % 32 == 0 && Nf >= 32 && Nf <= 256 && R > 0 &&
+        R <= (int64_t)INT32_MAX - WK && kslice % WK == 0 && Z >= 1 && J >= 1 && J <= 8))
+    return TLP_ERR_UNSUPPORTED;
+  if (!tma_ok(X, ldx) || !tma_ok(dY, ldy) || !tma_ok(part, Nf) || (J > 1 && cy0 % 4 != 0))
+    return TLP_ERR_UNSUPPORTED;
+  CUtensorMap mX, mY, mP;
+  const int64_t ycols = (J - 1) * cy0 + Nf;
+  if (!make_map(&mX, X, Mf, R, ldx, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B) ||
+      !make_map(&mY, dY, ycols, R, ldy, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B) ||
+      !make_map(&mP, part, Nf, (int64_t)J * Z * (Mf + 1), Nf, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B))
+    return TLP_ERR_UNSUPPORTED;
+  static const char* dbg = getenv("TLP_TMA_WGRAD_DEBUG");
+  WgradArgs a{R, kslice, (int)Mf, (int)Nf, Z, cy0, part, dbg ? atoi(dbg) : 0};
+  const dim3 grid((unsigned)J, (unsigned)Z);
+  if (colsum) {
+    TLP_SMEM_ATTR(tma_wgrad_kernel<true>, W_SMEM);
+    tma_wgrad_kernel<true><<<grid, W_THREADS, W_SMEM, s>>>(mX, mY, mP, a);
+  } else {
+    TLP_SMEM_ATTR(tma_wgrad_kernel<false>, W_SMEM);
+    tma_wgrad_kernel<false><<<grid, W_THREADS, W_SMEM, s>>>(mX, mY, mP, a);
   }
   TLP_LAUNCH_CHECK();
   return TLP_OK;

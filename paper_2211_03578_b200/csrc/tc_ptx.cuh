@@ -204,6 +204,22 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint
   // base offset 0, lbo mode 0, layout type [61,64) = 0: SWIZZLE_NONE
   return d;
 }
+// Swizzled variants: layout type [61,64) (sm_100 encoding: 2 = SWIZZLE_128B,
+// 1 = SWIZZLE_128B_BASE32B -- 32-byte chunks XOR (row % 4), the only swizzle a
+// kind::tf32 MN-major operand accepts: tools/tf32_sw128_probe.cu measured
+// SWIZZLE_128B tf32 MN-major operands reading as zeros), start address aligned
+// within the swizzle pattern (base offset 0).
+__device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return smem_desc(saddr, lbo, sbo) | ((uint64_t)2 << 61);
+}
+__device__ __forceinline__ uint64_t smem_desc_sw128_32b(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return smem_desc(saddr, lbo, sbo) | ((uint64_t)1 << 61);
+}
+// Instruction descriptor, kind::tf32: D fp32, A/B tf32 (fp32 bits, low 13 mantissa
+// bits ignored), a_mn / b_mn = MN-major operand.
+__host__ __device__ constexpr uint32_t idesc_tf32(uint32_t M, uint32_t N, uint32_t a_mn, uint32_t b_mn) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | (a_mn << 15) | (b_mn << 16) | ((N >> 3) << 17) | ((M >> 4) << 24);
+}
 // Instruction descriptor, kind::f16: D fp32, A/B bf16, both K-major, dense.
 __host__ __device__ constexpr uint32_t idesc_bf16(uint32_t M, uint32_t N) {
   return (1u << 4)            // [4,6)   D format: F32

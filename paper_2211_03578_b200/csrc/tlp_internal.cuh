@@ -235,6 +235,10 @@ tlp_status simt_backward(tlp_ctx* ctx, int64_t N, const float* dscores, cudaStre
 // (img = bimg_kernel's weight image); TLP_ERR_UNSUPPORTED = not applicable
 tlp_status tc_gemm_tma(tlp_ctx* ctx, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,
                        const uint8_t* img, float* C, int64_t ldc, const EpiParams& e, cudaStream_t s);
+// k_tc_tma.cu: TMA-fed kind::tf32 weight (+ bias) gradient partials, R52
+tlp_status tc_wgrad_tma(tlp_ctx* ctx, int64_t R, int64_t Mf, int64_t Nf, const float* X, int64_t ldx,
+                        const float* dY, int64_t ldy, float* part, int Z, int64_t kslice, bool colsum,
+                        int J, int64_t cy0, cudaStream_t s);
 tlp_status tc_gemm(tlp_ctx* ctx, bool ta, bool tb, int64_t M, int64_t N, int64_t K,
                    const float* A, int64_t lda, const float* B, int64_t ldb, float* C,
                    int64_t ldc, const EpiParams& e, int splits, int64_t kslice, cudaStream_t s);

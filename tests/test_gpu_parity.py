@@ -591,6 +591,34 @@ def test_train_gemm_building_block(tp, ta, tb, M, N, K, splits):
     assert rel_err(got, ref) <= 1e-4
 
 
+@pytest.mark.parametrize("M,K,N,J", [(204800, 256, 256, 1), (64000, 256, 128, 1), (64000, 128, 256, 1),
+                                     (3001, 256, 256, 1), (1775, 64, 64, 1), (70000, 256, 256, 3),
+                                     (2500, 22, 128, 1)])
+def test_wgrad_bias_building_block(tp, M, K, N, J):
+    """The weight + bias gradient of one training layer (tlp_debug_wgrad; J = 3:
+    three products sharing X, the Q/K/V case) vs fp64: dW = X^T dY within the
+    tf32 operand rounding (R52: each operand truncated to 10 mantissa bits,
+    <= 2 x 2^-10 per product), db = 1^T dY summed in fp32 (1e-5); covers ragged
+    slices, the 256 x 128 head and 128 x 256 upsample shapes, shapes the TMA
+    kernel does not take (K = 22, 64) and the bench's 204,800 rows."""
+    rng = np.random.default_rng(M + K + N)
+    X = rng.normal(size=(M, K)).astype(np.float32)
+    dY = rng.normal(size=(M, J * N)).astype(np.float32) * (rng.random((M, 1)) < 0.7)
+    m = tp.TLP(tp.TLPConfig(precision="bf16"))
+    Xd, Yd = torch.from_numpy(X).cuda(), torch.from_numpy(dY).cuda()
+    for j in range(J):
+        out = torch.zeros(K * N + N, dtype=torch.float32, device="cuda")
+        st = m.lib.tlp_debug_wgrad(m.h, M, K, N, Xd.data_ptr(), K, Yd[:, j * N:].data_ptr(), J * N,
+                                   out.data_ptr(), torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        assert st == 0
+        got = out.cpu().numpy()
+        Y = dY[:, j * N:(j + 1) * N].astype(np.float64)
+        ref_w = X.astype(np.float64).T @ Y
+        assert rel_err(got[:K * N].reshape(K, N), ref_w) <= 3e-3
+        assert rel_err(got[K * N:], Y.sum(axis=0)) <= 1e-5
+
+
 def test_bf16_scoring_needs_paper_shape(tp):
     m = tp.TLP(tp.tiny_config(precision="bf16"))  # training works at any shape
     m.set_params(np.zeros(m.num_params, np.float32))
