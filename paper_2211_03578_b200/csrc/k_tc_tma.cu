@@ -665,3 +665,9 @@ tlp_status tc_wgrad_tma(tlp_ctx* ctx, int64_t R, int64_t Mf, int64_t Nf, const f
   TLP_LAUNCH_CHECK();
   return TLP_OK;
 }
+
+bool make_tmap_f32_2d(CUtensorMap* m, const float* base, int64_t cols, int64_t rows, int64_t ld,
+                      uint32_t box_cols, uint32_t box_rows, int swizzle) {
+  if (!base || (reinterpret_cast<uintptr_t>(base) & 15) || (ld * 4) % 16 || rows < 1) return false;
+  return make_map(m, base, cols, rows, ld, box_cols, box_rows, static_cast<CUtensorMapSwizzle>(swizzle));
+}

@@ -27,6 +27,9 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t byt
       "r"(bytes)
       : "memory");
 }
+// Tight try_wait loop (no suspend-time hint): tried with CUTLASS's 0x989680
+// hint -- the parked waiters wake later than the barrier completes and the fused
+// forward slowed from 24.6 to 26.0 ms per C2 round (A/B on one box).
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   asm volatile(
       "{\n\t"

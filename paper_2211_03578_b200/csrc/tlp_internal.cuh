@@ -2,6 +2,7 @@
 // Product code: nothing here is shared with oracle/ (the CPU checker).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <stdint.h>
@@ -235,6 +236,10 @@ tlp_status simt_backward(tlp_ctx* ctx, int64_t N, const float* dscores, cudaStre
 // (img = bimg_kernel's weight image); TLP_ERR_UNSUPPORTED = not applicable
 tlp_status tc_gemm_tma(tlp_ctx* ctx, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,
                        const uint8_t* img, float* C, int64_t ldc, const EpiParams& e, cudaStream_t s);
+// k_tc_tma.cu: 2-D fp32 tensor map (row pitch ld floats, box box_rows x
+// box_cols); swizzle = CUtensorMapSwizzle value; false if it cannot be encoded
+bool make_tmap_f32_2d(CUtensorMap* m, const float* base, int64_t cols, int64_t rows, int64_t ld,
+                      uint32_t box_cols, uint32_t box_rows, int swizzle);
 // k_tc_tma.cu: TMA-fed kind::tf32 weight (+ bias) gradient partials, R52
 tlp_status tc_wgrad_tma(tlp_ctx* ctx, int64_t R, int64_t Mf, int64_t Nf, const float* X, int64_t ldx,
                         const float* dY, int64_t ldy, float* part, int Z, int64_t kslice, bool colsum,

@@ -1,0 +1,7 @@
+# A/B two library builds: forward score timing and train step, alternating
+for i in 1 2 3; do
+  for L in paper_2211_03578_b200/libtlp.so $1; do
+    echo -n "$(basename $L) "; TLP_LIB_PATH=$L timeout 120 python tools/time_fwd.py 10
+    echo -n "$(basename $L) "; TLP_LIB_PATH=$L timeout 120 python tools/time_train.py 10
+  done
+done
