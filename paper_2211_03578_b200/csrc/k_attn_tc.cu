@@ -8,12 +8,14 @@
 // dS = A (dA - rowdot) cancels to ~1e-3 of |dA| at the paper's initial scale and
 // the Wq / Wk gradients are ~1e-3 of the Wv one (measured: 53% error on Wk).
 //
-// forward:  S = Q K^T (32 MMAs), masked softmax in registers, A (probabilities,
-//           fp32) saved for the backward, O = A V (32 MMAs; A re-read from smem
-//           in the A-fragment layout)
+// forward:  one warp per (candidate, head): S = Q K^T (32 MMAs), masked softmax
+//           in registers, A (probabilities, fp32) saved for the backward,
+//           O = A V (32 MMAs; A re-read from smem in the A-fragment layout)
 // backward: dA = dO V^T, rowdot = sum_m dA A, dS = A (dA - rowdot);
 //           dQ = dS K / sqrt(d_h), dK = dS^T Q / sqrt(d_h), dV = A^T dO
-//           (5 x 32 MMAs; transposed operands are read from smem by index)
+//           (transposed operands are read from smem by index)
+// backward: one (candidate, head) per block of 4 warps, one 16 x 16 quadrant
+// each (a 4-warp forward measured slower: 344 vs 291 us per step).
 // Operands staged in smem as fp32 [32][36] (row stride 36 floats: the fragment
 // reads (4g + tig) mod 32 are bank-conflict free).
 #include "tlp_internal.cuh"
@@ -43,6 +45,57 @@ __device__ __forceinline__ void mma_tf32(float (&d)[4], uint32_t a0, uint32_t a1
       "{%0,%1,%2,%3};"
       : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+// One (candidate, head) per 4-warp block: warp w owns the 16 x 16 quadrant
+// (rows 16 (w & 1), columns 16 (w >> 1)) of every 32 x 32 product, so each
+// warp's dependent MMA chain is a quarter of the single-warp version's and
+// four times as many warps share an SM (ncu: the one-warp-per-pair kernels ran
+// at 12% / 24% occupancy, latency-bound).  Row reductions that span the two
+// column halves (softmax max / sum, the backward's rowdot) go through shared
+// memory in a fixed order (deterministic).
+// C[16 x 16 quadrant] = op(X) op(Y), k over 32 (3xTF32)
+template <bool TA, bool TB>
+__device__ __forceinline__ void gemm_q(const float* X, const float* Y, float (&c)[2][4], int mt, int nh,
+                                       int lane) {
+  const int g = lane >> 2, t = lane & 3;
+#pragma unroll
+  for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) c[nt][i] = 0.f;
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks) {
+    const int k0 = 8 * ks + t, k1 = k0 + 4;
+    const int r0 = 16 * mt + g, r1 = r0 + 8;
+    uint32_t ah[4], al[4];
+    split(TA ? X[k0 * LD + r0] : X[r0 * LD + k0], ah[0], al[0]);
+    split(TA ? X[k0 * LD + r1] : X[r1 * LD + k0], ah[1], al[1]);
+    split(TA ? X[k1 * LD + r0] : X[r0 * LD + k1], ah[2], al[2]);
+    split(TA ? X[k1 * LD + r1] : X[r1 * LD + k1], ah[3], al[3]);
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+      const int jj = 16 * nh + 8 * nt + g;
+      uint32_t bh0, bl0, bh1, bl1;
+      split(TB ? Y[jj * LD + k0] : Y[k0 * LD + jj], bh0, bl0);
+      split(TB ? Y[jj * LD + k1] : Y[k1 * LD + jj], bh1, bl1);
+      mma_tf32(c[nt], al[0], al[1], al[2], al[3], bh0, bh1);
+      mma_tf32(c[nt], ah[0], ah[1], ah[2], ah[3], bl0, bl1);
+      mma_tf32(c[nt], ah[0], ah[1], ah[2], ah[3], bh0, bh1);
+    }
+  }
+}
+
+// stage rows [0, L) of a [*, ld] fp32 matrix slice (32 columns), zero pad, with
+// the block's 128 threads (16-byte cp.async)
+__device__ __forceinline__ void stage128(float* dst, const float* src, int64_t ld, int L, int tid) {
+#pragma unroll
+  for (int i = 0; i < LP * DH / 4 / 128; ++i) {
+    const int e = tid + 128 * i, m = e >> 3, c = (e & 7) * 4;
+    const float* g = src + (int64_t)(m < L ? m : 0) * ld + c;
+    const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(dst + m * LD + c));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(g), "r"(m < L ? 16 : 0)
+                 : "memory");
+  }
 }
 
 // C[32 x 32] = op(X) op(Y): for every (m-tile, n-tile) of 16 x 8, k over 32.
@@ -188,83 +241,82 @@ __global__ void __launch_bounds__(128) attn_fwd_tc_kernel(const float* __restric
     }
 }
 
-__global__ void __launch_bounds__(64) attn_bwd_tc_kernel(const float* __restrict__ QKV,
-                                                         const float* __restrict__ Asave,
-                                                         const float* __restrict__ dO, int L, int H,
-                                                         int nh, int64_t pairs, float* __restrict__ dQKV) {
+__global__ void __launch_bounds__(128) attn_bwd_tc_kernel(const float* __restrict__ QKV,
+                                                          const float* __restrict__ Asave,
+                                                          const float* __restrict__ dO, int L, int H,
+                                                          int nh, float* __restrict__ dQKV) {
   extern __shared__ float sm[];
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t pair = (int64_t)blockIdx.x * (blockDim.x >> 5) + w;
-  if (pair >= pairs) return;
-  float* Qs = sm + w * 6 * MAT;  // Q, K, V, dO, A, dS
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  const int mt = w & 1, nhf = w >> 1;
+  float* Qs = sm;  // Q, K, V, dO, A, dS
   float* Ks = Qs + MAT;
   float* Vs = Ks + MAT;
   float* dOs = Vs + MAT;
-  float* As = dOs + MAT;  // A, then dS in place
+  float* As = dOs + MAT;
+  float* dSs = As + MAT;
+  float* red = dSs + MAT;  // [2 column halves][32 rows] partial rowdot
+  const int64_t pair = blockIdx.x;
   const int64_t n = pair / nh;
   const int hd = (int)(pair % nh);
   const int64_t row0 = n * L, ld = 3 * (int64_t)H;
-  stage(Qs, QKV + row0 * ld + hd * DH, ld, L, lane);
-  stage(Ks, QKV + row0 * ld + H + hd * DH, ld, L, lane);
-  stage(Vs, QKV + row0 * ld + 2 * H + hd * DH, ld, L, lane);
-  stage(dOs, dO + row0 * H + hd * DH, H, L, lane);
+  stage128(Qs, QKV + row0 * ld + hd * DH, ld, L, tid);
+  stage128(Ks, QKV + row0 * ld + H + hd * DH, ld, L, tid);
+  stage128(Vs, QKV + row0 * ld + 2 * H + hd * DH, ld, L, tid);
+  stage128(dOs, dO + row0 * H + hd * DH, H, L, tid);
   const float* Ab = Asave + (n * nh + hd) * (int64_t)L * L;
-  for (int e = lane; e < LP * LP; e += 32) {
+  for (int e = tid; e < LP * LP; e += 128) {
     const int l = e / LP, m = e % LP;
     As[l * LD + m] = (l < L && m < L) ? Ab[l * L + m] : 0.f;
   }
-  stage_wait();
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
   const int g = lane >> 2, t = lane & 3;
-  float c[2][4][4];
-  gemm32<false, true>(dOs, Vs, c, lane);  // dA = dO V^T
-  // dS = A (dA - rowdot), rowdot_l = sum_m dA[l,m] A[l,m]
+  float c[2][4];
+  gemm_q<false, true>(dOs, Vs, c, mt, nhf, lane);  // dA = dO V^T (quadrant: rows l, keys m)
+  // rowdot_l = sum_m dA[l,m] A[l,m]: this warp's 16 keys, then both halves in a fixed order
 #pragma unroll
-  for (int mt = 0; mt < 2; ++mt)
+  for (int half = 0; half < 2; ++half) {
+    const int l = 16 * mt + g + 8 * half;
+    float rd = 0.f;
 #pragma unroll
-    for (int half = 0; half < 2; ++half) {
-      const int l = 16 * mt + g + 8 * half;
-      float rd = 0.f;
+    for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
-      for (int nt = 0; nt < 4; ++nt)
+      for (int e = 0; e < 2; ++e) rd += c[nt][2 * half + e] * As[l * LD + 16 * nhf + 8 * nt + 2 * t + e];
+    rd += __shfl_xor_sync(0xffffffffu, rd, 1);
+    rd += __shfl_xor_sync(0xffffffffu, rd, 2);
+    if (t == 0) red[nhf * 32 + l] = rd;
+  }
+  __syncthreads();
 #pragma unroll
-        for (int e = 0; e < 2; ++e) rd += c[mt][nt][2 * half + e] * As[l * LD + 8 * nt + 2 * t + e];
-      rd += __shfl_xor_sync(0xffffffffu, rd, 1);
-      rd += __shfl_xor_sync(0xffffffffu, rd, 2);
+  for (int half = 0; half < 2; ++half) {
+    const int l = 16 * mt + g + 8 * half;
+    const float rd = red[l] + red[32 + l];
 #pragma unroll
-      for (int nt = 0; nt < 4; ++nt)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) c[mt][nt][2 * half + e] = As[l * LD + 8 * nt + 2 * t + e] * (c[mt][nt][2 * half + e] - rd);
+    for (int nt = 0; nt < 2; ++nt) {
+      const int m = 16 * nhf + 8 * nt + 2 * t;
+      const float2 a2 = *reinterpret_cast<const float2*>(As + l * LD + m);
+      *reinterpret_cast<float2*>(dSs + l * LD + m) =
+          make_float2(a2.x * (c[nt][2 * half] - rd), a2.y * (c[nt][2 * half + 1] - rd));  // dS = A (dA - rowdot)
     }
-  float* dSs = Qs + 5 * MAT;
-#pragma unroll
-  for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-    for (int half = 0; half < 2; ++half) {
-      const int l = 16 * mt + g + 8 * half;
-#pragma unroll
-      for (int nt = 0; nt < 4; ++nt)
-        *reinterpret_cast<float2*>(dSs + l * LD + 8 * nt + 2 * t) = make_float2(c[mt][nt][2 * half], c[mt][nt][2 * half + 1]);
-    }
-  __syncwarp();
+  }
+  __syncthreads();
   const float scale = 1.0f / sqrtf((float)DH);
-  auto store = [&](const float (&cc)[2][4][4], int64_t col, float f) {
+  auto store = [&](const float (&cc)[2][4], int64_t col, float f) {
 #pragma unroll
-    for (int mt = 0; mt < 2; ++mt)
+    for (int half = 0; half < 2; ++half) {
+      const int r = 16 * mt + g + 8 * half;
+      if (r >= L) continue;
 #pragma unroll
-      for (int half = 0; half < 2; ++half) {
-        const int r = 16 * mt + g + 8 * half;
-        if (r >= L) continue;
-#pragma unroll
-        for (int nt = 0; nt < 4; ++nt)
-          *reinterpret_cast<float2*>(dQKV + (row0 + r) * ld + col + 8 * nt + 2 * t) =
-              make_float2(cc[mt][nt][2 * half] * f, cc[mt][nt][2 * half + 1] * f);
-      }
+      for (int nt = 0; nt < 2; ++nt)
+        *reinterpret_cast<float2*>(dQKV + (row0 + r) * ld + col + 16 * nhf + 8 * nt + 2 * t) =
+            make_float2(cc[nt][2 * half] * f, cc[nt][2 * half + 1] * f);
+    }
   };
-  gemm32<false, false>(dSs, Ks, c, lane);  // dQ = dS K
+  gemm_q<false, false>(dSs, Ks, c, mt, nhf, lane);  // dQ = dS K
   store(c, hd * DH, scale);
-  gemm32<true, false>(dSs, Qs, c, lane);   // dK = dS^T Q
+  gemm_q<true, false>(dSs, Qs, c, mt, nhf, lane);   // dK = dS^T Q
   store(c, H + hd * DH, scale);
-  gemm32<true, false>(As, dOs, c, lane);   // dV = A^T dO
+  gemm_q<true, false>(As, dOs, c, mt, nhf, lane);   // dV = A^T dO
   store(c, 2 * H + hd * DH, 1.f);
 }
 
@@ -292,11 +344,10 @@ tlp_status attn_bwd_tc(tlp_ctx* ctx, const float* qkv, const float* A, const flo
                        float* dqkv, cudaStream_t s) {
   const tlp_config& c = ctx->cfg;
   const int64_t pairs = N * c.attn_heads;
-  const int warps = 2;
-  const size_t smem = (size_t)warps * 6 * MAT * sizeof(float);
+  if (pairs == 0) return TLP_OK;
+  const size_t smem = (6 * MAT + 64) * sizeof(float);
   TLP_SMEM_ATTR(attn_bwd_tc_kernel, smem);
-  attn_bwd_tc_kernel<<<(unsigned)cdiv(pairs, warps), warps * 32, smem, s>>>(qkv, A, dO, c.L, c.hidden,
-                                                                           c.attn_heads, pairs, dqkv);
+  attn_bwd_tc_kernel<<<(unsigned)pairs, 128, smem, s>>>(qkv, A, dO, c.L, c.hidden, c.attn_heads, dqkv);
   TLP_LAUNCH_CHECK();
   return TLP_OK;
 }
