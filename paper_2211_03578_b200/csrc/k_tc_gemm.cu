@@ -646,6 +646,17 @@ tlp_status tc_gemm(tlp_ctx* ctx, bool ta, bool tb, int64_t M, int64_t N, int64_t
     TLP_LAUNCH_CHECK();
     return TLP_OK;
   }
+  // 64 < N <= 128, row-major A: the TMA kernel (N padded to its 256-wide tile
+  // in the weight image: zero columns on a memory-bound kernel) when it applies
+  if (!ta && splits == 1 && N > 64 && N <= BN && N % 16 == 0 && K > 0 && M >= 4096) {
+    const int64_t nkb = cdiv(K, BK);
+    TLP_CUDA_TRY(ctx->ws_bimg.ensure((size_t)nkb * 2 * IMG_HALF));
+    uint8_t* img = ctx->ws_bimg.as<uint8_t>();
+    bimg_kernel<<<(unsigned)nkb, 256, 0, s>>>(B, ldb, tb ? 1 : 0, N, K, img);
+    TLP_LAUNCH_CHECK();
+    const tlp_status ts = tc_gemm_tma(ctx, M, N, K, A, lda, img, C, ldc, e, s);
+    if (ts != TLP_ERR_UNSUPPORTED) return ts;
+  }
   if (!ta && splits == 1 && N > BN && N <= BNI && K > 0) {
     TLP_SMEM_ATTR(tc_gemm_bimg_kernel, ISMEM);
     const int64_t nkb = cdiv(K, BK);

@@ -1,6 +1,6 @@
 // TMA-fed, warp-specialised, persistent tcgen05 GEMM for the dense layers of
 // bf16-context training ("the loss is back-propagated to update the
-// weights"): every forward layer and every dgrad whose output is 128 < N <= 256
+// weights"): every forward layer and every dgrad whose output is 64 < N <= 256
 // wide and whose activation operand A is row-major fp32 (the layers bench.py's
 // C3 step spends most of its time in).
 //
@@ -580,7 +580,7 @@ tlp_status tc_gemm_tma(tlp_ctx* ctx, int64_t M, int64_t N, int64_t K, const floa
                        const uint8_t* img, float* C, int64_t ldc, const EpiParams& e, cudaStream_t s) {
   static const char* env = getenv("TLP_TMA_GEMM");
   if (env && env[0] == '0') return TLP_ERR_UNSUPPORTED;
-  if (!(N > 128 && N <= TN && N % EC == 0 && K > 0 && M > 0 && M <= (int64_t)INT32_MAX - TM))
+  if (!(N > 64 && N <= TN && N % EC == 0 && K > 0 && M > 0 && M <= (int64_t)INT32_MAX - TM))
     return TLP_ERR_UNSUPPORTED;
   if (!tma_ok(A, lda) || !tma_ok(C, ldc)) return TLP_ERR_UNSUPPORTED;
   TmaArgs a{};

@@ -570,7 +570,8 @@ def test_bf16_full_size_sampled(tp, tokscale):
                                           (256, 256, 3000, 5), (200, 136, 777, 3),
                                           # ta = 0, splits = 1, 128 < N <= 256, N % 16 == 0: the
                                           # TMA-fed persistent kernel (k_tc_tma.cu), ragged M / K
-                                          (300, 256, 72, 1), (1000, 144, 256, 1), (40000, 256, 768, 1)])
+                                          (300, 256, 72, 1), (1000, 144, 256, 1), (40000, 256, 768, 1),
+                                          (5000, 128, 256, 1), (5000, 96, 128, 1)])
 def test_train_gemm_building_block(tp, ta, tb, M, N, K, splits):
     rng = np.random.default_rng(M + N + K + 10 * ta + tb)
     A = rng.normal(size=(K, M) if ta else (M, K)).astype(np.float32)
@@ -593,14 +594,14 @@ def test_train_gemm_building_block(tp, ta, tb, M, N, K, splits):
 
 @pytest.mark.parametrize("M,K,N,J", [(204800, 256, 256, 1), (64000, 256, 128, 1), (64000, 128, 256, 1),
                                      (3001, 256, 256, 1), (1775, 64, 64, 1), (70000, 256, 256, 3),
-                                     (2500, 22, 128, 1)])
+                                     (2500, 22, 128, 1), (204800, 22, 128, 1), (9000, 17, 256, 1)])
 def test_wgrad_bias_building_block(tp, M, K, N, J):
     """The weight + bias gradient of one training layer (tlp_debug_wgrad; J = 3:
     three products sharing X, the Q/K/V case) vs fp64: dW = X^T dY within the
     tf32 operand rounding (R52: each operand truncated to 10 mantissa bits,
     <= 2 x 2^-10 per product), db = 1^T dY summed in fp32 (1e-5); covers ragged
     slices, the 256 x 128 head and 128 x 256 upsample shapes, shapes the TMA
-    kernel does not take (K = 22, 64) and the bench's 204,800 rows."""
+    kernel does not take (K = 22 / 17) and the bench's 204,800 rows."""
     rng = np.random.default_rng(M + K + N)
     X = rng.normal(size=(M, K)).astype(np.float32)
     dY = rng.normal(size=(M, J * N)).astype(np.float32) * (rng.random((M, 1)) < 0.7)
