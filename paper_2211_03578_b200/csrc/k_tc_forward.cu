@@ -41,7 +41,6 @@
 #include "tc_ptx.cuh"
 
 #include <algorithm>
-#include <cstring>
 #include <array>
 #include <cmath>
 #include <vector>
@@ -118,14 +117,6 @@ struct TcArgs {
   int attn_mask;     // R42: mask padding keys (all-zero X rows)
   const float* pos;  // R43: positional table [L, 256] (16-byte aligned copy) or null
   long long* trace;  // diagnostics (TLP_TC_TRACE=1): CTA 0 epilogue phase timestamps
-  // X by TMA (x_tma): a tile's 5 x 2,200 B arrive as 11 boxes of 250 floats of
-  // a [N/10 rows x 5,500] view (10 candidates per 22,000-byte row) into the Q
-  // tile region, issued by the producer once the previous tile's attention is
-  // done (x_chunk = first weight chunk after the attention layers); tiles past
-  // x_tiles (a tail not covering a whole view row) load X with plain loads
-  int x_tma;
-  int x_chunk;
-  int64_t x_tiles;
 };
 
 // ---------------------------------------------------------------- epilogue helpers
@@ -437,8 +428,7 @@ __device__ __forceinline__ void commit(uint32_t bar) {
 }
 
 template <bool PAIR>
-__global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const __grid_constant__ CUtensorMap mX,
-                                                                 const TcArgs a) {
+__global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t sbase = tc::smem_u32(smem);
@@ -462,8 +452,6 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const __grid_co
   // the GEMM that follows starts on the first K half while the epilogue still
   // writes the second
   const uint32_t bar_opnd2 = bar_peer + 8 * NS;
-  const uint32_t bar_xfull = bar_opnd2 + 8;              // next tile's X landed (TMA tx)
-  const uint32_t bar_xfree = bar_xfull + 8;              // this tile's attention done: Q region free
   const uint32_t rank = PAIR ? cluster_rank() : 0u;      // pair: 0 = leader (issues the MMAs)
   const uint32_t E = PAIR ? 2u : 1u;                     // epilogue arrivals scale (both CTAs)
   uint32_t* tptr = reinterpret_cast<uint32_t*>(smem + OFF_TPTR);
@@ -487,8 +475,6 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const __grid_co
     for (int i = 0; i < 2; ++i) tc::mbar_init(bar_conv + 8 * i, E * kAttn);
     for (int i = 0; i < 4; ++i) tc::mbar_init(bar_attn + 8 * i, E * kAttn);
     for (int s = 0; s < NS; ++s) tc::mbar_init(bar_peer + 8 * s, 1);
-    tc::mbar_init(bar_xfull, 1);
-    tc::mbar_init(bar_xfree, kAttn);
     tc::fence_barrier_init();
   }
   if (warp == 1) {
@@ -529,22 +515,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const __grid_co
     // ------------------------------------------------ TMA producer
     if (lane == 0) {
       int stage = 0;
-      uint32_t phase = 0, xph = 0;
-      // X of tile t: 11 boxes of 250 floats at (x = (t % 2) * 2750 + 250 i, y = t / 2)
-      auto load_x = [&](int64_t t) {
-        tc::mbar_arrive_expect_tx(bar_xfull, 11 * 1000);
-        for (int i = 0; i < 11; ++i)
-          tc::tma_load_2d(sbase + OFF_Q + 1000 * i, &mX, (int)((t & 1) * 2750 + 250 * i), (int)(t >> 1), bar_xfull);
-      };
-      if (a.x_tma && it0 < n_it && tile_of(it0) < a.x_tiles) load_x(tile_of(it0));
+      uint32_t phase = 0;
       for (int64_t it = it0; it < n_it; it += it_step) {
         for (int c = 0; c < a.nchunks; ++c) {
-          if (a.x_tma && c == a.x_chunk) {
-            // the Q region is free once this tile's last attention head is done
-            tc::mbar_wait(bar_xfree, xph);
-            xph ^= 1;
-            if (it + it_step < n_it && tile_of(it + it_step) < a.x_tiles) load_x(tile_of(it + it_step));
-          }
           tc::mbar_wait(bar_empty + 8 * stage, phase ^ 1);
           const ChunkRef ch = a.chunks[c];
           // pair: this CTA's half of the chunk = rows [rank N/2, (rank+1) N/2) of the
@@ -752,19 +725,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const __grid_co
 #pragma unroll
           for (int i = 0; i < 16; ++i) pk[i] = 0;
           bool nz = false;
-          const bool xs = a.x_tma && tile < a.x_tiles;  // this tile's X is in the Q region
-          if (xs) {
-            tc::mbar_wait(bar_xfull, (uint32_t)(titer & 1));
-            if (real && n < a.N) {
-              const float2* src = reinterpret_cast<const float2*>(smem + OFF_Q + r * (kE * 4));
-#pragma unroll
-              for (int i = 0; i < kE / 2; ++i) {
-                const float2 x = src[i];
-                pk[i] = tc::pack_bf16(x.x, x.y);
-                nz |= (x.x != 0.f) | (x.y != 0.f);
-              }
-            }
-          } else if (real && n < a.N) {
+          if (real && n < a.N) {
             const float2* src = reinterpret_cast<const float2*>(a.X + (tile * kCand * kL + r) * kE);
 #pragma unroll
             for (int i = 0; i < kE / 2; ++i) {
@@ -856,10 +817,6 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const __grid_co
           tc::fence_proxy_async_smem();                   // O_j ready
           tc::tc_fence_before();
           arrive_mma(bar_attn + 8 * (j & 3));
-          if (a.x_tma && l == NA - 1 && j == kHeads - 1) {  // last head: Q region free for the next X
-            __syncwarp();
-            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], 32;" ::"r"(bar_xfree) : "memory");
-          }
           tr();
         }
         if (rowwise) {
@@ -964,7 +921,6 @@ struct TcWeights {
   TcArgs slots{};                                  // offsets into `vec`
   uint32_t smem = 0;
   float* pos = nullptr;                            // R43: aligned copy of the positional table
-  int x_chunk = 0;                                 // first weight chunk after the attention layers
 };
 
 bool tc_supported(const tlp_config& c) {
@@ -974,7 +930,7 @@ bool tc_supported(const tlp_config& c) {
 }
 
 // The weight chunks in the exact order tc_forward_kernel's MMA issuer consumes them.
-static std::vector<PackChunk> build_schedule(const tlp_ctx* ctx, int& x_chunk_index) {
+static std::vector<PackChunk> build_schedule(const tlp_ctx* ctx) {
   const tlp_config& c = ctx->cfg;
   const ParamOffsets& o = ctx->off;
   std::vector<PackChunk> v;
@@ -1004,7 +960,6 @@ static std::vector<PackChunk> build_schedule(const tlp_ctx* ctx, int& x_chunk_in
       add(256, 32, kDH * j, kH, {{0, o.Wo[l], kH, 0}});     // oproj_j once O_j is ready
     }
   }
-  x_chunk_index = (int)v.size();  // the first chunk after the attention layers
   for (int r = 0; r < c.n_res; ++r) {
     for (int k0 = 0; k0 < kH; k0 += 64) add(128, 64, k0, kH, {{0, o.Wa[r], kH, 0}});    // G1 half 0
     for (int k0 = 0; k0 < kH; k0 += 64) add(128, 64, k0, kH, {{0, o.Wa[r], kH, 128}});  // G1 half 1
@@ -1020,7 +975,7 @@ tlp_status tc_prepare(tlp_ctx* ctx, cudaStream_t s) {
   if (!ctx->tc) {
     ctx->tc = new TcWeights();
     TcWeights& w = *ctx->tc;
-    w.host = build_schedule(ctx, w.x_chunk);
+    w.host = build_schedule(ctx);
     w.nchunks = (int)w.host.size();
     w.bytes = w.host.back().dst + (size_t)w.host.back().N * w.host.back().Kc * 2;
     std::vector<ChunkRef> refs(w.nchunks);
@@ -1095,16 +1050,6 @@ tlp_status tc_forward(tlp_ctx* ctx, const float* feats, int64_t N, float* scores
   a.pos = ctx->cfg.pos_enc ? w.pos : nullptr;
   a.n_attn = c.n_attn; a.n_res = c.n_res; a.n_tasks = c.n_tasks;
   a.attn_mask = c.attn_mask;
-  // X by TMA: a [N/10, 5,500] fp32 view (22,000-byte rows: 16-byte multiples)
-  CUtensorMap mX;
-  std::memset(&mX, 0, sizeof(mX));
-  static const char* xe = getenv("TLP_TC_XTMA");
-  a.x_tma = 0;
-  a.x_chunk = w.x_chunk;
-  a.x_tiles = (N / 10) * 2;
-  if (!(xe && xe[0] == '0') && c.n_attn > 0 && a.x_tiles > 0 &&
-      make_tmap_f32_2d(&mX, feats, 5500, N / 10, 5500, 250, 1, 0))
-    a.x_tma = 1;
   // Experimental (TLP_TC_PAIR=1): cluster pairs with tcgen05 cta_group::2 -- one
   // M = 256 MMA stream per pair of SMs, each SM on its own tile.  Correct (the
   // parity tests pass in this mode) but slower today: the two tiles advance in
@@ -1135,10 +1080,9 @@ tlp_status tc_forward(tlp_ctx* ctx, const float* feats, int64_t N, float* scores
     at[0].val.clusterDim.x = 2; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    a.x_tma = 0;  // pair mode keeps plain X loads
-    TLP_CUDA_TRY(cudaLaunchKernelEx(&cfg, tc_forward_kernel<true>, mX, a));
+    TLP_CUDA_TRY(cudaLaunchKernelEx(&cfg, tc_forward_kernel<true>, a));
   } else {
-    tc_forward_kernel<false><<<grid, kThreads, w.smem, s>>>(mX, a);
+    tc_forward_kernel<false><<<grid, kThreads, w.smem, s>>>(a);
   }
   TLP_LAUNCH_CHECK();
   if (trace) {

@@ -41,11 +41,17 @@ def launches(tag: str):
     data = rows[start + 1:]
     agg, cnt = collections.OrderedDict(), collections.Counter()
     # the bench does 3 warm-up steps + 1 timed step (+ the e2e passes); take
-    # the launches of the last training/scoring step: the 4th tc_forward onward
+    # the launches of the timed step: from the encode (resolve_tokens /
+    # encode_*) that starts the round of the 4th tc_forward to the launch
+    # before the next step's encode -- the round (encode, fused forward, top-k)
+    # and the training step that follows it
     fwd = [i for i, r in enumerate(data) if "tc_forward_kernel" in r[ik]]
-    lo = fwd[3] if len(fwd) > 3 else 0
-    hi = fwd[4] if len(fwd) > 4 else len(data)
-    # extend to the end of the training step that follows the 4th round
+    k4 = fwd[3] if len(fwd) > 3 else (fwd[-1] if fwd else 0)
+    starts = [i for i, r in enumerate(data) if "resolve_tokens" in r[ik] or "encode_" in r[ik]]
+    lo = max([i for i in starts if i < k4] or [0])
+    while lo > 0 and ("resolve_tokens" in data[lo - 1][ik]):
+        lo -= 1
+    hi = min([i for i in starts if i > k4] or [len(data)])
     for r in data[lo:hi]:
         k = short(r[ik])
         agg[k] = agg.get(k, 0.0) + float(r[iv].replace(",", ""))
