@@ -54,8 +54,8 @@ __device__ __forceinline__ void mma_tf32(float (&d)[4], uint32_t a0, uint32_t a1
 // at 12% / 24% occupancy, latency-bound).  Row reductions that span the two
 // column halves (softmax max / sum, the backward's rowdot) go through shared
 // memory in a fixed order (deterministic).
-// C[16 x 16 quadrant] = op(X) op(Y), k over 32 (3xTF32)
-template <bool TA, bool TB>
+// C[16 x 16 quadrant] = op(X) op(Y), k over 32: 3xTF32 (SPLIT) or plain tf32
+template <bool TA, bool TB, bool SPLIT = true>
 __device__ __forceinline__ void gemm_q(const float* X, const float* Y, float (&c)[2][4], int mt, int nh,
                                        int lane) {
   const int g = lane >> 2, t = lane & 3;
@@ -68,19 +68,27 @@ __device__ __forceinline__ void gemm_q(const float* X, const float* Y, float (&c
     const int k0 = 8 * ks + t, k1 = k0 + 4;
     const int r0 = 16 * mt + g, r1 = r0 + 8;
     uint32_t ah[4], al[4];
-    split(TA ? X[k0 * LD + r0] : X[r0 * LD + k0], ah[0], al[0]);
-    split(TA ? X[k0 * LD + r1] : X[r1 * LD + k0], ah[1], al[1]);
-    split(TA ? X[k1 * LD + r0] : X[r0 * LD + k1], ah[2], al[2]);
-    split(TA ? X[k1 * LD + r1] : X[r1 * LD + k1], ah[3], al[3]);
+    const float x0 = TA ? X[k0 * LD + r0] : X[r0 * LD + k0], x1 = TA ? X[k0 * LD + r1] : X[r1 * LD + k0];
+    const float x2 = TA ? X[k1 * LD + r0] : X[r0 * LD + k1], x3 = TA ? X[k1 * LD + r1] : X[r1 * LD + k1];
+    if (SPLIT) {
+      split(x0, ah[0], al[0]); split(x1, ah[1], al[1]); split(x2, ah[2], al[2]); split(x3, ah[3], al[3]);
+    } else {
+      ah[0] = tf32(x0); ah[1] = tf32(x1); ah[2] = tf32(x2); ah[3] = tf32(x3);
+    }
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt) {
       const int jj = 16 * nh + 8 * nt + g;
-      uint32_t bh0, bl0, bh1, bl1;
-      split(TB ? Y[jj * LD + k0] : Y[k0 * LD + jj], bh0, bl0);
-      split(TB ? Y[jj * LD + k1] : Y[k1 * LD + jj], bh1, bl1);
-      mma_tf32(c[nt], al[0], al[1], al[2], al[3], bh0, bh1);
-      mma_tf32(c[nt], ah[0], ah[1], ah[2], ah[3], bl0, bl1);
-      mma_tf32(c[nt], ah[0], ah[1], ah[2], ah[3], bh0, bh1);
+      const float y0 = TB ? Y[jj * LD + k0] : Y[k0 * LD + jj], y1 = TB ? Y[jj * LD + k1] : Y[k1 * LD + jj];
+      if (SPLIT) {
+        uint32_t bh0, bl0, bh1, bl1;
+        split(y0, bh0, bl0);
+        split(y1, bh1, bl1);
+        mma_tf32(c[nt], al[0], al[1], al[2], al[3], bh0, bh1);
+        mma_tf32(c[nt], ah[0], ah[1], ah[2], ah[3], bl0, bl1);
+        mma_tf32(c[nt], ah[0], ah[1], ah[2], ah[3], bh0, bh1);
+      } else {
+        mma_tf32(c[nt], ah[0], ah[1], ah[2], ah[3], tf32(y0), tf32(y1));
+      }
     }
   }
 }
@@ -312,11 +320,13 @@ __global__ void __launch_bounds__(128) attn_bwd_tc_kernel(const float* __restric
             make_float2(cc[nt][2 * half] * f, cc[nt][2 * half + 1] * f);
     }
   };
-  gemm_q<false, false>(dSs, Ks, c, mt, nhf, lane);  // dQ = dS K
+  // dQ, dK, dV in plain tf32 (R53): no cancellation downstream of dS, and their
+  // weight gradients are tf32 products anyway (R52); only dA keeps 3xTF32
+  gemm_q<false, false, false>(dSs, Ks, c, mt, nhf, lane);  // dQ = dS K
   store(c, hd * DH, scale);
-  gemm_q<true, false>(dSs, Qs, c, mt, nhf, lane);   // dK = dS^T Q
+  gemm_q<true, false, false>(dSs, Qs, c, mt, nhf, lane);   // dK = dS^T Q
   store(c, H + hd * DH, scale);
-  gemm_q<true, false>(As, dOs, c, mt, nhf, lane);   // dV = A^T dO
+  gemm_q<true, false, false>(As, dOs, c, mt, nhf, lane);   // dV = A^T dO
   store(c, 2 * H + hd * DH, 1.f);
 }
 
