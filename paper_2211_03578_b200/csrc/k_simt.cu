@@ -146,7 +146,8 @@ __global__ void __launch_bounds__(256) sgemm_kernel(int64_t M, int64_t N, int64_
   }
 }
 
-// out[j] = sum_z part[z][j], fixed order.
+// out[j] = sum_z part[z][j], fixed order.  (A float4 variant with a quarter of
+// the threads measured slower: 249 vs 142 us per step -- fewer loads in flight.)
 __global__ void reduce_partials(const float* __restrict__ part, int64_t n, int Z,
                                 float* __restrict__ out) {
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;

@@ -332,12 +332,14 @@ constexpr uint32_t IMG_HALF = BNI * BK * 2;                       // 16 KB
 constexpr uint32_t ISTAGE = 2 * (BM * BK * 2) + 2 * IMG_HALF;     // A hi | A lo | B hi | B lo = 48 KB
 constexpr uint32_t ISMEM = STAGES * ISTAGE + 128;
 
+// blockIdx.x = k-block, blockIdx.y = 32-row group of n (8 per 256): 8x the
+// CTAs of one block per k-block (the image is launch-latency bound)
 __global__ void bimg_kernel(const float* __restrict__ B, int64_t ldb, int tb, int64_t N, int64_t K,
                             uint8_t* __restrict__ img) {
   const int64_t kb = blockIdx.x;
   uint8_t* dst = img + kb * 2 * IMG_HALF;
-  for (int e = threadIdx.x; e < BNI * BK; e += blockDim.x) {
-    const int n = e / BK, k = e % BK;
+  for (int e = threadIdx.x; e < 32 * BK; e += blockDim.x) {
+    const int n = 32 * (int)blockIdx.y + e / BK, k = e % BK;
     const int64_t gk = kb * BK + k;
     float x = 0.f;
     if (n < N && gk < K) x = tb ? B[(int64_t)n * ldb + gk] : B[gk * ldb + n];
@@ -652,7 +654,7 @@ tlp_status tc_gemm(tlp_ctx* ctx, bool ta, bool tb, int64_t M, int64_t N, int64_t
     const int64_t nkb = cdiv(K, BK);
     TLP_CUDA_TRY(ctx->ws_bimg.ensure((size_t)nkb * 2 * IMG_HALF));
     uint8_t* img = ctx->ws_bimg.as<uint8_t>();
-    bimg_kernel<<<(unsigned)nkb, 256, 0, s>>>(B, ldb, tb ? 1 : 0, N, K, img);
+    bimg_kernel<<<dim3((unsigned)nkb, BNI / 32), 256, 0, s>>>(B, ldb, tb ? 1 : 0, N, K, img);
     TLP_LAUNCH_CHECK();
     const tlp_status ts = tc_gemm_tma(ctx, M, N, K, A, lda, img, C, ldc, e, s);
     if (ts != TLP_ERR_UNSUPPORTED) return ts;
@@ -662,7 +664,7 @@ tlp_status tc_gemm(tlp_ctx* ctx, bool ta, bool tb, int64_t M, int64_t N, int64_t
     const int64_t nkb = cdiv(K, BK);
     TLP_CUDA_TRY(ctx->ws_bimg.ensure((size_t)nkb * 2 * IMG_HALF));
     uint8_t* img = ctx->ws_bimg.as<uint8_t>();
-    bimg_kernel<<<(unsigned)nkb, 256, 0, s>>>(B, ldb, tb ? 1 : 0, N, K, img);
+    bimg_kernel<<<dim3((unsigned)nkb, BNI / 32), 256, 0, s>>>(B, ldb, tb ? 1 : 0, N, K, img);
     TLP_LAUNCH_CHECK();
     // the TMA-fed persistent kernel (k_tc_tma.cu) when the operands allow it
     const tlp_status ts = tc_gemm_tma(ctx, M, N, K, A, lda, img, C, ldc, e, s);
