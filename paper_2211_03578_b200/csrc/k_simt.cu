@@ -157,6 +157,35 @@ __global__ void reduce_partials(const float* __restrict__ part, int64_t n, int Z
   out[j] = s;
 }
 
+// X [M, E] -> [M, 32] with zero columns E..31 (16-byte rows for TMA)
+__global__ void pad_cols_kernel(const float* __restrict__ X, int64_t M, int E, float* __restrict__ out) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= M * 32) return;
+  const int64_t r = e >> 5;
+  const int c = (int)(e & 31);
+  out[e] = c < E ? X[r * E + c] : 0.f;
+}
+
+// The padded first layer's weight + bias partials [Z][Kpad + 1][N] -> the R24
+// (W [Kreal][N], b [N]) pair (contiguous at out): rows >= Kreal of W are the
+// zero padding and are dropped; the bias is partial row Kpad.  Fixed order.
+// One warp per output (few outputs, many partials): lane-strided partial sums
+// combined by a fixed butterfly (deterministic).
+__global__ void reduce_partials_pad(const float* __restrict__ part, int Kreal, int Kpad, int N, int Z,
+                                    float* __restrict__ out) {
+  const int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (j >= (int64_t)(Kreal + 1) * N) return;
+  const int row = (int)(j / N), col = (int)(j % N);
+  const int srow = row < Kreal ? row : Kpad;
+  const int64_t stride = (int64_t)(Kpad + 1) * N;
+  float s = 0.f;
+  for (int z = lane; z < Z; z += 32) s += part[z * stride + (int64_t)srow * N + col];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) out[j] = s;
+}
+
 // Same sum for few outputs and many partials (column sums): one warp per
 // output, lane-strided partial sums combined by a fixed butterfly
 // (deterministic for given n, Z).
@@ -409,7 +438,20 @@ __global__ void head_pool_kernel(const float* __restrict__ U, int L, int hd, int
 // dU[n*L+l, k] = g[n,t] * w2[k] * (U > 0)
 __global__ void head_bwd_kernel(const float* __restrict__ U, int L, int hd, int64_t N,
                                 const float* __restrict__ w2, const float* __restrict__ g, int t,
-                                int nt, float* __restrict__ dU) {
+                                int nt, float* __restrict__ dU, int vec) {
+  if (vec) {  // float4 per thread, one row-segment: 32-bit row index, no 64-bit division
+    const int q = hd >> 2;
+    const int64_t e4 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e4 >= N * L * q) return;
+    const int64_t row = e4 / q;
+    const int k = (int)(e4 - row * q) * 4;
+    const float gn = __ldg(g + (row / L) * nt + t);
+    const float4 u = __ldg(reinterpret_cast<const float4*>(U) + e4);
+    const float4 w = __ldg(reinterpret_cast<const float4*>(w2 + k));
+    reinterpret_cast<float4*>(dU)[e4] = make_float4(u.x > 0.f ? gn * w.x : 0.f, u.y > 0.f ? gn * w.y : 0.f,
+                                                    u.z > 0.f ? gn * w.z : 0.f, u.w > 0.f ? gn * w.w : 0.f);
+    return;
+  }
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= N * L * hd) return;
   const int k = (int)(e % hd);
@@ -506,6 +548,7 @@ struct ActLayout {
   int64_t U[TLP_MAX_TASKS], pooled[TLP_MAX_TASKS];
   int64_t kvalid;  // R42 key-validity flags (attn_mask)
   int64_t hpos;    // R43 upsample output + positional table (pos_enc)
+  int64_t xpad;    // X padded to 32 columns (bf16 training: 16-byte rows for TMA), or -1
   // backward scratch
   int64_t dh, dtmp, dqkv, dU;
   int64_t total_fwd, total;
@@ -534,6 +577,7 @@ ActLayout act_layout(const tlp_config& c, int64_t N) {
   for (int t = 0; t < c.n_tasks; ++t) { a.U[t] = take(M * c.head_dim); a.pooled[t] = take(N * c.head_dim); }
   a.kvalid = take(M);
   a.hpos = take(M * H);
+  a.xpad = (c.precision == TLP_PREC_BF16 && c.E % 4 != 0 && c.E <= 32) ? take(M * 32) : -1;
   a.total_fwd = o;
   a.dh = take(M * H);
   a.dtmp = take(M * std::max<int64_t>(H, c.up_dims[0]));
@@ -680,6 +724,26 @@ static tlp_status wgrad_bias_tma(tlp_ctx* ctx, int J, int64_t M, int64_t K, int6
   return TLP_OK;
 }
 
+// The first layer's weight + bias gradient from the padded X [M, 32] (bf16
+// contexts, E <= 32): the TMA tf32 wgrad kernel over Kpad = 32 columns, then
+// reduce_partials_pad into W [Kreal][N] | b [N] (R52).  Falls back to the
+// generic path on the original X if the kernel does not apply.
+static tlp_status wgrad_bias_padded(tlp_ctx* ctx, int64_t M, int64_t Kreal, int64_t N, const float* X32,
+                                    const float* dY, float* dWdb, cudaStream_t s) {
+  int Z = std::max(1, ctx->num_sms);
+  const int64_t kslice = cdiv(cdiv(M, Z), 32) * 32;
+  Z = (int)cdiv(M, kslice);
+  TLP_CUDA_TRY(ctx->ws_partial.ensure((size_t)Z * 33 * N * sizeof(float)));
+  float* part = ctx->ws_partial.as<float>();
+  tlp_status st = tc_wgrad_tma(ctx, M, 32, N, X32, 32, dY, N, part, Z, kslice, true, 1, 0, s);
+  if (st == TLP_ERR_UNSUPPORTED)
+    return sgemm_wgrad_bias(ctx, M, Kreal, N, ctx->train_X, Kreal, dY, N, dWdb, dWdb + Kreal * N, s);
+  if (st != TLP_OK) return st;
+  reduce_partials_pad<<<(unsigned)cdiv((Kreal + 1) * N * 32, 256), 256, 0, s>>>(part, (int)Kreal, 32, (int)N, Z, dWdb);
+  TLP_LAUNCH_CHECK();
+  return TLP_OK;
+}
+
 tlp_status sgemm_wgrad_bias(tlp_ctx* ctx, int64_t M, int64_t K, int64_t N, const float* A, int64_t lda,
                             const float* dY, int64_t lddy, float* dW, float* db, cudaStream_t s) {
   if (db == dW + K * N) {
@@ -777,13 +841,23 @@ tlp_status simt_forward(tlp_ctx* ctx, const float* X, int64_t N, float* scores, 
       TLP_LAUNCH_CHECK();
       kvalid = W + lay.kvalid;
     }
-    int64_t din = c.E;
+    int64_t din = c.E, ldh = c.E;
+    if (save && lay.xpad >= 0) {
+      // E = 22 rows are 88 bytes, which TMA cannot address: one padded copy
+      // [M, 32] (zero columns E..31) feeds the first layer's TMA GEMM here and
+      // its weight gradient in the backward
+      pad_cols_kernel<<<(unsigned)cdiv(M * 32, 256), 256, 0, s>>>(h, M, c.E, W + lay.xpad);
+      TLP_LAUNCH_CHECK();
+      h = W + lay.xpad;
+      ldh = 32;
+    }
     for (int i = 0; i < c.n_up; ++i) {
       EpiParams e; e.bias = P + o.up_b[i]; e.relu = true;
-      TRY(sgemm(ctx, false, false, M, c.up_dims[i], din, h, din, P + o.up_W[i], c.up_dims[i],
+      TRY(sgemm(ctx, false, false, M, c.up_dims[i], din, h, ldh, P + o.up_W[i], c.up_dims[i],
                 W + lay.up[i], c.up_dims[i], e, s));
       h = W + lay.up[i];
       din = c.up_dims[i];
+      ldh = din;
     }
     if (c.pos_enc) {  // R43
       add_pos_kernel<<<(unsigned)cdiv(M * H, 256), 256, 0, s>>>(h, P + o.pos, M, c.L, (int)H, W + lay.hpos);
@@ -862,8 +936,11 @@ tlp_status simt_backward(tlp_ctx* ctx, int64_t N, const float* g, cudaStream_t s
                     : (c.n_attn ? W + lay.hattn[c.n_attn - 1] : (c.pos_enc ? W + lay.hpos : W + lay.up[c.n_up - 1]));
   // heads
   for (int t = 0; t < c.n_tasks; ++t) {
-    head_bwd_kernel<<<(unsigned)cdiv(M * hd, 256), 256, 0, s>>>(W + lay.U[t], c.L, hd, N,
-                                                                P + o.w2[t], g, t, c.n_tasks, dU);
+    // (the float4 path needs 16-byte aligned U / dU / w2: act_layout slots are
+    // 64-float aligned; w2's flat offset may not be)
+    const bool v4 = hd % 4 == 0 && (reinterpret_cast<uintptr_t>(P + o.w2[t]) & 15) == 0;
+    head_bwd_kernel<<<(unsigned)cdiv(v4 ? M * hd / 4 : M * hd, 256), 256, 0, s>>>(
+        W + lay.U[t], c.L, hd, N, P + o.w2[t], g, t, c.n_tasks, dU, v4 ? 1 : 0);
     TLP_LAUNCH_CHECK();
     TRY(sgemm_wgrad_bias(ctx, M, H, hd, hfin, H, dU, hd, G + o.W1[t], G + o.c1[t], s));
     TRY(sgemm_wgrad(ctx, N, hd, 1, W + lay.pooled[t], hd, g + t, c.n_tasks, G + o.w2[t], s));
@@ -961,7 +1038,11 @@ tlp_status simt_backward(tlp_ctx* ctx, int64_t N, const float* g, cudaStream_t s
       TLP_LAUNCH_CHECK();
     }
     const float* xin = i > 0 ? W + lay.up[i - 1] : ctx->train_X;
-    TRY(sgemm_wgrad_bias(ctx, M, din, w, xin, din, cur, w, G + o.up_W[i], G + o.up_b[i], s));
+    if (i == 0 && lay.xpad >= 0) {
+      TRY(wgrad_bias_padded(ctx, M, din, w, W + lay.xpad, cur, G + o.up_W[i], s));
+    } else {
+      TRY(sgemm_wgrad_bias(ctx, M, din, w, xin, din, cur, w, G + o.up_W[i], G + o.up_b[i], s));
+    }
     if (i > 0) {
       float* nxt = (cur == dh) ? dtmp : dh;
       EpiParams e0;  // the next layer's ReLU' rides in this dgrad's epilogue
