@@ -192,6 +192,128 @@ __global__ void __launch_bounds__(kRankThreads) rank_kernel(const float* __restr
   if (threadIdx.x == 0) loss_part[(int64_t)t * gridDim.x + g] = L;
 }
 
+// Split version (default): each (group, task) is spread over kRankSplit CTAs
+// (one CTA per group left 132 of 148 SMs idle on the C3 step).  Pass 1: every
+// CTA ranks its slice of the items against the whole group (R17) and writes
+// 1/log2(1 + rank) plus its partial ideal DCG; pass 2: every CTA sums the
+// partials in a fixed order (maxDCG), and runs the pair loop for its slice.
+// Same per-item arithmetic and order as rank_kernel (deterministic).
+constexpr int kRankSplit = 8;
+
+__device__ __forceinline__ void slice_of(int n, int sub, int& i0, int& i1) {
+  const int per = (n + kRankSplit - 1) / kRankSplit;
+  i0 = min(n, sub * per);
+  i1 = min(n, i0 + per);
+}
+
+__global__ void __launch_bounds__(kRankThreads) rank_prep_kernel(const float* __restrict__ scores,
+                                                             const float* __restrict__ labels,
+                                                             const int64_t* __restrict__ goff, int nt,
+                                                             float* __restrict__ iD_out,
+                                                             float* __restrict__ dcg_part) {
+  extern __shared__ float sm[];
+  __shared__ float red[32];
+  const int g = blockIdx.x / kRankSplit, sub = blockIdx.x % kRankSplit, t = blockIdx.y;
+  const int64_t lo = goff[g], hi = goff[g + 1];
+  const int cap = (int)(hi - lo);
+  float* s = sm;
+  float* y = s + cap;
+  int* idx = reinterpret_cast<int*>(y + cap);
+  const int n = gather_present(scores, labels, lo, hi, t, nt, s, y, idx);
+  int i0, i1;
+  slice_of(n, sub, i0, i1);
+  const int half = threadIdx.x & 1, nth = blockDim.x >> 1;
+  const int jm = n / 2, j0 = half ? jm : 0, j1 = half ? n : jm;
+  float dcg = 0.f;
+  for (int base = i0; base < i1; base += nth) {
+    const int i = base + (threadIdx.x >> 1);
+    const bool act = i < i1;
+    const float si = act ? s[i] : 0.f, yi = act ? y[i] : 0.f;
+    int rs = 0, ry = 0;
+    if (act) {
+      for (int j = j0; j < j1; ++j) {
+        const float sj = s[j], yj = y[j];
+        rs += (sj > si) || (sj == si && j < i);
+        ry += (yj > yi) || (yj == yi && j < i);
+      }
+    }
+    rs += __shfl_xor_sync(0xffffffffu, rs, 1);
+    ry += __shfl_xor_sync(0xffffffffu, ry, 1);
+    if (act && half == 0) {
+      iD_out[(int64_t)t * goff[gridDim.x / kRankSplit] + lo + i] = 1.0f / log2f(2.0f + (float)rs);
+      dcg += expm1f(yi * kLn2) / log2f(2.0f + (float)ry);
+    }
+  }
+  const float d = block_sum(dcg, red);
+  if (threadIdx.x == 0) dcg_part[((int64_t)t * (gridDim.x / kRankSplit) + g) * kRankSplit + sub] = d;
+}
+
+__global__ void __launch_bounds__(kRankThreads) rank_pair_kernel(const float* __restrict__ scores,
+                                                             const float* __restrict__ labels,
+                                                             const int64_t* __restrict__ goff, int nt,
+                                                             const float* __restrict__ iD_in,
+                                                             const float* __restrict__ dcg_part,
+                                                             float* __restrict__ loss_part,
+                                                             float* __restrict__ dscores) {
+  extern __shared__ float sm[];
+  __shared__ float red[32];
+  const int G = gridDim.x / kRankSplit;
+  const int g = blockIdx.x / kRankSplit, sub = blockIdx.x % kRankSplit, t = blockIdx.y;
+  const int64_t lo = goff[g], hi = goff[g + 1];
+  const int cap = (int)(hi - lo);
+  float* s = sm;
+  float* y = s + cap;
+  float* Gs = y + cap;
+  float* iD = Gs + cap;
+  int* idx = reinterpret_cast<int*>(iD + cap);
+  const int n = gather_present(scores, labels, lo, hi, t, nt, s, y, idx);
+  float dsum = 0.f;
+  for (int k = 0; k < kRankSplit; ++k) dsum += dcg_part[((int64_t)t * G + g) * kRankSplit + k];  // fixed order
+  const float maxdcg = fmaxf(dsum, 1e-10f);
+  const float* iDg = iD_in + (int64_t)t * goff[G] + lo;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    Gs[i] = expm1f(y[i] * kLn2) / maxdcg;
+    iD[i] = iDg[i];
+  }
+  __syncthreads();
+  int i0, i1;
+  slice_of(n, sub, i0, i1);
+  const int half = threadIdx.x & 1, nth = blockDim.x >> 1;
+  const int jm = n / 2, j0 = half ? jm : 0, j1 = half ? n : jm;
+  float lsum = 0.f;
+  for (int base = i0; base < i1; base += nth) {
+    const int i = base + (threadIdx.x >> 1);
+    const bool act = i < i1;
+    float gi = 0.f, li = 0.f;
+    if (act) {
+      const float si = s[i], yi = y[i], Gi = Gs[i], iDi = iD[i];
+      for (int j = j0; j < j1; ++j) {
+        const float yj = y[j];
+        if (yi == yj) continue;
+        const float w = fabsf(Gi - Gs[j]) * fabsf(iDi - iD[j]);
+        const float z = (yi > yj) ? (si - s[j]) : (s[j] - si);
+        const float e = expf(-fabsf(z));
+        const float r = __frcp_rn(1.0f + e);
+        const float sig = (z >= 0.f) ? e * r : r;
+        if (yi > yj) {
+          li += w * (fmaxf(-z, 0.f) + log1pf(e));
+          gi -= w * sig;
+        } else {
+          gi += w * sig;
+        }
+      }
+    }
+    gi += __shfl_xor_sync(0xffffffffu, gi, 1);
+    li += __shfl_xor_sync(0xffffffffu, li, 1);
+    if (act && half == 0) {
+      dscores[(lo + idx[i]) * nt + t] = gi * kInvLn2;
+      lsum += li * kInvLn2;
+    }
+  }
+  const float L = block_sum(lsum, red);
+  if (threadIdx.x == 0) loss_part[(int64_t)t * gridDim.x + blockIdx.x] = L;
+}
+
 __global__ void finalize_rank(const float* __restrict__ loss_part, int G, int nt,
                               const double* __restrict__ counts, float* __restrict__ dscores,
                               int64_t B, float* __restrict__ loss_out, uint32_t* err) {
@@ -305,7 +427,7 @@ tlp_status mse_loss_grad(tlp_ctx* ctx, const float* scores, const float* labels,
 }
 
 static size_t rank_ws_bytes(int G, int nt) {
-  return (size_t)G * nt * (sizeof(double) + sizeof(float)) + 64;
+  return (size_t)G * nt * (sizeof(double) + (1 + 2 * kRankSplit) * sizeof(float)) + 64;
 }
 
 tlp_status rank_pair_counts(tlp_ctx* ctx, const float* labels, const int64_t* d_goff, int G,
@@ -331,11 +453,30 @@ tlp_status rank_loss_grad(tlp_ctx* ctx, const float* scores, const float* labels
   float* loss_part = reinterpret_cast<float*>(ctx->ws_rank.as<char>() + (size_t)G * nt * sizeof(double));
   TLP_CUDA_TRY(cudaMemsetAsync(dscores, 0, (size_t)B * nt * sizeof(float), s));
   const size_t smem = (size_t)max_group * (4 * sizeof(float) + sizeof(int));
-  cudaFuncSetAttribute(rank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  rank_kernel<<<dim3(G, nt), kRankThreads, smem, s>>>(scores, labels, d_goff, nt, loss_part, dscores);
+  static const char* env = getenv("TLP_RANK_SPLIT");
+  if (env && env[0] == '0') {
+    cudaFuncSetAttribute(rank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    rank_kernel<<<dim3(G, nt), kRankThreads, smem, s>>>(scores, labels, d_goff, nt, loss_part, dscores);
+    TLP_LAUNCH_CHECK();
+    finalize_rank<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv((int64_t)B * nt, 256), 1024)), 256, 0, s>>>(
+        loss_part, G, nt, d_counts, dscores, B, loss_out, ctx->d_err);
+    TLP_LAUNCH_CHECK();
+    return TLP_OK;
+  }
+  // split: [nt][G][kRankSplit] loss and DCG partials, [nt][B] inverse discounts
+  float* dcg_part = loss_part + (size_t)G * nt * kRankSplit;
+  TLP_CUDA_TRY(ctx->ws_misc.ensure((size_t)nt * B * sizeof(float) + 256));
+  float* iD = ctx->ws_misc.as<float>();
+  const size_t smem1 = (size_t)max_group * (2 * sizeof(float) + sizeof(int));
+  cudaFuncSetAttribute(rank_prep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
+  rank_prep_kernel<<<dim3(G * kRankSplit, nt), kRankThreads, smem1, s>>>(scores, labels, d_goff, nt, iD, dcg_part);
+  TLP_LAUNCH_CHECK();
+  cudaFuncSetAttribute(rank_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  rank_pair_kernel<<<dim3(G * kRankSplit, nt), kRankThreads, smem, s>>>(scores, labels, d_goff, nt, iD, dcg_part,
+                                                                       loss_part, dscores);
   TLP_LAUNCH_CHECK();
   finalize_rank<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv((int64_t)B * nt, 256), 1024)), 256, 0, s>>>(
-      loss_part, G, nt, d_counts, dscores, B, loss_out, ctx->d_err);
+      loss_part, G * kRankSplit, nt, d_counts, dscores, B, loss_out, ctx->d_err);
   TLP_LAUNCH_CHECK();
   return TLP_OK;
 }
