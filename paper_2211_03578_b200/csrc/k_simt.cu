@@ -665,10 +665,36 @@ tlp_status sgemm(tlp_ctx* ctx, bool ta, bool tb, int64_t M, int64_t N, int64_t K
   return TLP_OK;
 }
 
+// dW[k] = sum_m A[m][k] dY[m] (a single output column: the head's w2
+// gradient): row slices per block, thread per k (coalesced rows), fp32 FMA in
+// row order; partials reduced in a fixed order.
+__global__ void wgrad_n1_kernel(int64_t M, int K, const float* __restrict__ A, int64_t lda,
+                                const float* __restrict__ dY, int64_t lddy, int64_t rows,
+                                float* __restrict__ part) {
+  const int64_t m0 = (int64_t)blockIdx.x * rows;
+  const int64_t m1 = M < m0 + rows ? M : m0 + rows;
+  for (int k = threadIdx.x; k < K; k += blockDim.x) {
+    float acc = 0.f;
+    for (int64_t m = m0; m < m1; ++m) acc = fmaf(A[m * lda + k], dY[m * lddy], acc);
+    part[(int64_t)blockIdx.x * K + k] = acc;
+  }
+}
+
 tlp_status sgemm_wgrad(tlp_ctx* ctx, int64_t M, int64_t K, int64_t N, const float* A, int64_t lda,
                        const float* dY, int64_t lddy, float* dW, cudaStream_t s) {
   // dW[K,N] = A^T dY with A [M,K] (ld lda), dY [M,N] (ld lddy).  Split over the
   // M rows into Z fixed slices (a function of M only) -> ordered reduction.
+  if (N == 1 && K <= 1024) {
+    const int Zn = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(M, 128), 256));
+    const int64_t rows = cdiv(M, Zn);
+    TLP_CUDA_TRY(ctx->ws_partial.ensure((size_t)Zn * K * sizeof(float)));
+    float* part = ctx->ws_partial.as<float>();
+    wgrad_n1_kernel<<<(unsigned)Zn, 128, 0, s>>>(M, (int)K, A, lda, dY, lddy, rows, part);
+    TLP_LAUNCH_CHECK();
+    reduce_partials<<<(unsigned)cdiv(K, 256), 256, 0, s>>>(part, K, Zn, dW);
+    TLP_LAUNCH_CHECK();
+    return TLP_OK;
+  }
   const int64_t slice = 2048;
   const int Z = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(M, slice), 256));
   const int64_t kslice = cdiv(cdiv(M, Z), BK) * BK;
