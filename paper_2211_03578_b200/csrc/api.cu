@@ -214,6 +214,10 @@ void tlp_destroy(tlp_ctx* ctx) {
   if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);
   for (cudaEvent_t e : ctx->bucket_ev)
     if (e) cudaEventDestroy(e);
+  for (int i = 0; i < tlp_ctx::kGoffRing; ++i) {
+    if (ctx->goff_ev[i]) cudaEventDestroy(ctx->goff_ev[i]);
+    if (ctx->goff_pinned[i]) cudaFreeHost(ctx->goff_pinned[i]);
+  }
   delete ctx;
 }
 
@@ -481,6 +485,42 @@ tlp_status check_groups(tlp_ctx* ctx, const int64_t* group_off, int32_t B, int32
   return TLP_OK;
 }
 
+// Upload a step's group offsets to the device copy `dst`.  The same layout as
+// the last upload to the same buffer on the same stream (a fixed training batch
+// shape) needs no copy; otherwise the offsets go through one slot of a pinned
+// staging ring (its previous copy is waited for first), never a pageable copy.
+tlp_status upload_goff(tlp_ctx* ctx, int64_t* dst, const int64_t* group_off, int32_t G, cudaStream_t s) {
+  const size_t n = (size_t)G + 1;
+  if (ctx->goff_dev == dst && ctx->goff_stream == s && ctx->goff_last.size() == n &&
+      std::memcmp(ctx->goff_last.data(), group_off, n * sizeof(int64_t)) == 0)
+    return TLP_OK;
+  if (n > ctx->goff_pinned_cap) {
+    for (int i = 0; i < tlp_ctx::kGoffRing; ++i) {
+      if (ctx->goff_ev[i]) TLP_CUDA_TRY(cudaEventSynchronize(ctx->goff_ev[i]));
+      if (ctx->goff_pinned[i]) cudaFreeHost(ctx->goff_pinned[i]);
+      ctx->goff_pinned[i] = nullptr;
+    }
+    ctx->goff_pinned_cap = 0;
+    const size_t cap = std::max<size_t>(n, 1024);
+    for (int i = 0; i < tlp_ctx::kGoffRing; ++i) {
+      TLP_CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&ctx->goff_pinned[i]), cap * sizeof(int64_t),
+                                 cudaHostAllocDefault));
+      if (!ctx->goff_ev[i]) TLP_CUDA_TRY(cudaEventCreateWithFlags(&ctx->goff_ev[i], cudaEventDisableTiming));
+    }
+    ctx->goff_pinned_cap = cap;
+  }
+  const int slot = ctx->goff_slot;
+  ctx->goff_slot = (slot + 1) % tlp_ctx::kGoffRing;
+  TLP_CUDA_TRY(cudaEventSynchronize(ctx->goff_ev[slot]));  // its last copy has read it
+  std::memcpy(ctx->goff_pinned[slot], group_off, n * sizeof(int64_t));
+  TLP_CUDA_TRY(cudaMemcpyAsync(dst, ctx->goff_pinned[slot], n * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+  TLP_CUDA_TRY(cudaEventRecord(ctx->goff_ev[slot], s));
+  ctx->goff_last.assign(group_off, group_off + n);
+  ctx->goff_dev = dst;
+  ctx->goff_stream = s;
+  return TLP_OK;
+}
+
 struct TrainWs {
   int64_t* goff;
   double* counts;
@@ -494,7 +534,9 @@ tlp_status train_ws(tlp_ctx* ctx, int B, int G, TrainWs* w) {
   const size_t b_goff = ((size_t)(G + 1) * sizeof(int64_t) + 255) / 256 * 256;
   const size_t b_cnt = 256;
   const size_t b_sc = ((size_t)B * nt * sizeof(float) + 255) / 256 * 256;
+  const size_t had = ctx->ws_train.bytes;
   TLP_CUDA_TRY(ctx->ws_train.ensure(b_goff + b_cnt + 2 * b_sc + 256));
+  if (ctx->ws_train.bytes != had) ctx->goff_dev = nullptr;  // reallocated: the uploaded offsets are gone
   char* p = ctx->ws_train.as<char>();
   w->goff = reinterpret_cast<int64_t*>(p); p += b_goff;
   w->counts = reinterpret_cast<double*>(p); p += b_cnt;
@@ -515,7 +557,7 @@ tlp_status grads_impl(tlp_ctx* ctx, const float* feats, const float* labels,
   cudaSetDevice(ctx->device);
   TrainWs w;
   if ((st = train_ws(ctx, B, G, &w)) != TLP_OK) return st;
-  TLP_CUDA_TRY(cudaMemcpyAsync(w.goff, group_off, (G + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+  if ((st = upload_goff(ctx, w.goff, group_off, G, s)) != TLP_OK) return st;
   const int nt = ctx->cfg.n_tasks;
   // C-0: per-task loss denominators (labels only), summed over ranks: strict
   // pairs for LambdaRank (R16), present labels for MSE (R41).
@@ -618,7 +660,7 @@ tlp_status tlp_lambdarank(tlp_ctx* ctx, const float* scores, const float* labels
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   TrainWs w;
   if ((st = train_ws(ctx, B, G, &w)) != TLP_OK) return st;
-  TLP_CUDA_TRY(cudaMemcpyAsync(w.goff, group_off, (G + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+  if ((st = upload_goff(ctx, w.goff, group_off, G, s)) != TLP_OK) return st;
   if ((st = rank_pair_counts(ctx, labels, w.goff, G, max_group, w.counts, s)) != TLP_OK) return st;
   return rank_loss_grad(ctx, scores, labels, w.goff, G, B, max_group, w.counts, loss_out,
                         dscores_out, s);

@@ -909,13 +909,23 @@ tlp_status simt_forward(tlp_ctx* ctx, const float* X, int64_t N, float* scores, 
       }
       h = W + lay.hattn[l];
     }
+    const int64_t wcat_stride = ((3 * H * H + 3 * H) + 63) / 64 * 64;  // floats per layer
+    if (c.n_attn && c.backbone == 0)
+      TLP_CUDA_TRY(ctx->ws_wcat.ensure((size_t)c.n_attn * wcat_stride * sizeof(float)));
     for (int l = 0; l < c.n_attn && c.backbone == 0; ++l) {
       float* qkv = W + lay.qkv[l];
       const int64_t wq[3] = {o.Wq[l], o.Wk[l], o.Wv[l]}, bq[3] = {o.bq[l], o.bk[l], o.bv[l]};
+      // [Q | K | V] = h [Wq | Wk | Wv] + [bq | bk | bv] as ONE N = 3H GEMM (h read
+      // once); Wcat[i][jH + k] = W_j[i][k], kept for the backward's fused dgrad
+      float* wcat = ctx->ws_wcat.as<float>() + l * wcat_stride;
+      float* bcat = wcat + 3 * H * H;
       for (int j = 0; j < 3; ++j) {
-        EpiParams e; e.bias = P + bq[j];
-        TRY(sgemm(ctx, false, false, M, H, H, h, H, P + wq[j], H, qkv + j * H, 3 * H, e, s));
+        TLP_CUDA_TRY(cudaMemcpy2DAsync(wcat + j * H, 3 * H * sizeof(float), P + wq[j], H * sizeof(float),
+                                       H * sizeof(float), H, cudaMemcpyDeviceToDevice, s));
+        TLP_CUDA_TRY(cudaMemcpyAsync(bcat + j * H, P + bq[j], H * sizeof(float), cudaMemcpyDeviceToDevice, s));
       }
+      EpiParams eq; eq.bias = bcat;
+      TRY(sgemm(ctx, false, false, M, 3 * H, H, h, H, wcat, 3 * H, qkv, 3 * H, eq, s));
       TRY(attn_fwd(ctx, qkv, n, W + lay.O[l], save ? W + lay.A[l] : nullptr, kvalid, s));
       EpiParams e; e.bias = P + o.bo[l]; e.resid = h; e.ldr = H;
       TRY(sgemm(ctx, false, false, M, H, H, W + lay.O[l], H, P + o.Wo[l], H, W + lay.hattn[l], H, e, s));
@@ -1035,12 +1045,9 @@ tlp_status simt_backward(tlp_ctx* ctx, int64_t N, const float* g, cudaStream_t s
         TRY(sgemm_wgrad_bias(ctx, M, H, H, hin, H, dqkv + j * H, 3 * H, G + wq[j], G + bq[j], s));
     }
     // dh += [dQ | dK | dV] [Wq | Wk | Wv]^T as ONE K = 3H GEMM (dqkv read once,
-    // dh read and written once instead of three times); Wcat[i][jH + k] = W_j[i][k]
-    TLP_CUDA_TRY(ctx->ws_wcat.ensure((size_t)H * 3 * H * sizeof(float)));
-    float* wcat = ctx->ws_wcat.as<float>();
-    for (int j = 0; j < 3; ++j)
-      TLP_CUDA_TRY(cudaMemcpy2DAsync(wcat + j * H, 3 * H * sizeof(float), P + wq[j], H * sizeof(float),
-                                     H * sizeof(float), H, cudaMemcpyDeviceToDevice, s));
+    // dh read and written once instead of three times), on the Wcat the
+    // forward built (simt_backward always follows simt_forward(save))
+    const float* wcat = ctx->ws_wcat.as<float>() + l * ((((3 * H * H + 3 * H) + 63) / 64) * 64);
     EpiParams ea; ea.accumulate = true;
     if (l == 0 && !c.pos_enc) {  // dh is final here: fold the upsample ReLU' (relu_mask) in
       ea.mask = W + lay.up[c.n_up - 1]; ea.ldm = H; ea.mask_after = true;

@@ -332,18 +332,20 @@ constexpr uint32_t IMG_HALF = BNI * BK * 2;                       // 16 KB
 constexpr uint32_t ISTAGE = 2 * (BM * BK * 2) + 2 * IMG_HALF;     // A hi | A lo | B hi | B lo = 48 KB
 constexpr uint32_t ISMEM = STAGES * ISTAGE + 128;
 
-// blockIdx.x = k-block, blockIdx.y = 32-row group of n (8 per 256): 8x the
-// CTAs of one block per k-block (the image is launch-latency bound)
+// blockIdx.x = k-block, blockIdx.y = 32-row group of n (8 per 256-wide column
+// block nb = blockIdx.y / 8, whose image is [nb][K/32 blocks]): 8x the CTAs of
+// one block per k-block (the image is launch-latency bound)
 __global__ void bimg_kernel(const float* __restrict__ B, int64_t ldb, int tb, int64_t N, int64_t K,
                             uint8_t* __restrict__ img) {
-  const int64_t kb = blockIdx.x;
-  uint8_t* dst = img + kb * 2 * IMG_HALF;
+  const int64_t kb = blockIdx.x, nb = blockIdx.y / (BNI / 32);
+  uint8_t* dst = img + (nb * gridDim.x + kb) * 2 * IMG_HALF;
   for (int e = threadIdx.x; e < 32 * BK; e += blockDim.x) {
-    const int n = 32 * (int)blockIdx.y + e / BK, k = e % BK;
+    const int nl = 32 * (int)(blockIdx.y % (BNI / 32)) + e / BK, k = e % BK;
+    const int64_t n = nb * BNI + nl;
     const int64_t gk = kb * BK + k;
     float x = 0.f;
     if (n < N && gk < K) x = tb ? B[(int64_t)n * ldb + gk] : B[gk * ldb + n];
-    const uint32_t off = (n >> 3) * 512 + (k >> 3) * 128 + (n & 7) * 16 + (k & 7) * 2;
+    const uint32_t off = (nl >> 3) * 512 + (k >> 3) * 128 + (nl & 7) * 16 + (k & 7) * 2;
     const __nv_bfloat16 h = __float2bfloat16_rn(x);
     *reinterpret_cast<__nv_bfloat16*>(dst + off) = h;
     *reinterpret_cast<__nv_bfloat16*>(dst + IMG_HALF + off) = __float2bfloat16_rn(x - __bfloat162float(h));
@@ -655,6 +657,17 @@ tlp_status tc_gemm(tlp_ctx* ctx, bool ta, bool tb, int64_t M, int64_t N, int64_t
     TLP_CUDA_TRY(ctx->ws_bimg.ensure((size_t)nkb * 2 * IMG_HALF));
     uint8_t* img = ctx->ws_bimg.as<uint8_t>();
     bimg_kernel<<<dim3((unsigned)nkb, BNI / 32), 256, 0, s>>>(B, ldb, tb ? 1 : 0, N, K, img);
+    TLP_LAUNCH_CHECK();
+    const tlp_status ts = tc_gemm_tma(ctx, M, N, K, A, lda, img, C, ldc, e, s);
+    if (ts != TLP_ERR_UNSUPPORTED) return ts;
+  }
+  // N a multiple of 256 above it (the fused Q/K/V projection, the LSTM gate
+  // GEMMs): one launch over [row block x 256-wide column block] tiles
+  if (!ta && splits == 1 && N > BNI && N % BNI == 0 && K > 0 && M >= 4096) {
+    const int64_t nkb = cdiv(K, BK), ntn = N / BNI;
+    TLP_CUDA_TRY(ctx->ws_bimg.ensure((size_t)ntn * nkb * 2 * IMG_HALF));
+    uint8_t* img = ctx->ws_bimg.as<uint8_t>();
+    bimg_kernel<<<dim3((unsigned)nkb, (unsigned)(ntn * BNI / 32)), 256, 0, s>>>(B, ldb, tb ? 1 : 0, N, K, img);
     TLP_LAUNCH_CHECK();
     const tlp_status ts = tc_gemm_tma(ctx, M, N, K, A, lda, img, C, ldc, e, s);
     if (ts != TLP_ERR_UNSUPPORTED) return ts;

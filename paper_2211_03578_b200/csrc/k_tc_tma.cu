@@ -69,8 +69,9 @@ static_assert(SE >= 3, "the two-input epilogue uses stages 0-1 (inputs) and 2 (o
 
 struct TmaArgs {
   int64_t M, N, K;
-  int ntiles;
-  const uint8_t* img;    // bf16 hi/lo weight image, [K/32][hi 16 KB | lo 16 KB]
+  int ntiles;            // row blocks x ntn
+  int ntn;               // 256-wide column blocks (N > 256 only when N % 256 == 0)
+  const uint8_t* img;    // bf16 hi/lo weight image, [ntn][K/32][hi 16 KB | lo 16 KB]
   float* C;              // [M, ldc] output (and the old values when accumulating)
   int64_t ldc;
   const float* bias;     // [N] or null
@@ -103,7 +104,7 @@ __global__ void __launch_bounds__(THREADS, 1) tma_gemm_kernel(const __grid_const
   const uint32_t acc_full = conv_full + 8 * SC, acc_empty = acc_full + 16, e_full = acc_empty + 16;
   uint32_t* tptr = reinterpret_cast<uint32_t*>(smem + OFF_BAR + 480);
   const int nk = (int)((a.K + TK - 1) / TK);
-  const int nch = (int)((a.N + EC - 1) / EC);
+  const int nch = (int)((min(a.N, (int64_t)TN) + EC - 1) / EC);  // chunks per tile
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < SA; ++i) { tc::mbar_init(a_full + 8 * i, 1); tc::mbar_init(a_empty + 8 * i, 4); }
@@ -125,14 +126,17 @@ __global__ void __launch_bounds__(THREADS, 1) tma_gemm_kernel(const __grid_const
       int s = 0, t = 0;
       uint32_t ph = 0, pb = 0;
       for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
+        // column block fastest: the CTAs working on one row block at a time
+        // share its A tiles through L2
+        const int mt = tile / a.ntn, nb = tile - mt * a.ntn;
         for (int kb = 0; kb < nk; ++kb) {
           tc::mbar_wait(a_empty + 8 * s, ph ^ 1);
           tc::mbar_arrive_expect_tx(a_full + 8 * s, A_BYTES);
-          tc::tma_load_2d(sb + OFF_A + s * A_BYTES, &mA, kb * TK, tile * TM, a_full + 8 * s);
+          tc::tma_load_2d(sb + OFF_A + s * A_BYTES, &mA, kb * TK, mt * TM, a_full + 8 * s);
           if (++s == SA) { s = 0; ph ^= 1; }
           tc::mbar_wait(b_empty + 8 * t, pb ^ 1);
           tc::mbar_arrive_expect_tx(b_full + 8 * t, B_BYTES);
-          tc::bulk_g2s(sb + OFF_B + t * B_BYTES, a.img + (size_t)kb * B_BYTES, B_BYTES, b_full + 8 * t);
+          tc::bulk_g2s(sb + OFF_B + t * B_BYTES, a.img + ((size_t)nb * nk + kb) * B_BYTES, B_BYTES, b_full + 8 * t);
           if (++t == SB) { t = 0; pb ^= 1; }
         }
       }
@@ -239,11 +243,12 @@ __global__ void __launch_bounds__(THREADS, 1) tma_gemm_kernel(const __grid_const
     auto issue_in = [&](long long g) {  // this warp's g-th chunk overall
       if (NIN == 0 || g >= total) return;
       const int tile = blockIdx.x + (int)(g / nmine) * gridDim.x;
+      const int mt = tile / a.ntn, c0 = (tile - mt * a.ntn) * TN;
       const int c = hh + 2 * (int)(g % nmine);
       const int se = two ? 0 : (int)(g % SE);
       tc::mbar_arrive_expect_tx(my_e + 8 * se, (uint32_t)NIN * E_BYTES);
-      tc::tma_load_2d(my_buf + se * E_BYTES, &mIn0, c * EC, tile * TM + 32 * q, my_e + 8 * se);
-      if (two) tc::tma_load_2d(my_buf + E_BYTES, &mIn1, c * EC, tile * TM + 32 * q, my_e);
+      tc::tma_load_2d(my_buf + se * E_BYTES, &mIn0, c0 + c * EC, mt * TM + 32 * q, my_e + 8 * se);
+      if (two) tc::tma_load_2d(my_buf + E_BYTES, &mIn1, c0 + c * EC, mt * TM + 32 * q, my_e);
     };
     if (lane == 0)
       for (long long g = 0; g < (two ? 1 : SE - 1); ++g) issue_in(g);
@@ -252,6 +257,7 @@ __global__ void __launch_bounds__(THREADS, 1) tma_gemm_kernel(const __grid_const
     const int sw = (lane >> 1) & 3;  // 64B swizzle of box row `lane`: chunk j at j ^ ((lane >> 1) & 3)
     for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++t) {
       const int buf = t & 1;
+      const int mt = tile / a.ntn, c0 = (tile - mt * a.ntn) * TN;
       tc::mbar_wait(acc_full + 8 * buf, (t >> 1) & 1);
       tc::tc_fence_after();
       for (int c = hh; c < (a.dbg == 1 ? 0 : nch); c += 2, ++g) {
@@ -265,7 +271,7 @@ __global__ void __launch_bounds__(THREADS, 1) tma_gemm_kernel(const __grid_const
         if (a.bias) {
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
-            const float4 x = __ldg(reinterpret_cast<const float4*>(a.bias + c * EC) + i);
+            const float4 x = __ldg(reinterpret_cast<const float4*>(a.bias + c0 + c * EC) + i);
             b[4 * i] = x.x; b[4 * i + 1] = x.y; b[4 * i + 2] = x.z; b[4 * i + 3] = x.w;
           }
         } else {
@@ -329,7 +335,7 @@ __global__ void __launch_bounds__(THREADS, 1) tma_gemm_kernel(const __grid_const
         __syncwarp();
         if (lane == 0) {
           if (a.dbg != 3) {
-            tc::tma_store_2d(&mOut, c * EC, tile * TM + 32 * q, my_buf + so * E_BYTES);
+            tc::tma_store_2d(&mOut, c0 + c * EC, mt * TM + 32 * q, my_buf + so * E_BYTES);
             tc::bulk_commit();
           }
           if (!two) {
@@ -580,12 +586,14 @@ tlp_status tc_gemm_tma(tlp_ctx* ctx, int64_t M, int64_t N, int64_t K, const floa
                        const uint8_t* img, float* C, int64_t ldc, const EpiParams& e, cudaStream_t s) {
   static const char* env = getenv("TLP_TMA_GEMM");
   if (env && env[0] == '0') return TLP_ERR_UNSUPPORTED;
-  if (!(N > 64 && N <= TN && N % EC == 0 && K > 0 && M > 0 && M <= (int64_t)INT32_MAX - TM))
+  if (!(N > 64 && (N <= TN || N % TN == 0) && N % EC == 0 && K > 0 && M > 0 &&
+        cdiv(M, TM) * cdiv(N, TN) <= (int64_t)INT32_MAX / 2))
     return TLP_ERR_UNSUPPORTED;
   if (!tma_ok(A, lda) || !tma_ok(C, ldc)) return TLP_ERR_UNSUPPORTED;
   TmaArgs a{};
   a.M = M; a.N = N; a.K = K;
-  a.ntiles = (int)cdiv(M, TM);
+  a.ntn = (int)cdiv(N, TN);
+  a.ntiles = (int)(cdiv(M, TM) * a.ntn);
   a.img = img;
   a.bias = e.bias;
   a.relu = e.relu ? 1 : 0;

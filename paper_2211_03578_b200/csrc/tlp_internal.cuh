@@ -92,7 +92,8 @@ struct tlp_ctx {
   // workspaces
   DevBuf ws_tokens, ws_act, ws_train, ws_rank, ws_topk, ws_misc, ws_partial, ws_merge;
   DevBuf ws_bimg;  // bf16 hi/lo image of a training GEMM's weight operand (k_tc_gemm.cu)
-  DevBuf ws_wcat;  // [Wq | Wk | Wv] rows side by side: the fused Q/K/V dgrad operand (k_simt.cu)
+  DevBuf ws_wcat;  // per attention layer [Wq | Wk | Wv] rows side by side, then [bq | bk | bv]:
+                  // the fused Q/K/V forward GEMM and dgrad operands (k_simt.cu)
 
   // bf16 tensor-core path
   TcWeights* tc = nullptr;
@@ -117,6 +118,17 @@ struct tlp_ctx {
   // with a bound (TLP_NCCL_TIMEOUT_S) and aborts the communicator on timeout
   // or an asynchronous NCCL error
   cudaEvent_t coll_ev = nullptr;
+  // training group offsets (api.cu upload_goff): the last offsets uploaded,
+  // where and on which stream (an unchanged batch layout skips the copy), and a
+  // pinned staging ring for changed ones (no pageable copy per step)
+  std::vector<int64_t> goff_last;
+  const void* goff_dev = nullptr;
+  cudaStream_t goff_stream = nullptr;
+  static constexpr int kGoffRing = 4;
+  int64_t* goff_pinned[kGoffRing] = {};
+  size_t goff_pinned_cap = 0;
+  cudaEvent_t goff_ev[kGoffRing] = {};
+  int goff_slot = 0;
   // size of the token table (tlp_broadcast_state)
   int32_t tok_n = 0;
   int64_t tok_bytes = 0;

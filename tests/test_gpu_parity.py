@@ -253,6 +253,34 @@ def test_grads_parity(tp, tokscale, n_tasks, n_attn, seed, sizes, precision, tol
     assert not bad, bad
 
 
+def test_group_offsets_reused_and_changed(tp, tokscale):
+    """The group offsets are uploaded only when they change (api.cu upload_goff):
+    a step after a different layout, and the same layout again, give bitwise the
+    gradients of a fresh context given that layout alone."""
+    tokens, scale = tokscale
+    ocfg = oracle_cfg(n_tasks=1, n_attn=1, hidden=64, up=(32, 64), head_dim=32)
+    flat = flat_params(ocfg, seed=5).astype(np.float32)
+    X, y, off = train_inputs(tokens, scale, 1, sizes=(9, 16, 12, 16, 11, 7))
+    off2 = np.array([0, 20, 41, int(off[-1])], np.int64)
+    Xd, yd = torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda()
+
+    def fresh(o):
+        r = tp.TLP(product_cfg(ocfg, "fp32"))
+        r.set_params(flat)
+        r.compute_grads(Xd, yd, o)
+        r.sync()
+        return r.get_grads()
+
+    want = {1: fresh(off), 2: fresh(off2)}
+    m = tp.TLP(product_cfg(ocfg, "fp32"))
+    m.set_params(flat)
+    for which in (1, 1, 2, 1, 2, 2):
+        o = off if which == 1 else off2
+        m.compute_grads(Xd, yd, o.copy())
+        m.sync()
+        assert np.array_equal(m.get_grads().view(np.uint32), want[which].view(np.uint32)), which
+
+
 def test_mse_unit_parity(tp):
     """NEXT-3 MSE unit (tlp_mse) vs oracle mtl_mse on MTL labels with absent tasks."""
     rng = np.random.default_rng(4)
@@ -571,7 +599,10 @@ def test_bf16_full_size_sampled(tp, tokscale):
                                           # ta = 0, splits = 1, 128 < N <= 256, N % 16 == 0: the
                                           # TMA-fed persistent kernel (k_tc_tma.cu), ragged M / K
                                           (300, 256, 72, 1), (1000, 144, 256, 1), (40000, 256, 768, 1),
-                                          (5000, 128, 256, 1), (5000, 96, 128, 1)])
+                                          (5000, 128, 256, 1), (5000, 96, 128, 1),
+                                          # N > 256, N % 256 == 0: 256-wide column blocks
+                                          # (fused Q/K/V, LSTM gates), ragged M / K
+                                          (5000, 768, 256, 1), (40000, 1024, 256, 1), (4097, 512, 100, 1)])
 def test_train_gemm_building_block(tp, ta, tb, M, N, K, splits):
     rng = np.random.default_rng(M + N + K + 10 * ta + tb)
     A = rng.normal(size=(K, M) if ta else (M, K)).astype(np.float32)
