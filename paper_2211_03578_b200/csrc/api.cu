@@ -117,6 +117,14 @@ std::string check_config(const tlp_config& c) {
 
 }  // namespace
 
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("TLP_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 tlp_status dev_error_status(tlp_ctx* ctx) {
   uint32_t e = 0;
   TLP_CUDA_TRY(cudaMemcpy(&e, ctx->d_err, sizeof(e), cudaMemcpyDeviceToHost));

@@ -10,6 +10,8 @@ namespace {
 __global__ void adam_kernel(float* __restrict__ p, const float* __restrict__ g,
                             float* __restrict__ m, float* __restrict__ v, int64_t n, float lr,
                             float b1, float b2, float eps, float bc1, float bc2) {
+  pdl_wait();  // TLP_LAUNCH_PDL
+  pdl_trigger();
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     const float gi = g[i];
@@ -30,7 +32,7 @@ tlp_status adam_launch(tlp_ctx* ctx, cudaStream_t s) {
   const double bc2 = 1.0 - std::pow((double)c.beta2, (double)ctx->adam_t);
   const int64_t n = ctx->off.total;
   const unsigned grid = (unsigned)std::min<int64_t>(cdiv(n, 256), (int64_t)ctx->num_sms * 8);
-  adam_kernel<<<grid, 256, 0, s>>>(ctx->d_params, ctx->d_grads, ctx->d_m, ctx->d_v, n, c.lr,
+  TLP_LAUNCH_PDL(adam_kernel, grid, 256, 0, s, ctx->d_params, ctx->d_grads, ctx->d_m, ctx->d_v, n, c.lr,
                                    c.beta1, c.beta2, c.eps, (float)bc1, (float)bc2);
   TLP_LAUNCH_CHECK();
   ctx->tc_dirty = true;

@@ -167,6 +167,8 @@ __global__ void __launch_bounds__(128) attn_fwd_tc_kernel(const float* __restric
                                                           int nh, int64_t pairs, float* __restrict__ O,
                                                           float* __restrict__ Asave,
                                                           const float* __restrict__ kvalid) {
+  pdl_wait();  // TLP_LAUNCH_PDL
+  pdl_trigger();
   extern __shared__ float sm[];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t pair = (int64_t)blockIdx.x * (blockDim.x >> 5) + w;
@@ -253,6 +255,8 @@ __global__ void __launch_bounds__(128) attn_bwd_tc_kernel(const float* __restric
                                                           const float* __restrict__ Asave,
                                                           const float* __restrict__ dO, int L, int H,
                                                           int nh, float* __restrict__ dQKV) {
+  pdl_wait();  // TLP_LAUNCH_PDL
+  pdl_trigger();
   extern __shared__ float sm[];
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
   const int mt = w & 1, nhf = w >> 1;
@@ -344,7 +348,7 @@ tlp_status attn_fwd_tc(tlp_ctx* ctx, const float* qkv, int64_t N, float* O, floa
   const int warps = 4;
   const size_t smem = (size_t)warps * 3 * MAT * sizeof(float);
   TLP_SMEM_ATTR(attn_fwd_tc_kernel, smem);
-  attn_fwd_tc_kernel<<<(unsigned)cdiv(pairs, warps), warps * 32, smem, s>>>(qkv, c.L, c.hidden,
+  TLP_LAUNCH_PDL(attn_fwd_tc_kernel, (unsigned)cdiv(pairs, warps), warps * 32, smem, s, qkv, c.L, c.hidden,
                                                                            c.attn_heads, pairs, O, A, kvalid);
   TLP_LAUNCH_CHECK();
   return TLP_OK;
@@ -357,7 +361,7 @@ tlp_status attn_bwd_tc(tlp_ctx* ctx, const float* qkv, const float* A, const flo
   if (pairs == 0) return TLP_OK;
   const size_t smem = (6 * MAT + 64) * sizeof(float);
   TLP_SMEM_ATTR(attn_bwd_tc_kernel, smem);
-  attn_bwd_tc_kernel<<<(unsigned)pairs, 128, smem, s>>>(qkv, A, dO, c.L, c.hidden, c.attn_heads, dqkv);
+  TLP_LAUNCH_PDL(attn_bwd_tc_kernel, (unsigned)pairs, 128, smem, s, qkv, A, dO, c.L, c.hidden, c.attn_heads, dqkv);
   TLP_LAUNCH_CHECK();
   return TLP_OK;
 }

@@ -75,6 +75,8 @@ __device__ int gather_present(const float* __restrict__ scores, const float* __r
 __global__ void __launch_bounds__(kThreads) pair_count_kernel(const float* __restrict__ labels,
                                                               const int64_t* __restrict__ goff,
                                                               int nt, double* __restrict__ part) {
+  pdl_wait();  // TLP_LAUNCH_PDL
+  pdl_trigger();
   extern __shared__ float sm[];
   const int g = blockIdx.x, t = blockIdx.y;
   const int64_t lo = goff[g], hi = goff[g + 1];
@@ -102,6 +104,8 @@ __global__ void __launch_bounds__(kThreads) pair_count_kernel(const float* __res
 
 __global__ void sum_counts(const double* __restrict__ part, int G, int nt,
                            double* __restrict__ counts) {
+  pdl_wait();  // TLP_LAUNCH_PDL
+  pdl_trigger();
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= nt) return;
   double s = 0.0;
@@ -211,6 +215,8 @@ __global__ void __launch_bounds__(kRankThreads) rank_prep_kernel(const float* __
                                                              const int64_t* __restrict__ goff, int nt,
                                                              float* __restrict__ iD_out,
                                                              float* __restrict__ dcg_part) {
+  pdl_wait();  // TLP_LAUNCH_PDL
+  pdl_trigger();
   extern __shared__ float sm[];
   __shared__ float red[32];
   const int g = blockIdx.x / kRankSplit, sub = blockIdx.x % kRankSplit, t = blockIdx.y;
@@ -255,6 +261,8 @@ __global__ void __launch_bounds__(kRankThreads) rank_pair_kernel(const float* __
                                                              const float* __restrict__ dcg_part,
                                                              float* __restrict__ loss_part,
                                                              float* __restrict__ dscores) {
+  pdl_wait();  // TLP_LAUNCH_PDL
+  pdl_trigger();
   extern __shared__ float sm[];
   __shared__ float red[32];
   const int G = gridDim.x / kRankSplit;
@@ -317,6 +325,8 @@ __global__ void __launch_bounds__(kRankThreads) rank_pair_kernel(const float* __
 __global__ void finalize_rank(const float* __restrict__ loss_part, int G, int nt,
                               const double* __restrict__ counts, float* __restrict__ dscores,
                               int64_t B, float* __restrict__ loss_out, uint32_t* err) {
+  pdl_wait();  // TLP_LAUNCH_PDL
+  pdl_trigger();
   // scale gradients by 1/P_t, sum the task losses in a fixed order
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < B * nt; e += stride) {
@@ -437,9 +447,9 @@ tlp_status rank_pair_counts(tlp_ctx* ctx, const float* labels, const int64_t* d_
   double* part = ctx->ws_rank.as<double>();
   const size_t smem = (size_t)max_group * (2 * sizeof(float) + sizeof(int));
   cudaFuncSetAttribute(pair_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  pair_count_kernel<<<dim3(G, nt), kThreads, smem, s>>>(labels, d_goff, nt, part);
+  TLP_LAUNCH_PDL(pair_count_kernel, dim3(G, nt), kThreads, smem, s, labels, d_goff, nt, part);
   TLP_LAUNCH_CHECK();
-  sum_counts<<<1, 32, 0, s>>>(part, G, nt, d_counts);
+  TLP_LAUNCH_PDL(sum_counts, 1, 32, 0, s, part, G, nt, d_counts);
   TLP_LAUNCH_CHECK();
   return TLP_OK;
 }
@@ -458,7 +468,7 @@ tlp_status rank_loss_grad(tlp_ctx* ctx, const float* scores, const float* labels
     cudaFuncSetAttribute(rank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     rank_kernel<<<dim3(G, nt), kRankThreads, smem, s>>>(scores, labels, d_goff, nt, loss_part, dscores);
     TLP_LAUNCH_CHECK();
-    finalize_rank<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv((int64_t)B * nt, 256), 1024)), 256, 0, s>>>(
+    TLP_LAUNCH_PDL(finalize_rank, (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv((int64_t)B * nt, 256), 1024)), 256, 0, s, 
         loss_part, G, nt, d_counts, dscores, B, loss_out, ctx->d_err);
     TLP_LAUNCH_CHECK();
     return TLP_OK;
@@ -469,13 +479,13 @@ tlp_status rank_loss_grad(tlp_ctx* ctx, const float* scores, const float* labels
   float* iD = ctx->ws_misc.as<float>();
   const size_t smem1 = (size_t)max_group * (2 * sizeof(float) + sizeof(int));
   cudaFuncSetAttribute(rank_prep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
-  rank_prep_kernel<<<dim3(G * kRankSplit, nt), kRankThreads, smem1, s>>>(scores, labels, d_goff, nt, iD, dcg_part);
+  TLP_LAUNCH_PDL(rank_prep_kernel, dim3(G * kRankSplit, nt), kRankThreads, smem1, s, scores, labels, d_goff, nt, iD, dcg_part);
   TLP_LAUNCH_CHECK();
   cudaFuncSetAttribute(rank_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  rank_pair_kernel<<<dim3(G * kRankSplit, nt), kRankThreads, smem, s>>>(scores, labels, d_goff, nt, iD, dcg_part,
+  TLP_LAUNCH_PDL(rank_pair_kernel, dim3(G * kRankSplit, nt), kRankThreads, smem, s, scores, labels, d_goff, nt, iD, dcg_part,
                                                                        loss_part, dscores);
   TLP_LAUNCH_CHECK();
-  finalize_rank<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv((int64_t)B * nt, 256), 1024)), 256, 0, s>>>(
+  TLP_LAUNCH_PDL(finalize_rank, (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv((int64_t)B * nt, 256), 1024)), 256, 0, s, 
       loss_part, G * kRankSplit, nt, d_counts, dscores, B, loss_out, ctx->d_err);
   TLP_LAUNCH_CHECK();
   return TLP_OK;

@@ -150,6 +150,8 @@ __global__ void __launch_bounds__(256) sgemm_kernel(int64_t M, int64_t N, int64_
 // the threads measured slower: 249 vs 142 us per step -- fewer loads in flight.)
 __global__ void reduce_partials(const float* __restrict__ part, int64_t n, int Z,
                                 float* __restrict__ out) {
+  pdl_wait();  // TLP_LAUNCH_PDL
+  pdl_trigger();
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n) return;
   float s = 0.f;
@@ -159,6 +161,8 @@ __global__ void reduce_partials(const float* __restrict__ part, int64_t n, int Z
 
 // X [M, E] -> [M, 32] with zero columns E..31 (16-byte rows for TMA)
 __global__ void pad_cols_kernel(const float* __restrict__ X, int64_t M, int E, float* __restrict__ out) {
+  pdl_wait();  // TLP_LAUNCH_PDL
+  pdl_trigger();
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= M * 32) return;
   const int64_t r = e >> 5;
@@ -173,6 +177,8 @@ __global__ void pad_cols_kernel(const float* __restrict__ X, int64_t M, int E, f
 // combined by a fixed butterfly (deterministic).
 __global__ void reduce_partials_pad(const float* __restrict__ part, int Kreal, int Kpad, int N, int Z,
                                     float* __restrict__ out) {
+  pdl_wait();  // TLP_LAUNCH_PDL
+  pdl_trigger();
   const int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (j >= (int64_t)(Kreal + 1) * N) return;
@@ -421,6 +427,8 @@ __global__ void head_pool_kernel(const float* __restrict__ U, int L, int hd, int
                                  const float* __restrict__ w2, const float* __restrict__ c2,
                                  int t, int nt, float* __restrict__ pooled,
                                  float* __restrict__ scores) {
+  pdl_wait();  // TLP_LAUNCH_PDL
+  pdl_trigger();
   const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int64_t n = (int64_t)blockIdx.x * (blockDim.x / 32) + w;
   if (n >= N) return;
@@ -439,6 +447,8 @@ __global__ void head_pool_kernel(const float* __restrict__ U, int L, int hd, int
 __global__ void head_bwd_kernel(const float* __restrict__ U, int L, int hd, int64_t N,
                                 const float* __restrict__ w2, const float* __restrict__ g, int t,
                                 int nt, float* __restrict__ dU, int vec) {
+  pdl_wait();  // TLP_LAUNCH_PDL
+  pdl_trigger();
   if (vec) {  // float4 per thread, one row-segment: 32-bit row index, no 64-bit division
     const int q = hd >> 2;
     const int64_t e4 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -459,9 +469,30 @@ __global__ void head_bwd_kernel(const float* __restrict__ U, int L, int hd, int6
   dU[e] = U[e] > 0.f ? g[n * nt + t] * w2[k] : 0.f;
 }
 
+// Wcat = [Wq | Wk | Wv] rows side by side, then [bq | bk | bv] (the fused Q/K/V
+// GEMM operands, k_simt.cu simt_forward / simt_backward): one launch instead of
+// six device copies
+__global__ void pack_wcat_kernel(const float* __restrict__ P, int64_t w0, int64_t w1, int64_t w2,
+                                 int64_t b0, int64_t b1, int64_t b2, int H, float* __restrict__ wcat) {
+  pdl_wait();  // TLP_LAUNCH_PDL
+  pdl_trigger();
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t H3 = 3 * (int64_t)H, nW = H3 * H;
+  if (e < nW) {
+    const int64_t i = e / H3;
+    const int c = (int)(e - i * H3), j = c / H, k = c - j * H;
+    wcat[e] = P[(j == 0 ? w0 : j == 1 ? w1 : w2) + i * H + k];
+  } else if (e < nW + H3) {
+    const int c = (int)(e - nW), j = c / H, k = c - j * H;
+    wcat[e] = P[(j == 0 ? b0 : j == 1 ? b1 : b2) + k];
+  }
+}
+
 // out = L * sum_n g[n, t]   (single block, fixed order)
 __global__ void dc2_kernel(const float* __restrict__ g, int64_t N, int t, int nt, int L,
                            float* __restrict__ out) {
+  pdl_wait();  // TLP_LAUNCH_PDL
+  pdl_trigger();
   __shared__ float red[256];
   float s = 0.f;
   for (int64_t n = threadIdx.x; n < N; n += blockDim.x) s += g[n * nt + t];
@@ -671,6 +702,8 @@ tlp_status sgemm(tlp_ctx* ctx, bool ta, bool tb, int64_t M, int64_t N, int64_t K
 __global__ void wgrad_n1_kernel(int64_t M, int K, const float* __restrict__ A, int64_t lda,
                                 const float* __restrict__ dY, int64_t lddy, int64_t rows,
                                 float* __restrict__ part) {
+  pdl_wait();  // TLP_LAUNCH_PDL
+  pdl_trigger();
   const int64_t m0 = (int64_t)blockIdx.x * rows;
   const int64_t m1 = M < m0 + rows ? M : m0 + rows;
   for (int k = threadIdx.x; k < K; k += blockDim.x) {
@@ -689,9 +722,9 @@ tlp_status sgemm_wgrad(tlp_ctx* ctx, int64_t M, int64_t K, int64_t N, const floa
     const int64_t rows = cdiv(M, Zn);
     TLP_CUDA_TRY(ctx->ws_partial.ensure((size_t)Zn * K * sizeof(float)));
     float* part = ctx->ws_partial.as<float>();
-    wgrad_n1_kernel<<<(unsigned)Zn, 128, 0, s>>>(M, (int)K, A, lda, dY, lddy, rows, part);
+    TLP_LAUNCH_PDL(wgrad_n1_kernel, (unsigned)Zn, 128, 0, s, M, (int)K, A, lda, dY, lddy, rows, part);
     TLP_LAUNCH_CHECK();
-    reduce_partials<<<(unsigned)cdiv(K, 256), 256, 0, s>>>(part, K, Zn, dW);
+    TLP_LAUNCH_PDL(reduce_partials, (unsigned)cdiv(K, 256), 256, 0, s, part, K, Zn, dW);
     TLP_LAUNCH_CHECK();
     return TLP_OK;
   }
@@ -707,7 +740,7 @@ tlp_status sgemm_wgrad(tlp_ctx* ctx, int64_t M, int64_t K, int64_t N, const floa
     float* part = ctx->ws_partial.as<float>();
     tlp_status st = tc_gemm(ctx, true, false, K, N, M, A, lda, dY, lddy, part, N, none, Z, kslice, s);
     if (st != TLP_OK) return st;
-    reduce_partials<<<(unsigned)cdiv(K * N, 256), 256, 0, s>>>(part, K * N, Z, dW);
+    TLP_LAUNCH_PDL(reduce_partials, (unsigned)cdiv(K * N, 256), 256, 0, s, part, K * N, Z, dW);
     TLP_LAUNCH_CHECK();
     return TLP_OK;
   }
@@ -720,7 +753,7 @@ tlp_status sgemm_wgrad(tlp_ctx* ctx, int64_t M, int64_t K, int64_t N, const floa
   float* part = ctx->ws_partial.as<float>();
   sgemm_kernel<true, false><<<grid, 256, 0, s>>>(K, N, M, A, lda, dY, lddy, part, N, ed, kslice);
   TLP_LAUNCH_CHECK();
-  reduce_partials<<<(unsigned)cdiv(K * N, 256), 256, 0, s>>>(part, K * N, Z, dW);
+  TLP_LAUNCH_PDL(reduce_partials, (unsigned)cdiv(K * N, 256), 256, 0, s, part, K * N, Z, dW);
   TLP_LAUNCH_CHECK();
   return TLP_OK;
 }
@@ -744,7 +777,7 @@ static tlp_status wgrad_bias_tma(tlp_ctx* ctx, int J, int64_t M, int64_t K, int6
   tlp_status st = tc_wgrad_tma(ctx, M, K, N, A, lda, dY, lddy, part, Z, kslice, true, J, jcol, s);
   if (st != TLP_OK) return st;
   for (int j = 0; j < J; ++j) {
-    reduce_partials<<<(unsigned)cdiv((K + 1) * N, 256), 256, 0, s>>>(part + j * pj, (K + 1) * N, Z, dW[j]);
+    TLP_LAUNCH_PDL(reduce_partials, (unsigned)cdiv((K + 1) * N, 256), 256, 0, s, part + j * pj, (K + 1) * N, Z, dW[j]);
     TLP_LAUNCH_CHECK();
   }
   return TLP_OK;
@@ -765,7 +798,7 @@ static tlp_status wgrad_bias_padded(tlp_ctx* ctx, int64_t M, int64_t Kreal, int6
   if (st == TLP_ERR_UNSUPPORTED)
     return sgemm_wgrad_bias(ctx, M, Kreal, N, ctx->train_X, Kreal, dY, N, dWdb, dWdb + Kreal * N, s);
   if (st != TLP_OK) return st;
-  reduce_partials_pad<<<(unsigned)cdiv((Kreal + 1) * N * 32, 256), 256, 0, s>>>(part, (int)Kreal, 32, (int)N, Z, dWdb);
+  TLP_LAUNCH_PDL(reduce_partials_pad, (unsigned)cdiv((Kreal + 1) * N * 32, 256), 256, 0, s, part, (int)Kreal, 32, (int)N, Z, dWdb);
   TLP_LAUNCH_CHECK();
   return TLP_OK;
 }
@@ -786,7 +819,7 @@ tlp_status sgemm_wgrad_bias(tlp_ctx* ctx, int64_t M, int64_t K, int64_t N, const
     tlp_status st = TLP_OK;
     if (tc_wgrad_bias(ctx, K, N, M, A, lda, dY, lddy, part, Z, kslice, s, &st)) {
       if (st != TLP_OK) return st;
-      reduce_partials<<<(unsigned)cdiv((K + 1) * N, 256), 256, 0, s>>>(part, (K + 1) * N, Z, dW);
+      TLP_LAUNCH_PDL(reduce_partials, (unsigned)cdiv((K + 1) * N, 256), 256, 0, s, part, (K + 1) * N, Z, dW);
       TLP_LAUNCH_CHECK();
       return TLP_OK;
     }
@@ -817,7 +850,7 @@ tlp_status sgemm_wgrad_bias_shared(tlp_ctx* ctx, int J, int64_t M, int64_t K, in
     if (tc_wgrad_bias(ctx, K, N, M, A, lda, dY, lddy, part, Z, kslice, s, &st, J, jcol, pj)) {
       if (st != TLP_OK) return st;
       for (int j = 0; j < J; ++j) {
-        reduce_partials<<<(unsigned)cdiv((K + 1) * N, 256), 256, 0, s>>>(part + j * pj, (K + 1) * N, Z, dW[j]);
+        TLP_LAUNCH_PDL(reduce_partials, (unsigned)cdiv((K + 1) * N, 256), 256, 0, s, part + j * pj, (K + 1) * N, Z, dW[j]);
         TLP_LAUNCH_CHECK();
       }
       return TLP_OK;
@@ -872,7 +905,7 @@ tlp_status simt_forward(tlp_ctx* ctx, const float* X, int64_t N, float* scores, 
       // E = 22 rows are 88 bytes, which TMA cannot address: one padded copy
       // [M, 32] (zero columns E..31) feeds the first layer's TMA GEMM here and
       // its weight gradient in the backward
-      pad_cols_kernel<<<(unsigned)cdiv(M * 32, 256), 256, 0, s>>>(h, M, c.E, W + lay.xpad);
+      TLP_LAUNCH_PDL(pad_cols_kernel, (unsigned)cdiv(M * 32, 256), 256, 0, s, h, M, c.E, W + lay.xpad);
       TLP_LAUNCH_CHECK();
       h = W + lay.xpad;
       ldh = 32;
@@ -919,11 +952,9 @@ tlp_status simt_forward(tlp_ctx* ctx, const float* X, int64_t N, float* scores, 
       // once); Wcat[i][jH + k] = W_j[i][k], kept for the backward's fused dgrad
       float* wcat = ctx->ws_wcat.as<float>() + l * wcat_stride;
       float* bcat = wcat + 3 * H * H;
-      for (int j = 0; j < 3; ++j) {
-        TLP_CUDA_TRY(cudaMemcpy2DAsync(wcat + j * H, 3 * H * sizeof(float), P + wq[j], H * sizeof(float),
-                                       H * sizeof(float), H, cudaMemcpyDeviceToDevice, s));
-        TLP_CUDA_TRY(cudaMemcpyAsync(bcat + j * H, P + bq[j], H * sizeof(float), cudaMemcpyDeviceToDevice, s));
-      }
+      TLP_LAUNCH_PDL(pack_wcat_kernel, (unsigned)cdiv(3 * H * H + 3 * H, 256), 256, 0, s, P, wq[0], wq[1],
+                     wq[2], bq[0], bq[1], bq[2], (int)H, wcat);
+      TLP_LAUNCH_CHECK();
       EpiParams eq; eq.bias = bcat;
       TRY(sgemm(ctx, false, false, M, 3 * H, H, h, H, wcat, 3 * H, qkv, 3 * H, eq, s));
       TRY(attn_fwd(ctx, qkv, n, W + lay.O[l], save ? W + lay.A[l] : nullptr, kvalid, s));
@@ -942,7 +973,7 @@ tlp_status simt_forward(tlp_ctx* ctx, const float* X, int64_t N, float* scores, 
       EpiParams e; e.bias = P + o.c1[t];
       TRY(sgemm(ctx, false, false, M, c.head_dim, H, h, H, P + o.W1[t], c.head_dim, W + lay.U[t],
                 c.head_dim, e, s));
-      head_pool_kernel<<<(unsigned)cdiv(n, 8), 256, 0, s>>>(
+      TLP_LAUNCH_PDL(head_pool_kernel, (unsigned)cdiv(n, 8), 256, 0, s, 
           W + lay.U[t], c.L, c.head_dim, n, P + o.w2[t], P + o.c2[t], t, c.n_tasks,
           save ? W + lay.pooled[t] : nullptr, scores + n0 * c.n_tasks);
       TLP_LAUNCH_CHECK();
@@ -975,12 +1006,12 @@ tlp_status simt_backward(tlp_ctx* ctx, int64_t N, const float* g, cudaStream_t s
     // (the float4 path needs 16-byte aligned U / dU / w2: act_layout slots are
     // 64-float aligned; w2's flat offset may not be)
     const bool v4 = hd % 4 == 0 && (reinterpret_cast<uintptr_t>(P + o.w2[t]) & 15) == 0;
-    head_bwd_kernel<<<(unsigned)cdiv(v4 ? M * hd / 4 : M * hd, 256), 256, 0, s>>>(
+    TLP_LAUNCH_PDL(head_bwd_kernel, (unsigned)cdiv(v4 ? M * hd / 4 : M * hd, 256), 256, 0, s, 
         W + lay.U[t], c.L, hd, N, P + o.w2[t], g, t, c.n_tasks, dU, v4 ? 1 : 0);
     TLP_LAUNCH_CHECK();
     TRY(sgemm_wgrad_bias(ctx, M, H, hd, hfin, H, dU, hd, G + o.W1[t], G + o.c1[t], s));
     TRY(sgemm_wgrad(ctx, N, hd, 1, W + lay.pooled[t], hd, g + t, c.n_tasks, G + o.w2[t], s));
-    dc2_kernel<<<1, 256, 0, s>>>(g, N, t, c.n_tasks, c.L, G + o.c2[t]);
+    TLP_LAUNCH_PDL(dc2_kernel, 1, 256, 0, s, g, N, t, c.n_tasks, c.L, G + o.c2[t]);
     TLP_LAUNCH_CHECK();
     EpiParams e; e.accumulate = t > 0;
     TRY(sgemm(ctx, false, true, M, H, hd, dU, hd, P + o.W1[t], hd, dh, H, e, s));

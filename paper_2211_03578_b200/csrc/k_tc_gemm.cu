@@ -337,6 +337,8 @@ constexpr uint32_t ISMEM = STAGES * ISTAGE + 128;
 // one block per k-block (the image is launch-latency bound)
 __global__ void bimg_kernel(const float* __restrict__ B, int64_t ldb, int tb, int64_t N, int64_t K,
                             uint8_t* __restrict__ img) {
+  pdl_wait();  // img may still be read by the previous GEMM
+  pdl_trigger();
   const int64_t kb = blockIdx.x, nb = blockIdx.y / (BNI / 32);
   uint8_t* dst = img + (nb * gridDim.x + kb) * 2 * IMG_HALF;
   for (int e = threadIdx.x; e < 32 * BK; e += blockDim.x) {
@@ -656,7 +658,7 @@ tlp_status tc_gemm(tlp_ctx* ctx, bool ta, bool tb, int64_t M, int64_t N, int64_t
     const int64_t nkb = cdiv(K, BK);
     TLP_CUDA_TRY(ctx->ws_bimg.ensure((size_t)nkb * 2 * IMG_HALF));
     uint8_t* img = ctx->ws_bimg.as<uint8_t>();
-    bimg_kernel<<<dim3((unsigned)nkb, BNI / 32), 256, 0, s>>>(B, ldb, tb ? 1 : 0, N, K, img);
+    TLP_LAUNCH_PDL(bimg_kernel, dim3((unsigned)nkb, BNI / 32), 256, 0, s, B, ldb, tb ? 1 : 0, N, K, img);
     TLP_LAUNCH_CHECK();
     const tlp_status ts = tc_gemm_tma(ctx, M, N, K, A, lda, img, C, ldc, e, s);
     if (ts != TLP_ERR_UNSUPPORTED) return ts;
@@ -667,7 +669,7 @@ tlp_status tc_gemm(tlp_ctx* ctx, bool ta, bool tb, int64_t M, int64_t N, int64_t
     const int64_t nkb = cdiv(K, BK), ntn = N / BNI;
     TLP_CUDA_TRY(ctx->ws_bimg.ensure((size_t)ntn * nkb * 2 * IMG_HALF));
     uint8_t* img = ctx->ws_bimg.as<uint8_t>();
-    bimg_kernel<<<dim3((unsigned)nkb, (unsigned)(ntn * BNI / 32)), 256, 0, s>>>(B, ldb, tb ? 1 : 0, N, K, img);
+    TLP_LAUNCH_PDL(bimg_kernel, dim3((unsigned)nkb, (unsigned)(ntn * BNI / 32)), 256, 0, s, B, ldb, tb ? 1 : 0, N, K, img);
     TLP_LAUNCH_CHECK();
     const tlp_status ts = tc_gemm_tma(ctx, M, N, K, A, lda, img, C, ldc, e, s);
     if (ts != TLP_ERR_UNSUPPORTED) return ts;
@@ -677,7 +679,7 @@ tlp_status tc_gemm(tlp_ctx* ctx, bool ta, bool tb, int64_t M, int64_t N, int64_t
     const int64_t nkb = cdiv(K, BK);
     TLP_CUDA_TRY(ctx->ws_bimg.ensure((size_t)nkb * 2 * IMG_HALF));
     uint8_t* img = ctx->ws_bimg.as<uint8_t>();
-    bimg_kernel<<<dim3((unsigned)nkb, BNI / 32), 256, 0, s>>>(B, ldb, tb ? 1 : 0, N, K, img);
+    TLP_LAUNCH_PDL(bimg_kernel, dim3((unsigned)nkb, BNI / 32), 256, 0, s, B, ldb, tb ? 1 : 0, N, K, img);
     TLP_LAUNCH_CHECK();
     // the TMA-fed persistent kernel (k_tc_tma.cu) when the operands allow it
     const tlp_status ts = tc_gemm_tma(ctx, M, N, K, A, lda, img, C, ldc, e, s);

@@ -119,6 +119,8 @@ __global__ void __launch_bounds__(THREADS, 1) tma_gemm_kernel(const __grid_const
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = *tptr;
+  pdl_wait();  // setup above overlapped the previous kernel's tail (TLP_LAUNCH_PDL)
+  pdl_trigger();
 
   if (warp == 0) {
     // ------------------------------------------------ TMA producer: A tiles + weight image blocks
@@ -420,6 +422,8 @@ __global__ void __launch_bounds__(W_THREADS, 1) tma_wgrad_kernel(const __grid_co
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = *tptr;
+  pdl_wait();  // setup above overlapped the previous kernel's tail (TLP_LAUNCH_PDL)
+  pdl_trigger();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -628,13 +632,13 @@ tlp_status tc_gemm_tma(tlp_ctx* ctx, int64_t M, int64_t N, int64_t K, const floa
   const int grid = (int)std::min<int64_t>(a.ntiles, ctx->num_sms);
   if (a.n_in == 0) {
     TLP_SMEM_ATTR(tma_gemm_kernel<0>, SMEM_ALLOC);
-    tma_gemm_kernel<0><<<grid, THREADS, SMEM_ALLOC, s>>>(mA, mI0, mI1, mO, a);
+    TLP_LAUNCH_PDL(tma_gemm_kernel<0>, grid, THREADS, SMEM_ALLOC, s, mA, mI0, mI1, mO, a);
   } else if (a.n_in == 1) {
     TLP_SMEM_ATTR(tma_gemm_kernel<1>, SMEM_ALLOC);
-    tma_gemm_kernel<1><<<grid, THREADS, SMEM_ALLOC, s>>>(mA, mI0, mI1, mO, a);
+    TLP_LAUNCH_PDL(tma_gemm_kernel<1>, grid, THREADS, SMEM_ALLOC, s, mA, mI0, mI1, mO, a);
   } else {
     TLP_SMEM_ATTR(tma_gemm_kernel<2>, SMEM_ALLOC);
-    tma_gemm_kernel<2><<<grid, THREADS, SMEM_ALLOC, s>>>(mA, mI0, mI1, mO, a);
+    TLP_LAUNCH_PDL(tma_gemm_kernel<2>, grid, THREADS, SMEM_ALLOC, s, mA, mI0, mI1, mO, a);
   }
   TLP_LAUNCH_CHECK();
   return TLP_OK;
@@ -665,10 +669,10 @@ tlp_status tc_wgrad_tma(tlp_ctx* ctx, int64_t R, int64_t Mf, int64_t Nf, const f
   const dim3 grid((unsigned)J, (unsigned)Z);
   if (colsum) {
     TLP_SMEM_ATTR(tma_wgrad_kernel<true>, W_SMEM);
-    tma_wgrad_kernel<true><<<grid, W_THREADS, W_SMEM, s>>>(mX, mY, mP, a);
+    TLP_LAUNCH_PDL(tma_wgrad_kernel<true>, grid, W_THREADS, W_SMEM, s, mX, mY, mP, a);
   } else {
     TLP_SMEM_ATTR(tma_wgrad_kernel<false>, W_SMEM);
-    tma_wgrad_kernel<false><<<grid, W_THREADS, W_SMEM, s>>>(mX, mY, mP, a);
+    TLP_LAUNCH_PDL(tma_wgrad_kernel<false>, grid, W_THREADS, W_SMEM, s, mX, mY, mP, a);
   }
   TLP_LAUNCH_CHECK();
   return TLP_OK;

@@ -171,6 +171,42 @@ struct tlp_ctx {
 
 static inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// Programmatic dependent launch (PDL) for the training step's chain of kernels
+// (68 launches per C3 step, ~2 us of idle device time at each boundary): a
+// kernel launched by TLP_LAUNCH_PDL may be scheduled while its predecessor in
+// the stream drains, so it MUST call pdl_wait() before touching global memory
+// (griddepcontrol.wait returns once every prerequisite grid has completed and
+// its writes are visible; it is a no-op for a normal launch), and it calls
+// pdl_trigger() once its own CTAs are resident so that the next kernel's
+// launch overlaps its tail.  TLP_PDL=0 launches them normally (A/B).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+#define TLP_LAUNCH_PDL(kern, grid, block, smem, stream, ...)                  \
+  do {                                                                        \
+    cudaError_t _le = launch_pdl(kern, grid, block, smem, stream, __VA_ARGS__); \
+    if (_le != cudaSuccess) {                                                 \
+      ctx->last_error = std::string("CUDA launch: ") + cudaGetErrorString(_le) + \
+                        " at " __FILE__ ":" + std::to_string(__LINE__);       \
+      return TLP_ERR_CUDA;                                                    \
+    }                                                                         \
+  } while (0)  // follow with TLP_LAUNCH_CHECK() (launch count)
+
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is per device: remember per
 // call site which devices already have it (bit = device ordinal), so a process
 // with contexts on several GPUs sets it on each of them.

@@ -1,10 +1,12 @@
 """Summarise an ncu --set full report of one kernel: stall reasons and the
 hottest SASS lines with their source line (diagnostics).
-    python tools/ncu_hot.py REPORT.ncu-rep [N]"""
+    python tools/ncu_hot.py REPORT.ncu-rep [N] [sass|cuda] [LAUNCH_INDEX]"""
 import csv, io, subprocess, sys
 rep = sys.argv[1]
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 30
-raw = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", sys.argv[3] if len(sys.argv) > 3 else "sass"],
+sel = ["--launch-skip", sys.argv[4], "--launch-count", "1"] if len(sys.argv) > 4 else []
+raw = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source",
+                      sys.argv[3] if len(sys.argv) > 3 else "sass"] + sel,
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
 hdr_i = next(i for i, r in enumerate(rows) if r and r[0] == "Address" or (len(r) > 1 and r[1] == "Source"))
