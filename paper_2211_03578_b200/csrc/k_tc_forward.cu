@@ -86,7 +86,7 @@ constexpr uint32_t T_AOP0 = 384; // 64:  bf16 A operand (residual-block first ha
 // Compiled in only with -DTLP_TRACE (tools/abl_build.sh): even a never-taken
 // timestamp branch per head cost ~13% of the kernel (clock reads pin the
 // scheduling of the surrounding code).
-constexpr int kTrEv = 160, kTrW = 8 * kTrEv;
+constexpr int kTrEv = 160, kTrW = 8 * kTrEv, kTrM = 16;  // kTrM words per tile of MMA-issuer record
 #ifdef TLP_TRACE
 constexpr bool kTrace = true;
 #else
@@ -533,7 +533,17 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
+      const uintptr_t xb = reinterpret_cast<uintptr_t>(a.X);
+      const uintptr_t xe = (xb + (uintptr_t)a.N * kL * kE * sizeof(float)) & ~(uintptr_t)15;
       for (int64_t it = it0; it < n_it; it += it_step) {
+        // this CTA's next tile of X into L2 a whole tile ahead: E0's row loads
+        // then hit L2 instead of HBM (11,000 B per tile, 16-byte aligned cover)
+        if (it + it_step < n_it) {
+          const uintptr_t t0 = xb + (uintptr_t)tile_of(it + it_step) * kCand * kL * kE * sizeof(float);
+          const uintptr_t p0 = t0 & ~(uintptr_t)15;
+          const uintptr_t p1 = std::min<uintptr_t>((t0 + kCand * kL * kE * sizeof(float) + 15) & ~(uintptr_t)15, xe);
+          if (p1 > p0) tc::bulk_prefetch_l2(reinterpret_cast<const void*>(p0), (uint32_t)(p1 - p0));
+        }
         for (int c = 0; c < a.nchunks; ++c) {
           tc::mbar_wait(bar_empty + 8 * stage, phase ^ 1);
           const ChunkRef ch = a.chunks[c];
@@ -572,12 +582,20 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
       // diagnostics (a.trace, CTA 0): cycles the issuer spends waiting per tile on
       // weight chunks / QKV reads / O_j / other epilogue operands
       const bool trc = kTrace && a.trace != nullptr && blockIdx.x == 0;
-      long long wt[4] = {0, 0, 0, 0};
+      long long wt[4] = {0, 0, 0, 0}, wc[4] = {0, 0, 0, 0};  // wc: chunk waits per phase
+      int cph = 0;  // phase: 0 upsample, 1 attention, 2 residual blocks, 3 heads
       auto timed_wait = [&](int k, uint32_t bar, uint32_t ph) {
         const long long t0 = trc ? clock64() : 0;
         if (PAIR) mbar_wait_cluster(bar, ph);  // arrivals include the peer CTA's
         else tc::mbar_wait(bar, ph);
-        if (trc) wt[k] += clock64() - t0;
+        if (trc) {
+          wt[k] += clock64() - t0;
+          if (k == 0) wc[cph] += clock64() - t0;
+        }
+      };
+      auto mark = [&](int ph, int mt) {  // phase start clock (diagnostics)
+        cph = ph;
+        if (trc && mt < 8) a.trace[kTrW + mt * kTrM + 4 + ph] = clock64();
       };
       auto wait_opnd = [&]() {
         timed_wait(3, bar_opnd, op_phase);
@@ -617,10 +635,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
       };
       int mt = 0;
       for (int64_t it = it0; it < n_it; it += it_step, ++mt) {
-        if (trc && mt < 8) {
-          for (int k = 0; k < 4; ++k) wt[k] = 0;
-          a.trace[kTrW + mt * 8 + 4] = clock64();
-        }
+        if (trc && mt < 8)
+          for (int k = 0; k < 4; ++k) wt[k] = wc[k] = 0;
+        if (kTrace) mark(0, mt);
         wait_opnd();                                                      // E0: X
         gemm_w(false, OFF_X, kKX, T_B, 128, kKX, 32, false);              // up0 -> T_B
         commit<PAIR>(bar_acc);
@@ -630,6 +647,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
         commit<PAIR>(bar_acc);
         wait_opnd();                                                      // E2: h[:, :128]
         split = true;                                                     //     h[:, 128:]
+        if (kTrace) mark(1, mt);
         for (int l = 0; l < NA; ++l) {
           gemm_w(false, OFF_H, kH, T_QKV, 96, kH, 64, false);             // QKV_0 -> buf 0
           commit<PAIR>(bar_qkv);
@@ -652,6 +670,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
           wait_opnd();                                                    // E_resid h[:, :128]
           split = true;                                                   //         h[:, 128:]
         }
+        if (kTrace) mark(2, mt);
         for (int r = 0; r < NR; ++r) {
           // G1 half 1 goes ahead of G2 part 0 so that the epilogue of r_h1 overlaps
           // G2 part 0 (the two r halves live in separate TMEM operand slots)
@@ -667,13 +686,17 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
           wait_opnd();                                                    // E_resid h[:, :128]
           split = true;                                                   //         h[:, 128:]
         }
+        if (kTrace) mark(3, mt);
         for (int t = 0; t < NT; ++t) {
           gemm_w(false, OFF_H, kH, T_B, kHD, kH, 64, false);              // head t
           commit<PAIR>(bar_acc);
           if (t < NT - 1) wait_opnd();
         }
         if (trc && mt < 8)
-          for (int k = 0; k < 4; ++k) a.trace[kTrW + mt * 8 + k] = wt[k];
+          for (int k = 0; k < 4; ++k) {
+            a.trace[kTrW + mt * kTrM + k] = wt[k];
+            a.trace[kTrW + mt * kTrM + 8 + k] = wc[k];
+          }
       }
     }
   } else {
@@ -1088,8 +1111,8 @@ tlp_status tc_forward(tlp_ctx* ctx, const float* feats, int64_t N, float* scores
   static const bool trace = kTrace && getenv("TLP_TC_TRACE") != nullptr;
   long long* d_trace = nullptr;
   if (trace) {
-    TLP_CUDA_TRY(cudaMalloc(&d_trace, (kTrW + 64) * sizeof(long long)));
-    TLP_CUDA_TRY(cudaMemset(d_trace, 0, (kTrW + 64) * sizeof(long long)));
+    TLP_CUDA_TRY(cudaMalloc(&d_trace, (kTrW + 8 * kTrM) * sizeof(long long)));
+    TLP_CUDA_TRY(cudaMemset(d_trace, 0, (kTrW + 8 * kTrM) * sizeof(long long)));
   }
   a.trace = d_trace;
   if (pair) {
@@ -1109,7 +1132,7 @@ tlp_status tc_forward(tlp_ctx* ctx, const float* feats, int64_t N, float* scores
   }
   TLP_LAUNCH_CHECK();
   if (trace) {
-    std::vector<long long> h(kTrW + 64);
+    std::vector<long long> h(kTrW + 8 * kTrM);
     TLP_CUDA_TRY(cudaStreamSynchronize(s));
     TLP_CUDA_TRY(cudaMemcpy(h.data(), d_trace, h.size() * sizeof(long long), cudaMemcpyDeviceToHost));
     cudaFree(d_trace);
@@ -1117,9 +1140,12 @@ tlp_status tc_forward(tlp_ctx* ctx, const float* feats, int64_t N, float* scores
       fprintf(stderr, "tile %d:", t);
       for (int e = 1; e < kTrEv && h[t * kTrEv + e]; ++e) fprintf(stderr, " %lld", h[t * kTrEv + e] - h[t * kTrEv + e - 1]);
       fprintf(stderr, " | total %lld\n", h[(t + 1) * kTrEv] ? h[(t + 1) * kTrEv] - h[t * kTrEv] : 0LL);
-      const long long* m = &h[kTrW + t * 8];
+      const long long* m = &h[kTrW + t * kTrM];
       fprintf(stderr, "  mma issuer waits: chunks %lld, qkv-read %lld, O_j %lld, operands %lld (tile %lld)\n",
-              m[0], m[1], m[2], m[3], m[12] ? m[12] - m[4] : 0LL);
+              m[0], m[1], m[2], m[3], m[kTrM + 4] ? m[kTrM + 4] - m[4] : 0LL);
+      fprintf(stderr, "  mma phases (cycles / chunk waits): upsample %lld / %lld, attention %lld / %lld, "
+              "residual %lld / %lld, heads %lld / %lld\n", m[5] - m[4], m[8], m[6] - m[5], m[9],
+              m[7] - m[6], m[10], m[kTrM + 4] ? m[kTrM + 4] - m[7] : 0LL, m[11]);
     }
   }
   return TLP_OK;
