@@ -157,8 +157,9 @@ __device__ __forceinline__ void relu_pack32(const float (&v)[32], const float* b
   for (int i = 0; i < 16; ++i) {
 #ifndef TLP_RELU_F32
     // round, then a bf16x2 max with 0: bitwise equal (RN is monotone, RN(0) = 0)
-    const __nv_bfloat162 r2 = __hmax2(__floats2bfloat162_rn(v[2 * i] + b[2 * i], v[2 * i + 1] + b[2 * i + 1]),
-                                      __float2bfloat162_rn(0.f));
+    // (acc + bias) as one FADD2 per pair
+    const uint32_t a2 = tc::add_pack_bf16(v[2 * i], v[2 * i + 1], b[2 * i], b[2 * i + 1]);
+    const __nv_bfloat162 r2 = __hmax2(*reinterpret_cast<const __nv_bfloat162*>(&a2), __float2bfloat162_rn(0.f));
     pk[i] = *reinterpret_cast<const uint32_t*>(&r2);
 #else
     pk[i] = tc::pack_bf16(fmaxf(v[2 * i] + b[2 * i], 0.f), fmaxf(v[2 * i + 1] + b[2 * i + 1], 0.f));
@@ -256,8 +257,8 @@ __device__ __forceinline__ void residual32(uint8_t* smem, const float (&v)[32], 
     // (acc + bias) rounded to bf16, then one bf16x2 add (R33): 4 instructions per
     // pair instead of 7 -- the epilogues bound this kernel by issue slots (ncu:
     // 159K warp-instructions per 5-candidate tile); 23.6 -> 23.05 ms per round
-    const __nv_bfloat162 r2 = __floats2bfloat162_rn(v[2 * i] + b[2 * i], v[2 * i + 1] + b[2 * i + 1]);
-    const __nv_bfloat162 s2 = __hadd2(hb, r2);
+    const uint32_t a2 = tc::add_pack_bf16(v[2 * i], v[2 * i + 1], b[2 * i], b[2 * i + 1]);  // FADD2
+    const __nv_bfloat162 s2 = __hadd2(hb, *reinterpret_cast<const __nv_bfloat162*>(&a2));
     pk[i] = *reinterpret_cast<const uint32_t*>(&s2);
 #else
     const float2 hf = __bfloat1622float2(hb);
@@ -338,14 +339,17 @@ __device__ __forceinline__ void attn_unit_mma(uint8_t* smem, uint32_t sbase, uin
     const float off = mx * sm_scale;  // kmask is never empty: mx finite
     float sum = 0.f;
 #pragma unroll
-    for (int nt = 0; nt < 4; ++nt)
+    for (int nt = 0; nt < 4; ++nt) {
+      float x[2];  // s * scale - off for the pair, one FFMA2
+      tc::fma2(x[0], x[1], s[nt][2 * half], s[nt][2 * half + 1], sm_scale, sm_scale, -off, -off);
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const bool ok = MASK ? ((kmask >> (8 * nt + 2 * tig + e)) & 1u) : (8 * nt + 2 * (int)tig + e < kL);
-        const float p = ok ? ex2_approx(fmaf(s[nt][2 * half + e], sm_scale, -off)) : 0.f;
+        const float p = ok ? ex2_approx(x[e]) : 0.f;
         s[nt][2 * half + e] = p;
         sum += p;
       }
+    }
     sum += __shfl_xor_sync(0xffffffffu, sum, 1);
     sum += __shfl_xor_sync(0xffffffffu, sum, 2);
     // R29: approximate reciprocal on the bf16 path (sum >= 1: the row max term is
@@ -379,9 +383,12 @@ __device__ __forceinline__ void attn_unit_mma(uint8_t* smem, uint32_t sbase, uin
     if (kk < (uint32_t)kL) {
       const uint32_t row = kL * c + kk;
 #pragma unroll
-      for (int dn = 0; dn < 4; ++dn)
+      for (int dn = 0; dn < 4; ++dn) {
+        float y0, y1;  // O / rowsum, one FMUL2
+        tc::mul2(y0, y1, o[dn][2 * half], o[dn][2 * half + 1], inv[half], inv[half]);
         *reinterpret_cast<uint32_t*>(smem + o_off + tc::canon_off(row, 8 * dn + 2 * tig, kDH)) =
-            tc::pack_bf16(o[dn][2 * half] * inv[half], o[dn][2 * half + 1] * inv[half]);
+            tc::pack_bf16(y0, y1);
+      }
     }
   }
 }
@@ -815,7 +822,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
               vec32(vs + (hh == 0 ? a.bq[l] : hh == 1 ? a.bk[l] : a.bv[l]) + kDH * j, b);
               tc::tmem_wait_ld();
 #pragma unroll
-              for (int i = 0; i < 16; ++i) pk[i] = tc::pack_bf16(v[2 * i] + b[2 * i], v[2 * i + 1] + b[2 * i + 1]);
+              for (int i = 0; i < 16; ++i) pk[i] = tc::add_pack_bf16(v[2 * i], v[2 * i + 1], b[2 * i], b[2 * i + 1]);
               if (real) store_plain32(smem, (hh == 0 ? OFF_Q : hh == 1 ? OFF_K : OFF_V) + pos, pk);
             } else {  // two warps: Q + K[0:16) / K[16:32) + V, both loads before one wait
               float v[32], v2[16], b[32], b2[16];
@@ -832,9 +839,9 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
               }
               tc::tmem_wait_ld();
 #pragma unroll
-              for (int i = 0; i < 16; ++i) pk[i] = tc::pack_bf16(v[2 * i] + b[2 * i], v[2 * i + 1] + b[2 * i + 1]);
+              for (int i = 0; i < 16; ++i) pk[i] = tc::add_pack_bf16(v[2 * i], v[2 * i + 1], b[2 * i], b[2 * i + 1]);
 #pragma unroll
-              for (int i = 0; i < 8; ++i) pk2[i] = tc::pack_bf16(v2[2 * i] + b2[2 * i], v2[2 * i + 1] + b2[2 * i + 1]);
+              for (int i = 0; i < 8; ++i) pk2[i] = tc::add_pack_bf16(v2[2 * i], v2[2 * i + 1], b2[2 * i], b2[2 * i + 1]);
               if (real) {
                 store_plain32(smem, (hh == 0 ? OFF_Q : OFF_V) + pos, pk);
                 uint8_t* kd = smem + OFF_K + pos + 32 * hh;
