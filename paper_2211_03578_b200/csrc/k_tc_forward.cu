@@ -337,7 +337,7 @@ __device__ __forceinline__ void attn_unit_mma(uint8_t* smem, uint32_t sbase, uin
     mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
     mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
     const float off = mx * sm_scale;  // kmask is never empty: mx finite
-    float sum = 0.f;
+    float sum0 = 0.f, sum1 = 0.f;  // even / odd key columns, one FADD2 per pair
 #pragma unroll
     for (int nt = 0; nt < 4; ++nt) {
       float x[2];  // s * scale - off for the pair, one FFMA2
@@ -345,11 +345,11 @@ __device__ __forceinline__ void attn_unit_mma(uint8_t* smem, uint32_t sbase, uin
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const bool ok = MASK ? ((kmask >> (8 * nt + 2 * tig + e)) & 1u) : (8 * nt + 2 * (int)tig + e < kL);
-        const float p = ok ? ex2_approx(x[e]) : 0.f;
-        s[nt][2 * half + e] = p;
-        sum += p;
+        s[nt][2 * half + e] = ok ? ex2_approx(x[e]) : 0.f;
       }
+      tc::add2(sum0, sum1, sum0, sum1, s[nt][2 * half], s[nt][2 * half + 1]);
     }
+    float sum = sum0 + sum1;
     sum += __shfl_xor_sync(0xffffffffu, sum, 1);
     sum += __shfl_xor_sync(0xffffffffu, sum, 2);
     // R29: approximate reciprocal on the bf16 path (sum >= 1: the row max term is
@@ -890,7 +890,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
       }
       for (int t = 0; t < NT; ++t) {
         wait_on(bar_acc, ph_acc);
-        float dot = 0.f;
+        float dot = 0.f, dot1 = 0.f;
         for (int c = lo_of(kHD); c < hi_of(kHD); c += 32) {
           float v[32], b[32], w[32];
           tc::tmem_ld32(tl + T_B + c, v);
@@ -898,9 +898,13 @@ __global__ void __launch_bounds__(kThreads, 1) tc_forward_kernel(const TcArgs a)
           vec32(vs + a.w2[t] + c, w);
           tc::tmem_wait_ld();
 #pragma unroll
-          for (int i = 0; i < 32; ++i) dot = fmaf(fmaxf(v[i] + b[i], 0.f), w[i], dot);
+          for (int i = 0; i < 16; ++i) {  // even / odd columns: FADD2, two max, FFMA2
+            float x0, x1;
+            tc::add2(x0, x1, v[2 * i], v[2 * i + 1], b[2 * i], b[2 * i + 1]);
+            tc::fma2(dot, dot1, fmaxf(x0, 0.f), fmaxf(x1, 0.f), w[2 * i], w[2 * i + 1], dot, dot1);
+          }
         }
-        rowdot[hh * 128 + r] = dot;
+        rowdot[hh * 128 + r] = dot + dot1;
         tc::tc_fence_before();
         asm volatile("bar.sync 1, 256;" ::: "memory");
         if (hh == 0 && r < kCand) {
