@@ -22,12 +22,20 @@
 
 namespace {
 
-constexpr int DH = 32, LP = 32, LD = 36;
-constexpr int MAT = LP * LD;  // floats per staged matrix
+// Row strides of the staged fp32 [32][LD] matrices: an operand read with rows
+// on the lane's group id g and columns on its thread-in-group t (X[g][t]) is
+// bank-conflict free at LD = 36 (36 g + t distinct mod 32), one read
+// transposed (X[t][g]) at LD = 40 (40 t + g distinct): the forward's V (only
+// read transposed, by O = P V) is staged at LD = 40.  (The backward with Q, K
+// at LD = 40 and transposed copies of dS, A, dO measured slower: 25% fewer
+// conflicts but a lower occupancy and the extra transposes.)
+constexpr int DH = 32, LP = 32, LD = 36, LDT = 40;
+constexpr int MAT = LP * LD;    // floats per staged matrix
+constexpr int MATT = LP * LDT;  // ... read transposed
 
 __device__ __forceinline__ uint32_t tf32(float x) {
   uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  asm("cvt.rn.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));  // one F2FP (cvt.rna: four instructions)
   return r;
 }
 
@@ -55,7 +63,7 @@ __device__ __forceinline__ void mma_tf32(float (&d)[4], uint32_t a0, uint32_t a1
 // column halves (softmax max / sum, the backward's rowdot) go through shared
 // memory in a fixed order (deterministic).
 // C[16 x 16 quadrant] = op(X) op(Y), k over 32: 3xTF32 (SPLIT) or plain tf32
-template <bool TA, bool TB, bool SPLIT = true>
+template <bool TA, bool TB, bool SPLIT = true, int LX = LD, int LY = LD>
 __device__ __forceinline__ void gemm_q(const float* X, const float* Y, float (&c)[2][4], int mt, int nh,
                                        int lane) {
   const int g = lane >> 2, t = lane & 3;
@@ -68,8 +76,8 @@ __device__ __forceinline__ void gemm_q(const float* X, const float* Y, float (&c
     const int k0 = 8 * ks + t, k1 = k0 + 4;
     const int r0 = 16 * mt + g, r1 = r0 + 8;
     uint32_t ah[4], al[4];
-    const float x0 = TA ? X[k0 * LD + r0] : X[r0 * LD + k0], x1 = TA ? X[k0 * LD + r1] : X[r1 * LD + k0];
-    const float x2 = TA ? X[k1 * LD + r0] : X[r0 * LD + k1], x3 = TA ? X[k1 * LD + r1] : X[r1 * LD + k1];
+    const float x0 = TA ? X[k0 * LX + r0] : X[r0 * LX + k0], x1 = TA ? X[k0 * LX + r1] : X[r1 * LX + k0];
+    const float x2 = TA ? X[k1 * LX + r0] : X[r0 * LX + k1], x3 = TA ? X[k1 * LX + r1] : X[r1 * LX + k1];
     if (SPLIT) {
       split(x0, ah[0], al[0]); split(x1, ah[1], al[1]); split(x2, ah[2], al[2]); split(x3, ah[3], al[3]);
     } else {
@@ -78,7 +86,7 @@ __device__ __forceinline__ void gemm_q(const float* X, const float* Y, float (&c
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt) {
       const int jj = 16 * nh + 8 * nt + g;
-      const float y0 = TB ? Y[jj * LD + k0] : Y[k0 * LD + jj], y1 = TB ? Y[jj * LD + k1] : Y[k1 * LD + jj];
+      const float y0 = TB ? Y[jj * LY + k0] : Y[k0 * LY + jj], y1 = TB ? Y[jj * LY + k1] : Y[k1 * LY + jj];
       if (SPLIT) {
         uint32_t bh0, bl0, bh1, bl1;
         split(y0, bh0, bl0);
@@ -95,12 +103,13 @@ __device__ __forceinline__ void gemm_q(const float* X, const float* Y, float (&c
 
 // stage rows [0, L) of a [*, ld] fp32 matrix slice (32 columns), zero pad, with
 // the block's 128 threads (16-byte cp.async)
+template <int LS = LD>
 __device__ __forceinline__ void stage128(float* dst, const float* src, int64_t ld, int L, int tid) {
 #pragma unroll
   for (int i = 0; i < LP * DH / 4 / 128; ++i) {
     const int e = tid + 128 * i, m = e >> 3, c = (e & 7) * 4;
     const float* g = src + (int64_t)(m < L ? m : 0) * ld + c;
-    const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(dst + m * LD + c));
+    const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(dst + m * LS + c));
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(g), "r"(m < L ? 16 : 0)
                  : "memory");
   }
@@ -108,7 +117,7 @@ __device__ __forceinline__ void stage128(float* dst, const float* src, int64_t l
 
 // C[32 x 32] = op(X) op(Y): for every (m-tile, n-tile) of 16 x 8, k over 32.
 //   A element (row i, k) = TA ? X[k][i] : X[i][k];  B element (k, col j) = TB ? Y[j][k] : Y[k][j]
-template <bool TA, bool TB>
+template <bool TA, bool TB, int LX = LD, int LY = LD>
 __device__ __forceinline__ void gemm32(const float* X, const float* Y, float (&c)[2][4][4], int lane) {
   const int g = lane >> 2, t = lane & 3;
 #pragma unroll
@@ -124,17 +133,17 @@ __device__ __forceinline__ void gemm32(const float* X, const float* Y, float (&c
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt) {
       const int r0 = 16 * mt + g, r1 = r0 + 8;
-      split(TA ? X[k0 * LD + r0] : X[r0 * LD + k0], ah[mt][0], al[mt][0]);
-      split(TA ? X[k0 * LD + r1] : X[r1 * LD + k0], ah[mt][1], al[mt][1]);
-      split(TA ? X[k1 * LD + r0] : X[r0 * LD + k1], ah[mt][2], al[mt][2]);
-      split(TA ? X[k1 * LD + r1] : X[r1 * LD + k1], ah[mt][3], al[mt][3]);
+      split(TA ? X[k0 * LX + r0] : X[r0 * LX + k0], ah[mt][0], al[mt][0]);
+      split(TA ? X[k0 * LX + r1] : X[r1 * LX + k0], ah[mt][1], al[mt][1]);
+      split(TA ? X[k1 * LX + r0] : X[r0 * LX + k1], ah[mt][2], al[mt][2]);
+      split(TA ? X[k1 * LX + r1] : X[r1 * LX + k1], ah[mt][3], al[mt][3]);
     }
 #pragma unroll
     for (int nt = 0; nt < 4; ++nt) {
       const int j = 8 * nt + g;
       uint32_t bh0, bl0, bh1, bl1;
-      split(TB ? Y[j * LD + k0] : Y[k0 * LD + j], bh0, bl0);
-      split(TB ? Y[j * LD + k1] : Y[k1 * LD + j], bh1, bl1);
+      split(TB ? Y[j * LY + k0] : Y[k0 * LY + j], bh0, bl0);
+      split(TB ? Y[j * LY + k1] : Y[k1 * LY + j], bh1, bl1);
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt) {
         mma_tf32(c[mt][nt], al[mt][0], al[mt][1], al[mt][2], al[mt][3], bh0, bh1);
@@ -148,12 +157,13 @@ __device__ __forceinline__ void gemm32(const float* X, const float* Y, float (&c
 // stage rows [0, L) of a [*, ld] fp32 matrix slice (32 columns), zero pad:
 // 16-byte cp.async (all eight chunks of every row in flight at once; rows of
 // the QKV / dO buffers are 16-byte aligned), zero-fill for the pad rows
+template <int LS = LD>
 __device__ __forceinline__ void stage(float* dst, const float* src, int64_t ld, int L, int lane) {
 #pragma unroll
   for (int i = 0; i < LP * DH / 4 / 32; ++i) {
     const int e = lane + 32 * i, m = e >> 3, c = (e & 7) * 4;
     const float* g = src + (int64_t)(m < L ? m : 0) * ld + c;
-    const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(dst + m * LD + c));
+    const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(dst + m * LS + c));
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(g), "r"(m < L ? 16 : 0)
                  : "memory");
   }
@@ -173,15 +183,15 @@ __global__ void __launch_bounds__(128) attn_fwd_tc_kernel(const float* __restric
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t pair = (int64_t)blockIdx.x * (blockDim.x >> 5) + w;
   if (pair >= pairs) return;
-  float* Qs = sm + w * 3 * MAT;
-  float* Ks = Qs + MAT;
-  float* Vs = Ks + MAT;  // reused for P after S
+  float* Qs = sm + w * (2 * MAT + MATT);
+  float* Ks = Qs + MAT;  // reused for P after S
+  float* Vs = Ks + MAT;  // read transposed by O = P V: LDT
   const int64_t n = pair / nh;
   const int hd = (int)(pair % nh);
   const int64_t row0 = n * L, ld = 3 * (int64_t)H;
   stage(Qs, QKV + row0 * ld + hd * DH, ld, L, lane);
   stage(Ks, QKV + row0 * ld + H + hd * DH, ld, L, lane);
-  stage(Vs, QKV + row0 * ld + 2 * H + hd * DH, ld, L, lane);
+  stage<LDT>(Vs, QKV + row0 * ld + 2 * H + hd * DH, ld, L, lane);
   stage_wait();
   float c[2][4][4];
   gemm32<false, true>(Qs, Ks, c, lane);  // S = Q K^T
@@ -237,7 +247,7 @@ __global__ void __launch_bounds__(128) attn_fwd_tc_kernel(const float* __restric
         }
     }
   __syncwarp();
-  gemm32<false, false>(Ps, Vs, c, lane);  // O = A V
+  gemm32<false, false, LD, LDT>(Ps, Vs, c, lane);  // O = A V
 #pragma unroll
   for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
@@ -346,7 +356,7 @@ tlp_status attn_fwd_tc(tlp_ctx* ctx, const float* qkv, int64_t N, float* O, floa
   const tlp_config& c = ctx->cfg;
   const int64_t pairs = N * c.attn_heads;
   const int warps = 4;
-  const size_t smem = (size_t)warps * 3 * MAT * sizeof(float);
+  const size_t smem = (size_t)warps * (2 * MAT + MATT) * sizeof(float);
   TLP_SMEM_ATTR(attn_fwd_tc_kernel, smem);
   TLP_LAUNCH_PDL(attn_fwd_tc_kernel, (unsigned)cdiv(pairs, warps), warps * 32, smem, s, qkv, c.L, c.hidden,
                                                                            c.attn_heads, pairs, O, A, kvalid);
