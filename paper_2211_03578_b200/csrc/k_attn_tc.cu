@@ -270,19 +270,22 @@ __global__ void __launch_bounds__(128) attn_bwd_tc_kernel(const float* __restric
   extern __shared__ float sm[];
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
   const int mt = w & 1, nhf = w >> 1;
-  float* Qs = sm;  // Q, K, V, dO, A, dS
-  float* Ks = Qs + MAT;
-  float* Vs = Ks + MAT;
+  // Q, K (read transposed only: LDT), V, dO, A; dS overwrites V once every
+  // warp is past dA = dO V^T (the rowdot barrier) -- 24 KB per block, 9
+  // blocks (36 warps) per SM
+  float* Qs = sm;
+  float* Ks = Qs + MATT;
+  float* Vs = Ks + MATT;
   float* dOs = Vs + MAT;
   float* As = dOs + MAT;
-  float* dSs = As + MAT;
-  float* red = dSs + MAT;  // [2 column halves][32 rows] partial rowdot
+  float* dSs = Vs;
+  float* red = As + MAT;  // [2 column halves][32 rows] partial rowdot
   const int64_t pair = blockIdx.x;
   const int64_t n = pair / nh;
   const int hd = (int)(pair % nh);
   const int64_t row0 = n * L, ld = 3 * (int64_t)H;
-  stage128(Qs, QKV + row0 * ld + hd * DH, ld, L, tid);
-  stage128(Ks, QKV + row0 * ld + H + hd * DH, ld, L, tid);
+  stage128<LDT>(Qs, QKV + row0 * ld + hd * DH, ld, L, tid);
+  stage128<LDT>(Ks, QKV + row0 * ld + H + hd * DH, ld, L, tid);
   stage128(Vs, QKV + row0 * ld + 2 * H + hd * DH, ld, L, tid);
   stage128(dOs, dO + row0 * H + hd * DH, H, L, tid);
   const float* Ab = Asave + (n * nh + hd) * (int64_t)L * L;
@@ -336,9 +339,9 @@ __global__ void __launch_bounds__(128) attn_bwd_tc_kernel(const float* __restric
   };
   // dQ, dK, dV in plain tf32 (R53): no cancellation downstream of dS, and their
   // weight gradients are tf32 products anyway (R52); only dA keeps 3xTF32
-  gemm_q<false, false, false>(dSs, Ks, c, mt, nhf, lane);  // dQ = dS K
+  gemm_q<false, false, false, LD, LDT>(dSs, Ks, c, mt, nhf, lane);  // dQ = dS K
   store(c, hd * DH, scale);
-  gemm_q<true, false, false>(dSs, Qs, c, mt, nhf, lane);   // dK = dS^T Q
+  gemm_q<true, false, false, LD, LDT>(dSs, Qs, c, mt, nhf, lane);   // dK = dS^T Q
   store(c, H + hd * DH, scale);
   gemm_q<true, false, false>(As, dOs, c, mt, nhf, lane);   // dV = A^T dO
   store(c, 2 * H + hd * DH, 1.f);
@@ -369,7 +372,7 @@ tlp_status attn_bwd_tc(tlp_ctx* ctx, const float* qkv, const float* A, const flo
   const tlp_config& c = ctx->cfg;
   const int64_t pairs = N * c.attn_heads;
   if (pairs == 0) return TLP_OK;
-  const size_t smem = (6 * MAT + 64) * sizeof(float);
+  const size_t smem = (2 * MATT + 3 * MAT + 64) * sizeof(float);
   TLP_SMEM_ATTR(attn_bwd_tc_kernel, smem);
   TLP_LAUNCH_PDL(attn_bwd_tc_kernel, (unsigned)pairs, 128, smem, s, qkv, A, dO, c.L, c.hidden, c.attn_heads, dqkv);
   TLP_LAUNCH_CHECK();
