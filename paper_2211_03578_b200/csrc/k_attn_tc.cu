@@ -270,7 +270,8 @@ __global__ void __launch_bounds__(128) attn_bwd_tc_kernel(const float* __restric
   extern __shared__ float sm[];
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
   const int mt = w & 1, nhf = w >> 1;
-  // Q, K (read transposed only: LDT), V, dO, A; dS overwrites V once every
+  // Q, K (read transposed only: LDT), V, dO, A (LDT: read transposed by dV);
+  // dS overwrites V once every
   // warp is past dA = dO V^T (the rowdot barrier) -- 24 KB per block, 9
   // blocks (36 warps) per SM
   float* Qs = sm;
@@ -279,7 +280,7 @@ __global__ void __launch_bounds__(128) attn_bwd_tc_kernel(const float* __restric
   float* dOs = Vs + MAT;
   float* As = dOs + MAT;
   float* dSs = Vs;
-  float* red = As + MAT;  // [2 column halves][32 rows] partial rowdot
+  float* red = As + MATT;  // [2 column halves][32 rows] partial rowdot
   const int64_t pair = blockIdx.x;
   const int64_t n = pair / nh;
   const int hd = (int)(pair % nh);
@@ -291,7 +292,7 @@ __global__ void __launch_bounds__(128) attn_bwd_tc_kernel(const float* __restric
   const float* Ab = Asave + (n * nh + hd) * (int64_t)L * L;
   for (int e = tid; e < LP * LP; e += 128) {
     const int l = e / LP, m = e % LP;
-    As[l * LD + m] = (l < L && m < L) ? Ab[l * L + m] : 0.f;
+    As[l * LDT + m] = (l < L && m < L) ? Ab[l * L + m] : 0.f;  // LDT: read transposed by dV
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
@@ -306,7 +307,7 @@ __global__ void __launch_bounds__(128) attn_bwd_tc_kernel(const float* __restric
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
-      for (int e = 0; e < 2; ++e) rd += c[nt][2 * half + e] * As[l * LD + 16 * nhf + 8 * nt + 2 * t + e];
+      for (int e = 0; e < 2; ++e) rd += c[nt][2 * half + e] * As[l * LDT + 16 * nhf + 8 * nt + 2 * t + e];
     rd += __shfl_xor_sync(0xffffffffu, rd, 1);
     rd += __shfl_xor_sync(0xffffffffu, rd, 2);
     if (t == 0) red[nhf * 32 + l] = rd;
@@ -319,7 +320,7 @@ __global__ void __launch_bounds__(128) attn_bwd_tc_kernel(const float* __restric
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt) {
       const int m = 16 * nhf + 8 * nt + 2 * t;
-      const float2 a2 = *reinterpret_cast<const float2*>(As + l * LD + m);
+      const float2 a2 = *reinterpret_cast<const float2*>(As + l * LDT + m);
       *reinterpret_cast<float2*>(dSs + l * LD + m) =
           make_float2(a2.x * (c[nt][2 * half] - rd), a2.y * (c[nt][2 * half + 1] - rd));  // dS = A (dA - rowdot)
     }
@@ -343,7 +344,7 @@ __global__ void __launch_bounds__(128) attn_bwd_tc_kernel(const float* __restric
   store(c, hd * DH, scale);
   gemm_q<true, false, false, LD, LDT>(dSs, Qs, c, mt, nhf, lane);   // dK = dS^T Q
   store(c, H + hd * DH, scale);
-  gemm_q<true, false, false>(As, dOs, c, mt, nhf, lane);   // dV = A^T dO
+  gemm_q<true, false, false, LDT, LD>(As, dOs, c, mt, nhf, lane);   // dV = A^T dO
   store(c, 2 * H + hd * DH, 1.f);
 }
 
@@ -372,7 +373,7 @@ tlp_status attn_bwd_tc(tlp_ctx* ctx, const float* qkv, const float* A, const flo
   const tlp_config& c = ctx->cfg;
   const int64_t pairs = N * c.attn_heads;
   if (pairs == 0) return TLP_OK;
-  const size_t smem = (2 * MATT + 3 * MAT + 64) * sizeof(float);
+  const size_t smem = (3 * MATT + 2 * MAT + 64) * sizeof(float);
   TLP_SMEM_ATTR(attn_bwd_tc_kernel, smem);
   TLP_LAUNCH_PDL(attn_bwd_tc_kernel, (unsigned)pairs, 128, smem, s, qkv, A, dO, c.L, c.hidden, c.attn_heads, dqkv);
   TLP_LAUNCH_CHECK();
