@@ -86,7 +86,19 @@ __device__ __forceinline__ void named_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
-template <int NIN>  // epilogue inputs (a.n_in), specialised: the epilogue bounds the kernel
+// PAIR (experiment, TLP_TMA_PAIR=1; off by default): clusters of two CTAs run tcgen05
+// cta_group::2 -- one M = 256 MMA per instruction over a 256-row tile pair,
+// each CTA holding its own 128 A rows and HALF of the weight image block (the
+// N rows [128 rank, 128 rank + 128)); the rank-0 CTA issues, commits arrive in
+// both CTAs.  Per 256 rows the weight image crosses L2 once instead of twice
+// and the MMA issue count halves -- the single-CTA kernel's main loop waited
+// for operands ~45% of the time (A 16 KB + B 32 KB per k-block and CTA).
+// Correct (training parity green in this mode) but SLOWER: every launch of the
+// C3 step took 1.2-1.5x longer (QKV forward 410 -> 554 us under ncu, step 3.60
+// -> 4.41 ms), also with a 5-deep converted-A ring; the leader's per-k-block
+// wait on both CTAs' conversions and on the relayed half-block arrivals is on
+// the critical path.
+template <int NIN, bool PAIR>  // epilogue inputs (a.n_in), specialised: the epilogue bounds the kernel
 __global__ void __launch_bounds__(THREADS, 1) tma_gemm_kernel(const __grid_constant__ CUtensorMap mA,
                                                               const __grid_constant__ CUtensorMap mIn0,
                                                               const __grid_constant__ CUtensorMap mIn1,
@@ -97,28 +109,58 @@ __global__ void __launch_bounds__(THREADS, 1) tma_gemm_kernel(const __grid_const
   const uint32_t sb = (sraw + 1023u) & ~1023u;  // 1 KB aligned (128B-swizzle atoms)
   uint8_t* smem = smem_raw + (sb - sraw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t bar = sb + OFF_BAR;
+  // pair: the weight ring holds half blocks (hi 8 KB | lo 8 KB), twice as many
+  // pair: half blocks (hi 8 KB | lo 8 KB) in SB stages, and the 48 KB this
+  // frees deepens the converted-A ring (SC -> 5): the leader's MMAs wait on
+  // both CTAs' conversions, so the ring must cover a cross-CTA round trip
+  constexpr int NSB = SB;
+  constexpr uint32_t BSTG = PAIR ? B_BYTES / 2 : B_BYTES;
+  constexpr int SCN = PAIR ? 5 : SC;
+  constexpr uint32_t OFF_CK = OFF_B + NSB * BSTG;
+  constexpr uint32_t OFF_EK = OFF_CK + SCN * C_STAGE;
+  constexpr uint32_t OFF_BK = OFF_EK + EW * SE * E_BYTES;
+  static_assert(OFF_BK + 512 <= SMEM_USED, "pair layout fits the single-CTA budget");
+  const uint32_t bar = sb + OFF_BK;
   const uint32_t a_full = bar, a_empty = a_full + 8 * SA;
-  const uint32_t b_full = a_empty + 8 * SA, b_empty = b_full + 8 * SB;
-  const uint32_t c_empty = b_empty + 8 * SB, conv_full = c_empty + 8 * SC;
-  const uint32_t acc_full = conv_full + 8 * SC, acc_empty = acc_full + 16, e_full = acc_empty + 16;
-  uint32_t* tptr = reinterpret_cast<uint32_t*>(smem + OFF_BAR + 480);
+  const uint32_t b_full = a_empty + 8 * SA, b_empty = b_full + 8 * NSB;
+  const uint32_t c_empty = b_empty + 8 * NSB, conv_full = c_empty + 8 * SCN;
+  const uint32_t acc_full = conv_full + 8 * SCN, acc_empty = acc_full + 16, e_full = acc_empty + 16;
+  const uint32_t b_peer = e_full + 8 * EW * SE;  // [NSB] pair: the peer's half block landed
+  uint32_t* tptr = reinterpret_cast<uint32_t*>(smem + OFF_BK + 480);
   const int nk = (int)((a.K + TK - 1) / TK);
   const int nch = (int)((min(a.N, (int64_t)TN) + EC - 1) / EC);  // chunks per tile
+  const uint32_t rank = PAIR ? tc::cl_rank() : 0u;
+  const uint32_t P2 = PAIR ? 2u : 1u;  // CTAs whose threads arrive on the leader's barriers
+  // tile walk: single -> 128-row tiles blockIdx.x + k gridDim.x; pair -> 256-row
+  // tile pairs (cluster + k clusters), this CTA's rows = row block 2 mt2 + rank
+  const int wstart = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int wstep = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+  const int nwalk = a.ntiles;  // host: tile pairs when PAIR
+  auto row_block = [&](int tile) { return PAIR ? 2 * (tile / a.ntn) + (int)rank : tile / a.ntn; };
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < SA; ++i) { tc::mbar_init(a_full + 8 * i, 1); tc::mbar_init(a_empty + 8 * i, 4); }
-    for (int i = 0; i < SB; ++i) { tc::mbar_init(b_full + 8 * i, 1); tc::mbar_init(b_empty + 8 * i, 1); }
-    for (int i = 0; i < SC; ++i) { tc::mbar_init(c_empty + 8 * i, 1); tc::mbar_init(conv_full + 8 * i, 4); }
-    for (int i = 0; i < 2; ++i) { tc::mbar_init(acc_full + 8 * i, 1); tc::mbar_init(acc_empty + 8 * i, EW); }
+    for (int i = 0; i < NSB; ++i) {
+      tc::mbar_init(b_full + 8 * i, 1); tc::mbar_init(b_empty + 8 * i, 1); tc::mbar_init(b_peer + 8 * i, 1);
+    }
+    for (int i = 0; i < SCN; ++i) { tc::mbar_init(c_empty + 8 * i, 1); tc::mbar_init(conv_full + 8 * i, 4 * P2); }
+    for (int i = 0; i < 2; ++i) { tc::mbar_init(acc_full + 8 * i, 1); tc::mbar_init(acc_empty + 8 * i, EW * P2); }
     for (int i = 0; i < EW * SE; ++i) tc::mbar_init(e_full + 8 * i, 1);
     tc::fence_barrier_init();
   }
-  if (warp == 1) tc::tmem_alloc(tc::smem_u32(tptr), 512);
+  if (warp == 1) {
+    if (PAIR) tc::tmem_alloc_pair(tc::smem_u32(tptr), 512);
+    else tc::tmem_alloc(tc::smem_u32(tptr), 512);
+  }
   tc::tc_fence_before();
-  __syncthreads();
+  if (PAIR) tc::cluster_sync(); else __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = *tptr;
+  // arrivals on the leader's barriers (the peer's go through the cluster window)
+  auto arrive_leader = [&](uint32_t b) {
+    if (PAIR && rank != 0) tc::mbar_arrive_cluster(tc::map_cluster(b, 0));
+    else tc::mbar_arrive(b);
+  };
   pdl_wait();  // setup above overlapped the previous kernel's tail (TLP_LAUNCH_PDL)
   pdl_trigger();
 
@@ -127,53 +169,82 @@ __global__ void __launch_bounds__(THREADS, 1) tma_gemm_kernel(const __grid_const
     if (lane == 0) {
       int s = 0, t = 0;
       uint32_t ph = 0, pb = 0;
-      for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
+      for (int tile = wstart; tile < nwalk; tile += wstep) {
         // column block fastest: the CTAs working on one row block at a time
         // share its A tiles through L2
-        const int mt = tile / a.ntn, nb = tile - mt * a.ntn;
+        const int mt = row_block(tile), nb = tile % a.ntn;
         for (int kb = 0; kb < nk; ++kb) {
           tc::mbar_wait(a_empty + 8 * s, ph ^ 1);
           tc::mbar_arrive_expect_tx(a_full + 8 * s, A_BYTES);
           tc::tma_load_2d(sb + OFF_A + s * A_BYTES, &mA, kb * TK, mt * TM, a_full + 8 * s);
           if (++s == SA) { s = 0; ph ^= 1; }
           tc::mbar_wait(b_empty + 8 * t, pb ^ 1);
-          tc::mbar_arrive_expect_tx(b_full + 8 * t, B_BYTES);
-          tc::bulk_g2s(sb + OFF_B + t * B_BYTES, a.img + ((size_t)nb * nk + kb) * B_BYTES, B_BYTES, b_full + 8 * t);
-          if (++t == SB) { t = 0; pb ^= 1; }
+          tc::mbar_arrive_expect_tx(b_full + 8 * t, BSTG);
+          const uint8_t* blk = a.img + ((size_t)nb * nk + kb) * B_BYTES;
+          if (PAIR) {  // this CTA's N half of the hi and of the lo block
+            tc::bulk_g2s(sb + OFF_B + t * BSTG, blk + rank * (B_BYTES / 4), B_BYTES / 4, b_full + 8 * t);
+            tc::bulk_g2s(sb + OFF_B + t * BSTG + B_BYTES / 4, blk + B_BYTES / 2 + rank * (B_BYTES / 4),
+                         B_BYTES / 4, b_full + 8 * t);
+          } else {
+            tc::bulk_g2s(sb + OFF_B + t * BSTG, blk, B_BYTES, b_full + 8 * t);
+          }
+          if (++t == NSB) { t = 0; pb ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      const uint32_t idesc = tc::idesc_bf16(TM, TN);
+    // ------------------------------------------------ MMA issuer (pair: the leader;
+    // the peer's lane 0 relays "my half block landed" to the leader)
+    if (PAIR && rank != 0 && lane == 0) {
+      int sbk = 0;
+      uint32_t pb = 0;
+      const uint32_t peer0 = tc::map_cluster(b_peer, 0);
+      for (int tile = wstart; tile < nwalk; tile += wstep)
+        for (int kb = 0; kb < nk; ++kb) {
+          tc::mbar_wait(b_full + 8 * sbk, pb);
+          tc::mbar_arrive_cluster(peer0 + 8 * sbk);
+          if (++sbk == NSB) { sbk = 0; pb ^= 1; }
+        }
+    }
+    if (lane == 0 && rank == 0) {
+      const uint32_t idesc = tc::idesc_bf16(PAIR ? 2 * TM : TM, TN);
       int s = 0, t = 0, sbk = 0;
       uint32_t ph = 0, pb = 0;
-      for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++t) {
+      auto wait = [&](uint32_t b, uint32_t par) {
+        if (PAIR) tc::mbar_wait_cluster(b, par); else tc::mbar_wait(b, par);
+      };
+      auto mma = [&](uint32_t d, uint64_t ad, uint64_t bd, uint32_t en) {
+        if (PAIR) tc::mma_bf16_pair(d, ad, bd, idesc, en); else tc::mma_bf16(d, ad, bd, idesc, en);
+      };
+      auto commit = [&](uint32_t b) {
+        if (PAIR) tc::mma_commit_pair(b); else tc::mma_commit(b);
+      };
+      for (int tile = wstart; tile < nwalk; tile += wstep, ++t) {
         const int buf = t & 1;
-        tc::mbar_wait(acc_empty + 8 * buf, ((t >> 1) & 1) ^ 1);
+        wait(acc_empty + 8 * buf, ((t >> 1) & 1) ^ 1);
         tc::tc_fence_after();
         const uint32_t d = tmem + (uint32_t)(buf * TN);
         for (int kb = 0; kb < nk; ++kb) {
-          tc::mbar_wait(conv_full + 8 * s, ph);
+          wait(conv_full + 8 * s, ph);
           tc::mbar_wait(b_full + 8 * sbk, pb);
+          if (PAIR) tc::mbar_wait_cluster(b_peer + 8 * sbk, pb);
           tc::tc_fence_after();
-          const uint32_t ah = sb + OFF_C + s * C_STAGE, al = ah + AH_BYTES;
-          const uint32_t bh = sb + OFF_B + sbk * B_BYTES, bl = bh + B_BYTES / 2;
+          const uint32_t ah = sb + OFF_CK + s * C_STAGE, al = ah + AH_BYTES;
+          const uint32_t bh = sb + OFF_B + sbk * BSTG, bl = bh + BSTG / 2;
 #pragma unroll
           for (int ks = 0; ks < TK / 16; ++ks) {
             const uint64_t dah = tc::smem_desc(ah + ks * 256, 128, 512), dal = tc::smem_desc(al + ks * 256, 128, 512);
             const uint64_t dbh = tc::smem_desc(bh + ks * 256, 128, 512), dbl = tc::smem_desc(bl + ks * 256, 128, 512);
-            tc::mma_bf16(d, dal, dbh, idesc, (kb > 0 || ks > 0) ? 1u : 0u);  // Al.Bh
-            tc::mma_bf16(d, dah, dbl, idesc, 1u);                          // Ah.Bl
-            tc::mma_bf16(d, dah, dbh, idesc, 1u);                          // Ah.Bh
+            mma(d, dal, dbh, (kb > 0 || ks > 0) ? 1u : 0u);  // Al.Bh
+            mma(d, dah, dbl, 1u);                          // Ah.Bl
+            mma(d, dah, dbh, 1u);                          // Ah.Bh
           }
-          tc::mma_commit(c_empty + 8 * s);
-          tc::mma_commit(b_empty + 8 * sbk);
-          if (++s == SC) { s = 0; ph ^= 1; }
-          if (++sbk == SB) { sbk = 0; pb ^= 1; }
+          commit(c_empty + 8 * s);
+          commit(b_empty + 8 * sbk);
+          if (++s == SCN) { s = 0; ph ^= 1; }
+          if (++sbk == NSB) { sbk = 0; pb ^= 1; }
         }
-        tc::mma_commit(acc_full + 8 * buf);
+        commit(acc_full + 8 * buf);
       }
     }
   } else if (warp < 6) {
@@ -181,11 +252,11 @@ __global__ void __launch_bounds__(THREADS, 1) tma_gemm_kernel(const __grid_const
     const int cw = warp - 2;
     int sa = 0, sc = 0;
     uint32_t pa = 0, pc = 0;
-    for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
+    for (int tile = wstart; tile < nwalk; tile += wstep) {
       for (int kb = 0; kb < nk; ++kb) {
         tc::mbar_wait(a_full + 8 * sa, pa);
         tc::mbar_wait(c_empty + 8 * sc, pc ^ 1);  // the MMAs of this stage's last use are done
-        const uint32_t cst = OFF_C + sc * C_STAGE;
+        const uint32_t cst = OFF_CK + sc * C_STAGE;
         const uint8_t* src = smem + OFF_A + sa * A_BYTES;
         uint8_t* hi = smem + cst;
         uint8_t* lo = hi + AH_BYTES;
@@ -213,10 +284,10 @@ __global__ void __launch_bounds__(THREADS, 1) tma_gemm_kernel(const __grid_const
         __syncwarp();
         if (lane == 0) {
           tc::mbar_arrive(a_empty + 8 * sa);
-          tc::mbar_arrive(conv_full + 8 * sc);
+          arrive_leader(conv_full + 8 * sc);
         }
         if (++sa == SA) { sa = 0; pa ^= 1; }
-        if (++sc == SC) { sc = 0; pc ^= 1; }
+        if (++sc == SCN) { sc = 0; pc ^= 1; }
       }
     }
   } else {
@@ -231,9 +302,9 @@ __global__ void __launch_bounds__(THREADS, 1) tma_gemm_kernel(const __grid_const
     const int r = 32 * q + lane;
     const uint32_t tl = tmem + ((uint32_t)(32 * q) << 16);
     const uint32_t my_e = e_full + 8 * SE * ew;
-    const uint32_t my_buf = sb + OFF_E + (uint32_t)ew * SE * E_BYTES;
+    const uint32_t my_buf = sb + OFF_EK + (uint32_t)ew * SE * E_BYTES;
     const int nmine = (nch - hh + 1) / 2;  // chunks per tile for this warp
-    const long long tiles_mine = a.ntiles > (int)blockIdx.x ? (a.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const long long tiles_mine = nwalk > wstart ? (nwalk - 1 - wstart) / wstep + 1 : 0;
     const long long total = tiles_mine * nmine;
     // One input (n_in <= 1): stage g % SE holds chunk g's input, then its result
     // for the TMA store; the input of chunk g + SE - 1 is loaded into stage
@@ -244,8 +315,8 @@ __global__ void __launch_bounds__(THREADS, 1) tma_gemm_kernel(const __grid_const
     constexpr bool two = NIN == 2;
     auto issue_in = [&](long long g) {  // this warp's g-th chunk overall
       if (NIN == 0 || g >= total) return;
-      const int tile = blockIdx.x + (int)(g / nmine) * gridDim.x;
-      const int mt = tile / a.ntn, c0 = (tile - mt * a.ntn) * TN;
+      const int tile = wstart + (int)(g / nmine) * wstep;
+      const int mt = row_block(tile), c0 = (tile % a.ntn) * TN;
       const int c = hh + 2 * (int)(g % nmine);
       const int se = two ? 0 : (int)(g % SE);
       tc::mbar_arrive_expect_tx(my_e + 8 * se, (uint32_t)NIN * E_BYTES);
@@ -257,9 +328,9 @@ __global__ void __launch_bounds__(THREADS, 1) tma_gemm_kernel(const __grid_const
     long long g = 0;
     int t = 0;
     const int sw = (lane >> 1) & 3;  // 64B swizzle of box row `lane`: chunk j at j ^ ((lane >> 1) & 3)
-    for (int tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, ++t) {
+    for (int tile = wstart; tile < nwalk; tile += wstep, ++t) {
       const int buf = t & 1;
-      const int mt = tile / a.ntn, c0 = (tile - mt * a.ntn) * TN;
+      const int mt = row_block(tile), c0 = (tile % a.ntn) * TN;
       tc::mbar_wait(acc_full + 8 * buf, (t >> 1) & 1);
       tc::tc_fence_after();
       for (int c = hh; c < (a.dbg == 1 ? 0 : nch); c += 2, ++g) {
@@ -349,15 +420,16 @@ __global__ void __launch_bounds__(THREADS, 1) tma_gemm_kernel(const __grid_const
       }
       tc::tc_fence_before();
       __syncwarp();
-      if (lane == 0) tc::mbar_arrive(acc_empty + 8 * buf);
+      if (lane == 0) arrive_leader(acc_empty + 8 * buf);
     }
     if (lane == 0) tc::bulk_wait_all();
   }
   tc::tc_fence_before();
-  __syncthreads();
+  if (PAIR) tc::cluster_sync(); else __syncthreads();
   if (warp == 1) {
     tc::tc_fence_after();
-    tc::tmem_dealloc(tmem, 512);
+    if (PAIR) tc::tmem_dealloc_pair(tmem, 512);
+    else tc::tmem_dealloc(tmem, 512);
   }
 }
 
@@ -629,16 +701,49 @@ tlp_status tc_gemm_tma(tlp_ctx* ctx, int64_t M, int64_t N, int64_t K, const floa
     return TLP_ERR_UNSUPPORTED;
   if (a.n_in > 1 && !make_map(&mI1, ins[1], N, M, lds[1], EC, 32, CU_TENSOR_MAP_SWIZZLE_64B))
     return TLP_ERR_UNSUPPORTED;
+  static const char* penv = getenv("TLP_TMA_PAIR");  // cta_group::2 pairs (experiment, default off)
+  const bool pair = penv && penv[0] == '1' && ctx->num_sms >= 2 && M > TM;
+  if (pair) {
+    a.ntiles = (int)(cdiv(M, 2 * TM) * a.ntn);  // 256-row tile pairs
+    const int grid = 2 * (int)std::min<int64_t>(a.ntiles, ctx->num_sms / 2);
+    // (the three kernels share one function-pointer type: no per-call-site
+    // static here -- TLP_SMEM_ATTR would then cover only the first of them)
+    auto launch = [&](auto kern) -> cudaError_t {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_ALLOC);
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)grid);
+      cfg.blockDim = dim3(THREADS);
+      cfg.dynamicSmemBytes = SMEM_ALLOC;
+      cfg.stream = s;
+      cudaLaunchAttribute at[2];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = 2; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+      at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[1].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = at;
+      static const char* ppdl = getenv("TLP_TMA_PAIR_PDL");  // cluster + PDL launch (experiment)
+      cfg.numAttrs = (ppdl && ppdl[0] == '1' && pdl_enabled()) ? 2 : 1;
+      return cudaLaunchKernelEx(&cfg, kern, mA, mI0, mI1, mO, a);
+    };
+    cudaError_t le = a.n_in == 0 ? launch(tma_gemm_kernel<0, true>)
+                   : a.n_in == 1 ? launch(tma_gemm_kernel<1, true>) : launch(tma_gemm_kernel<2, true>);
+    if (le != cudaSuccess) {
+      ctx->last_error = std::string("CUDA launch (tma_gemm pair): ") + cudaGetErrorString(le);
+      return TLP_ERR_CUDA;
+    }
+    TLP_LAUNCH_CHECK();
+    return TLP_OK;
+  }
   const int grid = (int)std::min<int64_t>(a.ntiles, ctx->num_sms);
   if (a.n_in == 0) {
-    TLP_SMEM_ATTR(tma_gemm_kernel<0>, SMEM_ALLOC);
-    TLP_LAUNCH_PDL(tma_gemm_kernel<0>, grid, THREADS, SMEM_ALLOC, s, mA, mI0, mI1, mO, a);
+    TLP_SMEM_ATTR((tma_gemm_kernel<0, false>), SMEM_ALLOC);
+    TLP_LAUNCH_PDL((tma_gemm_kernel<0, false>), grid, THREADS, SMEM_ALLOC, s, mA, mI0, mI1, mO, a);
   } else if (a.n_in == 1) {
-    TLP_SMEM_ATTR(tma_gemm_kernel<1>, SMEM_ALLOC);
-    TLP_LAUNCH_PDL(tma_gemm_kernel<1>, grid, THREADS, SMEM_ALLOC, s, mA, mI0, mI1, mO, a);
+    TLP_SMEM_ATTR((tma_gemm_kernel<1, false>), SMEM_ALLOC);
+    TLP_LAUNCH_PDL((tma_gemm_kernel<1, false>), grid, THREADS, SMEM_ALLOC, s, mA, mI0, mI1, mO, a);
   } else {
-    TLP_SMEM_ATTR(tma_gemm_kernel<2>, SMEM_ALLOC);
-    TLP_LAUNCH_PDL(tma_gemm_kernel<2>, grid, THREADS, SMEM_ALLOC, s, mA, mI0, mI1, mO, a);
+    TLP_SMEM_ATTR((tma_gemm_kernel<2, false>), SMEM_ALLOC);
+    TLP_LAUNCH_PDL((tma_gemm_kernel<2, false>), grid, THREADS, SMEM_ALLOC, s, mA, mI0, mI1, mO, a);
   }
   TLP_LAUNCH_CHECK();
   return TLP_OK;
