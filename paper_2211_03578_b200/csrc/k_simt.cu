@@ -154,8 +154,19 @@ __global__ void reduce_partials(const float* __restrict__ part, int64_t n, int Z
   pdl_trigger();
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n) return;
+  // 16 loads in flight per thread (one partial row per load), then added in
+  // z order: the same fixed-order sum, 16x the memory-level parallelism (a
+  // (K+1) x N output is only ~65K threads -- 14 warps per SM)
   float s = 0.f;
-  for (int z = 0; z < Z; ++z) s += part[(int64_t)z * n + j];
+  int z = 0;
+  for (; z + 16 <= Z; z += 16) {
+    float v[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __ldg(part + (int64_t)(z + i) * n + j);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) s += v[i];
+  }
+  for (; z < Z; ++z) s += part[(int64_t)z * n + j];
   out[j] = s;
 }
 
