@@ -85,22 +85,26 @@ __global__ void __launch_bounds__(kThreads) pair_count_kernel(const float* __res
   float* y = s + cap;
   int* idx = reinterpret_cast<int*>(y + cap);
   const int n = gather_present(nullptr, labels, lo, hi, t, nt, s, y, idx);
-  float cnt = 0.f;  // per-thread count < 2^24 for n <= 8192
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const float yi = y[i];
+  // slice blockIdx.z of the items i (gridDim.z slices: 16 groups alone left
+  // 132 SMs idle), eight threads per i each scanning every eighth j
+  const int S = gridDim.z, sl = blockIdx.z;
+  const int chunk = (n + S - 1) / S, i0 = sl * chunk, i1 = min(n, i0 + chunk);
+  unsigned long long cnt = 0;  // exact integers: any summation order
+  for (int e = threadIdx.x; e < (i1 - i0) * 8; e += blockDim.x) {
+    const float yi = y[i0 + (e >> 3)];
     int c = 0;
-    for (int j = 0; j < n; ++j) c += yi > y[j];
-    cnt += (float)c;
+    for (int j = e & 7; j < n; j += 8) c += yi > y[j];
+    cnt += (unsigned long long)c;
   }
-  // exact integer sum: per-thread counts < 2^24 and the total < 2^26 * 512 fits
-  // in double; reduce in double via two float halves is overkill -> do it in int.
   __shared__ unsigned long long tot;
   if (threadIdx.x == 0) tot = 0;
   __syncthreads();
-  atomicAdd(&tot, (unsigned long long)cnt);
+  atomicAdd(&tot, cnt);
   __syncthreads();
-  if (threadIdx.x == 0) part[(int64_t)t * gridDim.x + g] = (double)tot;
+  if (threadIdx.x == 0) part[((int64_t)t * gridDim.x + g) * S + sl] = (double)tot;
 }
+
+constexpr int kCountSplit = 8;  // pair_count_kernel slices per (group, task)
 
 __global__ void sum_counts(const double* __restrict__ part, int G, int nt,
                            double* __restrict__ counts) {
@@ -108,8 +112,8 @@ __global__ void sum_counts(const double* __restrict__ part, int G, int nt,
   pdl_trigger();
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= nt) return;
-  double s = 0.0;
-  for (int g = 0; g < G; ++g) s += part[(int64_t)t * G + g];
+  double s = 0.0;  // integers < 2^53: exact
+  for (int g = 0; g < G * kCountSplit; ++g) s += part[(int64_t)t * G * kCountSplit + g];
   counts[t] = s;
 }
 
@@ -437,7 +441,7 @@ tlp_status mse_loss_grad(tlp_ctx* ctx, const float* scores, const float* labels,
 }
 
 static size_t rank_ws_bytes(int G, int nt) {
-  return (size_t)G * nt * (sizeof(double) + (1 + 2 * kRankSplit) * sizeof(float)) + 64;
+  return (size_t)G * nt * (kCountSplit * sizeof(double) + (1 + 2 * kRankSplit) * sizeof(float)) + 64;
 }
 
 tlp_status rank_pair_counts(tlp_ctx* ctx, const float* labels, const int64_t* d_goff, int G,
@@ -447,7 +451,7 @@ tlp_status rank_pair_counts(tlp_ctx* ctx, const float* labels, const int64_t* d_
   double* part = ctx->ws_rank.as<double>();
   const size_t smem = (size_t)max_group * (2 * sizeof(float) + sizeof(int));
   cudaFuncSetAttribute(pair_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  TLP_LAUNCH_PDL(pair_count_kernel, dim3(G, nt), kThreads, smem, s, labels, d_goff, nt, part);
+  TLP_LAUNCH_PDL(pair_count_kernel, dim3(G, nt, kCountSplit), kThreads, smem, s, labels, d_goff, nt, part);
   TLP_LAUNCH_CHECK();
   TLP_LAUNCH_PDL(sum_counts, 1, 32, 0, s, part, G, nt, d_counts);
   TLP_LAUNCH_CHECK();
@@ -460,7 +464,7 @@ tlp_status rank_loss_grad(tlp_ctx* ctx, const float* scores, const float* labels
                           cudaStream_t s) {
   const int nt = ctx->cfg.n_tasks;
   TLP_CUDA_TRY(ctx->ws_rank.ensure(rank_ws_bytes(G, nt)));
-  float* loss_part = reinterpret_cast<float*>(ctx->ws_rank.as<char>() + (size_t)G * nt * sizeof(double));
+  float* loss_part = reinterpret_cast<float*>(ctx->ws_rank.as<char>() + (size_t)G * nt * kCountSplit * sizeof(double));
   TLP_CUDA_TRY(cudaMemsetAsync(dscores, 0, (size_t)B * nt * sizeof(float), s));
   const size_t smem = (size_t)max_group * (4 * sizeof(float) + sizeof(int));
   static const char* env = getenv("TLP_RANK_SPLIT");
