@@ -44,31 +44,42 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
 }
 
 // Compact the present items of (group, task) into shared memory, in index order.
+// Block-wide: one item per thread per pass, warp ballots + a prefix over the
+// warps' counts (the single-warp version walked a 512-item group in 16
+// dependent steps and dominated the rank kernels).  Call from every thread.
 __device__ int gather_present(const float* __restrict__ scores, const float* __restrict__ labels,
                               int64_t lo, int64_t hi, int t, int nt, float* s, float* y,
                               int* idx) {
-  __shared__ int base;
-  if (threadIdx.x == 0) base = 0;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    for (int64_t c = lo; c < hi; c += 32) {
-      const int64_t i = c + threadIdx.x;
-      float yi = 0.f, si = 0.f;
-      bool pres = false;
-      if (i < hi) {
-        yi = labels[i * nt + t];
-        si = scores ? scores[i * nt + t] : 0.f;
-        pres = !isnan(yi);
-      }
-      const unsigned m = __ballot_sync(0xffffffffu, pres);
-      const int pos = base + __popc(m & ((1u << threadIdx.x) - 1));
-      if (pres) { s[pos] = si; y[pos] = yi; idx[pos] = (int)(i - lo); }
-      __syncwarp();
-      if (threadIdx.x == 0) base += __popc(m);
-      __syncwarp();
+  __shared__ int wsum[32];  // inclusive prefix of the warps' present counts
+  const int nw = blockDim.x >> 5, w = threadIdx.x >> 5, ln = threadIdx.x & 31;
+  int base = 0;
+  for (int64_t c = lo; c < hi; c += blockDim.x) {
+    const int64_t i = c + threadIdx.x;
+    float yi = 0.f, si = 0.f;
+    bool pres = false;
+    if (i < hi) {
+      yi = labels[i * nt + t];
+      si = scores ? scores[i * nt + t] : 0.f;
+      pres = !isnan(yi);
     }
+    const unsigned m = __ballot_sync(0xffffffffu, pres);
+    if (ln == 0) wsum[w] = __popc(m);
+    __syncthreads();
+    if (w == 0) {
+      int v = ln < nw ? wsum[ln] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, v, o);
+        if (ln >= o) v += u;
+      }
+      if (ln < nw) wsum[ln] = v;
+    }
+    __syncthreads();
+    const int pos = base + (w ? wsum[w - 1] : 0) + __popc(m & ((1u << ln) - 1u));
+    if (pres) { s[pos] = si; y[pos] = yi; idx[pos] = (int)(i - lo); }
+    base += wsum[nw - 1];
+    __syncthreads();
   }
-  __syncthreads();
   return base;
 }
 
