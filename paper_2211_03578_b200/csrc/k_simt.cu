@@ -446,7 +446,15 @@ __global__ void head_pool_kernel(const float* __restrict__ U, int L, int hd, int
   float dot = 0.f;
   for (int k = lane; k < hd; k += 32) {
     float p = 0.f;
-    for (int l = 0; l < L; ++l) p += fmaxf(U[(n * L + l) * hd + k], 0.f);
+    int l = 0;
+    for (; l + 8 <= L; l += 8) {  // 8 row loads in flight, summed in row order
+      float v[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = __ldg(U + (n * L + l + i) * hd + k);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) p += fmaxf(v[i], 0.f);
+    }
+    for (; l < L; ++l) p += fmaxf(U[(n * L + l) * hd + k], 0.f);
     if (pooled) pooled[n * hd + k] = p;
     dot = fmaf(p, w2[k], dot);
   }
@@ -719,7 +727,18 @@ __global__ void wgrad_n1_kernel(int64_t M, int K, const float* __restrict__ A, i
   const int64_t m1 = M < m0 + rows ? M : m0 + rows;
   for (int k = threadIdx.x; k < K; k += blockDim.x) {
     float acc = 0.f;
-    for (int64_t m = m0; m < m1; ++m) acc = fmaf(A[m * lda + k], dY[m * lddy], acc);
+    int64_t m = m0;
+    for (; m + 8 <= m1; m += 8) {  // 8 row loads in flight, then the same fixed-order chain
+      float a[8], d[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        a[i] = __ldg(A + (m + i) * lda + k);
+        d[i] = __ldg(dY + (m + i) * lddy);
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc = fmaf(a[i], d[i], acc);
+    }
+    for (; m < m1; ++m) acc = fmaf(A[m * lda + k], dY[m * lddy], acc);
     part[(int64_t)blockIdx.x * K + k] = acc;
   }
 }
@@ -729,7 +748,7 @@ tlp_status sgemm_wgrad(tlp_ctx* ctx, int64_t M, int64_t K, int64_t N, const floa
   // dW[K,N] = A^T dY with A [M,K] (ld lda), dY [M,N] (ld lddy).  Split over the
   // M rows into Z fixed slices (a function of M only) -> ordered reduction.
   if (N == 1 && K <= 1024) {
-    const int Zn = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(M, 128), 256));
+    const int Zn = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(M, 32), 512));  // slices of 32 rows
     const int64_t rows = cdiv(M, Zn);
     TLP_CUDA_TRY(ctx->ws_partial.ensure((size_t)Zn * K * sizeof(float)));
     float* part = ctx->ws_partial.as<float>();
