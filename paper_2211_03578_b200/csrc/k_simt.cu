@@ -444,6 +444,30 @@ __global__ void head_pool_kernel(const float* __restrict__ U, int L, int hd, int
   const int64_t n = (int64_t)blockIdx.x * (blockDim.x / 32) + w;
   if (n >= N) return;
   float dot = 0.f;
+  if (hd == 128 && ((reinterpret_cast<uintptr_t>(U) | reinterpret_cast<uintptr_t>(w2) |
+                     reinterpret_cast<uintptr_t>(pooled)) & 15) == 0) {
+    // hd = 128: lane owns columns 4 lane .. 4 lane + 3 (16-byte loads)
+    const float4* U4 = reinterpret_cast<const float4*>(U);
+    float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
+    int l = 0;
+    for (; l + 8 <= L; l += 8) {  // 8 row loads in flight, summed in row order
+      float4 v[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = __ldg(U4 + (n * L + l + i) * 32 + lane);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        p.x += fmaxf(v[i].x, 0.f); p.y += fmaxf(v[i].y, 0.f);
+        p.z += fmaxf(v[i].z, 0.f); p.w += fmaxf(v[i].w, 0.f);
+      }
+    }
+    for (; l < L; ++l) {
+      const float4 v = __ldg(U4 + (n * L + l) * 32 + lane);
+      p.x += fmaxf(v.x, 0.f); p.y += fmaxf(v.y, 0.f); p.z += fmaxf(v.z, 0.f); p.w += fmaxf(v.w, 0.f);
+    }
+    if (pooled) reinterpret_cast<float4*>(pooled + n * hd)[lane] = p;
+    const float4 w = __ldg(reinterpret_cast<const float4*>(w2) + lane);
+    dot = fmaf(p.w, w.w, fmaf(p.z, w.z, fmaf(p.y, w.y, p.x * w.x)));
+  } else
   for (int k = lane; k < hd; k += 32) {
     float p = 0.f;
     int l = 0;
