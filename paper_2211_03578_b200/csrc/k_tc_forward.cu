@@ -316,38 +316,13 @@ __device__ __forceinline__ void attn_unit_mma(uint8_t* smem, uint32_t sbase, uin
     }
   float s[4][4];
 #pragma unroll
-  for (int nt = 0; nt < 3; ++nt) {
+  for (int nt = 0; nt < 4; ++nt) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) s[nt][i] = 0.f;
     uint32_t kb[4];  // (ks0: b0,b1) (ks1: b0,b1)
     tc::ldsm_x4(sbase + OFF_K + (k0 + 8 * nt + (lane & 7)) * kRowB + 16 * (lane >> 3), kb);
     tc::mma16816(s[nt], qa[0], kb[0], kb[1]);
     tc::mma16816(s[nt], qa[1], kb[2], kb[3]);
-  }
-  {
-    // n-tile 3 holds one real key (24; kL = 25): its two scores per lane group
-    // on the FMA pipe -- the units' mma.sync share the tensor pipe with the
-    // QKV tcgen05 MMAs, which measurably stretches them.  Lane
-    // (g, t) owns 8 of the 32 dims of rows g and g + 8 (its A fragments); the
-    // quad sums them (bf16 products are exact in fp32, like the MMA's).
-    const uint8_t* k24 = smem + OFF_K + (k0 + 24) * kRowB + 4 * tig;
-    float d0 = 0.f, d1 = 0.f;
-#pragma unroll
-    for (int ks = 0; ks < 2; ++ks)
-#pragma unroll
-      for (int hi = 0; hi < 2; ++hi) {
-        const uint32_t kw = *reinterpret_cast<const uint32_t*>(k24 + 32 * ks + 16 * hi);
-        const float2 kf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&kw));
-        const float2 qg = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&qa[ks][2 * hi]));
-        const float2 qh = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&qa[ks][2 * hi + 1]));
-        d0 = fmaf(qg.y, kf.y, fmaf(qg.x, kf.x, d0));
-        d1 = fmaf(qh.y, kf.y, fmaf(qh.x, kf.x, d1));
-      }
-    d0 += __shfl_xor_sync(0xffffffffu, d0, 1);
-    d1 += __shfl_xor_sync(0xffffffffu, d1, 1);
-    d0 += __shfl_xor_sync(0xffffffffu, d0, 2);
-    d1 += __shfl_xor_sync(0xffffffffu, d1, 2);
-    s[3][0] = d0; s[3][1] = 0.f; s[3][2] = d1; s[3][3] = 0.f;  // key 24 = column 2 tig + e at tig = e = 0
   }
   float inv[2];
 #pragma unroll
