@@ -197,6 +197,26 @@ def test_lambdarank_unit_parity(tp):
     assert not g.cpu().numpy()[np.isnan(y)].any()
 
 
+def test_lambdarank_large_groups_parity(tp):
+    """Groups larger than a block (1,100 and 2,600 items: the present-label
+    compaction and the pair counts take several block-wide passes; the rank
+    kernels split each group over 8 CTAs) with absent labels, vs the oracle."""
+    m = tp.TLP(tp.TLPConfig(precision="fp32", n_tasks=2))
+    rng = np.random.default_rng(7)
+    sizes = [1100, 2600, 33]
+    off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    B = int(off[-1])
+    s = rng.normal(size=(B, 2)).astype(np.float32)
+    y = rng.uniform(0.05, 1.0, (B, 2)).astype(np.float32)
+    y[rng.random(B) < 0.3, 0] = np.nan
+    loss_ref, g_ref = OLR.mtl_lambdarank(s.astype(np.float64), y.astype(np.float64), off)
+    loss, g = m.lambdarank(torch.from_numpy(s).cuda(), torch.from_numpy(y).cuda(), off)
+    m.sync()
+    assert abs(float(loss.cpu()) - loss_ref) <= 1e-5 * abs(loss_ref)
+    assert rel_err(g.cpu().numpy(), g_ref) <= 1e-5
+    assert not g.cpu().numpy()[np.isnan(y)].any()
+
+
 # ---------------------------------------------------------------- training (fp32)
 def train_inputs(tokens, scale, n_tasks=1, seed=31, sizes=(9, 16, 12, 16, 11, 7)):
     off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
