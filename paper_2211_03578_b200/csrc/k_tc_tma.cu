@@ -45,9 +45,14 @@
 namespace {
 
 constexpr int TM = 128, TN = 256, TK = 32;
-constexpr int SA = 3;                        // fp32 A ring (TMA)
-constexpr int SB = 3;                        // B image ring (bulk copies, issued with A)
-constexpr int SC = 2;                        // converted A hi/lo ring (MMA operands)
+#ifndef TLP_TMA_SA  // ring depths (A/B experiments: -DTLP_TMA_SA=.. etc.)
+#define TLP_TMA_SA 3
+#define TLP_TMA_SB 3
+#define TLP_TMA_SC 2
+#endif
+constexpr int SA = TLP_TMA_SA;               // fp32 A ring (TMA)
+constexpr int SB = TLP_TMA_SB;               // B image ring (bulk copies, issued with A)
+constexpr int SC = TLP_TMA_SC;               // converted A hi/lo ring (MMA operands)
 constexpr int SE = 3;                        // epilogue input ring per warp (16-column chunks)
 constexpr int EC = 16;                       // epilogue chunk columns
 constexpr uint32_t A_BYTES = TM * TK * 4;    // 16 KB fp32 tile
