@@ -174,11 +174,18 @@ __global__ void reduce_partials(const float* __restrict__ part, int64_t n, int Z
 __global__ void pad_cols_kernel(const float* __restrict__ X, int64_t M, int E, float* __restrict__ out) {
   pdl_wait();  // TLP_LAUNCH_PDL
   pdl_trigger();
+  // one 16-byte output group (4 columns) per thread: 8 threads per row
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= M * 32) return;
-  const int64_t r = e >> 5;
-  const int c = (int)(e & 31);
-  out[e] = c < E ? X[r * E + c] : 0.f;
+  if (e >= M * 8) return;
+  const int64_t r = e >> 3;
+  const int c = (int)(e & 7) * 4;
+  const float* x = X + r * E;
+  float4 v;
+  v.x = c < E ? __ldg(x + c) : 0.f;
+  v.y = c + 1 < E ? __ldg(x + c + 1) : 0.f;
+  v.z = c + 2 < E ? __ldg(x + c + 2) : 0.f;
+  v.w = c + 3 < E ? __ldg(x + c + 3) : 0.f;
+  reinterpret_cast<float4*>(out)[e] = v;
 }
 
 // The padded first layer's weight + bias partials [Z][Kpad + 1][N] -> the R24
@@ -959,7 +966,7 @@ tlp_status simt_forward(tlp_ctx* ctx, const float* X, int64_t N, float* scores, 
       // E = 22 rows are 88 bytes, which TMA cannot address: one padded copy
       // [M, 32] (zero columns E..31) feeds the first layer's TMA GEMM here and
       // its weight gradient in the backward
-      TLP_LAUNCH_PDL(pad_cols_kernel, (unsigned)cdiv(M * 32, 256), 256, 0, s, h, M, c.E, W + lay.xpad);
+      TLP_LAUNCH_PDL(pad_cols_kernel, (unsigned)cdiv(M * 8, 256), 256, 0, s, h, M, c.E, W + lay.xpad);
       TLP_LAUNCH_CHECK();
       h = W + lay.xpad;
       ldh = 32;
