@@ -224,6 +224,15 @@ __device__ __forceinline__ void slice_of(int n, int sub, int& i0, int& i1) {
   i0 = min(n, sub * per);
   i1 = min(n, i0 + per);
 }
+// threads per item of a slice: the largest power of two <= 32 that still covers
+// the slice's items with the block in one pass (a 512-item group split 8 ways
+// leaves 64 items for 1024 threads: 16 per item, each scanning n / 16 of the
+// j); the per-item partials combine by a fixed butterfly (deterministic)
+__device__ __forceinline__ int threads_per_item(int items) {
+  int tpi = 32;
+  while (tpi > 2 && tpi * items > (int)blockDim.x) tpi >>= 1;
+  return tpi;
+}
 
 __global__ void __launch_bounds__(kRankThreads) rank_prep_kernel(const float* __restrict__ scores,
                                                              const float* __restrict__ labels,
@@ -243,24 +252,26 @@ __global__ void __launch_bounds__(kRankThreads) rank_prep_kernel(const float* __
   const int n = gather_present(scores, labels, lo, hi, t, nt, s, y, idx);
   int i0, i1;
   slice_of(n, sub, i0, i1);
-  const int half = threadIdx.x & 1, nth = blockDim.x >> 1;
-  const int jm = n / 2, j0 = half ? jm : 0, j1 = half ? n : jm;
+  const int tpi = threads_per_item(i1 - i0), lt = 31 - __clz(tpi);
+  const int h = threadIdx.x & (tpi - 1), nth = blockDim.x >> lt;
   float dcg = 0.f;
   for (int base = i0; base < i1; base += nth) {
-    const int i = base + (threadIdx.x >> 1);
+    const int i = base + (threadIdx.x >> lt);
     const bool act = i < i1;
     const float si = act ? s[i] : 0.f, yi = act ? y[i] : 0.f;
     int rs = 0, ry = 0;
     if (act) {
-      for (int j = j0; j < j1; ++j) {
+      for (int j = h; j < n; j += tpi) {  // interleaved j: conflict-free shared reads
         const float sj = s[j], yj = y[j];
         rs += (sj > si) || (sj == si && j < i);
         ry += (yj > yi) || (yj == yi && j < i);
       }
     }
-    rs += __shfl_xor_sync(0xffffffffu, rs, 1);
-    ry += __shfl_xor_sync(0xffffffffu, ry, 1);
-    if (act && half == 0) {
+    for (int o = 1; o < tpi; o <<= 1) {  // exact integer ranks
+      rs += __shfl_xor_sync(0xffffffffu, rs, o);
+      ry += __shfl_xor_sync(0xffffffffu, ry, o);
+    }
+    if (act && h == 0) {
       iD_out[(int64_t)t * goff[gridDim.x / kRankSplit] + lo + i] = 1.0f / log2f(2.0f + (float)rs);
       dcg += expm1f(yi * kLn2) / log2f(2.0f + (float)ry);
     }
@@ -301,16 +312,16 @@ __global__ void __launch_bounds__(kRankThreads) rank_pair_kernel(const float* __
   __syncthreads();
   int i0, i1;
   slice_of(n, sub, i0, i1);
-  const int half = threadIdx.x & 1, nth = blockDim.x >> 1;
-  const int jm = n / 2, j0 = half ? jm : 0, j1 = half ? n : jm;
+  const int tpi = threads_per_item(i1 - i0), lt = 31 - __clz(tpi);
+  const int h = threadIdx.x & (tpi - 1), nth = blockDim.x >> lt;
   float lsum = 0.f;
   for (int base = i0; base < i1; base += nth) {
-    const int i = base + (threadIdx.x >> 1);
+    const int i = base + (threadIdx.x >> lt);
     const bool act = i < i1;
     float gi = 0.f, li = 0.f;
     if (act) {
       const float si = s[i], yi = y[i], Gi = Gs[i], iDi = iD[i];
-      for (int j = j0; j < j1; ++j) {
+      for (int j = h; j < n; j += tpi) {  // interleaved j: conflict-free shared reads
         const float yj = y[j];
         if (yi == yj) continue;
         const float w = fabsf(Gi - Gs[j]) * fabsf(iDi - iD[j]);
@@ -326,9 +337,11 @@ __global__ void __launch_bounds__(kRankThreads) rank_pair_kernel(const float* __
         }
       }
     }
-    gi += __shfl_xor_sync(0xffffffffu, gi, 1);
-    li += __shfl_xor_sync(0xffffffffu, li, 1);
-    if (act && half == 0) {
+    for (int o = 1; o < tpi; o <<= 1) {  // fixed butterfly over the item's threads
+      gi += __shfl_xor_sync(0xffffffffu, gi, o);
+      li += __shfl_xor_sync(0xffffffffu, li, o);
+    }
+    if (act && h == 0) {
       dscores[(lo + idx[i]) * nt + t] = gi * kInvLn2;
       lsum += li * kInvLn2;
     }
