@@ -110,7 +110,11 @@ __global__ void __launch_bounds__(kThreads) pair_count_kernel(const float* __res
   __shared__ unsigned long long tot;
   if (threadIdx.x == 0) tot = 0;
   __syncthreads();
-  atomicAdd(&tot, cnt);
+  // warp sums first: one shared 64-bit atomic per warp (512 on one address
+  // serialise) -- exact integers, any order
+#pragma unroll
+  for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(&tot, cnt);
   __syncthreads();
   if (threadIdx.x == 0) part[((int64_t)t * gridDim.x + g) * S + sl] = (double)tot;
 }
