@@ -214,7 +214,7 @@ void tlp_destroy(tlp_ctx* ctx) {
   cudaFree(ctx->d_tblob); cudaFree(ctx->d_toff);
   for (DevBuf* b : {&ctx->ws_tokens, &ctx->ws_act, &ctx->ws_train, &ctx->ws_rank, &ctx->ws_topk,
                     &ctx->ws_misc, &ctx->ws_partial, &ctx->ws_merge, &ctx->ws_round_in,
-                    &ctx->ws_round_feats, &ctx->ws_round_scores, &ctx->ws_bimg, &ctx->ws_wcat})
+                    &ctx->ws_round_feats, &ctx->ws_round_scores, &ctx->ws_bimg, &ctx->ws_wcat, &ctx->ws_hcat})
     b->release();
   for (cudaEvent_t& e : ctx->round_ev)
     if (e) cudaEventDestroy(e);

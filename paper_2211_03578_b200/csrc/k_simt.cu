@@ -441,7 +441,7 @@ __global__ void __launch_bounds__(64) attn_bwd_kernel(const float* __restrict__ 
 
 // ---------------------------------------------------------------------------
 // head: pooled[n,k] = sum_l relu(U[n*L+l, k]); s[n,t] = pooled . w2 + L c2
-__global__ void head_pool_kernel(const float* __restrict__ U, int L, int hd, int64_t N,
+__global__ void head_pool_kernel(const float* __restrict__ U, int64_t uld, int L, int hd, int64_t N,
                                  const float* __restrict__ w2, const float* __restrict__ c2,
                                  int t, int nt, float* __restrict__ pooled,
                                  float* __restrict__ scores) {
@@ -451,8 +451,8 @@ __global__ void head_pool_kernel(const float* __restrict__ U, int L, int hd, int
   const int64_t n = (int64_t)blockIdx.x * (blockDim.x / 32) + w;
   if (n >= N) return;
   float dot = 0.f;
-  if (hd == 128 && ((reinterpret_cast<uintptr_t>(U) | reinterpret_cast<uintptr_t>(w2) |
-                     reinterpret_cast<uintptr_t>(pooled)) & 15) == 0) {
+  if (hd == 128 && uld % 4 == 0 && ((reinterpret_cast<uintptr_t>(U) | reinterpret_cast<uintptr_t>(w2) |
+                                     reinterpret_cast<uintptr_t>(pooled)) & 15) == 0) {
     // hd = 128: lane owns columns 4 lane .. 4 lane + 3 (16-byte loads)
     const float4* U4 = reinterpret_cast<const float4*>(U);
     float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -460,7 +460,7 @@ __global__ void head_pool_kernel(const float* __restrict__ U, int L, int hd, int
     for (; l + 8 <= L; l += 8) {  // 8 row loads in flight, summed in row order
       float4 v[8];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) v[i] = __ldg(U4 + (n * L + l + i) * 32 + lane);
+      for (int i = 0; i < 8; ++i) v[i] = __ldg(U4 + (n * L + l + i) * (uld >> 2) + lane);
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         p.x += fmaxf(v[i].x, 0.f); p.y += fmaxf(v[i].y, 0.f);
@@ -468,7 +468,7 @@ __global__ void head_pool_kernel(const float* __restrict__ U, int L, int hd, int
       }
     }
     for (; l < L; ++l) {
-      const float4 v = __ldg(U4 + (n * L + l) * 32 + lane);
+      const float4 v = __ldg(U4 + (n * L + l) * (uld >> 2) + lane);
       p.x += fmaxf(v.x, 0.f); p.y += fmaxf(v.y, 0.f); p.z += fmaxf(v.z, 0.f); p.w += fmaxf(v.w, 0.f);
     }
     if (pooled) reinterpret_cast<float4*>(pooled + n * hd)[lane] = p;
@@ -481,11 +481,11 @@ __global__ void head_pool_kernel(const float* __restrict__ U, int L, int hd, int
     for (; l + 8 <= L; l += 8) {  // 8 row loads in flight, summed in row order
       float v[8];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) v[i] = __ldg(U + (n * L + l + i) * hd + k);
+      for (int i = 0; i < 8; ++i) v[i] = __ldg(U + (n * L + l + i) * uld + k);
 #pragma unroll
       for (int i = 0; i < 8; ++i) p += fmaxf(v[i], 0.f);
     }
-    for (; l < L; ++l) p += fmaxf(U[(n * L + l) * hd + k], 0.f);
+    for (; l < L; ++l) p += fmaxf(U[(n * L + l) * uld + k], 0.f);
     if (pooled) pooled[n * hd + k] = p;
     dot = fmaf(p, w2[k], dot);
   }
@@ -494,7 +494,7 @@ __global__ void head_pool_kernel(const float* __restrict__ U, int L, int hd, int
 }
 
 // dU[n*L+l, k] = g[n,t] * w2[k] * (U > 0)
-__global__ void head_bwd_kernel(const float* __restrict__ U, int L, int hd, int64_t N,
+__global__ void head_bwd_kernel(const float* __restrict__ U, int64_t uld, int L, int hd, int64_t N,
                                 const float* __restrict__ w2, const float* __restrict__ g, int t,
                                 int nt, float* __restrict__ dU, int vec) {
   pdl_wait();  // TLP_LAUNCH_PDL
@@ -506,17 +506,18 @@ __global__ void head_bwd_kernel(const float* __restrict__ U, int L, int hd, int6
     const int64_t row = e4 / q;
     const int k = (int)(e4 - row * q) * 4;
     const float gn = __ldg(g + (row / L) * nt + t);
-    const float4 u = __ldg(reinterpret_cast<const float4*>(U) + e4);
+    const int64_t o4 = (row * uld + k) >> 2;  // U and dU share the row stride
+    const float4 u = __ldg(reinterpret_cast<const float4*>(U) + o4);
     const float4 w = __ldg(reinterpret_cast<const float4*>(w2 + k));
-    reinterpret_cast<float4*>(dU)[e4] = make_float4(u.x > 0.f ? gn * w.x : 0.f, u.y > 0.f ? gn * w.y : 0.f,
+    reinterpret_cast<float4*>(dU)[o4] = make_float4(u.x > 0.f ? gn * w.x : 0.f, u.y > 0.f ? gn * w.y : 0.f,
                                                     u.z > 0.f ? gn * w.z : 0.f, u.w > 0.f ? gn * w.w : 0.f);
     return;
   }
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= N * L * hd) return;
   const int k = (int)(e % hd);
-  const int64_t n = e / ((int64_t)L * hd);
-  dU[e] = U[e] > 0.f ? g[n * nt + t] * w2[k] : 0.f;
+  const int64_t row = e / hd, n = row / L, o = row * uld + k;
+  dU[o] = U[o] > 0.f ? g[n * nt + t] * w2[k] : 0.f;
 }
 
 // Wcat = [Wq | Wk | Wv] rows side by side, then [bq | bk | bv] (the fused Q/K/V
@@ -535,6 +536,24 @@ __global__ void pack_wcat_kernel(const float* __restrict__ P, int64_t w0, int64_
   } else if (e < nW + H3) {
     const int c = (int)(e - nW), j = c / H, k = c - j * H;
     wcat[e] = P[(j == 0 ? b0 : j == 1 ? b1 : b2) + k];
+  }
+}
+
+// [W1_0 | W1_1 | ...] ([H, nt hd], row stride nt hd) then [c1_0 | c1_1 | ...]
+struct HeadOffs { int64_t w[TLP_MAX_TASKS], c[TLP_MAX_TASKS]; };
+__global__ void pack_heads_kernel(const float* __restrict__ P, HeadOffs o, int nt, int H, int hd,
+                                  float* __restrict__ out) {
+  pdl_wait();  // TLP_LAUNCH_PDL
+  pdl_trigger();
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t W = (int64_t)nt * hd, nW = (int64_t)H * W;
+  if (e < nW) {
+    const int64_t i = e / W;
+    const int cc = (int)(e - i * W), t = cc / hd, k = cc - t * hd;
+    out[e] = P[o.w[t] + i * hd + k];
+  } else if (e < nW + W) {
+    const int cc = (int)(e - nW), t = cc / hd, k = cc - t * hd;
+    out[e] = P[o.c[t] + k];
   }
 }
 
@@ -655,7 +674,10 @@ ActLayout act_layout(const tlp_config& c, int64_t N) {
     a.hattn[l] = take(M * H);
   }
   for (int r = 0; r < c.n_res; ++r) { a.r[r] = take(M * H); a.hres[r] = take(M * H); }
-  for (int t = 0; t < c.n_tasks; ++t) { a.U[t] = take(M * c.head_dim); a.pooled[t] = take(N * c.head_dim); }
+  // the heads' first-layer outputs side by side, [M, n_tasks hd] (row stride
+  // uld): one GEMM for every task's first layer, one K = n_tasks hd dgrad
+  const int64_t ucat = take(M * c.n_tasks * c.head_dim);
+  for (int t = 0; t < c.n_tasks; ++t) { a.U[t] = ucat + t * c.head_dim; a.pooled[t] = take(N * c.head_dim); }
   a.kvalid = take(M);
   a.hpos = take(M * H);
   a.xpad = (c.precision == TLP_PREC_BF16 && c.E % 4 != 0 && c.E <= 32) ? take(M * 32) : -1;
@@ -663,7 +685,7 @@ ActLayout act_layout(const tlp_config& c, int64_t N) {
   a.dh = take(M * H);
   a.dtmp = take(M * std::max<int64_t>(H, c.up_dims[0]));
   a.dqkv = take(M * 3 * H);
-  a.dU = take(M * c.head_dim);
+  a.dU = take(M * c.n_tasks * c.head_dim);  // [M, n_tasks hd] like U
   if (c.backbone == 1 && c.n_attn > 0) {
     a.dG = take(M * 4 * H);
     a.dcar = take(N * H);
@@ -939,6 +961,11 @@ tlp_status colsum(tlp_ctx* ctx, int64_t M, int64_t N, const float* X, int64_t ld
 
 #define TRY(x) do { tlp_status _s = (x); if (_s != TLP_OK) return _s; } while (0)
 
+static bool heads_cat(const tlp_config& c) {
+  const int64_t uld = (int64_t)c.n_tasks * c.head_dim;
+  return c.n_tasks > 1 && (uld <= 256 || uld % 256 == 0);
+}
+
 tlp_status simt_forward(tlp_ctx* ctx, const float* X, int64_t N, float* scores, bool save,
                         cudaStream_t s) {
   const tlp_config& c = ctx->cfg;
@@ -951,6 +978,18 @@ tlp_status simt_forward(tlp_ctx* ctx, const float* X, int64_t N, float* scores, 
   ActLayout lay = act_layout(c, chunk);
   TLP_CUDA_TRY(ctx->ws_act.ensure((size_t)(save ? lay.total : lay.total_fwd) * sizeof(float)));
   float* W = ctx->ws_act.as<float>();
+  // MTL: the heads' first layers side by side (one N = n_tasks hd GEMM) when
+  // the TMA GEMM takes that width (<= 256 or a multiple of 256)
+  const bool hcat = heads_cat(c);
+  if (hcat) {
+    const int64_t uld = (int64_t)c.n_tasks * c.head_dim;
+    TLP_CUDA_TRY(ctx->ws_hcat.ensure((size_t)(H * uld + uld) * sizeof(float)));
+    HeadOffs ho{};
+    for (int t = 0; t < c.n_tasks; ++t) { ho.w[t] = o.W1[t]; ho.c[t] = o.c1[t]; }
+    TLP_LAUNCH_PDL(pack_heads_kernel, (unsigned)cdiv(H * uld + uld, 256), 256, 0, s, P, ho, c.n_tasks, (int)H,
+                   c.head_dim, ctx->ws_hcat.as<float>());
+    TLP_LAUNCH_CHECK();
+  }
   for (int64_t n0 = 0; n0 < N; n0 += chunk) {
     const int64_t n = std::min(chunk, N - n0);
     const int64_t M = n * c.L;
@@ -1030,12 +1069,19 @@ tlp_status simt_forward(tlp_ctx* ctx, const float* X, int64_t N, float* scores, 
       TRY(sgemm(ctx, false, false, M, H, H, W + lay.r[r], H, P + o.Wb[r], H, W + lay.hres[r], H, e2, s));
       h = W + lay.hres[r];
     }
+    const int64_t uld = (int64_t)c.n_tasks * c.head_dim;
+    if (hcat) {  // every task's first head layer as ONE GEMM (h read once)
+      EpiParams e; e.bias = ctx->ws_hcat.as<float>() + H * uld;
+      TRY(sgemm(ctx, false, false, M, uld, H, h, H, ctx->ws_hcat.as<float>(), uld, W + lay.U[0], uld, e, s));
+    }
     for (int t = 0; t < c.n_tasks; ++t) {
-      EpiParams e; e.bias = P + o.c1[t];
-      TRY(sgemm(ctx, false, false, M, c.head_dim, H, h, H, P + o.W1[t], c.head_dim, W + lay.U[t],
-                c.head_dim, e, s));
+      if (!hcat) {
+        EpiParams e; e.bias = P + o.c1[t];
+        TRY(sgemm(ctx, false, false, M, c.head_dim, H, h, H, P + o.W1[t], c.head_dim, W + lay.U[t],
+                  uld, e, s));
+      }
       TLP_LAUNCH_PDL(head_pool_kernel, (unsigned)cdiv(n, 8), 256, 0, s, 
-          W + lay.U[t], c.L, c.head_dim, n, P + o.w2[t], P + o.c2[t], t, c.n_tasks,
+          W + lay.U[t], uld, c.L, c.head_dim, n, P + o.w2[t], P + o.c2[t], t, c.n_tasks,
           save ? W + lay.pooled[t] : nullptr, scores + n0 * c.n_tasks);
       TLP_LAUNCH_CHECK();
     }
@@ -1062,20 +1108,36 @@ tlp_status simt_backward(tlp_ctx* ctx, int64_t N, const float* g, cudaStream_t s
   float* dU = W + lay.dU;
   const float* hfin = c.n_res ? W + lay.hres[c.n_res - 1]
                     : (c.n_attn ? W + lay.hattn[c.n_attn - 1] : (c.pos_enc ? W + lay.hpos : W + lay.up[c.n_up - 1]));
-  // heads
+  // heads (dU of task t at columns [t hd, t hd + hd) of a [M, n_tasks hd] block)
+  const int64_t uld = (int64_t)c.n_tasks * hd;
+  const bool hcat = heads_cat(c);
+  bool w1c1 = true;  // R24: c1_t right after W1_t (one shared-X weight-gradient launch)
+  for (int t = 0; t < c.n_tasks; ++t) w1c1 &= o.c1[t] == o.W1[t] + H * hd;
   for (int t = 0; t < c.n_tasks; ++t) {
     // (the float4 path needs 16-byte aligned U / dU / w2: act_layout slots are
     // 64-float aligned; w2's flat offset may not be)
     const bool v4 = hd % 4 == 0 && (reinterpret_cast<uintptr_t>(P + o.w2[t]) & 15) == 0;
     TLP_LAUNCH_PDL(head_bwd_kernel, (unsigned)cdiv(v4 ? M * hd / 4 : M * hd, 256), 256, 0, s, 
-        W + lay.U[t], c.L, hd, N, P + o.w2[t], g, t, c.n_tasks, dU, v4 ? 1 : 0);
+        W + lay.U[t], uld, c.L, hd, N, P + o.w2[t], g, t, c.n_tasks, dU + t * hd, v4 ? 1 : 0);
     TLP_LAUNCH_CHECK();
-    TRY(sgemm_wgrad_bias(ctx, M, H, hd, hfin, H, dU, hd, G + o.W1[t], G + o.c1[t], s));
+    if (!(hcat && w1c1))
+      TRY(sgemm_wgrad_bias(ctx, M, H, hd, hfin, H, dU + t * hd, uld, G + o.W1[t], G + o.c1[t], s));
     TRY(sgemm_wgrad(ctx, N, hd, 1, W + lay.pooled[t], hd, g + t, c.n_tasks, G + o.w2[t], s));
     TLP_LAUNCH_PDL(dc2_kernel, 1, 256, 0, s, g, N, t, c.n_tasks, c.L, G + o.c2[t]);
     TLP_LAUNCH_CHECK();
-    EpiParams e; e.accumulate = t > 0;
-    TRY(sgemm(ctx, false, true, M, H, hd, dU, hd, P + o.W1[t], hd, dh, H, e, s));
+    if (!hcat) {
+      EpiParams e; e.accumulate = t > 0;
+      TRY(sgemm(ctx, false, true, M, H, hd, dU + t * hd, uld, P + o.W1[t], hd, dh, H, e, s));
+    }
+  }
+  if (hcat && w1c1) {  // every task's W1 | c1 gradient from one pass over hfin
+    float* dws[TLP_MAX_TASKS];
+    for (int t = 0; t < c.n_tasks; ++t) dws[t] = G + o.W1[t];
+    TRY(sgemm_wgrad_bias_shared(ctx, c.n_tasks, M, H, hd, hfin, H, dU, uld, hd, dws, s));
+  }
+  if (hcat) {  // dh = [dU_0 | dU_1 | ...] [W1_0 | W1_1 | ...]^T: one K = n_tasks hd GEMM
+    EpiParams e;
+    TRY(sgemm(ctx, false, true, M, H, uld, dU, uld, ctx->ws_hcat.as<float>(), uld, dh, H, e, s));
   }
   // C-1 buckets in reverse R24 order: heads | residual blocks | attention (or
   // LSTM) layers | upsample + positional table

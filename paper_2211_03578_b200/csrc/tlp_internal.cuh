@@ -92,6 +92,7 @@ struct tlp_ctx {
   // workspaces
   DevBuf ws_tokens, ws_act, ws_train, ws_rank, ws_topk, ws_misc, ws_partial, ws_merge;
   DevBuf ws_bimg;  // bf16 hi/lo image of a training GEMM's weight operand (k_tc_gemm.cu)
+  DevBuf ws_hcat;  // MTL heads side by side: [W1_0 | W1_1 | ...] [H, nt hd] then [c1_0 | c1_1 | ...]
   DevBuf ws_wcat;  // per attention layer [Wq | Wk | Wv] rows side by side, then [bq | bk | bv]:
                   // the fused Q/K/V forward GEMM and dgrad operands (k_simt.cu)
 
