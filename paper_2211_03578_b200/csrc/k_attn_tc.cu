@@ -16,8 +16,8 @@
 //           (transposed operands are read from smem by index)
 // backward: one (candidate, head) per block of 4 warps, one 16 x 16 quadrant
 // each (a 4-warp forward measured slower: 344 vs 291 us per step).
-// Operands staged in smem as fp32 [32][36] (row stride 36 floats: the fragment
-// reads (4g + tig) mod 32 are bank-conflict free).
+// Operands staged in smem as fp32 [32][LD] (LD = 36 or 40 per access pattern,
+// below).
 #include "tlp_internal.cuh"
 
 namespace {
@@ -25,10 +25,11 @@ namespace {
 // Row strides of the staged fp32 [32][LD] matrices: an operand read with rows
 // on the lane's group id g and columns on its thread-in-group t (X[g][t]) is
 // bank-conflict free at LD = 36 (36 g + t distinct mod 32), one read
-// transposed (X[t][g]) at LD = 40 (40 t + g distinct): the forward's V (only
-// read transposed, by O = P V) is staged at LD = 40.  (The backward with Q, K
-// at LD = 40 and transposed copies of dS, A, dO measured slower: 25% fewer
-// conflicts but a lower occupancy and the extra transposes.)
+// transposed (X[t][g]) at LD = 40 (40 t + g distinct): the forward's V (read
+// transposed by O = P V) and the backward's Q, K (read transposed only) and A
+// (transposed by dV = A^T dO) are staged at LD = 40.  (Transposed copies of
+// dS, A and dO as well measured slower: 25% fewer conflicts but a lower
+// occupancy and the extra transposes.)
 constexpr int DH = 32, LP = 32, LD = 36, LDT = 40;
 constexpr int MAT = LP * LD;    // floats per staged matrix
 constexpr int MATT = LP * LDT;  // ... read transposed
