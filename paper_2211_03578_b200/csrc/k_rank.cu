@@ -132,7 +132,7 @@ __global__ void sum_counts(const double* __restrict__ part, int G, int nt,
   counts[t] = s;
 }
 
-constexpr int kRankThreads = 1024;  // two threads per item of a 512-item group
+constexpr int kRankThreads = 1024;  // rank_kernel: two threads per item of a 512-item group; the split kernels size it to the slice
 
 __global__ void __launch_bounds__(kRankThreads) rank_kernel(const float* __restrict__ scores,
                                                         const float* __restrict__ labels,
