@@ -61,9 +61,43 @@ __global__ void __launch_bounds__(kThreads) topk_chunk_kernel(
     si[j] = id;
   }
   __syncthreads();
-  // bitonic sort, "better" first
-  for (int size = 2; size <= kChunk; size <<= 1) {
-    for (int half = size >> 1; half > 0; half >>= 1) {
+  // bitonic sort, "better" first.  Thread = warp w, lane l holds elements
+  // e = 64 w + 2 l + b (b = 0, 1) in registers: every stage with half <= 32
+  // pairs elements of one warp (half 1: inside the thread; 2..32: partner lane
+  // l ^ half / 2, by shuffles), only half >= 64 goes through shared memory
+  // (15 block barriers instead of 66).  Same network, same result.
+  const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
+  const int e0 = 64 * w + 2 * ln;
+  float rs[2] = {ss[e0], ss[e0 + 1]};
+  int64_t ri[2] = {si[e0], si[e0 + 1]};
+  auto warp_stages = [&](int size, int top) {
+    for (int half = top; half >= 2; half >>= 1) {
+      const int lm = half >> 1;
+      const bool lower = (ln & lm) == 0;
+      const bool up = (e0 & size) == 0;
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        const float ps = __shfl_xor_sync(0xffffffffu, rs[b], lm);
+        const int64_t pi = __shfl_xor_sync(0xffffffffu, ri[b], lm);
+        // the lower element keeps the better (up) / worse (down) of the pair
+        const bool take = lower == up ? better(ps, pi, rs[b], ri[b]) : better(rs[b], ri[b], ps, pi);
+        if (take) { rs[b] = ps; ri[b] = pi; }
+      }
+    }
+    {  // half = 1: both elements in this thread
+      const bool up = (e0 & size) == 0;
+      const bool swap = up ? better(rs[1], ri[1], rs[0], ri[0]) : better(rs[0], ri[0], rs[1], ri[1]);
+      if (swap) {
+        const float ts = rs[0]; rs[0] = rs[1]; rs[1] = ts;
+        const int64_t ti = ri[0]; ri[0] = ri[1]; ri[1] = ti;
+      }
+    }
+  };
+  for (int size = 2; size <= 64; size <<= 1) warp_stages(size, size >> 1);
+  for (int size = 128; size <= kChunk; size <<= 1) {
+    ss[e0] = rs[0]; ss[e0 + 1] = rs[1]; si[e0] = ri[0]; si[e0 + 1] = ri[1];
+    __syncthreads();
+    for (int half = size >> 1; half >= 64; half >>= 1) {
       const int t = threadIdx.x;  // kChunk / 2 compare-exchanges
       const int i = 2 * half * (t / half) + (t % half);
       const int j = i + half;
@@ -74,7 +108,12 @@ __global__ void __launch_bounds__(kThreads) topk_chunk_kernel(
       if (swap) { ss[i] = b; ss[j] = a; si[i] = bi; si[j] = ai; }
       __syncthreads();
     }
+    rs[0] = ss[e0]; rs[1] = ss[e0 + 1]; ri[0] = si[e0]; ri[1] = si[e0 + 1];
+    __syncthreads();  // the next size's stores follow every thread's reads
+    warp_stages(size, 32);
   }
+  ss[e0] = rs[0]; ss[e0 + 1] = rs[1]; si[e0] = ri[0]; si[e0 + 1] = ri[1];
+  __syncthreads();
   for (int j = threadIdx.x; j < k; j += blockDim.x) {
     const int64_t o = (int64_t)it.out * k + j;
     if (j < kChunk && si[j] >= 0) { out_s[o] = ss[j]; out_i[o] = si[j]; }
