@@ -43,33 +43,14 @@ __global__ void __launch_bounds__(kThreads) topk_chunk_kernel(
   __shared__ float ss[kChunk];
   __shared__ int64_t si[kChunk];
   const WorkItem it = items[blockIdx.x];
-  for (int j = threadIdx.x; j < kChunk; j += blockDim.x) {
-    float s = -INFINITY;
-    int64_t id = -1;
-    if (j < it.count) {
-      if (round0) {
-        const int64_t row = it.start + j;
-        s = scores[row * stride + head];
-        id = base + row;
-        if (isnan(s)) atomicOr(err, DERR_NONFINITE);
-      } else {
-        s = in_s[it.start + j];
-        id = in_i[it.start + j];
-      }
-    }
-    ss[j] = s;
-    si[j] = id;
-  }
-  __syncthreads();
-  // bitonic sort, "better" first.  Thread = warp w, lane l holds elements
-  // e = 64 w + 2 l + b (b = 0, 1) in registers: every stage with half <= 32
-  // pairs elements of one warp (half 1: inside the thread; 2..32: partner lane
-  // l ^ half / 2, by shuffles), only half >= 64 goes through shared memory
-  // (15 block barriers instead of 66).  Same network, same result.
+  // Thread = warp w, lane l holds elements e = 64 w + 2 l + b (b = 0, 1) in
+  // registers during the bitonic sort below; every stage with half <= 32 pairs
+  // elements of one warp (half 1: inside the thread; 2..32: partner lane
+  // l ^ half / 2, by shuffles).
   const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
   const int e0 = 64 * w + 2 * ln;
-  float rs[2] = {ss[e0], ss[e0 + 1]};
-  int64_t ri[2] = {si[e0], si[e0 + 1]};
+  float rs[2];
+  int64_t ri[2];
   auto warp_stages = [&](int size, int top) {
     for (int half = top; half >= 2; half >>= 1) {
       const int lm = half >> 1;
@@ -93,6 +74,53 @@ __global__ void __launch_bounds__(kThreads) topk_chunk_kernel(
       }
     }
   };
+  if (it.count <= 64 && !round0) {
+    // a merge chunk of <= 64 survivors (later rounds): one warp, registers only
+    if (w != 0) return;
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      const int j = 2 * ln + b;
+      rs[b] = j < it.count ? in_s[it.start + j] : -INFINITY;
+      ri[b] = j < it.count ? in_i[it.start + j] : -1;
+    }
+    for (int size = 2; size <= 64; size <<= 1) warp_stages(size, size >> 1);
+    for (int jb = 0; jb < k; jb += 32) {  // (uniform trip count: every lane shuffles)
+      const int j = jb + ln;              // element j sits in lane j / 2, slot j % 2
+      const int src = (j < 64 ? j : 0) >> 1;
+      const float s0 = __shfl_sync(0xffffffffu, rs[0], src), s1 = __shfl_sync(0xffffffffu, rs[1], src);
+      const int64_t i0 = __shfl_sync(0xffffffffu, ri[0], src), i1 = __shfl_sync(0xffffffffu, ri[1], src);
+      const float sv = (j & 1) ? s1 : s0;
+      const int64_t iv = (j & 1) ? i1 : i0;
+      if (j >= k) continue;
+      const int64_t o = (int64_t)it.out * k + j;
+      if (j < 64 && iv >= 0) { out_s[o] = sv; out_i[o] = iv; }
+      else { out_s[o] = -INFINITY; out_i[o] = -1; }
+    }
+    return;
+  }
+  for (int j = threadIdx.x; j < kChunk; j += blockDim.x) {
+    float s = -INFINITY;
+    int64_t id = -1;
+    if (j < it.count) {
+      if (round0) {
+        const int64_t row = it.start + j;
+        s = scores[row * stride + head];
+        id = base + row;
+        if (isnan(s)) atomicOr(err, DERR_NONFINITE);
+      } else {
+        s = in_s[it.start + j];
+        id = in_i[it.start + j];
+      }
+    }
+    ss[j] = s;
+    si[j] = id;
+  }
+  __syncthreads();
+  // bitonic sort, "better" first: the warp stages above for half <= 32, only
+  // half >= 64 goes through shared memory (15 block barriers instead of 66).
+  // Same network, same result.
+  rs[0] = ss[e0]; rs[1] = ss[e0 + 1];
+  ri[0] = si[e0]; ri[1] = si[e0 + 1];
   for (int size = 2; size <= 64; size <<= 1) warp_stages(size, size >> 1);
   for (int size = 128; size <= kChunk; size <<= 1) {
     ss[e0] = rs[0]; ss[e0 + 1] = rs[1]; si[e0] = ri[0]; si[e0 + 1] = ri[1];
