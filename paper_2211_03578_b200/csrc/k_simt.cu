@@ -978,6 +978,18 @@ tlp_status simt_forward(tlp_ctx* ctx, const float* X, int64_t N, float* scores, 
   ActLayout lay = act_layout(c, chunk);
   TLP_CUDA_TRY(ctx->ws_act.ensure((size_t)(save ? lay.total : lay.total_fwd) * sizeof(float)));
   float* W = ctx->ws_act.as<float>();
+  // Wcat[i][jH + k] = W_j[i][k] per attention layer, packed up front: the
+  // weight images of the GEMMs are built ahead of their GEMMs (bimg_kernel)
+  // and must only read operands final since the step began
+  if (c.n_attn && c.backbone == 0) {
+    const int64_t wcat_stride = ((3 * H * H + 3 * H) + 63) / 64 * 64;  // floats per layer
+    TLP_CUDA_TRY(ctx->ws_wcat.ensure((size_t)c.n_attn * wcat_stride * sizeof(float)));
+    for (int l = 0; l < c.n_attn; ++l) {
+      TLP_LAUNCH_PDL(pack_wcat_kernel, (unsigned)cdiv(3 * H * H + 3 * H, 256), 256, 0, s, P, o.Wq[l], o.Wk[l],
+                     o.Wv[l], o.bq[l], o.bk[l], o.bv[l], (int)H, ctx->ws_wcat.as<float>() + l * wcat_stride);
+      TLP_LAUNCH_CHECK();
+    }
+  }
   // MTL: the heads' first layers side by side (one N = n_tasks hd GEMM) when
   // the TMA GEMM takes that width (<= 256 or a multiple of 256)
   const bool hcat = heads_cat(c);
@@ -1043,18 +1055,12 @@ tlp_status simt_forward(tlp_ctx* ctx, const float* X, int64_t N, float* scores, 
       h = W + lay.hattn[l];
     }
     const int64_t wcat_stride = ((3 * H * H + 3 * H) + 63) / 64 * 64;  // floats per layer
-    if (c.n_attn && c.backbone == 0)
-      TLP_CUDA_TRY(ctx->ws_wcat.ensure((size_t)c.n_attn * wcat_stride * sizeof(float)));
     for (int l = 0; l < c.n_attn && c.backbone == 0; ++l) {
       float* qkv = W + lay.qkv[l];
-      const int64_t wq[3] = {o.Wq[l], o.Wk[l], o.Wv[l]}, bq[3] = {o.bq[l], o.bk[l], o.bv[l]};
       // [Q | K | V] = h [Wq | Wk | Wv] + [bq | bk | bv] as ONE N = 3H GEMM (h read
-      // once); Wcat[i][jH + k] = W_j[i][k], kept for the backward's fused dgrad
+      // once); Wcat (packed before the chunk loop) kept for the backward's fused dgrad
       float* wcat = ctx->ws_wcat.as<float>() + l * wcat_stride;
       float* bcat = wcat + 3 * H * H;
-      TLP_LAUNCH_PDL(pack_wcat_kernel, (unsigned)cdiv(3 * H * H + 3 * H, 256), 256, 0, s, P, wq[0], wq[1],
-                     wq[2], bq[0], bq[1], bq[2], (int)H, wcat);
-      TLP_LAUNCH_CHECK();
       EpiParams eq; eq.bias = bcat;
       TRY(sgemm(ctx, false, false, M, 3 * H, H, h, H, wcat, 3 * H, qkv, 3 * H, eq, s));
       TRY(attn_fwd(ctx, qkv, n, W + lay.O[l], save ? W + lay.A[l] : nullptr, kvalid, s));

@@ -335,9 +335,37 @@ constexpr uint32_t ISMEM = STAGES * ISTAGE + 128;
 // blockIdx.x = k-block, blockIdx.y = 32-row group of n (8 per 256-wide column
 // block nb = blockIdx.y / 8, whose image is [nb][K/32 blocks]): 8x the CTAs of
 // one block per k-block (the image is launch-latency bound)
+}  // namespace
+// The next weight image's half of ws_bimg (alternating; grown to the largest
+// image so far, the halves at fixed offsets).
+// An image launched after an earlier one of the SAME call (its TMA GEMM did not
+// apply) goes without PDL: a plain launch waits for that image, which waits
+// for the GEMM still reading this half.
+#define BIMG_LAUNCH(grid, block, smem, stream, ...)                                  \
+  do {                                                                              \
+    if (img_launched) {                                                             \
+      bimg_kernel<<<grid, block, smem, stream>>>(__VA_ARGS__);                      \
+    } else {                                                                        \
+      TLP_LAUNCH_PDL(bimg_kernel, grid, block, smem, stream, __VA_ARGS__);          \
+    }                                                                               \
+    img_launched = true;                                                            \
+  } while (0)
+static uint8_t* bimg_buffer(tlp_ctx* ctx, size_t bytes, cudaError_t* err) {
+  bytes = (bytes + 255) & ~(size_t)255;
+  if (bytes > ctx->bimg_half) ctx->bimg_half = bytes;
+  *err = ctx->ws_bimg.ensure(2 * ctx->bimg_half);
+  ctx->bimg_flip ^= 1;
+  return ctx->ws_bimg.as<uint8_t>() + (ctx->bimg_flip ? ctx->bimg_half : 0);
+}
+namespace {
 __global__ void bimg_kernel(const float* __restrict__ B, int64_t ldb, int tb, int64_t N, int64_t K,
                             uint8_t* __restrict__ img) {
-  pdl_wait();  // img may still be read by the previous GEMM
+  // Programmatic dependent launch: the image goes to the half of the buffer
+  // the previous GEMM does not read (bimg_buffer) and depends only on weights
+  // final since the step began (P, or Wcat / the head concatenation packed at
+  // its start), so it is built while the previous kernel still runs; the wait
+  // at the END keeps the chain -- this grid completes only after its
+  // predecessor did, so the GEMM that follows still sees every earlier result.
   pdl_trigger();
   const int64_t kb = blockIdx.x, nb = blockIdx.y / (BNI / 32);
   uint8_t* dst = img + (nb * gridDim.x + kb) * 2 * IMG_HALF;
@@ -352,6 +380,7 @@ __global__ void bimg_kernel(const float* __restrict__ B, int64_t ldb, int tb, in
     *reinterpret_cast<__nv_bfloat16*>(dst + off) = h;
     *reinterpret_cast<__nv_bfloat16*>(dst + IMG_HALF + off) = __float2bfloat16_rn(x - __bfloat162float(h));
   }
+  pdl_wait();
 }
 
 __global__ void __launch_bounds__(THREADS, 2) tc_gemm_bimg_kernel(int64_t M, int64_t N, int64_t K,
@@ -639,6 +668,7 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 
 tlp_status tc_gemm(tlp_ctx* ctx, bool ta, bool tb, int64_t M, int64_t N, int64_t K,
                    const float* A, int64_t lda, const float* B, int64_t ldb, float* C,
                    int64_t ldc, const EpiParams& e, int splits, int64_t kslice, cudaStream_t s) {
+  bool img_launched = false;  // BIMG_LAUNCH
   TLP_SMEM_ATTR((tc_gemm_kernel<false, false>), SMEM_BYTES);
   TLP_SMEM_ATTR((tc_gemm_kernel<false, true>), SMEM_BYTES);
   TLP_SMEM_ATTR((tc_gemm_kernel<true, false>), SMEM_BYTES);
@@ -656,9 +686,10 @@ tlp_status tc_gemm(tlp_ctx* ctx, bool ta, bool tb, int64_t M, int64_t N, int64_t
   // in the weight image: zero columns on a memory-bound kernel) when it applies
   if (!ta && splits == 1 && N > 64 && N <= BN && N % 16 == 0 && K > 0 && M >= 4096) {
     const int64_t nkb = cdiv(K, BK);
-    TLP_CUDA_TRY(ctx->ws_bimg.ensure((size_t)nkb * 2 * IMG_HALF));
-    uint8_t* img = ctx->ws_bimg.as<uint8_t>();
-    TLP_LAUNCH_PDL(bimg_kernel, dim3((unsigned)nkb, BNI / 32), 256, 0, s, B, ldb, tb ? 1 : 0, N, K, img);
+    cudaError_t be;
+    uint8_t* img = bimg_buffer(ctx, (size_t)nkb * 2 * IMG_HALF, &be);
+    TLP_CUDA_TRY(be);
+    BIMG_LAUNCH( dim3((unsigned)nkb, BNI / 32), 256, 0, s, B, ldb, tb ? 1 : 0, N, K, img);
     TLP_LAUNCH_CHECK();
     const tlp_status ts = tc_gemm_tma(ctx, M, N, K, A, lda, img, C, ldc, e, s);
     if (ts != TLP_ERR_UNSUPPORTED) return ts;
@@ -667,9 +698,10 @@ tlp_status tc_gemm(tlp_ctx* ctx, bool ta, bool tb, int64_t M, int64_t N, int64_t
   // GEMMs): one launch over [row block x 256-wide column block] tiles
   if (!ta && splits == 1 && N > BNI && N % BNI == 0 && K > 0 && M >= 4096) {
     const int64_t nkb = cdiv(K, BK), ntn = N / BNI;
-    TLP_CUDA_TRY(ctx->ws_bimg.ensure((size_t)ntn * nkb * 2 * IMG_HALF));
-    uint8_t* img = ctx->ws_bimg.as<uint8_t>();
-    TLP_LAUNCH_PDL(bimg_kernel, dim3((unsigned)nkb, (unsigned)(ntn * BNI / 32)), 256, 0, s, B, ldb, tb ? 1 : 0, N, K, img);
+    cudaError_t be;
+    uint8_t* img = bimg_buffer(ctx, (size_t)ntn * nkb * 2 * IMG_HALF, &be);
+    TLP_CUDA_TRY(be);
+    BIMG_LAUNCH( dim3((unsigned)nkb, (unsigned)(ntn * BNI / 32)), 256, 0, s, B, ldb, tb ? 1 : 0, N, K, img);
     TLP_LAUNCH_CHECK();
     const tlp_status ts = tc_gemm_tma(ctx, M, N, K, A, lda, img, C, ldc, e, s);
     if (ts != TLP_ERR_UNSUPPORTED) return ts;
@@ -677,9 +709,10 @@ tlp_status tc_gemm(tlp_ctx* ctx, bool ta, bool tb, int64_t M, int64_t N, int64_t
   if (!ta && splits == 1 && N > BN && N <= BNI && K > 0) {
     TLP_SMEM_ATTR(tc_gemm_bimg_kernel, ISMEM);
     const int64_t nkb = cdiv(K, BK);
-    TLP_CUDA_TRY(ctx->ws_bimg.ensure((size_t)nkb * 2 * IMG_HALF));
-    uint8_t* img = ctx->ws_bimg.as<uint8_t>();
-    TLP_LAUNCH_PDL(bimg_kernel, dim3((unsigned)nkb, BNI / 32), 256, 0, s, B, ldb, tb ? 1 : 0, N, K, img);
+    cudaError_t be;
+    uint8_t* img = bimg_buffer(ctx, (size_t)nkb * 2 * IMG_HALF, &be);
+    TLP_CUDA_TRY(be);
+    BIMG_LAUNCH( dim3((unsigned)nkb, BNI / 32), 256, 0, s, B, ldb, tb ? 1 : 0, N, K, img);
     TLP_LAUNCH_CHECK();
     // the TMA-fed persistent kernel (k_tc_tma.cu) when the operands allow it
     const tlp_status ts = tc_gemm_tma(ctx, M, N, K, A, lda, img, C, ldc, e, s);

@@ -91,7 +91,11 @@ struct tlp_ctx {
 
   // workspaces
   DevBuf ws_tokens, ws_act, ws_train, ws_rank, ws_topk, ws_misc, ws_partial, ws_merge;
-  DevBuf ws_bimg;  // bf16 hi/lo image of a training GEMM's weight operand (k_tc_gemm.cu)
+  DevBuf ws_bimg;  // bf16 hi/lo images of the training GEMMs' weight operands, two halves
+                   // used alternately (k_tc_gemm.cu: the next image is built while the
+                   // previous GEMM still reads its own)
+  size_t bimg_half = 0;
+  int bimg_flip = 0;
   DevBuf ws_hcat;  // MTL heads side by side: [W1_0 | W1_1 | ...] [H, nt hd] then [c1_0 | c1_1 | ...]
   DevBuf ws_wcat;  // per attention layer [Wq | Wk | Wv] rows side by side, then [bq | bk | bv]:
                   // the fused Q/K/V forward GEMM and dgrad operands (k_simt.cu)
